@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py -- cubic-spline build + eval on B200 (arXiv 2001.09253 hot path).
+
+One step = the whole hot path over one batch: spline_build (validate, assemble rows,
+forward elimination, back-substitution) then spline_eval (locate + Eq. nr_formula),
+through the C ABI, on inputs resident in HBM.  Default workload: BASELINE.json
+configs[1] (65,536 curves x 64 knots, fp32, clamped, 256 unsorted queries per curve).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling -- every rank builds and evaluates
+its own shard of curves (same shape, its own seed); no collective on the data path.
+Timing: CUDA events on the launching stream around every step, L2 flushed (256 MiB
+write) between steps outside the events, barrier + synchronize around the K steps, max
+over ranks.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "spline build+eval knots/s and queries/s; achieved HBM GB/s vs B200 peak"
+SPEC_HBM_GBS = 8000.0  # BASELINE.json's "~8 TB/s" denominator (context)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_for(workload_key: str, kernel: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(workload_key, {}).get(kernel)
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            import torch
+            h = None
+            try:
+                bus = torch.cuda.get_device_properties(dev_index).pci_bus_id
+                for i in range(pynvml.nvmlDeviceGetCount()):
+                    hh = pynvml.nvmlDeviceGetHandleByIndex(i)
+                    b = pynvml.nvmlDeviceGetPciInfo(hh).busId
+                    b = b.decode() if isinstance(b, bytes) else b
+                    if b.lower().endswith(bus.lower()[-7:]):
+                        h = hh
+            except Exception:
+                h = None
+            self.h = h if h is not None else pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        rs = [name for bit, name in self.REASONS.items() if self.reasons & bit and name != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": rs, "samples": len(self.samples)}
+
+
+def algorithmic_bytes(B, n, m, s):
+    """build 3 s B/knot (read x, y; write y2) + 2 s per clamped curve;
+    eval (2 s + 4) B/query (read q; write out, int32 idx) + 3 n s per curve (x, y, y2)."""
+    build = 3 * s * B * n
+    evalb = (2 * s + 4) * B * m + 3 * n * s * B
+    return build, evalb
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, timed on the host cores (rank 0)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_2001_09253_b200 import workloads
+    spec = workloads.CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    sample_curves = {1: 1, 2: 8192, 3: 65536, 4: 8, 5: 1}[args.config]
+    kw = dict(batch=sample_curves)
+    if args.config == 5:
+        kw.update(n=1 << 20, m=1 << 20)
+    wl = workloads.generate(args.config, **kw)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        y2, _ = oracle.build_y2(wl.x, wl.y, wl.bc, wl.yp1, wl.ypn, nthreads=cores)
+        oracle.evaluate(wl.x, wl.y, y2, wl.q, nthreads=cores)
+        t1 = time.perf_counter()
+        if it >= args.warmup:
+            times.append(t1 - t0)
+    t = statistics.mean(times)
+    qps = wl.batch * wl.m / t
+    sample = f"{wl.batch} curves x n={wl.n} x m={wl.m} of {spec.name} per step (build + eval)"
+    line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle; inputs widened)",
+            "data": "synthetic (seeded, BASELINE.json config recipe)",
+            "config": {"workload": spec.name, "batch": wl.batch, "n": wl.n, "m": wl.m},
+            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "knots_per_s": wl.batch * wl.n / t}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, wl_full):
+    import oracle
+    cores = os.cpu_count() or 1
+    wl = wl_full
+    if args.config in (4, 5):  # bound the sample to ~10-30 s of CPU work
+        from paper_2001_09253_b200 import workloads
+        wl = workloads.generate(args.config, batch=64 if args.config == 4 else None,
+                                n=None if args.config == 4 else 1 << 22, m=None if args.config == 4 else 1 << 24)
+    t0 = time.perf_counter()
+    y2, _ = oracle.build_y2(wl.x, wl.y, wl.bc, wl.yp1, wl.ypn, nthreads=cores)
+    oracle.evaluate(wl.x, wl.y, y2, wl.q, nthreads=cores)
+    t = time.perf_counter() - t0
+    return {"value": wl.batch * wl.m / t, "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "sample": f"{wl.batch} curves x n={wl.n} x m={wl.m} (build + eval, {cores} threads), "
+                      f"{t:.2f} s", "knots_per_s": wl.batch * wl.n / t}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2001_09253_b200 import api, workloads
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    spec = workloads.CONFIGS[args.config]
+    wl = workloads.generate(args.config, shard=rank)
+    B, n, m = wl.batch, wl.n, wl.m
+    s = 4 if spec.dtype == "f32" else 8
+    stream = torch.cuda.current_stream()
+
+    def dev_t(a):
+        return torch.from_numpy(a).to(dev) if a is not None else None
+
+    x, y, q = dev_t(wl.x), dev_t(wl.y), dev_t(wl.q)
+    yp1, ypn = dev_t(wl.yp1), dev_t(wl.ypn)
+    y2 = torch.empty_like(x)
+    out = torch.empty_like(q)
+    idx = torch.empty(q.shape, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        api.build(x, y, wl.bc, yp1, ypn, out=y2)
+        api.evaluate(x, y, y2, q, wl.flags, out=out, idx=idx)
+
+    api.status()
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if api.status() != 0:
+        raise RuntimeError("data-error status raised on the benchmark inputs")
+
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(K):
+            flush.zero_()  # evict L2 (126 MB) between steps, outside the timed events
+            ev[k][0].record(stream)
+            api.build(x, y, wl.bc, yp1, ypn, out=y2)
+            ev[k][1].record(stream)
+            api.evaluate(x, y, y2, q, wl.flags, out=out, idx=idx)
+            ev[k][2].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    build_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
+    eval_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
+    step_ms = statistics.mean(b + e for b, e in zip(build_ms, eval_ms))
+    t = torch.tensor([step_ms, statistics.mean(build_ms), statistics.mean(eval_ms)], dtype=torch.float64,
+                     device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms, bms, ems = t.tolist()
+
+    # ---- end to end through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e:
+        h_in = [torch.from_numpy(a).pin_memory() for a in (wl.x, wl.y, wl.q)]
+        h_sl = [torch.from_numpy(a).pin_memory() if a is not None else None for a in (wl.yp1, wl.ypn)]
+        h_y2 = torch.empty(x.shape, dtype=x.dtype).pin_memory()
+        h_out = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+        h_idx = torch.empty(q.shape, dtype=torch.int32).pin_memory()
+        d_x, d_y, d_q = torch.empty_like(x), torch.empty_like(y), torch.empty_like(q)
+        d_s = [torch.empty_like(a) if a is not None else None for a in (yp1, ypn)]
+
+        def e2e_step():
+            d_x.copy_(h_in[0], non_blocking=True)
+            d_y.copy_(h_in[1], non_blocking=True)
+            d_q.copy_(h_in[2], non_blocking=True)
+            for d, h in zip(d_s, h_sl):
+                if d is not None:
+                    d.copy_(h, non_blocking=True)
+            api.build(d_x, d_y, wl.bc, d_s[0], d_s[1], out=y2)
+            api.evaluate(d_x, d_y, y2, d_q, wl.flags, out=out, idx=idx)
+            h_y2.copy_(y2, non_blocking=True)
+            h_out.copy_(out, non_blocking=True)
+            h_idx.copy_(idx, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        KE = max(1, min(args.e2e_steps, K))
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(KE):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / KE], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = sum(a.nbytes for a in (wl.x, wl.y, wl.q)) + sum(a.nbytes for a in (wl.yp1, wl.ypn) if a is not None)
+        d2h = x.numel() * s + q.numel() * s + q.numel() * 4
+        e2e = {"value": world * B * m / (te.item() * 1e-3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": te.item(), "pinned": True,
+               "path": "api.build/api.evaluate (C ABI) with pinned host in/out, copies on the same stream"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    bbytes, ebytes = algorithmic_bytes(B, n, m, s)
+    peak, peak_src = peaks()
+    ach = ebytes / (ems * 1e-3) / 1e9
+    wkey = f"cfg{args.config}"
+    launches = 2 * K  # 1 build kernel + 1 eval kernel per step for configs 1-4
+    if n > 256 * (16 if s == 8 else 32):
+        launches = 4 * K  # tiled SPIKE: reduce + top + finish, then eval
+    line = {
+        "metric": METRIC,
+        "value": world * B * m / (step_ms * 1e-3),
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": spec.dtype,
+        "data": "synthetic (seeded PCG64, BASELINE.json config recipe; DESIGN.md input recipe)",
+        "config": {"workload": spec.name, "batch_per_gpu": B, "n": n, "m": m, "bc": wl.bc, "flags": wl.flags,
+                   "l2": "flushed (256 MiB write) between steps, outside the timed events",
+                   "parallelism": f"dp{world} (curve shards, no data-path collective)"},
+        "knots_per_s": world * B * n / (step_ms * 1e-3),
+        "hbm_gbs_step": (bbytes + ebytes) / (step_ms * 1e-3) / 1e9,
+        "frac_of_spec_8tbs_step": (bbytes + ebytes) / (step_ms * 1e-3) / 1e9 / SPEC_HBM_GBS,
+        "build_ms": bms,
+        "eval_ms": ems,
+        "build_gbs": bbytes / (bms * 1e-3) / 1e9,
+        "roofline": {"kernel": "k_eval_staged" if 3 * n * s <= 96 * 1024 else "k_eval_global", "bound": "hbm",
+                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": traffic_for(wkey, "eval"), "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": ebytes,
+                     "build": {"achieved": bbytes / (bms * 1e-3) / 1e9, "frac": bbytes / (bms * 1e-3) / 1e9 / peak,
+                               "algorithmic_bytes_per_launch": bbytes, "traffic": traffic_for(wkey, "build")}},
+        "cpu_baseline": None,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args, wl)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

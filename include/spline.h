@@ -1,0 +1,141 @@
+/*
+ * spline.h -- C ABI of the B200-native cubic-spline library (libfastspline.so).
+ *
+ * The hot path of Hornbeck, "Fast Cubic Spline Interpolation" (arXiv 2001.09253):
+ *   construction  -- the knot second derivatives y2 ("y''") solve the tridiagonal
+ *                    system of Eq. init_val with natural ends
+ *                    (y2 = 0) or clamped ends
+ *                    (P:955-971 start row; P:1017-1018 end row);
+ *   evaluation    -- each query q is located in its knot interval j and the cubic
+ *                    of Eq. nr_formula is applied.
+ *
+ * Conventions (all entry points):
+ *   - Every array argument is a DEVICE pointer owned by the caller (e.g. a torch
+ *     CUDA tensor's data_ptr()), C-contiguous and curve-major: x, y, y2 are
+ *     [batch][n]; q, out, idx are [batch][m]; yp1, ypn are [batch].  Element type
+ *     is float (SPLINE_F32) or double (SPLINE_F64), selected by `dtype` or by the
+ *     _f32/_f64 wrapper.  idx is int32 (0-based interval index).
+ *   - All curves of one call share n, and all share m (ragged batches: one call
+ *     per (n, m) group).
+ *   - Work is enqueued on `stream` (NULL = the legacy default stream) and the call
+ *     returns without synchronising.  The library is re-entrant; the only shared
+ *     mutable state is the device-wide data-error word read by spline_status().
+ *   - Temporary workspace (long-curve SPIKE records only) comes from the
+ *     stream-ordered allocator (cudaMallocAsync on `stream`).
+ *
+ * Errors:
+ *   - Argument errors are synchronous: the call returns SPLINE_EINVAL and enqueues
+ *     nothing (NULL required pointer, n < 3 [P:746, P:1047], batch < 0, m < 0,
+ *     unknown bc/dtype, NULL yp1/ypn for a clamped end, n or m >= 2^31).
+ *     batch == 0 or m == 0 is a valid no-op.
+ *   - CUDA launch/allocation failures return SPLINE_ECUDA / SPLINE_ENOMEM.
+ *   - Data errors are asynchronous (cuSOLVER devInfo pattern) and OR'ed into the
+ *     device-wide status word read (and cleared) by spline_status():
+ *       SPLINE_STATUS_BAD_KNOTS: a curve's knots are not strictly increasing or a
+ *         value/slope is not finite; that curve's y2 is all NaN.
+ *       SPLINE_STATUS_Q_OUT_OF_RANGE: a query is outside [x_0, x_{n-1}] or NaN
+ *         (Eq. nr_formula requires x_j <= x <= x_{j+1}); its idx is -1 and
+ *         its out is NaN.  No extrapolation.
+ */
+#ifndef FASTSPLINE_SPLINE_H
+#define FASTSPLINE_SPLINE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *spline_stream_t; /* identical to cudaStream_t */
+
+enum { SPLINE_F32 = 0, SPLINE_F64 = 1 };
+enum { SPLINE_OK = 0, SPLINE_EINVAL = -1, SPLINE_ECUDA = -2, SPLINE_ENOMEM = -3 };
+/* Boundary condition: a bitmask, the two ends are independent (the paper tests
+ * its natural-end sentinel separately per end).  The 0.99e30
+ * sentinel itself is never interpreted by the library. */
+enum {
+  SPLINE_BC_NATURAL = 0,     /* y2_0 = y2_{n-1} = 0 */
+  SPLINE_BC_CLAMP_START = 1, /* y'(x_0) = yp1[c]: 2h_0 y2_0 + h_0 y2_1 = 6(dd_0 - yp1) */
+  SPLINE_BC_CLAMP_END = 2,   /* y'(x_{n-1}) = ypn[c]: h y2_{n-2} + 2h y2_{n-1} = 6(ypn - dd_{n-2}) */
+  SPLINE_BC_CLAMPED = 3
+};
+/* Evaluation hints: may change speed, never results (every guess is corrected by
+ * comparisons against the same locate rule). */
+enum { SPLINE_Q_SORTED = 1, SPLINE_X_UNIFORM = 2 };
+/* Asynchronous data-error bits (spline_status). */
+enum { SPLINE_STATUS_BAD_KNOTS = 1, SPLINE_STATUS_Q_OUT_OF_RANGE = 2 };
+
+/*
+ * spline_build -- knot second derivatives for `batch` independent curves.
+ *   x, y   [batch][n] knots (strictly increasing per curve) and values.
+ *   bc     SPLINE_BC_* bitmask; yp1 / ypn are [batch] end slopes, required
+ *          (non-NULL) iff that end is clamped, ignored otherwise.
+ *   y2     [batch][n] output: the unique solution of the (strictly diagonally
+ *          dominant) tridiagonal system; natural ends are exactly 0.
+ * Kernels by n: <= 128 batched Thomas (one thread per curve);
+ * <= 4096 (f64) / 8192 (f32) one CTA per curve (partition + merge tree);
+ * longer: tiled SPIKE (tile records -> reduced solve -> finish).
+ */
+int spline_build(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1,
+                 const void *ypn, void *y2, int dtype, spline_stream_t stream);
+
+/*
+ * spline_eval -- fused locate + evaluate.
+ *   x, y, y2  [batch][n] as produced/consumed by spline_build.
+ *   q         [batch][m] queries of curve c are q[c*m .. c*m+m-1].
+ *   out       [batch][m] Eq. nr_formula at q on interval idx.
+ *   idx       [batch][m] int32, nullable: the largest j in [0, n-2] with
+ *             x_j <= q (so a query on an interior knot x_k gets k, q = x_{n-1}
+ *             gets n-2); -1 if q is outside [x_0, x_{n-1}] or NaN.
+ *   flags     SPLINE_Q_SORTED | SPLINE_X_UNIFORM hints (speed only).
+ */
+int spline_eval(const void *x, const void *y, const void *y2, int64_t n, int64_t batch, const void *q,
+                int64_t m, void *out, int32_t *idx, int flags, int dtype, spline_stream_t stream);
+
+/* Typed thin wrappers (same semantics). */
+int spline_build_f32(const float *x, const float *y, int64_t n, int64_t batch, int bc, const float *yp1,
+                     const float *ypn, float *y2, spline_stream_t stream);
+int spline_build_f64(const double *x, const double *y, int64_t n, int64_t batch, int bc, const double *yp1,
+                     const double *ypn, double *y2, spline_stream_t stream);
+int spline_eval_f32(const float *x, const float *y, const float *y2, int64_t n, int64_t batch, const float *q,
+                    int64_t m, float *out, int32_t *idx, int flags, spline_stream_t stream);
+int spline_eval_f64(const double *x, const double *y, const double *y2, int64_t n, int64_t batch,
+                    const double *q, int64_t m, double *out, int32_t *idx, int flags, spline_stream_t stream);
+
+/* Synchronises `stream`, writes the OR of the data-error bits raised since the
+ * last call into *bits_out (host pointer) and clears them.  Returns SPLINE_OK or
+ * SPLINE_ECUDA. */
+int spline_status(spline_stream_t stream, unsigned int *bits_out);
+
+/*
+ * Two-phase SPIKE seam for one long curve whose rows are partitioned across
+ * ranks (the partition method with a merge tree of block
+ * records).  Rank r owns rows [row_begin, row_end) of the n-row system and holds
+ * the full x and y (replicated, device).  A block record is 6 values of dtype:
+ *   (Gp, Vp, Wp, Gq, Vq, Wq) with y_p = Gp - Vp*y_{p-1} - Wp*y_{q+1} and
+ *   y_q = Gq - Vq*y_{p-1} - Wq*y_{q+1} for the block's first row p and last row q.
+ *
+ * spline_spike_reduce: writes this rank's block record (6 values) to `record`.
+ * The caller all-gathers the G records in rank order into `all_records` [G][6].
+ * spline_spike_finish: solves the G-record reduced system redundantly, then writes
+ *   y2 for rows [row_begin, row_end) into y2_shard[0 .. row_end-row_begin).
+ * `workspace` (device, spline_spike_workspace_size bytes) must be the same buffer
+ * for the reduce and finish calls of one rank.  bc/yp1/ypn as spline_build
+ * (yp1/ypn point to one value each).  Data errors: as spline_build, per shard.
+ */
+size_t spline_spike_workspace_size(int64_t n, int64_t row_begin, int64_t row_end, int dtype);
+int spline_spike_reduce(const void *x, const void *y, int64_t n, int64_t row_begin, int64_t row_end, int bc,
+                        const void *yp1, const void *ypn, void *record, void *workspace, int dtype,
+                        spline_stream_t stream);
+int spline_spike_finish(const void *x, const void *y, int64_t n, int64_t row_begin, int64_t row_end, int bc,
+                        const void *yp1, const void *ypn, const void *all_records, int nranks, int rank,
+                        void *y2_shard, void *workspace, int dtype, spline_stream_t stream);
+
+/* Library version string (static storage). */
+const char *spline_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTSPLINE_SPLINE_H */

@@ -6,11 +6,11 @@ calling any op without the built library raises.
 """
 from .workloads import CONFIGS, generate  # noqa: F401
 
-__all__ = ["CONFIGS", "generate", "api"]
+__all__ = ["CONFIGS", "generate", "api", "dist"]
 
 
 def __getattr__(name):
-    if name == "api":
-        from . import api
-        return api
+    if name in ("api", "dist"):
+        import importlib
+        return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

@@ -1,0 +1,118 @@
+"""torch-tensor front end of the C ABI (include/spline.h).
+
+PyTorch provides device memory and streams only; every step of build and eval runs
+in libfastspline's sm_100a kernels.  All tensors are CUDA, C-contiguous, curve-major:
+x, y, y2 (B, n); q, out (B, m); idx (B, m) int32; yp1, ypn (B,).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import (BC_CLAMP_END, BC_CLAMP_START, BC_CLAMPED, BC_NATURAL, Q_SORTED,  # noqa: F401
+                   STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE, X_UNIFORM)
+
+_DT = {torch.float32: _lib.SPLINE_F32, torch.float64: _lib.SPLINE_F64}
+
+
+def _stream(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _check_curves(x, *others):
+    if not (isinstance(x, torch.Tensor) and x.is_cuda):
+        raise ValueError("spline ops take CUDA tensors (no CPU fallback)")
+    if x.dtype not in _DT:
+        raise ValueError(f"dtype must be float32 or float64, got {x.dtype}")
+    for t in (x, *others):
+        if t is None:
+            continue
+        if t.device != x.device or t.dtype != x.dtype or not t.is_contiguous():
+            raise ValueError("all arrays must be contiguous, on the same device, same dtype")
+
+
+def _as2d(t):
+    return t.unsqueeze(0) if t is not None and t.dim() == 1 else t
+
+
+def build(x: torch.Tensor, y: torch.Tensor, bc: int = BC_NATURAL, yp1=None, ypn=None, out=None, stream=None):
+    """Second derivatives y2 of the curves (x, y): (B, n) or (n,).  Returns y2."""
+    squeeze = x.dim() == 1
+    x, y = _as2d(x), _as2d(y)
+    B, n = x.shape
+    if yp1 is not None and not isinstance(yp1, torch.Tensor):
+        yp1 = torch.full((B,), float(yp1), dtype=x.dtype, device=x.device)
+    if ypn is not None and not isinstance(ypn, torch.Tensor):
+        ypn = torch.full((B,), float(ypn), dtype=x.dtype, device=x.device)
+    _check_curves(x, y, yp1, ypn)
+    if y.shape != x.shape:
+        raise ValueError("x and y must have the same shape")
+    y2 = torch.empty_like(x) if out is None else _as2d(out)
+    _check_curves(x, y2)
+    rc = _lib.load().spline_build(_p(x), _p(y), n, B, bc, _p(yp1), _p(ypn), _p(y2), _DT[x.dtype],
+                                  ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_build")
+    return y2[0] if squeeze else y2
+
+
+def evaluate(x, y, y2, q, flags: int = 0, out=None, idx=None, want_idx: bool = True, stream=None):
+    """Locate + evaluate queries q (B, m) on curves (B, n).  Returns (out, idx or None)."""
+    squeeze = x.dim() == 1
+    x, y, y2, q = _as2d(x), _as2d(y), _as2d(y2), _as2d(q)
+    B, n = x.shape
+    m = q.shape[1]
+    _check_curves(x, y, y2, q)
+    if q.shape[0] != B:
+        raise ValueError("q must be (B, m)")
+    o = torch.empty_like(q) if out is None else _as2d(out)
+    i = None
+    if want_idx:
+        i = torch.empty(q.shape, dtype=torch.int32, device=q.device) if idx is None else _as2d(idx)
+        if i.dtype != torch.int32 or not i.is_contiguous():
+            raise ValueError("idx must be contiguous int32")
+    rc = _lib.load().spline_eval(_p(x), _p(y), _p(y2), n, B, _p(q), m, _p(o), _p(i), flags, _DT[x.dtype],
+                                 ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_eval")
+    if squeeze:
+        return o[0], (None if i is None else i[0])
+    return o, i
+
+
+def status(stream=None) -> int:
+    """Synchronise the stream, return and clear the data-error bits (STATUS_*)."""
+    bits = ctypes.c_uint(0)
+    rc = _lib.load().spline_status(ctypes.c_void_p(_stream(stream)), ctypes.byref(bits))
+    _lib.check(rc, "spline_status")
+    return bits.value
+
+
+def spike_workspace(n: int, row_begin: int, row_end: int, dtype, device) -> torch.Tensor:
+    nbytes = _lib.load().spline_spike_workspace_size(n, row_begin, row_end, _DT[dtype])
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+def spike_reduce(x, y, row_begin: int, row_end: int, bc: int, yp1, ypn, record, workspace, stream=None):
+    n = x.shape[-1]
+    rc = _lib.load().spline_spike_reduce(_p(x), _p(y), n, row_begin, row_end, bc, _p(yp1), _p(ypn), _p(record),
+                                         _p(workspace), _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_spike_reduce")
+
+
+def spike_finish(x, y, row_begin: int, row_end: int, bc: int, yp1, ypn, all_records, nranks: int, rank: int,
+                 y2_shard, workspace, stream=None):
+    n = x.shape[-1]
+    rc = _lib.load().spline_spike_finish(_p(x), _p(y), n, row_begin, row_end, bc, _p(yp1), _p(ypn),
+                                         _p(all_records), nranks, rank, _p(y2_shard), _p(workspace),
+                                         _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_spike_finish")
+
+
+def version() -> str:
+    return _lib.load().spline_version().decode()

@@ -1,0 +1,346 @@
+// build_tile.cuh -- K2..K5: partitioned tridiagonal solve (mid-length curves and long curves).
+//
+// The system is the one of Eq. init_val with natural (P:1062-1064,
+// P:1096-1098) or clamped end rows.  It is strictly diagonally
+// dominant and symmetric positive definite, so every elimination below is
+// pivot-free (the paper's justification for Thomas), and the GPU remark of
+// P:815-821 (fewer serial steps via the parallel tridiagonal literature) is what this
+// file implements.
+//
+// Block record.  For a contiguous block of rows [p, q] whose couplings to the outside
+// unknowns L = y_{p-1} and R = y_{q+1} are moved to the right-hand side, the block's
+// solution is affine in (L, R).  Only its two tips are kept:
+//     y_p = Gp - Vp L - Wp R,        y_q = Gq - Vq L - Wq R          (6 scalars)
+// (SURVEY.md Appendix A's spike tips g, v, w).  Records of adjacent blocks merge
+// associatively (a 2x2 solve for the two rows at the seam, determinant 1 - A.Wq B.Vp > 0
+// by diagonal dominance), and the merge is reversed top-down once the outer L, R are
+// known.  One machinery serves three levels:
+//   leaf   : one thread, R consecutive rows -- a Thomas forward sweep with
+//            three right-hand sides (d, a_p e_1, c_q e_q) and a backward Horner pass;
+//   tile   : one CTA, 256 leaves -- merge tree in shared memory;
+//   curve  : tiles of one long curve (and ranks of a multi-GPU curve) -- k4_top.
+// The final per-row solve is the paper's back-substitution:
+// y_i = g'_i - v'_i L - c'_i y_{i+1}.
+#pragma once
+#include "common.cuh"
+
+namespace fs {
+
+template <typename T> struct Rec { T Gp, Vp, Wp, Gq, Vq, Wq; };
+
+// Merge adjacent block records A = [p, m], B = [m+1, q] into [p, q].
+template <typename T> __device__ __forceinline__ Rec<T> merge_rec(const Rec<T> &A, const Rec<T> &B) {
+  const T iD = T(1) / (T(1) - A.Wq * B.Vp);
+  const T Gm = (A.Gq - A.Wq * B.Gp) * iD, Vm = A.Vq * iD, Wm = -(A.Wq * B.Wp) * iD;    // y_m
+  const T Gm1 = (B.Gp - B.Vp * A.Gq) * iD, Vm1 = -(B.Vp * A.Vq) * iD, Wm1 = B.Wp * iD;  // y_{m+1}
+  Rec<T> o;
+  o.Gp = A.Gp - A.Wp * Gm1;
+  o.Vp = A.Vp - A.Wp * Vm1;
+  o.Wp = -(A.Wp * Wm1);
+  o.Gq = B.Gq - B.Vq * Gm;
+  o.Vq = -(B.Vq * Vm);
+  o.Wq = B.Wq - B.Vq * Wm;
+  return o;
+}
+
+// Given the outer unknowns (L, R) of a merged block, recover the two seam rows
+// y_m (last row of A) and y_{m+1} (first row of B) from A's q-tip and B's p-tip.
+template <typename T>
+__device__ __forceinline__ void split_seam(T AGq, T AVq, T AWq, T BGp, T BVp, T BWp, T L, T R, T &ym, T &ym1) {
+  const T alpha = AGq - AVq * L;
+  const T beta = BGp - BWp * R;
+  ym = (alpha - AWq * beta) / (T(1) - AWq * BVp);
+  ym1 = beta - BVp * ym;
+}
+
+// Block-level merge tree over nleaf records held in shared memory.  Level s (1, 2, 4..)
+// merges rec[i] and rec[i+s] for i a multiple of 2s into rec[i]; the six seam values of
+// every merge are saved in mi[] for the top-down pass.  Ends with __syncthreads().
+template <typename T> __device__ void tree_up(Rec<T> *rec, T *mi, int nleaf) {
+  int off = 0;
+  for (int s = 1; s < nleaf; s <<= 1) {
+    const int nn = (nleaf + 2 * s - 1) / (2 * s);
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+      const int i = k * 2 * s, j = i + s;
+      if (j < nleaf) {
+        const Rec<T> A = rec[i], B = rec[j];
+        T *o = mi + 6 * (off + k);
+        o[0] = A.Gq; o[1] = A.Vq; o[2] = A.Wq; o[3] = B.Gp; o[4] = B.Vp; o[5] = B.Wp;
+        rec[i] = merge_rec(A, B);
+      }
+    }
+    off += nn;
+    __syncthreads();
+  }
+}
+
+// Top-down: ext[i] = (L, R) of leaf i, given the root's (L, R).  Ends with __syncthreads().
+template <typename T> __device__ void tree_down(const T *mi, T *ext, int nleaf, T L, T R) {
+  if (threadIdx.x == 0) { ext[0] = L; ext[1] = R; }
+  int smax = 1, total = 0;
+  for (int s = 1; s < nleaf; s <<= 1) { smax = s; total += (nleaf + 2 * s - 1) / (2 * s); }
+  __syncthreads();
+  if (nleaf == 1) return;
+  int off = total;
+  for (int s = smax; s >= 1; s >>= 1) {
+    const int nn = (nleaf + 2 * s - 1) / (2 * s);
+    off -= nn;
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+      const int i = k * 2 * s, j = i + s;
+      if (j < nleaf) {
+        const T *o = mi + 6 * (off + k);
+        const T Li = ext[2 * i], Ri = ext[2 * i + 1];
+        T ym, ym1;
+        split_seam(o[0], o[1], o[2], o[3], o[4], o[5], Li, Ri, ym, ym1);
+        ext[2 * i + 1] = ym1;
+        ext[2 * j] = ym;
+        ext[2 * j + 1] = Ri;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+enum { TILE_FULL = 0, TILE_REDUCE = 1, TILE_FINISH = 2 };
+constexpr int kTileThreads = 256;
+
+template <typename T, int R> __host__ __device__ constexpr size_t tile_smem_bytes() {
+  return sizeof(T) * (2 * (size_t)kTileThreads * (R + 1) + 6 * kTileThreads + 6 * kTileThreads);
+}
+
+// One CTA solves rows [P, Q] of curve blockIdx.y (P = row_begin + blockIdx.x * 256R).
+//  FULL   : the tile is the whole curve (row_begin = 0, row_end = n <= 256R); writes y2.
+//  REDUCE : writes the tile's block record to tile_rec[(c*ntiles + t)*6].
+//  FINISH : reads the tile's outer (L, R) from tile_ext[(c*ntiles + t)*2]; writes y2 rows
+//           [P, Q] to y2 + c*(row_end-row_begin) + (P - row_begin).
+template <typename T, int R, int MODE>
+__global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, const T *__restrict__ y, int64_t n,
+                                                      int64_t row_begin, int64_t row_end, int bc,
+                                                      const T *__restrict__ yp1, const T *__restrict__ ypn,
+                                                      T *__restrict__ y2, T *__restrict__ tile_rec,
+                                                      const T *__restrict__ tile_ext, int *__restrict__ badflag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int NT = kTileThreads;
+  constexpr int TR = NT * R;
+  T *X = reinterpret_cast<T *>(smem_raw);
+  T *Y = X + NT * (R + 1);
+  Rec<T> *rec = reinterpret_cast<Rec<T> *>(Y + NT * (R + 1));
+  T *mi = reinterpret_cast<T *>(rec + NT);
+  T *ext = reinterpret_cast<T *>(rec);  // aliases rec: used only after tree_up
+
+  const int64_t c = blockIdx.y;
+  const int ntiles = gridDim.x;
+  const int64_t P = row_begin + (int64_t)blockIdx.x * TR;
+  const int nrows = (int)min64(TR, row_end - P);
+  const int nleaf = (nrows + R - 1) / R;
+  const T *xc = x + c * n;
+  const T *yc = y + c * n;
+  auto pad = [](int i) { return i + i / R; };
+
+  for (int e = threadIdx.x; e < nrows; e += NT) {
+    X[pad(e)] = ld_stream(xc + P + e);
+    Y[pad(e)] = ld_stream(yc + P + e);
+  }
+  __syncthreads();
+
+  const int l = threadIdx.x;
+  const int p = l * R;
+  const int rows = min(R, nrows - p);
+  T v[R];
+  bool ok = true;
+  T xm1 = T(0), ym1 = T(0), xq1 = T(0), yq1 = T(0);
+  if (l < nleaf) {
+    if (l == 0) {
+      if (P > 0) { xm1 = xc[P - 1]; ym1 = yc[P - 1]; }
+    } else {
+      xm1 = X[pad(p - 1)];
+      ym1 = Y[pad(p - 1)];
+    }
+    const int q = p + rows - 1;
+    if (l == nleaf - 1) {
+      if (P + q + 1 < n) { xq1 = xc[P + q + 1]; yq1 = yc[P + q + 1]; }
+    } else {
+      xq1 = X[pad(q + 1)];
+      yq1 = Y[pad(q + 1)];
+    }
+  }
+  __syncthreads();  // every neighbour value is in registers before the sweeps overwrite X/Y
+
+  if (l < nleaf) {
+    const T s0 = (bc & 1) ? yp1[c] : T(0);
+    const T s1 = (bc & 2) ? ypn[c] : T(0);
+    if (bc & 1) ok = ok && finite(s0);
+    if (bc & 2) ok = ok && finite(s1);
+    T xi = X[pad(p)], yi = Y[pad(p)];
+    T hprev = T(0), ddprev = T(0);
+    if (P + p > 0) {
+      hprev = xi - xm1;
+      ddprev = (yi - ym1) / hprev;
+    }
+    T cprev = T(0), gprev = T(0), vprev = T(0);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (k < rows) {
+        const int i = p + k;
+        const int64_t gi = P + i;
+        T xn = T(0), yn = T(0), h = T(0), dd = T(0);
+        ok = ok && finite(xi) && finite(yi);
+        if (gi < n - 1) {
+          if (k < rows - 1) { xn = X[pad(i + 1)]; yn = Y[pad(i + 1)]; }
+          else { xn = xq1; yn = yq1; }
+          ok = ok && (xn > xi);
+          h = xn - xi;
+          dd = (yn - yi) / h;
+        }
+        T a, b, cc, d;
+        if (gi == 0) {
+          a = T(0);
+          if (bc & 1) { b = T(2) * h; cc = h; d = T(6) * (dd - s0); }
+          else { b = T(1); cc = T(0); d = T(0); }                       // y2_0 = 0
+        } else if (gi == n - 1) {
+          cc = T(0);
+          if (bc & 2) { a = hprev; b = T(2) * hprev; d = T(6) * (s1 - ddprev); }
+          else { a = T(0); b = T(1); d = T(0); }                                   // y2_{n-1} = 0
+        } else {  // Eq. init_val
+          a = hprev; b = T(2) * (hprev + h); cc = h; d = T(6) * (dd - ddprev);
+        }
+        const T inv = T(1) / (k == 0 ? b : b - a * cprev);
+        const T cp = cc * inv;
+        const T gp = (k == 0 ? d : d - a * gprev) * inv;
+        const T vp = (k == 0 ? a : -(a * vprev)) * inv;
+        X[pad(i)] = cp;
+        Y[pad(i)] = gp;
+        v[k] = vp;
+        cprev = cp; gprev = gp; vprev = vp;
+        xi = xn; yi = yn; hprev = h; ddprev = dd;
+      }
+    }
+    Rec<T> r;
+    r.Gq = gprev; r.Vq = vprev; r.Wq = cprev;
+    T G = T(0), V = T(0), W = T(-1);  // y_{q+1} = R
+#pragma unroll
+    for (int k = R - 1; k >= 0; --k) {
+      if (k < rows) {
+        const T ck = X[pad(p + k)], gk = Y[pad(p + k)];
+        G = gk - ck * G;
+        V = v[k] - ck * V;
+        W = -(ck * W);
+      }
+    }
+    r.Gp = G; r.Vp = V; r.Wp = W;
+    rec[l] = r;
+  }
+  const bool bad = __syncthreads_or(!ok);
+  tree_up(rec, mi, nleaf);
+
+  if (MODE == TILE_REDUCE) {
+    if (threadIdx.x == 0) {
+      const Rec<T> r = rec[0];
+      T *o = tile_rec + (c * ntiles + blockIdx.x) * 6;
+      o[0] = r.Gp; o[1] = r.Vp; o[2] = r.Wp; o[3] = r.Gq; o[4] = r.Vq; o[5] = r.Wq;
+      if (bad) { atomicOr(badflag + c, 1); raise_status(kBadKnots); }
+    }
+    return;
+  }
+
+  T *y2o = (MODE == TILE_FULL) ? y2 + c * n + P : y2 + c * (row_end - row_begin) + (P - row_begin);
+  const bool curve_bad = (MODE == TILE_FULL) ? bad : (badflag[c] != 0);
+  if (curve_bad) {
+    if (MODE == TILE_FULL && threadIdx.x == 0) raise_status(kBadKnots);
+    for (int e = threadIdx.x; e < nrows; e += NT) y2o[e] = qnan<T>();
+    return;
+  }
+  T Lr = T(0), Rr = T(0);
+  if (MODE == TILE_FINISH) {
+    Lr = tile_ext[(c * ntiles + blockIdx.x) * 2];
+    Rr = tile_ext[(c * ntiles + blockIdx.x) * 2 + 1];
+  }
+  tree_down(mi, ext, nleaf, Lr, Rr);
+  if (l < nleaf) {
+    const T L = ext[2 * l];
+    T ynext = ext[2 * l + 1];
+#pragma unroll
+    for (int k = R - 1; k >= 0; --k) {
+      if (k < rows) {
+        const int i = p + k;
+        const T yv = Y[pad(i)] - v[k] * L - X[pad(i)] * ynext;  // y_i = g'_i - v'_i L - c'_i y_{i+1}
+        X[pad(i)] = yv;
+        ynext = yv;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nrows; e += NT) y2o[e] = X[pad(e)];
+}
+
+// K4: merge the per-tile records of each curve (grid = batch, one CTA per curve) and,
+// unless up_only, push the root's outer (L, R) back down to per-tile (L, R).
+// Each of the kTopThreads threads folds a contiguous chunk of tiles sequentially
+// (saving the running q-tips in foldq for the way down), then a shared-memory tree
+// merges the chunk records.
+constexpr int kTopThreads = 512;
+template <typename T> __host__ __device__ constexpr size_t top_smem_bytes() {
+  return sizeof(T) * (6 * kTopThreads + 6 * kTopThreads);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTopThreads) k4_top(const T *__restrict__ recs, int ntiles, int up_only,
+                                                      const T *__restrict__ root_ext, T *__restrict__ tile_ext,
+                                                      T *__restrict__ root_out, T *__restrict__ foldq) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Rec<T> *rec = reinterpret_cast<Rec<T> *>(smem_raw);
+  T *mi = reinterpret_cast<T *>(rec + kTopThreads);
+  T *ext = reinterpret_cast<T *>(rec);
+  const int64_t c = blockIdx.x;
+  const T *rc = recs + c * ntiles * 6;
+  T *fq = foldq + c * ntiles * 3;
+  const int chunk = (ntiles + kTopThreads - 1) / kTopThreads;
+  const int nleaf = (ntiles + chunk - 1) / chunk;
+  const int th = threadIdx.x;
+  const int first = th * chunk;
+  const int last = min(ntiles, first + chunk) - 1;
+  auto load = [&](int t) {
+    Rec<T> r;
+    r.Gp = rc[6 * t]; r.Vp = rc[6 * t + 1]; r.Wp = rc[6 * t + 2];
+    r.Gq = rc[6 * t + 3]; r.Vq = rc[6 * t + 4]; r.Wq = rc[6 * t + 5];
+    return r;
+  };
+  if (th < nleaf) {
+    Rec<T> acc = load(first);
+    for (int t = first + 1; t <= last; ++t) {
+      fq[3 * t] = acc.Gq; fq[3 * t + 1] = acc.Vq; fq[3 * t + 2] = acc.Wq;
+      acc = merge_rec(acc, load(t));
+    }
+    rec[th] = acc;
+  }
+  __syncthreads();
+  tree_up(rec, mi, nleaf);
+  if (up_only) {
+    if (th == 0) {
+      const Rec<T> r = rec[0];
+      T *o = root_out + c * 6;
+      o[0] = r.Gp; o[1] = r.Vp; o[2] = r.Wp; o[3] = r.Gq; o[4] = r.Vq; o[5] = r.Wq;
+    }
+    return;
+  }
+  const T L0 = root_ext ? root_ext[2 * c] : T(0);
+  const T R0 = root_ext ? root_ext[2 * c + 1] : T(0);
+  tree_down(mi, ext, nleaf, L0, R0);
+  if (th < nleaf) {
+    const T L = ext[2 * th];
+    T Rv = ext[2 * th + 1];
+    T *te = tile_ext + c * ntiles * 2;
+    for (int t = last; t > first; --t) {
+      const Rec<T> B = load(t);
+      T ym, ym1;
+      split_seam(fq[3 * t], fq[3 * t + 1], fq[3 * t + 2], B.Gp, B.Vp, B.Wp, L, Rv, ym, ym1);
+      te[2 * t] = ym;
+      te[2 * t + 1] = Rv;
+      Rv = ym1;
+    }
+    te[2 * first] = L;
+    te[2 * first + 1] = Rv;
+  }
+}
+
+}  // namespace fs

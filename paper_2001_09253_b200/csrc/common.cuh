@@ -1,0 +1,62 @@
+// common.cuh -- small device helpers shared by the sm_100a kernels of libfastspline.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fs {
+
+// Device-wide data-error word (see spline_status in include/spline.h).  The library is a
+// single translation unit (spline_abi.cu), so the definition lives here.
+__device__ unsigned int g_status = 0;
+
+constexpr unsigned kBadKnots = 1u;
+constexpr unsigned kOutOfRange = 2u;
+
+__device__ __forceinline__ void raise_status(unsigned bits) { atomicOr(&g_status, bits); }
+
+// Warp-aggregated status raise: one atomic per warp at most.
+__device__ __forceinline__ void raise_status_warp(bool pred, unsigned bits) {
+  unsigned mask = __activemask();
+  unsigned any = __ballot_sync(mask, pred);
+  if (any && (threadIdx.x & 31) == (__ffs(mask) - 1)) atomicOr(&g_status, bits);
+}
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+template <typename T> __device__ __forceinline__ T qnan();
+template <> __device__ __forceinline__ float qnan<float>() { return __int_as_float(0x7fc00000); }
+template <> __device__ __forceinline__ double qnan<double>() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+template <typename T> __device__ __forceinline__ bool finite(T v) { return isfinite(v); }
+
+// Unsigned division by a runtime constant d: floor(e / d) == __umulhi(e, M) with
+// M = ceil(2^32 / d), exact whenever e * d < 2^32 (M = (2^32 + r)/d with r < d, so the
+// rounding term e*r/(d*2^32) stays below 1/d).  Callers keep e * d < 2^32.
+struct FastDiv {
+  uint32_t d, M;
+  __host__ __device__ FastDiv() : d(1), M(0) {}
+  __host__ explicit FastDiv(uint32_t dd) : d(dd), M((uint32_t)((((uint64_t)1 << 32) + dd - 1) / dd)) {}
+  __device__ __forceinline__ uint32_t div(uint32_t e) const { return d == 1 ? e : __umulhi(e, M); }
+};
+
+// Streaming (read-once) global loads / stores: do not pollute L1, evict early from L2.
+__device__ __forceinline__ float ld_stream(const float *p) { return __ldcs(p); }
+__device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float *p, float v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double *p, double v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(int32_t *p, int32_t v) { __stcs(p, v); }
+
+// Eq. nr_formula on one interval, with one reciprocal of h:
+//   A = (x1 - q)/h, B = (q - x0)/h, out = A y0 + B y1 + ((A^3-A) y2_0 + (B^3-B) y2_1) h^2/6.
+template <typename T>
+__device__ __forceinline__ T nr_interp(T q, T x0, T x1, T y0, T y1, T z0, T z1) {
+  const T h = x1 - x0;
+  const T ih = T(1) / h;  // IEEE division (no fast-math)
+  const T A = (x1 - q) * ih;
+  const T B = (q - x0) * ih;
+  const T C = A * (A * A - T(1));
+  const T D = B * (B * B - T(1));
+  return A * y0 + B * y1 + (C * z0 + D * z1) * (h * h * (T(1) / T(6)));
+}
+
+}  // namespace fs

@@ -1,0 +1,353 @@
+// spline_abi.cu -- the C ABI of include/spline.h: argument checks, kernel dispatch, launches.
+//
+// Dispatch (build, by n and dtype):
+//   n <= 128                      K1 k1_thomas_batched   one thread per curve
+//   n <= 256*RMAX (4096 f64,      K2 k_tile<FULL>        one CTA per curve: 256 leaves x R rows,
+//                  8192 f32)                              merge tree in shared memory
+//   longer                        K3 k_tile<REDUCE> -> K4 k4_top -> K5 k_tile<FINISH>   (tiled SPIKE)
+// Dispatch (eval, by the curve's staged footprint 3 n s):
+//   <= 96 KiB                     k_eval_staged<MODE>    curves staged in shared memory
+//   larger                        k_eval_global          interpolation guess + gallop in HBM
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+
+#include "../../include/spline.h"
+#include "build_thomas.cuh"
+#include "build_tile.cuh"
+#include "common.cuh"
+#include "eval.cuh"
+
+using namespace fs;
+
+namespace {
+
+constexpr int kK1MaxN = 128;
+constexpr size_t kStageMax = 96 * 1024;
+
+template <typename T> constexpr int rmax() { return sizeof(T) == 8 ? 16 : 32; }
+
+inline int cuda_rc(cudaError_t e) {
+  if (e == cudaSuccess) return SPLINE_OK;
+  if (e == cudaErrorMemoryAllocation) return SPLINE_ENOMEM;
+  return SPLINE_ECUDA;
+}
+
+template <typename K> int set_smem(K kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return SPLINE_OK;
+  return cuda_rc(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+inline int launch_rc() { return cuda_rc(cudaGetLastError()); }
+
+// ------------------------------------------------------------------------ build
+
+template <typename T, int R>
+int launch_tile_full(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+                     cudaStream_t st) {
+  auto kern = k_tile<T, R, TILE_FULL>;
+  const size_t sm = tile_smem_bytes<T, R>();
+  if (int rc = set_smem(kern, sm)) return rc;
+  kern<<<dim3(1, (unsigned)batch), kTileThreads, sm, st>>>(x, y, n, 0, n, bc, yp1, ypn, y2, nullptr, nullptr,
+                                                           nullptr);
+  return launch_rc();
+}
+
+template <typename T>
+int build_mid(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+              cudaStream_t st) {
+  if (n <= 256 * 1) return launch_tile_full<T, 1>(x, y, n, batch, bc, yp1, ypn, y2, st);
+  if (n <= 256 * 2) return launch_tile_full<T, 2>(x, y, n, batch, bc, yp1, ypn, y2, st);
+  if (n <= 256 * 4) return launch_tile_full<T, 4>(x, y, n, batch, bc, yp1, ypn, y2, st);
+  if (n <= 256 * 8) return launch_tile_full<T, 8>(x, y, n, batch, bc, yp1, ypn, y2, st);
+  if (n <= 256 * 16) return launch_tile_full<T, 16>(x, y, n, batch, bc, yp1, ypn, y2, st);
+  if constexpr (rmax<T>() >= 32) {
+    if (n <= 256 * 32) return launch_tile_full<T, 32>(x, y, n, batch, bc, yp1, ypn, y2, st);
+  }
+  return SPLINE_EINVAL;
+}
+
+struct SpikeWs {
+  void *tile_rec, *tile_ext, *foldq, *badflag, *rank_ext, *rank_foldq;
+};
+constexpr int kMaxRanks = 1024;
+
+template <typename T> size_t spike_ws_layout(int64_t ntiles, int64_t batch, SpikeWs *ws, char *base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    void *p = base ? base + off : nullptr;
+    off += (bytes + 255) & ~(size_t)255;
+    return p;
+  };
+  SpikeWs w;
+  w.tile_rec = take(sizeof(T) * 6 * ntiles * batch);
+  w.tile_ext = take(sizeof(T) * 2 * ntiles * batch);
+  w.foldq = take(sizeof(T) * 3 * ntiles * batch);
+  w.badflag = take(sizeof(int) * batch);
+  w.rank_ext = take(sizeof(T) * 2 * kMaxRanks);
+  w.rank_foldq = take(sizeof(T) * 3 * kMaxRanks);
+  if (ws) *ws = w;
+  return off;
+}
+
+template <typename T> int launch_top(const T *recs, int ntiles, int64_t batch, int up_only, const T *root_ext,
+                                     T *tile_ext, T *root_out, T *foldq, cudaStream_t st) {
+  auto kern = k4_top<T>;
+  const size_t sm = top_smem_bytes<T>();
+  if (int rc = set_smem(kern, sm)) return rc;
+  kern<<<(unsigned)batch, kTopThreads, sm, st>>>(recs, ntiles, up_only, root_ext, tile_ext, root_out, foldq);
+  return launch_rc();
+}
+
+template <typename T, int MODE>
+int launch_tile_part(const T *x, const T *y, int64_t n, int64_t rb, int64_t re, int64_t batch, int bc, const T *yp1,
+                     const T *ypn, T *y2, const SpikeWs &w, cudaStream_t st) {
+  constexpr int R = rmax<T>();
+  const int64_t ntiles = (re - rb + 256 * R - 1) / (256 * R);
+  auto kern = k_tile<T, R, MODE>;
+  const size_t sm = tile_smem_bytes<T, R>();
+  if (int rc = set_smem(kern, sm)) return rc;
+  kern<<<dim3((unsigned)ntiles, (unsigned)batch), kTileThreads, sm, st>>>(
+      x, y, n, rb, re, bc, yp1, ypn, y2, (T *)w.tile_rec, (const T *)w.tile_ext, (int *)w.badflag);
+  return launch_rc();
+}
+
+template <typename T>
+int build_long(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+               cudaStream_t st) {
+  constexpr int R = rmax<T>();
+  const int64_t ntiles = (n + 256 * R - 1) / (256 * R);
+  const size_t bytes = spike_ws_layout<T>(ntiles, batch, nullptr, nullptr);
+  void *base = nullptr;
+  if (int rc = cuda_rc(cudaMallocAsync(&base, bytes, st))) return rc;
+  SpikeWs w;
+  spike_ws_layout<T>(ntiles, batch, &w, (char *)base);
+  int rc = cuda_rc(cudaMemsetAsync(w.badflag, 0, sizeof(int) * batch, st));
+  if (!rc) rc = launch_tile_part<T, TILE_REDUCE>(x, y, n, 0, n, batch, bc, yp1, ypn, y2, w, st);
+  if (!rc) rc = launch_top<T>((const T *)w.tile_rec, (int)ntiles, batch, 0, nullptr, (T *)w.tile_ext, nullptr,
+                              (T *)w.foldq, st);
+  if (!rc) rc = launch_tile_part<T, TILE_FINISH>(x, y, n, 0, n, batch, bc, yp1, ypn, y2, w, st);
+  cudaFreeAsync(base, st);
+  return rc;
+}
+
+template <typename T>
+int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+            cudaStream_t st) {
+  if (n <= kK1MaxN) {
+    const int S = (int)(n | 1);
+    int cpb = 64;
+    if ((size_t)2 * cpb * S * sizeof(T) > 64 * 1024) cpb = 32;
+    const size_t sm = (size_t)2 * cpb * S * sizeof(T);
+    auto kern = k1_thomas_batched<T>;
+    if (int rc = set_smem(kern, sm)) return rc;
+    const int64_t grid = (batch + cpb - 1) / cpb;
+    kern<<<(unsigned)grid, cpb, sm, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, S, FastDiv((uint32_t)n));
+    return launch_rc();
+  }
+  if (n <= 256 * rmax<T>()) return build_mid<T>(x, y, n, batch, bc, yp1, ypn, y2, st);
+  return build_long<T>(x, y, n, batch, bc, yp1, ypn, y2, st);
+}
+
+// ------------------------------------------------------------------------- eval
+
+template <typename T, int MODE>
+int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
+                  int32_t *idx, cudaStream_t st) {
+  const size_t per_curve = 3 * (size_t)n * sizeof(T);
+  int cpb = 1, nchunks = 1, qchunk = (int)m;
+  int64_t grid;
+  if (m >= 2048 || batch == 1) {
+    // One curve per CTA; split a curve's queries if there are too few curves to fill the GPU.
+    const int64_t want = (4 * 148 + batch - 1) / batch;
+    nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (m + 1023) / 1024));
+    qchunk = (int)((m + nchunks - 1) / nchunks);
+    grid = batch * nchunks;
+  } else {
+    int64_t c = std::max<int64_t>(1, 2048 / m);
+    c = std::min<int64_t>(c, (int64_t)(kStageMax / per_curve));
+    c = std::min<int64_t>(c, batch);
+    while (c > 1 && (uint64_t)c * m * m >= (1ull << 32)) c >>= 1;  // FastDiv range
+    cpb = (int)std::max<int64_t>(1, c);
+    grid = (batch + cpb - 1) / cpb;
+    if (cpb == 1) { nchunks = 1; qchunk = (int)m; grid = batch; }
+  }
+  const size_t sm = per_curve * cpb;
+  auto kern = k_eval_staged<T, MODE>;
+  if (int rc = set_smem(kern, sm)) return rc;
+  kern<<<(unsigned)grid, kEvalThreads, sm, st>>>(x, y, y2, n, batch, q, (int)m, out, idx, cpb, nchunks, qchunk,
+                                                 FastDiv((uint32_t)n), FastDiv((uint32_t)m));
+  return launch_rc();
+}
+
+template <typename T>
+int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const T *q, int64_t m, T *out,
+           int32_t *idx, int flags, cudaStream_t st) {
+  const size_t per_curve = 3 * (size_t)n * sizeof(T);
+  if (per_curve <= kStageMax) {
+    if (flags & SPLINE_Q_SORTED)
+      return launch_staged<T, MODE_SORTED>(x, y, y2, (int)n, batch, q, m, out, idx, st);
+    if (flags & SPLINE_X_UNIFORM)
+      return launch_staged<T, MODE_UNIFORM>(x, y, y2, (int)n, batch, q, m, out, idx, st);
+    return launch_staged<T, MODE_BSEARCH>(x, y, y2, (int)n, batch, q, m, out, idx, st);
+  }
+  const int64_t total = batch * m;
+  const int64_t grid = std::min<int64_t>((total + 255) / 256, 148 * 64);
+  k_eval_global<T><<<(unsigned)grid, 256, 0, st>>>(x, y, y2, (int)n, batch, q, m, out, idx);
+  return launch_rc();
+}
+
+int check_build(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1, const void *ypn,
+                const void *y2, int dtype) {
+  if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
+  if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
+  if (bc < 0 || bc > 3) return SPLINE_EINVAL;
+  if (batch == 0) return SPLINE_OK;
+  if (!x || !y || !y2) return SPLINE_EINVAL;
+  if ((bc & 1) && !yp1) return SPLINE_EINVAL;
+  if ((bc & 2) && !ypn) return SPLINE_EINVAL;
+  return SPLINE_OK;
+}
+
+}  // namespace
+
+namespace {
+template <typename T>
+int spike_reduce_t(const T *x, const T *y, int64_t n, int64_t rb, int64_t re, int bc, const T *yp1, const T *ypn,
+                   T *record, void *workspace, cudaStream_t st) {
+  constexpr int R = rmax<T>();
+  const int64_t ntiles = (re - rb + 256 * R - 1) / (256 * R);
+  SpikeWs w;
+  spike_ws_layout<T>(ntiles, 1, &w, (char *)workspace);
+  int rc = cuda_rc(cudaMemsetAsync(w.badflag, 0, sizeof(int), st));
+  if (!rc) rc = launch_tile_part<T, TILE_REDUCE>(x, y, n, rb, re, 1, bc, yp1, ypn, nullptr, w, st);
+  if (!rc) rc = launch_top<T>((const T *)w.tile_rec, (int)ntiles, 1, 1, nullptr, nullptr, record, (T *)w.foldq, st);
+  return rc;
+}
+
+template <typename T>
+int spike_finish_t(const T *x, const T *y, int64_t n, int64_t rb, int64_t re, int bc, const T *yp1, const T *ypn,
+                   const T *all_records, int nranks, int rank, T *y2_shard, void *workspace, cudaStream_t st) {
+  constexpr int R = rmax<T>();
+  const int64_t ntiles = (re - rb + 256 * R - 1) / (256 * R);
+  SpikeWs w;
+  spike_ws_layout<T>(ntiles, 1, &w, (char *)workspace);
+  // Rank level: every rank solves the G-record reduced system redundantly (the outer
+  // (L, R) of the whole curve are irrelevant: a_0 = 0 and c_{n-1} = 0).
+  int rc = launch_top<T>(all_records, nranks, 1, 0, nullptr, (T *)w.rank_ext, nullptr, (T *)w.rank_foldq, st);
+  if (!rc) rc = launch_top<T>((const T *)w.tile_rec, (int)ntiles, 1, 0, (const T *)w.rank_ext + 2 * rank,
+                              (T *)w.tile_ext, nullptr, (T *)w.foldq, st);
+  if (!rc) rc = launch_tile_part<T, TILE_FINISH>(x, y, n, rb, re, 1, bc, yp1, ypn, y2_shard, w, st);
+  return rc;
+}
+
+int check_spike(const void *x, const void *y, int64_t n, int64_t rb, int64_t re, int bc, const void *yp1,
+                const void *ypn, const void *ws, int dtype) {
+  if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
+  if (n < 3 || n >= (int64_t(1) << 31) || rb < 0 || re > n || re <= rb || bc < 0 || bc > 3) return SPLINE_EINVAL;
+  if (!x || !y || !ws) return SPLINE_EINVAL;
+  if (((bc & 1) && !yp1) || ((bc & 2) && !ypn)) return SPLINE_EINVAL;
+  return SPLINE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int spline_build(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1, const void *ypn,
+                 void *y2, int dtype, spline_stream_t stream) {
+  if (int rc = check_build(x, y, n, batch, bc, yp1, ypn, y2, dtype)) return rc;
+  if (batch == 0) return SPLINE_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SPLINE_F32)
+    return build_t<float>((const float *)x, (const float *)y, n, batch, bc, (const float *)yp1, (const float *)ypn,
+                          (float *)y2, st);
+  return build_t<double>((const double *)x, (const double *)y, n, batch, bc, (const double *)yp1,
+                         (const double *)ypn, (double *)y2, st);
+}
+
+int spline_eval(const void *x, const void *y, const void *y2, int64_t n, int64_t batch, const void *q, int64_t m,
+                void *out, int32_t *idx, int flags, int dtype, spline_stream_t stream) {
+  if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
+  if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || m < 0 || m >= (int64_t(1) << 31)) return SPLINE_EINVAL;
+  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM)) return SPLINE_EINVAL;
+  if (batch == 0 || m == 0) return SPLINE_OK;
+  if (!x || !y || !y2 || !q || !out) return SPLINE_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SPLINE_F32)
+    return eval_t<float>((const float *)x, (const float *)y, (const float *)y2, n, batch, (const float *)q, m,
+                         (float *)out, idx, flags, st);
+  return eval_t<double>((const double *)x, (const double *)y, (const double *)y2, n, batch, (const double *)q, m,
+                        (double *)out, idx, flags, st);
+}
+
+int spline_build_f32(const float *x, const float *y, int64_t n, int64_t batch, int bc, const float *yp1,
+                     const float *ypn, float *y2, spline_stream_t stream) {
+  return spline_build(x, y, n, batch, bc, yp1, ypn, y2, SPLINE_F32, stream);
+}
+int spline_build_f64(const double *x, const double *y, int64_t n, int64_t batch, int bc, const double *yp1,
+                     const double *ypn, double *y2, spline_stream_t stream) {
+  return spline_build(x, y, n, batch, bc, yp1, ypn, y2, SPLINE_F64, stream);
+}
+int spline_eval_f32(const float *x, const float *y, const float *y2, int64_t n, int64_t batch, const float *q,
+                    int64_t m, float *out, int32_t *idx, int flags, spline_stream_t stream) {
+  return spline_eval(x, y, y2, n, batch, q, m, out, idx, flags, SPLINE_F32, stream);
+}
+int spline_eval_f64(const double *x, const double *y, const double *y2, int64_t n, int64_t batch, const double *q,
+                    int64_t m, double *out, int32_t *idx, int flags, spline_stream_t stream) {
+  return spline_eval(x, y, y2, n, batch, q, m, out, idx, flags, SPLINE_F64, stream);
+}
+
+int spline_status(spline_stream_t stream, unsigned int *bits_out) {
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned int bits = 0;
+  const unsigned int zero = 0;
+  cudaError_t e = cudaMemcpyFromSymbolAsync(&bits, fs::g_status, sizeof(bits), 0, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(fs::g_status, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (bits_out) *bits_out = bits;
+  return cuda_rc(e);
+}
+
+size_t spline_spike_workspace_size(int64_t n, int64_t row_begin, int64_t row_end, int dtype) {
+  (void)n;
+  const int R = dtype == SPLINE_F64 ? rmax<double>() : rmax<float>();
+  const int64_t ntiles = (row_end - row_begin + 256 * R - 1) / (256 * R);
+  return dtype == SPLINE_F64 ? spike_ws_layout<double>(ntiles, 1, nullptr, nullptr)
+                             : spike_ws_layout<float>(ntiles, 1, nullptr, nullptr);
+}
+
+
+int spline_spike_reduce(const void *x, const void *y, int64_t n, int64_t row_begin, int64_t row_end, int bc,
+                        const void *yp1, const void *ypn, void *record, void *workspace, int dtype,
+                        spline_stream_t stream) {
+  if (int rc = check_spike(x, y, n, row_begin, row_end, bc, yp1, ypn, workspace, dtype)) return rc;
+  if (!record) return SPLINE_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SPLINE_F32)
+    return spike_reduce_t<float>((const float *)x, (const float *)y, n, row_begin, row_end, bc, (const float *)yp1,
+                                 (const float *)ypn, (float *)record, workspace, st);
+  return spike_reduce_t<double>((const double *)x, (const double *)y, n, row_begin, row_end, bc,
+                                (const double *)yp1, (const double *)ypn, (double *)record, workspace, st);
+}
+
+int spline_spike_finish(const void *x, const void *y, int64_t n, int64_t row_begin, int64_t row_end, int bc,
+                        const void *yp1, const void *ypn, const void *all_records, int nranks, int rank,
+                        void *y2_shard, void *workspace, int dtype, spline_stream_t stream) {
+  if (int rc = check_spike(x, y, n, row_begin, row_end, bc, yp1, ypn, workspace, dtype)) return rc;
+  if (!all_records || !y2_shard || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+    return SPLINE_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SPLINE_F32)
+    return spike_finish_t<float>((const float *)x, (const float *)y, n, row_begin, row_end, bc, (const float *)yp1,
+                                 (const float *)ypn, (const float *)all_records, nranks, rank, (float *)y2_shard,
+                                 workspace, st);
+  return spike_finish_t<double>((const double *)x, (const double *)y, n, row_begin, row_end, bc,
+                                (const double *)yp1, (const double *)ypn, (const double *)all_records, nranks, rank,
+                                (double *)y2_shard, workspace, st);
+}
+
+const char *spline_version(void) { return "fastspline-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

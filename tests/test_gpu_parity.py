@@ -1,0 +1,162 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the CPU oracle, element by element.
+
+Sizes span several tiles / CTAs and a ragged tail; full BASELINE sizes are covered in
+test_gpu_fullsize.py.  Every case is seeded (paper_2001_09253_b200.workloads).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import parity
+from paper_2001_09253_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2001_09253_b200 import api as a
+    a.status()
+    return a
+
+
+# ------------------------------------------------------------ the five configs, scaled
+
+@pytest.mark.parametrize("kw", [dict(), dict(batch=3)])
+def test_cfg1(api, kw):
+    parity.check_case(api, workloads.generate(1, **kw))
+
+
+@pytest.mark.parametrize("kw", [dict(batch=4096), dict(batch=1001, m=255), dict(batch=77, n=63, m=31)])
+def test_cfg2_k1_thomas_f32(api, kw):
+    parity.check_case(api, workloads.generate(2, **kw))
+
+
+@pytest.mark.parametrize("kw", [dict(batch=20000), dict(batch=4099, m=33), dict(batch=50, n=3, m=7)])
+def test_cfg3_uniform_f32(api, kw):
+    parity.check_case(api, workloads.generate(3, **kw))
+    parity.check_case(api, workloads.generate(3, **kw), flags=0)  # same answer without the hint
+
+
+@pytest.mark.parametrize("kw", [dict(batch=6, n=4096, m=16384), dict(batch=5, n=1000, m=3001),
+                                dict(batch=3, n=129, m=2048), dict(batch=2, n=3000, m=100)])
+def test_cfg4_tile_sorted_f64(api, kw):
+    parity.check_case(api, workloads.generate(4, **kw))
+    parity.check_case(api, workloads.generate(4, **kw), flags=0)
+
+
+@pytest.mark.parametrize("kw", [dict(n=(1 << 17), m=1 << 18), dict(n=(1 << 17) + 123, m=10007),
+                                dict(n=600 * 4096 + 17, m=1 << 16)])
+def test_cfg5_spike_f64(api, kw):
+    parity.check_case(api, workloads.generate(5, **kw), nthreads=8)
+
+
+# ------------------------------------------------------------ every kernel x dtype
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [3, 5, 64, 128, 129, 700, 4096, 4097, 9000, 70000])
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
+def test_build_all_paths(api, dt, n, bc):
+    rng = np.random.default_rng(n * 10 + bc)
+    B = 3
+    x = np.cumsum(rng.exponential(1.0, (B, n)) + 0.05, axis=1).astype(dt)
+    y = np.cumsum(rng.normal(size=(B, n)), axis=1).astype(dt)
+    yp1 = rng.normal(size=B).astype(dt)
+    ypn = rng.normal(size=B).astype(dt)
+    wl = workloads.Workload(workloads.CONFIGS[2], x, y, x[:, :4].copy(), yp1, ypn, bc, 0)
+    wl.spec = workloads.ConfigSpec(0, "t", B, n, 4, "f32" if dt == np.float32 else "f64", bc, 0, 0)
+    parity.check_case(api, wl, y2_only=True)
+    if not bc & 1 or not bc & 2:
+        _, _, y2 = parity.gpu_build(api, wl)
+        y2 = y2.cpu().numpy()
+        if not bc & 1:
+            assert np.all(y2[:, 0] == 0)
+        if not bc & 2:
+            assert np.all(y2[:, -1] == 0)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("n,m,flags", [(16, 1000, 0), (64, 256, 1), (8, 32, 2), (4096, 20000, 1),
+                                       (4096, 3000, 0), (5000, 4000, 0), (200000, 5000, 0), (200000, 5000, 1)])
+def test_eval_all_paths_with_ties(api, dt, n, m, flags):
+    """Queries on exact knots (interior ties, x_0, x_{n-1}), out of range and NaN; bit-exact idx."""
+    rng = np.random.default_rng(n + m)
+    B = 2
+    x = np.cumsum(rng.exponential(1.0, (B, n)) + 0.01, axis=1).astype(dt)
+    y = rng.normal(size=(B, n)).astype(dt)
+    y2 = rng.normal(size=(B, n)).astype(dt)
+    q = rng.uniform(x[:, :1], x[:, -1:], (B, m)).astype(dt)
+    q[:, : m // 10] = x[:, rng.integers(0, n, m // 10)][0]          # exact knot hits
+    q[:, 0], q[:, 1] = x[:, 0], x[:, -1]
+    q[:, 2] = x[:, 0] - 1
+    q[:, 3] = x[:, -1] + 1
+    q[:, 4] = np.nan
+    q[1] = x[1, :1] + (q[0] - x[0, :1])  # different curve, shifted queries
+    if flags & 1:
+        q = np.sort(q, axis=1)  # NaN sorts to the end
+    out_ref, idx_ref, nbad = oracle.evaluate(x, y, y2, q)
+    api.status()
+    out, idx = api.evaluate(parity.to_dev(x), parity.to_dev(y), parity.to_dev(y2), parity.to_dev(q), flags)
+    bits = api.status()
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_ref)
+    e = parity.out_rel_err(out.cpu().numpy(), out_ref, y)
+    assert np.all(e <= parity.tol_for(dt))
+    assert (bits & api.STATUS_Q_OUT_OF_RANGE) == (api.STATUS_Q_OUT_OF_RANGE if nbad else 0)
+
+
+def test_wrong_hints_do_not_change_results(api):
+    wl = workloads.generate(2, batch=500)  # unsorted, non-uniform
+    x, y, y2 = parity.gpu_build(api, wl)
+    q = parity.to_dev(wl.q)
+    base = api.evaluate(x, y, y2, q, 0)
+    for flags in (1, 2, 3):
+        o, i = api.evaluate(x, y, y2, q, flags)
+        assert torch.equal(i, base[1])
+        assert torch.allclose(o, base[0], rtol=0, atol=0, equal_nan=True)
+
+
+@pytest.mark.parametrize("n", [6, 64, 1000, 20000])
+def test_bad_knots_status_and_nan(api, n):
+    rng = np.random.default_rng(n)
+    x = np.cumsum(rng.uniform(0.5, 1.5, (4, n)), axis=1)
+    y = rng.normal(size=(4, n))
+    x[1, n // 2] = x[1, n // 2 - 1]  # duplicate knot
+    y[2, 1] = np.inf
+    api.status()
+    y2 = api.build(parity.to_dev(x), parity.to_dev(y), 0).cpu().numpy()
+    bits = api.status()
+    assert bits & api.STATUS_BAD_KNOTS
+    assert np.all(np.isnan(y2[1])) and np.all(np.isnan(y2[2]))
+    ref, _ = oracle.build_y2(x[[0, 3]], y[[0, 3]], 0)
+    assert np.all(parity.y2_rel_err(y2[[0, 3]], ref) <= 1e-12)
+
+
+def test_idx_optional_and_empty(api):
+    wl = workloads.generate(2, batch=64)
+    x, y, y2 = parity.gpu_build(api, wl)
+    q = parity.to_dev(wl.q)
+    o1, i1 = api.evaluate(x, y, y2, q, 0)
+    o2, i2 = api.evaluate(x, y, y2, q, 0, want_idx=False)
+    assert i2 is None and torch.equal(o1, o2)
+    e = torch.empty((64, 0), dtype=x.dtype, device=x.device)
+    o3, _ = api.evaluate(x, y, y2, e, 0)
+    assert o3.shape == (64, 0)
+    z = torch.empty((0, 64), dtype=x.dtype, device=x.device)
+    assert api.build(z, z, 0).shape == (0, 64)
+
+
+def test_linear_and_cubic_closed_forms_gpu(api):
+    """Closed forms through the GPU path: linear data -> y2 == 0; clamped cubic reproduced."""
+    x = np.linspace(-1.0, 2.0, 300)
+    y = 3 * x - 2
+    y2 = api.build(parity.to_dev(x), parity.to_dev(y), 0).cpu().numpy()
+    assert np.max(np.abs(y2)) <= 1e-12 * 6 * 3 / (3 / 299)   # reading c2's fallback scale
+    f = lambda t: 1 - t + 0.5 * t ** 2 + 0.25 * t ** 3
+    fp = lambda t: -1 + t + 0.75 * t ** 2
+    for n in (50, 3000, 100000):
+        xx = np.linspace(-2.0, 2.0, n)
+        y2 = api.build(parity.to_dev(xx), parity.to_dev(f(xx)), 3, fp(-2.0), fp(2.0)).cpu().numpy()
+        assert np.max(np.abs(y2 - (1 + 1.5 * xx))) <= 1e-9 * 4
