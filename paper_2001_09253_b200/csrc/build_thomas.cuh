@@ -17,13 +17,16 @@
 
 namespace fs {
 
+constexpr int kK1Threads = 256;
+
+// blockDim = 256 threads stage the tile (all loads in flight at once); the first CPB
+// threads (one per curve) run the sweeps.
 template <typename T>
-__global__ void __launch_bounds__(128) k1_thomas_batched(const T *__restrict__ x, const T *__restrict__ y, int n,
-                                                         int64_t batch, int bc, const T *__restrict__ yp1,
-                                                         const T *__restrict__ ypn, T *__restrict__ y2, int S,
-                                                         FastDiv divn) {
+__global__ void __launch_bounds__(kK1Threads, 4) k1_thomas_batched(const T *__restrict__ x, const T *__restrict__ y,
+                                                                int n, int64_t batch, int bc,
+                                                                const T *__restrict__ yp1, const T *__restrict__ ypn,
+                                                                T *__restrict__ y2, int S, int CPB, FastDiv divn) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int CPB = blockDim.x;
   T *X = reinterpret_cast<T *>(smem_raw);
   T *Y = X + (size_t)CPB * S;
 
@@ -33,12 +36,29 @@ __global__ void __launch_bounds__(128) k1_thomas_batched(const T *__restrict__ x
   const T *xb = x + c0 * n;
   const T *yb = y + c0 * n;
 
-  // Stage: flat coalesced loads, scattered into the odd-stride tiles.
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int c = (int)divn.div((uint32_t)e);
-    const int j = e - c * n;
-    X[c * S + j] = ld_stream(xb + e);
-    Y[c * S + j] = ld_stream(yb + e);
+  // Stage: flat coalesced loads (UL per array per thread in flight), scattered into the
+  // odd-stride tiles.
+  constexpr int UL = sizeof(T) == 4 ? 16 : 8;
+  for (int base = threadIdx.x; base < tot; base += UL * kK1Threads) {
+    T vx[UL], vy[UL];
+#pragma unroll
+    for (int u = 0; u < UL; ++u) {
+      const int e = base + u * kK1Threads;
+      if (e < tot) {
+        vx[u] = ld_stream(xb + e);
+        vy[u] = ld_stream(yb + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UL; ++u) {
+      const int e = base + u * kK1Threads;
+      if (e < tot) {
+        const int c = (int)divn.div((uint32_t)e);
+        const int j = e - c * n;
+        X[c * S + j] = vx[u];
+        Y[c * S + j] = vy[u];
+      }
+    }
   }
   __syncthreads();
 
@@ -108,7 +128,7 @@ __global__ void __launch_bounds__(128) k1_thomas_batched(const T *__restrict__ x
   __syncthreads();
 
   T *y2b = y2 + c0 * n;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+  for (int e = threadIdx.x; e < tot; e += kK1Threads) {
     const int c = (int)divn.div((uint32_t)e);
     const int j = e - c * n;
     y2b[e] = Y[c * S + j];

@@ -60,3 +60,80 @@ __device__ __forceinline__ T nr_interp(T q, T x0, T x1, T y0, T y1, T z0, T z1) 
 }
 
 }  // namespace fs
+
+namespace fs {
+
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on a shared-memory mbarrier.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+// Global -> shared bulk copy of `bytes` (multiple of 16, both addresses 16-byte aligned).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---- 16-byte vector types per element type
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using V = float4; using I = int4; static constexpr int N = 4; };
+template <> struct Vec16<double> { using V = double2; using I = int2; static constexpr int N = 2; };
+
+template <typename T, int V> struct VecIO {
+  // loads V consecutive elements (16-byte aligned when V > 1)
+  static __device__ __forceinline__ void load(const T *p, T *v) {
+    if constexpr (V == 1) {
+      v[0] = ld_stream(p);
+    } else {
+      using VT = typename Vec16<T>::V;
+      const VT t = __ldcs(reinterpret_cast<const VT *>(p));
+      const T *tt = reinterpret_cast<const T *>(&t);
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = tt[i];
+    }
+  }
+  static __device__ __forceinline__ void store(T *p, const T *v) {
+    if constexpr (V == 1) {
+      st_stream(p, v[0]);
+    } else {
+      using VT = typename Vec16<T>::V;
+      VT t;
+      T *tt = reinterpret_cast<T *>(&t);
+#pragma unroll
+      for (int i = 0; i < V; ++i) tt[i] = v[i];
+      __stcs(reinterpret_cast<VT *>(p), t);
+    }
+  }
+  static __device__ __forceinline__ void store_idx(int32_t *p, const int *j) {
+    if constexpr (V == 1) {
+      st_stream(p, j[0]);
+    } else if constexpr (V == 4) {
+      __stcs(reinterpret_cast<int4 *>(p), make_int4(j[0], j[1], j[2], j[3]));
+    } else {
+      __stcs(reinterpret_cast<int2 *>(p), make_int2(j[0], j[1]));
+    }
+  }
+};
+
+}  // namespace fs

@@ -95,17 +95,26 @@ __device__ __forceinline__ void eval_one(const T *X, const T *Y, const T *Z, int
 }
 
 constexpr int kEvalThreads = 256;
+constexpr int kStageHeader = 16;  // mbarrier (8 B) + pad, ahead of the staged arrays
 
-// Grid: cpb > 1 -> blockIdx.x = group of cpb curves (all m queries each);
+// Grid: cpb > 1  -> blockIdx.x = group of cpb curves (all m queries of each);
 //       cpb == 1 -> blockIdx.x = curve * nchunks + chunk (queries [chunk*qchunk, ..)).
-template <typename T, int MODE>
+// Staging: BULK -> one thread issues three cp.async.bulk copies (x, y, y2 of the CTA's
+// curves, contiguous in HBM) completing on an mbarrier, while every thread already has
+// its first batch of query loads in flight; otherwise coalesced loads + __syncthreads.
+// Queries: each warp owns a contiguous run of the CTA's queries; lane l takes groups of V
+// consecutive queries (one 16-byte vector load / store when V > 1), U groups per batch in
+// flight.  MODE_SORTED carries the warp's bracket from one 32V-query step to the next.
+template <typename T, int MODE, int V, bool BULK>
 __global__ void __launch_bounds__(kEvalThreads) k_eval_staged(const T *__restrict__ x, const T *__restrict__ y,
                                                              const T *__restrict__ y2, int n, int64_t batch,
                                                              const T *__restrict__ q, int m, T *__restrict__ out,
                                                              int32_t *__restrict__ idx, int cpb, int nchunks,
-                                                             int qchunk, FastDiv divn, FastDiv divm) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *X = reinterpret_cast<T *>(smem_raw);
+                                                             int qchunk, FastDiv divm) {
+  constexpr int U = sizeof(T) == 4 ? 4 : 8;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
+  T *X = reinterpret_cast<T *>(smem_raw + kStageHeader);
   T *Y = X + (size_t)cpb * n;
   T *Z = Y + (size_t)cpb * n;
 
@@ -123,98 +132,148 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_staged(const T *__restric
     k0 = c0 * m + (int64_t)ch * qchunk;
     k1 = min64(c0 * m + m, k0 + qchunk);
   }
-  {
-    const int tot = nc * n;
+  const int tot = nc * n;
+  if (BULK) {
+    if (threadIdx.x == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)(tot * sizeof(T));
+      mbar_expect_tx(bar, 3 * bytes);
+      bulk_g2s(X, x + c0 * n, bytes, bar);
+      bulk_g2s(Y, y + c0 * n, bytes, bar);
+      bulk_g2s(Z, y2 + c0 * n, bytes, bar);
+    }
+  } else {
     const T *xs = x + c0 * n, *ys = y + c0 * n, *zs = y2 + c0 * n;
     for (int e = threadIdx.x; e < tot; e += blockDim.x) {
       X[e] = xs[e];
       Y[e] = ys[e];
       Z[e] = zs[e];
     }
+    __syncthreads();
   }
-  __syncthreads();
-  const int cnt = (int)(k1 - k0);
+
+  const int ngroups = (int)(k1 - k0) / V;
   const T *qb = q + k0;
   T *ob = out + k0;
   int32_t *ib = idx ? idx + k0 : nullptr;
-  bool oor = false;
-
-  if (MODE == MODE_SORTED) {
-    // Each warp owns a contiguous run of the CTA's queries, 32 at a time.
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int per = ((cnt + nw - 1) / nw + 31) & ~31;
-    const int wb = w * per, we = min(cnt, wb + per);
-    int jcarry = 0;
-    for (int base = wb; base < we; base += 32) {
-      const int k = base + lane;
-      const bool act = k < we;
-      const int cl = (cpb > 1 && act) ? (int)divm.div((uint32_t)k) : 0;
-      int j = -1;
-      T val = T(0);
-      if (act) {
-        const T qq = ld_stream(qb + k);
-        eval_one<T, MODE_SORTED>(X + cl * n, Y + cl * n, Z + cl * n, n, qq, jcarry, val, j);
-        st_stream(ob + k, val);
-        if (ib) st_stream(ib + k, (int32_t)j);
-        oor |= (j < 0);
-      }
-      const int jmax = __reduce_max_sync(0xffffffffu, act ? j : -1);
-      if (jmax >= 0) jcarry = jmax;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int per = (ngroups + nw - 1) / nw;
+  const int wb = w * per, we = min(ngroups, wb + per);
+  bool oor = false, staged = !BULK;
+  int jcarry = 0;
+  for (int gb = wb; gb < we; gb += 32 * U) {
+    T qv[U][V];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int g = gb + u * 32 + lane;
+      if (g < we) VecIO<T, V>::load(qb + (int64_t)g * V, qv[u]);
     }
-  } else {
-    constexpr int U = 4;
-    for (int base = threadIdx.x; base < cnt; base += U * blockDim.x) {
-      T qq[U];
+    if (!staged) {
+      mbar_wait(bar, 0);
+      staged = true;
+    }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = base + u * blockDim.x;
-        qq[u] = (k < cnt) ? ld_stream(qb + k) : T(0);
-      }
+    for (int u = 0; u < U; ++u) {
+      const int g = gb + u * 32 + lane;
+      int jl = -1;
+      if (g < we) {
+        T val[V];
+        int jj[V];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = base + u * blockDim.x;
-        if (k < cnt) {
+        for (int i = 0; i < V; ++i) {
+          const int k = g * V + i;
           const int cl = (cpb > 1) ? (int)divm.div((uint32_t)k) : 0;
-          int jc = 0, j;
-          T val;
-          eval_one<T, MODE>(X + cl * n, Y + cl * n, Z + cl * n, n, qq[u], jc, val, j);
-          st_stream(ob + k, val);
-          if (ib) st_stream(ib + k, (int32_t)j);
-          oor |= (j < 0);
+          eval_one<T, MODE>(X + cl * n, Y + cl * n, Z + cl * n, n, qv[u][i], jcarry, val[i], jj[i]);
+          oor |= (jj[i] < 0);
+          if (MODE == MODE_SORTED && jj[i] >= 0) jcarry = jj[i];
+          jl = max(jl, jj[i]);
         }
+        VecIO<T, V>::store(ob + (int64_t)g * V, val);
+        if (ib) VecIO<T, V>::store_idx(ib + (int64_t)g * V, jj);
+      }
+      if (MODE == MODE_SORTED) {
+        const int jmax = __reduce_max_sync(0xffffffffu, jl);
+        if (jmax >= 0) jcarry = jmax;
       }
     }
   }
+  if (!staged) mbar_wait(bar, 0);  // never leave a bulk copy in flight past the CTA's exit
   if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
 }
 
-// Long curves: one query per thread-iteration, everything gathered from global memory.
+// Long curves (not stageable): locate in HBM.  Each thread carries U independent queries
+// through the three dependent round trips (q -> x pair at the interpolation guess -> y, y2
+// pairs) so that U x (threads per SM) gathers are in flight.  The guess
+// (q - x_0)(n-1)/(x_{n-1} - x_0) is exact up to +-1 interval on near-uniform grids; any
+// other outcome falls back to galloping + bisection (correct for every grid).
 template <typename T>
 __global__ void __launch_bounds__(256) k_eval_global(const T *__restrict__ x, const T *__restrict__ y,
                                                      const T *__restrict__ y2, int n, int64_t batch,
                                                      const T *__restrict__ q, int64_t m, T *__restrict__ out,
                                                      int32_t *__restrict__ idx) {
+  constexpr int U = 4;
   const int64_t total = batch * m;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   bool oor = false;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = (batch == 1) ? 0 : k / m;
-    const T *X = x + c * n;
-    const T qq = ld_stream(q + k);
-    const T x0 = __ldg(X), xn = __ldg(X + n - 1);
-    int j = -1;
-    T val = qnan<T>();
-    if (qq >= x0 && qq <= xn) {
-      int g = (int)((qq - x0) * (T)(n - 1) / (xn - x0));
-      g = max(0, min(g, n - 2));
-      j = locate_from(X, n, g, qq);
-      const T *Y = y + c * n, *Z = y2 + c * n;
-      val = nr_interp(qq, __ldg(X + j), __ldg(X + j + 1), __ldg(Y + j), __ldg(Y + j + 1), __ldg(Z + j),
-                      __ldg(Z + j + 1));
-    } else {
-      oor = true;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += U * stride) {
+    T qq[U], xa[U], xb[U];
+    int g[U];
+    int64_t off[U];
+    bool act[U], in[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = base + u * stride;
+      act[u] = k < total;
+      qq[u] = act[u] ? ld_stream(q + k) : T(0);
+      off[u] = act[u] ? ((batch == 1) ? 0 : (k / m) * n) : 0;
     }
-    st_stream(out + k, val);
-    if (idx) st_stream(idx + k, (int32_t)j);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const T *X = x + off[u];
+      const T x0 = __ldg(X), xn = __ldg(X + n - 1);
+      in[u] = act[u] && (qq[u] >= x0 && qq[u] <= xn);
+      int gg = in[u] ? (int)((qq[u] - x0) * (T)(n - 1) / (xn - x0)) : 0;
+      g[u] = max(0, min(gg, n - 2));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      xa[u] = __ldg(x + off[u] + g[u]);
+      xb[u] = __ldg(x + off[u] + g[u] + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (in[u] && !(xa[u] <= qq[u] && (qq[u] < xb[u] || g[u] == n - 2))) {
+        const T *X = x + off[u];
+        g[u] = locate_from(X, n, g[u], qq[u]);
+        xa[u] = __ldg(X + g[u]);
+        xb[u] = __ldg(X + g[u] + 1);
+      }
+    }
+    T ya[U], yb[U], za[U], zb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = in[u] ? g[u] : 0;
+      ya[u] = __ldg(y + off[u] + j);
+      yb[u] = __ldg(y + off[u] + j + 1);
+      za[u] = __ldg(y2 + off[u] + j);
+      zb[u] = __ldg(y2 + off[u] + j + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!act[u]) continue;
+      const int64_t k = base + u * stride;
+      T val = qnan<T>();
+      int j = -1;
+      if (in[u]) {
+        j = g[u];
+        val = nr_interp(qq[u], xa[u], xb[u], ya[u], yb[u], za[u], zb[u]);
+      } else {
+        oor = true;
+      }
+      st_stream(out + k, val);
+      if (idx) st_stream(idx + k, (int32_t)j);
+    }
   }
   if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
 }

@@ -144,7 +144,8 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
     auto kern = k1_thomas_batched<T>;
     if (int rc = set_smem(kern, sm)) return rc;
     const int64_t grid = (batch + cpb - 1) / cpb;
-    kern<<<(unsigned)grid, cpb, sm, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, S, FastDiv((uint32_t)n));
+    kern<<<(unsigned)grid, kK1Threads, sm, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, S, cpb,
+                                                 FastDiv((uint32_t)n));
     return launch_rc();
   }
   if (n <= 256 * rmax<T>()) return build_mid<T>(x, y, n, batch, bc, yp1, ypn, y2, st);
@@ -153,9 +154,23 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
 
 // ------------------------------------------------------------------------- eval
 
+template <typename T, int MODE, int V, bool BULK>
+int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
+                    int32_t *idx, int cpb, int nchunks, int qchunk, int64_t grid, cudaStream_t st) {
+  const size_t sm = kStageHeader + 3 * (size_t)n * sizeof(T) * cpb;
+  auto kern = k_eval_staged<T, MODE, V, BULK>;
+  if (int rc = set_smem(kern, sm)) return rc;
+  kern<<<(unsigned)grid, kEvalThreads, sm, st>>>(x, y, y2, n, batch, q, (int)m, out, idx, cpb, nchunks, qchunk,
+                                                 FastDiv((uint32_t)m));
+  return launch_rc();
+}
+
+inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
 template <typename T, int MODE>
 int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
                   int32_t *idx, cudaStream_t st) {
+  constexpr int VW = 16 / sizeof(T);
   const size_t per_curve = 3 * (size_t)n * sizeof(T);
   int cpb = 1, nchunks = 1, qchunk = (int)m;
   int64_t grid;
@@ -164,6 +179,8 @@ int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, con
     const int64_t want = (4 * 148 + batch - 1) / batch;
     nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (m + 1023) / 1024));
     qchunk = (int)((m + nchunks - 1) / nchunks);
+    qchunk = (qchunk + VW - 1) / VW * VW;
+    nchunks = (int)((m + qchunk - 1) / qchunk);
     grid = batch * nchunks;
   } else {
     int64_t c = std::max<int64_t>(1, 2048 / m);
@@ -172,14 +189,15 @@ int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, con
     while (c > 1 && (uint64_t)c * m * m >= (1ull << 32)) c >>= 1;  // FastDiv range
     cpb = (int)std::max<int64_t>(1, c);
     grid = (batch + cpb - 1) / cpb;
-    if (cpb == 1) { nchunks = 1; qchunk = (int)m; grid = batch; }
   }
-  const size_t sm = per_curve * cpb;
-  auto kern = k_eval_staged<T, MODE>;
-  if (int rc = set_smem(kern, sm)) return rc;
-  kern<<<(unsigned)grid, kEvalThreads, sm, st>>>(x, y, y2, n, batch, q, (int)m, out, idx, cpb, nchunks, qchunk,
-                                                 FastDiv((uint32_t)n), FastDiv((uint32_t)m));
-  return launch_rc();
+  // 16-byte vector query I/O when every curve's query run is whole vectors and aligned.
+  const bool vec = (m % VW == 0) && aligned16(q) && aligned16(out) && (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0));
+  // TMA bulk staging when every curve block is a whole number of 16-byte units and aligned.
+  const bool bulk = ((n * sizeof(T)) % 16 == 0) && aligned16(x) && aligned16(y) && aligned16(y2);
+  if (vec && bulk) return launch_staged_k<T, MODE, VW, true>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, grid, st);
+  if (vec) return launch_staged_k<T, MODE, VW, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, grid, st);
+  if (bulk) return launch_staged_k<T, MODE, 1, true>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, grid, st);
+  return launch_staged_k<T, MODE, 1, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, grid, st);
 }
 
 template <typename T>
@@ -194,7 +212,7 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
     return launch_staged<T, MODE_BSEARCH>(x, y, y2, (int)n, batch, q, m, out, idx, st);
   }
   const int64_t total = batch * m;
-  const int64_t grid = std::min<int64_t>((total + 255) / 256, 148 * 64);
+  const int64_t grid = std::min<int64_t>((total + 1023) / 1024, 148 * 16);
   k_eval_global<T><<<(unsigned)grid, 256, 0, st>>>(x, y, y2, (int)n, batch, q, m, out, idx);
   return launch_rc();
 }
