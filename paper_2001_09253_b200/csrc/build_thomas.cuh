@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(kK1Threads, 4) k1_thomas_batched(const T *__re
                                                                 int n, int64_t batch, int bc,
                                                                 const T *__restrict__ yp1, const T *__restrict__ ypn,
                                                                 T *__restrict__ y2, int S, int CPB, FastDiv divn) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T *X = reinterpret_cast<T *>(smem_raw);
   T *Y = X + (size_t)CPB * S;
 

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
                                                       const T *__restrict__ yp1, const T *__restrict__ ypn,
                                                       T *__restrict__ y2, T *__restrict__ tile_rec,
                                                       const T *__restrict__ tile_ext, int *__restrict__ badflag) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int NT = kTileThreads;
   constexpr int TR = NT * R;
   T *X = reinterpret_cast<T *>(smem_raw);
@@ -287,7 +287,7 @@ template <typename T>
 __global__ void __launch_bounds__(kTopThreads) k4_top(const T *__restrict__ recs, int ntiles, int up_only,
                                                       const T *__restrict__ root_ext, T *__restrict__ tile_ext,
                                                       T *__restrict__ root_out, T *__restrict__ foldq) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   Rec<T> *rec = reinterpret_cast<Rec<T> *>(smem_raw);
   T *mi = reinterpret_cast<T *>(rec + kTopThreads);
   T *ext = reinterpret_cast<T *>(rec);

@@ -46,17 +46,38 @@ __device__ __forceinline__ void st_stream(float *p, float v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double *p, double v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(int32_t *p, int32_t v) { __stcs(p, v); }
 
-// Eq. nr_formula on one interval, with one reciprocal of h:
-//   A = (x1 - q)/h, B = (q - x0)/h, out = A y0 + B y1 + ((A^3-A) y2_0 + (B^3-B) y2_1) h^2/6.
+// Explicitly rounded arithmetic (no contraction freedom): every eval kernel and every
+// hint produces bitwise-identical out for the same (interval, query).
+__device__ __forceinline__ float r_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double r_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float r_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double r_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float r_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double r_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float r_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double r_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float r_rcp(float a) { return __frcp_rn(a); }   // correctly rounded 1/a
+__device__ __forceinline__ double r_rcp(double a) { return __drcp_rn(a); }
+
+// Eq. nr_formula on one interval, given ih = 1/h (the paper's inv_ba):
+//   A = (x1 - q) ih, B = (q - x0) ih,
+//   out = A y0 + B y1 + ((A^3 - A) y2_0 + (B^3 - B) y2_1) h^2 / 6.
+template <typename T>
+__device__ __forceinline__ T interp_core(T q, T x0, T x1, T y0, T y1, T z0, T z1, T ih) {
+  const T A = r_mul(r_sub(x1, q), ih);
+  const T B = r_mul(r_sub(q, x0), ih);
+  const T h = r_sub(x1, x0);
+  const T h26 = r_mul(r_mul(h, h), T(1) / T(6));
+  const T C = r_mul(A, r_fma(A, A, T(-1)));
+  const T D = r_mul(B, r_fma(B, B, T(-1)));
+  const T t = r_fma(C, z0, r_mul(D, z1));
+  const T r = r_fma(A, y0, r_mul(B, y1));
+  return r_fma(t, h26, r);
+}
+
 template <typename T>
 __device__ __forceinline__ T nr_interp(T q, T x0, T x1, T y0, T y1, T z0, T z1) {
-  const T h = x1 - x0;
-  const T ih = T(1) / h;  // IEEE division (no fast-math)
-  const T A = (x1 - q) * ih;
-  const T B = (q - x0) * ih;
-  const T C = A * (A * A - T(1));
-  const T D = B * (B * B - T(1));
-  return A * y0 + B * y1 + (C * z0 + D * z1) * (h * h * (T(1) / T(6)));
+  return interp_core(q, x0, x1, y0, y1, z0, z1, r_rcp(r_sub(x1, x0)));
 }
 
 }  // namespace fs

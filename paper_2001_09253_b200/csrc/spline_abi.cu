@@ -6,7 +6,8 @@
 //                  8192 f32)                              merge tree in shared memory
 //   longer                        K3 k_tile<REDUCE> -> K4 k4_top -> K5 k_tile<FINISH>   (tiled SPIKE)
 // Dispatch (eval, by the curve's staged footprint 3 n s):
-//   <= 96 KiB                     k_eval_staged<MODE>    curves staged in shared memory
+//   fits shared memory (2 stages) k_eval_staged<MODE>    curves staged in shared memory (TABLE: packed
+//                                                          knots + bucket table; SORTED; UNIFORM; BSEARCH)
 //   larger                        k_eval_global          interpolation guess + gallop in HBM
 #include <cuda_runtime.h>
 
@@ -25,7 +26,6 @@ using namespace fs;
 namespace {
 
 constexpr int kK1MaxN = 128;
-constexpr size_t kStageMax = 96 * 1024;
 
 template <typename T> constexpr int rmax() { return sizeof(T) == 8 ? 16 : 32; }
 
@@ -154,62 +154,85 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
 
 // ------------------------------------------------------------------------- eval
 
+inline int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
 template <typename T, int MODE, int V, bool BULK>
 int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
-                    int32_t *idx, int cpb, int nchunks, int qchunk, int64_t grid, cudaStream_t st) {
-  const size_t sm = kStageHeader + 3 * (size_t)n * sizeof(T) * cpb;
+                    int32_t *idx, int cpb, int nchunks, int qchunk, int64_t nitems, cudaStream_t st) {
+  const StageLayout<T> L(cpb, n, MODE == MODE_TABLE || MODE == MODE_UNIFORM, MODE == MODE_TABLE);
+  const size_t sm = L.total;
   auto kern = k_eval_staged<T, MODE, V, BULK>;
   if (int rc = set_smem(kern, sm)) return rc;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, sm) != cudaSuccess || occ < 1) occ = 1;
+  const int64_t grid = std::min<int64_t>(nitems, (int64_t)occ * num_sms());
   kern<<<(unsigned)grid, kEvalThreads, sm, st>>>(x, y, y2, n, batch, q, (int)m, out, idx, cpb, nchunks, qchunk,
-                                                 FastDiv((uint32_t)m));
+                                                 nitems, FastDiv((uint32_t)n), FastDiv((uint32_t)m));
   return launch_rc();
 }
 
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
+constexpr size_t kSmemCap = 220 * 1024;   // per-CTA dynamic shared memory we allow ourselves
+constexpr size_t kItemSmem = 40 * 1024;   // target per-CTA footprint for multi-curve items
+
+template <typename T> size_t stage_total(int cpb, int n, int mode) {
+  return StageLayout<T>(cpb, n, mode == MODE_TABLE || mode == MODE_UNIFORM, mode == MODE_TABLE).total;
+}
+
 template <typename T, int MODE>
 int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
                   int32_t *idx, cudaStream_t st) {
   constexpr int VW = 16 / sizeof(T);
-  const size_t per_curve = 3 * (size_t)n * sizeof(T);
   int cpb = 1, nchunks = 1, qchunk = (int)m;
-  int64_t grid;
+  int64_t nitems;
   if (m >= 2048 || batch == 1) {
-    // One curve per CTA; split a curve's queries if there are too few curves to fill the GPU.
+    // One curve per item; split a curve's queries if there are too few curves to fill the GPU.
     const int64_t want = (4 * 148 + batch - 1) / batch;
     nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (m + 1023) / 1024));
     qchunk = (int)((m + nchunks - 1) / nchunks);
     qchunk = (qchunk + VW - 1) / VW * VW;
     nchunks = (int)((m + qchunk - 1) / qchunk);
-    grid = batch * nchunks;
+    nitems = batch * nchunks;
   } else {
     int64_t c = std::max<int64_t>(1, 2048 / m);
-    c = std::min<int64_t>(c, (int64_t)(kStageMax / per_curve));
     c = std::min<int64_t>(c, batch);
+    while (c > 1 && stage_total<T>((int)c, n, MODE) > kItemSmem) c >>= 1;
     while (c > 1 && (uint64_t)c * m * m >= (1ull << 32)) c >>= 1;  // FastDiv range
     cpb = (int)std::max<int64_t>(1, c);
-    grid = (batch + cpb - 1) / cpb;
+    nitems = (batch + cpb - 1) / cpb;
   }
   // 16-byte vector query I/O when every curve's query run is whole vectors and aligned.
   const bool vec = (m % VW == 0) && aligned16(q) && aligned16(out) && (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0));
   // TMA bulk staging when every curve block is a whole number of 16-byte units and aligned.
   const bool bulk = ((n * sizeof(T)) % 16 == 0) && aligned16(x) && aligned16(y) && aligned16(y2);
-  if (vec && bulk) return launch_staged_k<T, MODE, VW, true>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, grid, st);
-  if (vec) return launch_staged_k<T, MODE, VW, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, grid, st);
-  if (bulk) return launch_staged_k<T, MODE, 1, true>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, grid, st);
-  return launch_staged_k<T, MODE, 1, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, grid, st);
+  if (vec && bulk) return launch_staged_k<T, MODE, VW, true>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+  if (vec) return launch_staged_k<T, MODE, VW, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+  if (bulk) return launch_staged_k<T, MODE, 1, true>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+  return launch_staged_k<T, MODE, 1, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
 }
 
 template <typename T>
 int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const T *q, int64_t m, T *out,
            int32_t *idx, int flags, cudaStream_t st) {
-  const size_t per_curve = 3 * (size_t)n * sizeof(T);
-  if (per_curve <= kStageMax) {
-    if (flags & SPLINE_Q_SORTED)
-      return launch_staged<T, MODE_SORTED>(x, y, y2, (int)n, batch, q, m, out, idx, st);
-    if (flags & SPLINE_X_UNIFORM)
-      return launch_staged<T, MODE_UNIFORM>(x, y, y2, (int)n, batch, q, m, out, idx, st);
-    return launch_staged<T, MODE_BSEARCH>(x, y, y2, (int)n, batch, q, m, out, idx, st);
+  if (n < 65535) {
+    const int nn = (int)n;
+    if ((flags & SPLINE_Q_SORTED) && stage_total<T>(1, nn, MODE_SORTED) <= kSmemCap)
+      return launch_staged<T, MODE_SORTED>(x, y, y2, nn, batch, q, m, out, idx, st);
+    if ((flags & SPLINE_X_UNIFORM) && stage_total<T>(1, nn, MODE_UNIFORM) <= kSmemCap)
+      return launch_staged<T, MODE_UNIFORM>(x, y, y2, nn, batch, q, m, out, idx, st);
+    if (stage_total<T>(1, nn, MODE_TABLE) <= kSmemCap)
+      return launch_staged<T, MODE_TABLE>(x, y, y2, nn, batch, q, m, out, idx, st);
+    if (stage_total<T>(1, nn, MODE_BSEARCH) <= kSmemCap)
+      return launch_staged<T, MODE_BSEARCH>(x, y, y2, nn, batch, q, m, out, idx, st);
   }
   const int64_t total = batch * m;
   const int64_t grid = std::min<int64_t>((total + 1023) / 1024, 148 * 16);
