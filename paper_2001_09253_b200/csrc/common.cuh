@@ -116,6 +116,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // ---- 16-byte vector types per element type
 template <typename T> struct Vec16;
 template <> struct Vec16<float> { using V = float4; using I = int4; static constexpr int N = 4; };

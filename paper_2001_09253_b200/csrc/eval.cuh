@@ -3,29 +3,27 @@
 // Locate rule (reading c1): idx = the largest j in [0, n-2] with x_j <= q;
 // -1 (and out = NaN, status bit) when q is outside [x_0, x_{n-1}] or NaN, because
 // Eq. nr_formula only holds for x_j <= x <= x_{j+1}.  Every search below ends in
-// comparisons against this rule, so guesses (sorted-run carry, uniform-grid index,
-// interpolation guess) change speed, never idx.
-// Evaluate: Eq. nr_formula, see nr_interp in common.cuh.
+// comparisons against this rule, so guesses (bucket table, uniform-grid index, sorted-run
+// carry, interpolation guess) change speed, never idx.
+// Evaluate: Eq. nr_formula, interp_core in common.cuh (explicitly rounded, so
+// all kernels and hints give bitwise-identical out).
 //
-//  k_eval_staged : the curves' x, y, y2 fit in shared memory (3 n s bytes per curve).
-//                  A CTA stages a group of curves (coalesced), then each thread
-//                  locates its queries in shared memory:
-//                    MODE_TABLE    -- (unsorted default) packed knots + per-curve bucket
-//                                     table bracketing each query, then bisection;
-//                    MODE_BSEARCH  -- bisection (curves too large for the table);
-//                    MODE_SORTED   -- a warp takes a contiguous run of queries; the
-//                                     bracket of the previous 32 is carried forward
-//                                     (generalising the paper's forward scan)
-//                                     and each lane gallops from it;
-//                    MODE_UNIFORM  -- direct index (q-x_0)(n-1)/(x_{n-1}-x_0), corrected.
-//  k_eval_global : long curves (beyond shared memory): interpolation guess in global
-//                  memory, corrected by galloping + bisection; gathers x, y, y2.
+//  k_eval_staged : unsorted queries on curves that fit in shared memory.  Persistent CTAs,
+//                  TMA bulk staging (double-buffered), packed knots {x, y, y2, 1/h}:
+//                    MODE_TABLE   -- per-curve bucket table brackets each query
+//                    MODE_UNIFORM -- direct index (q-x_0)(n-1)/(x_{n-1}-x_0), corrected
+//                    MODE_BSEARCH -- bisection on the raw arrays (curves too big to pack)
+//  k_eval_sorted : SPLINE_Q_SORTED.  A warp walks a contiguous run of queries with a
+//                  carried bracket (the paper's forward scan, made
+//                  warp-cooperative); knots are read through L1 (no staging), any n.
+//  k_eval_global : unsorted queries on long curves: interpolation guess in HBM, corrected
+//                  by galloping + bisection; gathers x, y, y2.
 #pragma once
 #include "common.cuh"
 
 namespace fs {
 
-enum { MODE_BSEARCH = 0, MODE_SORTED = 1, MODE_UNIFORM = 2, MODE_TABLE = 3 };
+enum { MODE_BSEARCH = 0, MODE_UNIFORM = 2, MODE_TABLE = 3 };
 
 // Largest j in [lo, n-2] with X[j] <= q, given X[lo] <= q <= X[n-1].
 template <typename T> __device__ __forceinline__ int gallop_up(const T *X, int n, int lo, T q) {
@@ -75,20 +73,15 @@ template <typename T> __device__ __forceinline__ int bisect(const T *X, int n, T
   return lo;
 }
 
-template <typename T, int MODE>
-__device__ __forceinline__ void eval_one(const T *X, const T *Y, const T *Z, int n, T q, int &jcarry, T &val,
-                                         int &j) {
+template <typename T>
+__device__ __forceinline__ void eval_one(const T *X, const T *Y, const T *Z, int n, T q, T &val, int &j) {
   const T x0 = X[0], xn = X[n - 1];
   if (!(q >= x0 && q <= xn)) {  // out of range or NaN
     j = -1;
     val = qnan<T>();
     return;
   }
-  if (MODE == MODE_SORTED) {
-    j = (X[jcarry] <= q) ? gallop_up(X, n, jcarry, q) : bisect(X, n, q);
-  } else {
-    j = bisect(X, n, q);
-  }
+  j = bisect(X, n, q);
   val = nr_interp(q, X[j], X[j + 1], Y[j], Y[j + 1], Z[j], Z[j + 1]);
 }
 
@@ -103,45 +96,55 @@ __device__ __forceinline__ void eval_one(const T *X, const T *Y, const T *Z, int
 // j* = max{ j : x_j <= q } satisfies Tb[b] <= j* <= Tb[b+1]: the table only brackets the
 // search, which still ends in comparisons x_j <= q (bit-exact idx on any grid).
 template <typename T> struct Knot { T x, y, z, ih; };
+// Per staged curve: range and bucket scale (one vector load per group of V queries).
+template <typename T> struct CurveHdr { T x0, xn, s, pad; };
+
+constexpr int kBucketsPerKnot = 2;  // nb = 2n buckets of [x_0, x_{n-1}]
 
 template <typename T> __device__ __forceinline__ int bucket_of(T v, T x0, T s, int nb) {
-  const T f = (v - x0) * s;
-  return (f >= T(0)) ? min((int)f, nb) : 0;  // f is NaN-free for finite knots
+  const T f = r_mul(r_sub(v, x0), s);
+  return (f >= T(0)) ? min((int)f, nb) : 0;  // (int) truncates; f >= 0 here
 }
 
-template <typename T>
-__device__ __forceinline__ void eval_packed(const Knot<T> *K, const uint16_t *Tb, T s, int n, T q, int mode,
-                                            T &val, int &j) {
-  const T x0 = K[0].x, xn = K[n - 1].x;
-  if (!(q >= x0 && q <= xn)) {
-    j = -1;
-    val = qnan<T>();
-    return;
-  }
+// Locate + evaluate one query against a packed curve.  Branch-light: out-of-range / NaN
+// queries run the same path on a clamped stand-in and are masked at the end.  The search
+// is a short forward scan from a lower bound lo to an upper bound hi (both exact bounds of
+// the answer), with a bisection fallback when the bracket is wide.
+template <typename T, int MODE>
+__device__ __forceinline__ void eval_packed(const Knot<T> *K, const uint16_t *Tb, const CurveHdr<T> &hd, int n,
+                                            int nb, T q, T &val, int &j) {
+  const bool in = (q >= hd.x0) && (q <= hd.xn);  // false for NaN
+  const T qc = in ? q : hd.x0;
   int lo, hi;
-  if (mode == MODE_TABLE) {
-    const int b = bucket_of(q, x0, s, n);
+  if (MODE == MODE_TABLE) {
+    const int b = bucket_of(qc, hd.x0, hd.s, nb);
     lo = min((int)Tb[b], n - 2);  // clamps keep invalid (non-monotone) knots memory-safe
     hi = max(lo, min((int)Tb[b + 1], n - 2));
-  } else {  // MODE_UNIFORM: direct index on the (hinted) uniform grid, then corrected
-    int g = (int)((q - x0) * s);
-    g = max(0, min(g, n - 2));
-    if (K[g].x > q) {
-      hi = g - 1;
-      lo = (g >= 1 && K[g - 1].x <= q) ? g - 1 : 0;
+  } else {  // MODE_UNIFORM: direct index on the (hinted) uniform grid
+    lo = max(0, min((int)r_mul(r_sub(qc, hd.x0), hd.s), n - 2));
+    if (K[lo].x > qc) {  // the guess overshot (rounding, or a wrong hint)
+      hi = lo - 1;
+      lo = 0;
     } else {
-      lo = g; hi = n - 2;
-      if (g + 1 <= n - 2 && K[g + 1].x > q) hi = g;  // the common case: settled in one compare
+      hi = n - 2;
     }
   }
-  while (lo < hi) {  // largest j in [lo, hi] with x_j <= q
-    const int mid = (lo + hi + 1) >> 1;
-    if (K[mid].x <= q) lo = mid;
-    else hi = mid - 1;
+  if (hi - lo > 4) {  // wide bracket (clustered knots or a wrong hint): bisect it down
+    do {
+      const int mid = (lo + hi + 1) >> 1;
+      if (K[mid].x <= qc) lo = mid;
+      else hi = mid - 1;
+    } while (hi - lo > 4);
   }
-  j = lo;
-  const Knot<T> a = K[j], b = K[j + 1];
-  val = interp_core(q, a.x, b.x, a.y, b.y, a.z, b.z, a.ih);
+  Knot<T> a = K[lo], b = K[lo + 1];
+  while (lo < hi && b.x <= qc) {  // largest j in [lo, hi] with x_j <= q
+    ++lo;
+    a = b;
+    b = K[lo + 1];
+  }
+  const T v = interp_core(qc, a.x, b.x, a.y, b.y, a.z, b.z, a.ih);
+  j = in ? lo : -1;
+  val = in ? v : qnan<T>();
 }
 
 constexpr int kEvalThreads = 256;
@@ -161,9 +164,9 @@ template <typename T> struct StageLayout {
     knots = off;
     if (packed) off = align16(off + sizeof(Knot<T>) * (size_t)cpb * n);
     scale = off;
-    if (packed) off = align16(off + sizeof(T) * (size_t)cpb);
+    if (packed) off = align16(off + sizeof(CurveHdr<T>) * (size_t)cpb);
     table = off;
-    if (table_) off = align16(off + sizeof(uint16_t) * (size_t)cpb * (n + 2));
+    if (table_) off = align16(off + sizeof(uint16_t) * (size_t)cpb * (kBucketsPerKnot * n + 2));
     total = off;
   }
 };
@@ -198,21 +201,23 @@ __device__ __forceinline__ Item item_of(int64_t it, int64_t batch, int m, int cp
 //   * query batches are register double-buffered: batch b+1 (possibly the next item's
 //     first batch) is loaded before batch b is evaluated.
 // Each warp owns a contiguous run of an item's queries; lane l takes groups of V
-// consecutive queries (16-byte vectors when V > 1), U groups per batch.
+// consecutive queries (16-byte vectors when V > 1), U groups per batch.  A group's V
+// queries belong to one curve (m % V == 0 on the vector path).
 template <typename T, int MODE, int V, bool BULK>
-__global__ void __launch_bounds__(kEvalThreads) k_eval_staged(const T *__restrict__ x, const T *__restrict__ y,
+__global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3) k_eval_staged(const T *__restrict__ x, const T *__restrict__ y,
                                                              const T *__restrict__ y2, int n, int64_t batch,
                                                              const T *__restrict__ q, int m, T *__restrict__ out,
                                                              int32_t *__restrict__ idx, int cpb, int nchunks,
                                                              int qchunk, int64_t nitems, FastDiv divn,
                                                              FastDiv divm) {
-  constexpr int U = 4;
+  constexpr int U = (V >= 4) ? 1 : 2;  // groups per lane per batch (x2 buffered)
   constexpr bool PACKED = (MODE == MODE_TABLE || MODE == MODE_UNIFORM);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const StageLayout<T> L(cpb, n, PACKED, MODE == MODE_TABLE);
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);  // bar[0], bar[1]
   Knot<T> *K = reinterpret_cast<Knot<T> *>(smem_raw + L.knots);
-  T *Sc = reinterpret_cast<T *>(smem_raw + L.scale);
+  CurveHdr<T> *Hd = reinterpret_cast<CurveHdr<T> *>(smem_raw + L.scale);
+  const int nb = kBucketsPerKnot * n;
   uint16_t *Tb = reinterpret_cast<uint16_t *>(smem_raw + L.table);
   const int64_t G = gridDim.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -293,13 +298,13 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_staged(const T *__restric
         kk.ih = (j < n - 1) ? r_rcp(r_sub(X[e + 1], xj)) : T(0);
         K[e] = kk;
         const T x0 = X[c * n], xn = X[c * n + n - 1];
-        const T sc = (MODE == MODE_TABLE) ? (T)n / (xn - x0) : (T)(n - 1) / (xn - x0);
-        if (j == 0) Sc[c] = sc;
+        const T sc = (MODE == MODE_TABLE) ? (T)nb / (xn - x0) : (T)(n - 1) / (xn - x0);
+        if (j == 0) Hd[c] = CurveHdr<T>{x0, xn, sc, T(0)};
         if (MODE == MODE_TABLE && j < n - 1) {
-          uint16_t *Tc = Tb + c * (n + 2);
+          uint16_t *Tc = Tb + c * (nb + 2);
           if (j == 0) Tc[0] = 0;
-          const int blo = bucket_of(xj, x0, sc, n);
-          const int bhi = (j == n - 2) ? n + 1 : bucket_of(X[e + 1], x0, sc, n);
+          const int blo = bucket_of(xj, x0, sc, nb);
+          const int bhi = (j == n - 2) ? nb + 1 : bucket_of(X[e + 1], x0, sc, nb);
           for (int b = blo + 1; b <= bhi; ++b) Tc[b] = (uint16_t)j;
         }
       }
@@ -315,7 +320,6 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_staged(const T *__restric
       In = item_of(itn, batch, m, cpb, nchunks, qchunk);
       wrange(In, wbn, wen);
     }
-    int jcarry = 0;
     for (int gb = wb; gb < we; gb += 32 * U) {
       const bool last = gb + 32 * U >= we;
       if (!last) load_batch(I, gb + 32 * U, we, qn);
@@ -323,29 +327,29 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_staged(const T *__restric
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int g = gb + u * 32 + lane;
-        int jl = -1;
         if (g < we) {
           T val[V];
           int jj[V];
+          // a group's V queries belong to one curve (m % V == 0 on the vector path)
+          const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(I.k0 - I.c0 * m + g * V)) : 0;
+          if (PACKED) {
+            const CurveHdr<T> hd = Hd[cl];
+            const Knot<T> *Kc = K + cl * n;
+            const uint16_t *Tc = Tb + cl * (nb + 2);
 #pragma unroll
-          for (int i = 0; i < V; ++i) {
-            const int k = g * V + i;
-            const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(I.k0 - I.c0 * m + k)) : 0;
-            if (PACKED) {
-              eval_packed(K + cl * n, Tb + cl * (n + 2), Sc[cl], n, qa[u][i], MODE, val[i], jj[i]);
-            } else {
-              eval_one<T, MODE>(X + cl * n, Y + cl * n, Z + cl * n, n, qa[u][i], jcarry, val[i], jj[i]);
-              if (MODE == MODE_SORTED && jj[i] >= 0) jcarry = jj[i];
+            for (int i = 0; i < V; ++i) {
+              eval_packed<T, MODE>(Kc, Tc, hd, n, nb, qa[u][i], val[i], jj[i]);
+              oor |= (jj[i] < 0);
             }
-            oor |= (jj[i] < 0);
-            jl = max(jl, jj[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+              eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qa[u][i], val[i], jj[i]);
+              oor |= (jj[i] < 0);
+            }
           }
           VecIO<T, V>::store(out + I.k0 + (int64_t)g * V, val);
           if (idx) VecIO<T, V>::store_idx(idx + I.k0 + (int64_t)g * V, jj);
-        }
-        if (MODE == MODE_SORTED) {
-          const int jmax = __reduce_max_sync(0xffffffffu, jl);
-          if (jmax >= 0) jcarry = jmax;
         }
       }
 #pragma unroll
@@ -362,6 +366,106 @@ __global__ void __launch_bounds__(kEvalThreads) k_eval_staged(const T *__restric
     s ^= 1;
   }
   if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
+}
+
+// ---- sorted query runs ------------------------------------------------------------------
+
+// Warp-cooperative 32-ary search (all lanes hold the same q, X[0] <= q <= X[n-1]):
+// 32 probes per round, a ballot keeps the last probe with X[p] <= q.  ~log_33(n) rounds of
+// one parallel load each (3 rounds for n = 4096) instead of log2(n) dependent loads.
+template <typename T> __device__ __forceinline__ int warp_locate(const T *X, int n, T q, int lane) {
+  int lo = 0, hi = n - 1;  // invariant: X[lo] <= q, and hi == n-1 or X[hi] > q
+  while (hi - lo > 1) {
+    const int span = hi - lo;
+    const int p = lo + (int)(((int64_t)span * (lane + 1)) / 33);
+    const bool le = (p > lo) && (__ldg(X + p) <= q);
+    const unsigned ball = __ballot_sync(0xffffffffu, le);
+    const int k = ball ? 31 - __clz(ball) : -1;  // X[p] <= q is monotone in the lane index
+    const int nlo = (k >= 0) ? __shfl_sync(0xffffffffu, p, k) : lo;
+    const int nhi = (k < 31) ? __shfl_sync(0xffffffffu, p, k + 1) : hi;
+    lo = nlo;
+    hi = max(nhi, lo + 1);
+  }
+  return min(lo, n - 2);
+}
+
+// SPLINE_Q_SORTED: one warp per run of `qrun` consecutive queries of one curve.  Lane l
+// takes groups of V consecutive queries, 32V per warp step; every lane starts from the
+// warp's carried bracket jc (the largest interval found in the previous step) and scans
+// forward -- with sorted queries that is a few comparisons, generalising the paper's
+// "while x[i+1] < q: i += 1" sweep to 32 lanes.  A query below the carry (a
+// wrong hint) falls back to bisection; a long scan switches to galloping.  Knots are read
+// with read-only loads through L1: a warp's 32V queries touch a handful of knots, so almost
+// every gather is an L1 hit and each knot leaves HBM about once.
+template <typename T, int V>
+__global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x, const T *__restrict__ y,
+                                                       const T *__restrict__ y2, int n, const T *__restrict__ q,
+                                                       int64_t m, T *__restrict__ out, int32_t *__restrict__ idx,
+                                                       int64_t qrun, int64_t runs_per_curve, int64_t ntasks) {
+  const int lane = threadIdx.x & 31;
+  const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (task >= ntasks) return;  // whole warp; no block-level synchronisation below
+  const int64_t c = task / runs_per_curve;
+  const int64_t k0 = (task - c * runs_per_curve) * qrun;
+  const int64_t k1 = min64(m, k0 + qrun);
+  const T *X = x + c * n, *Y = y + c * n, *Z = y2 + c * n;
+  const T *qb = q + c * m;
+  T *ob = out + c * m;
+  int32_t *ib = idx ? idx + c * m : nullptr;
+  const T x0 = __ldg(X), xn = __ldg(X + n - 1);
+
+  // initial bracket from the run's first query (clamped into range)
+  T qf = __ldg(qb + k0);
+  qf = (qf >= x0 && qf <= xn) ? qf : x0;
+  int jc = warp_locate(X, n, qf, lane);
+  bool oor = false;
+
+  T qa[V], qn[V];
+  int64_t kb = k0 + (int64_t)lane * V;
+  if (kb < k1) VecIO<T, V>::load(qb + kb, qa);
+  for (int64_t base = k0; base < k1; base += 32 * V) {
+    const int64_t k = base + (int64_t)lane * V;
+    const int64_t kn = k + 32 * V;
+    if (kn < k1) VecIO<T, V>::load(qb + kn, qn);  // next step in flight
+    if (lane < 3) prefetch_l1((lane == 0 ? X : lane == 1 ? Y : Z) + min(jc + 32, n - 1));
+    int jl = -1;
+    if (k < k1) {
+      T val[V];
+      int jj[V];
+      int j = jc;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const T qq = qa[i];
+        const bool in = (qq >= x0) && (qq <= xn);
+        const T qc = in ? qq : x0;
+        if (__ldg(X + j) > qc) {
+          j = bisect(X, n, qc);  // below the carry: unsorted input despite the hint
+        } else {
+          int steps = 0;
+          while (j < n - 2 && __ldg(X + j + 1) <= qc) {
+            ++j;
+            if (++steps == 8) {  // sparse queries: gallop the rest of the way
+              j = gallop_up(X, n, j, qc);
+              break;
+            }
+          }
+        }
+        const T xa = __ldg(X + j), xb = __ldg(X + j + 1);
+        const T v = nr_interp(qc, xa, xb, __ldg(Y + j), __ldg(Y + j + 1), __ldg(Z + j), __ldg(Z + j + 1));
+        val[i] = in ? v : qnan<T>();
+        jj[i] = in ? j : -1;
+        oor |= !in;
+        if (in) jl = j;
+      }
+      VecIO<T, V>::store(ob + k, val);
+      if (ib) VecIO<T, V>::store_idx(ib + k, jj);
+    }
+    const int jm = __reduce_max_sync(0xffffffffu, jl);
+    if (jm >= 0) jc = jm;
+#pragma unroll
+    for (int i = 0; i < V; ++i) qa[i] = qn[i];
+  }
+  raise_status_warp(oor, kOutOfRange);
 }
 
 // Long curves (not stageable): locate in HBM.  Each thread carries U independent queries

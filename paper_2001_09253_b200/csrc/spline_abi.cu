@@ -220,13 +220,31 @@ int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, con
   return launch_staged_k<T, MODE, 1, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
 }
 
+template <typename T, int V>
+int launch_sorted_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
+                    int32_t *idx, cudaStream_t st) {
+  // runs of ~2048 queries per warp, but at least ~8 warps per SM of work
+  int64_t qrun = 2048;
+  while (qrun > 256 && batch * ((m + qrun - 1) / qrun) < 148 * 32) qrun >>= 1;
+  qrun = (qrun + 32 * V - 1) / (32 * V) * (32 * V);
+  const int64_t rpc = (m + qrun - 1) / qrun;
+  const int64_t ntasks = batch * rpc;
+  const int64_t grid = (ntasks + 7) / 8;
+  k_eval_sorted<T, V><<<(unsigned)grid, 256, 0, st>>>(x, y, y2, n, q, m, out, idx, qrun, rpc, ntasks);
+  return launch_rc();
+}
+
 template <typename T>
 int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const T *q, int64_t m, T *out,
            int32_t *idx, int flags, cudaStream_t st) {
+  if (flags & SPLINE_Q_SORTED) {
+    constexpr int VW = 16 / sizeof(T);
+    const bool vec = (m % VW == 0) && aligned16(q) && aligned16(out) && (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0));
+    if (vec) return launch_sorted_k<T, VW>(x, y, y2, (int)n, batch, q, m, out, idx, st);
+    return launch_sorted_k<T, 1>(x, y, y2, (int)n, batch, q, m, out, idx, st);
+  }
   if (n < 65535) {
     const int nn = (int)n;
-    if ((flags & SPLINE_Q_SORTED) && stage_total<T>(1, nn, MODE_SORTED) <= kSmemCap)
-      return launch_staged<T, MODE_SORTED>(x, y, y2, nn, batch, q, m, out, idx, st);
     if ((flags & SPLINE_X_UNIFORM) && stage_total<T>(1, nn, MODE_UNIFORM) <= kSmemCap)
       return launch_staged<T, MODE_UNIFORM>(x, y, y2, nn, batch, q, m, out, idx, st);
     if (stage_total<T>(1, nn, MODE_TABLE) <= kSmemCap)
