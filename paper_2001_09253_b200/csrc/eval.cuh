@@ -10,6 +10,7 @@
 //
 //  k_eval_staged : unsorted queries on curves that fit in shared memory.  Persistent CTAs,
 //                  TMA bulk staging (double-buffered), packed knots {x, y, y2, 1/h}:
+//                    MODE_BISECT  -- branch-free bisection over +inf-padded knots (short curves)
 //                    MODE_TABLE   -- per-curve bucket table brackets each query
 //                    MODE_UNIFORM -- direct index (q-x_0)(n-1)/(x_{n-1}-x_0), corrected
 //                    MODE_BSEARCH -- bisection on the raw arrays (curves too big to pack)
@@ -23,7 +24,7 @@
 
 namespace fs {
 
-enum { MODE_BSEARCH = 0, MODE_UNIFORM = 2, MODE_TABLE = 3 };
+enum { MODE_BSEARCH = 0, MODE_BISECT = 1, MODE_UNIFORM = 2, MODE_TABLE = 3 };
 
 // Largest j in [lo, n-2] with X[j] <= q, given X[lo] <= q <= X[n-1].
 template <typename T> __device__ __forceinline__ int gallop_up(const T *X, int n, int lo, T q) {
@@ -85,21 +86,25 @@ __device__ __forceinline__ void eval_one(const T *X, const T *Y, const T *Z, int
   val = nr_interp(q, X[j], X[j + 1], Y[j], Y[j + 1], Z[j], Z[j + 1]);
 }
 
-// ---- packed knots + bucket table (MODE_TABLE, MODE_UNIFORM) ---------------------------
+// ---- packed knots (MODE_BISECT, MODE_TABLE, MODE_UNIFORM) -------------------------------
 // Per staged curve: K[j] = {x_j, y_j, y2_j, 1/h_j} (one 16/32-byte record per knot, so the
 // gather is two vector loads and the per-query division becomes a multiply by the
-// interval's precomputed reciprocal -- the paper's inv_ba), and for MODE_TABLE
-// a bucket table over nb = n equal-width buckets of [x_0, x_{n-1}]:
-//     bucket(v) = min(nb, (int)((v - x_0) * s)),   s = nb / (x_{n-1} - x_0)
-//     Tb[b]     = max{ j in [0, n-2] : bucket(x_j) < b }   (Tb[0] = 0).
-// bucket() is monotone in v, so for an in-range query q in bucket b the answer
-// j* = max{ j : x_j <= q } satisfies Tb[b] <= j* <= Tb[b+1]: the table only brackets the
-// search, which still ends in comparisons x_j <= q (bit-exact idx on any grid).
+// interval's precomputed reciprocal -- the paper's inv_ba).
+//   MODE_BISECT : branch-free bisection over Xs, the knots padded with +inf to P = 2^k >=
+//                 n-1 entries: log2(P) uniform steps, no divergence (short curves).
+//   MODE_TABLE  : bucket table over nb = 2n equal-width buckets of [x_0, x_{n-1}]:
+//                   bucket(v) = min(nb, (int)((v - x_0) * s)),   s = nb / (x_{n-1} - x_0)
+//                   Tb[b]     = max{ j in [0, n-2] : bucket(x_j) < b }   (Tb[0] = 0).
+//                 bucket() is monotone in v, so for an in-range query q in bucket b the
+//                 answer j* = max{ j : x_j <= q } satisfies Tb[b] <= j* <= Tb[b+1]: the
+//                 table only brackets the search (long curves, many queries per knot).
+//   MODE_UNIFORM: direct index (q - x_0)(n-1)/(x_{n-1} - x_0) on the hinted uniform grid.
+// Every search ends in comparisons x_j <= q, so idx is exact on any grid.
 template <typename T> struct Knot { T x, y, z, ih; };
-// Per staged curve: range and bucket scale (one vector load per group of V queries).
+// Per staged curve: range and scale (one vector load per group of V queries).
 template <typename T> struct CurveHdr { T x0, xn, s, pad; };
 
-constexpr int kBucketsPerKnot = 2;  // nb = 2n buckets of [x_0, x_{n-1}]
+constexpr int kBucketsPerKnot = 2;
 
 template <typename T> __device__ __forceinline__ int bucket_of(T v, T x0, T s, int nb) {
   const T f = r_mul(r_sub(v, x0), s);
@@ -107,145 +112,151 @@ template <typename T> __device__ __forceinline__ int bucket_of(T v, T x0, T s, i
 }
 
 // Locate + evaluate one query against a packed curve.  Branch-light: out-of-range / NaN
-// queries run the same path on a clamped stand-in and are masked at the end.  The search
-// is a short forward scan from a lower bound lo to an upper bound hi (both exact bounds of
-// the answer), with a bisection fallback when the bracket is wide.
+// queries run the same path on a clamped stand-in and are masked at the end.
 template <typename T, int MODE>
-__device__ __forceinline__ void eval_packed(const Knot<T> *K, const uint16_t *Tb, const CurveHdr<T> &hd, int n,
-                                            int nb, T q, T &val, int &j) {
+__device__ __forceinline__ void eval_packed(const Knot<T> *K, const T *Xs, int P, const uint16_t *Tb,
+                                            const CurveHdr<T> &hd, int n, int nb, T q, T &val, int &j) {
   const bool in = (q >= hd.x0) && (q <= hd.xn);  // false for NaN
   const T qc = in ? q : hd.x0;
-  int lo, hi;
-  if (MODE == MODE_TABLE) {
-    const int b = bucket_of(qc, hd.x0, hd.s, nb);
-    lo = min((int)Tb[b], n - 2);  // clamps keep invalid (non-monotone) knots memory-safe
-    hi = max(lo, min((int)Tb[b + 1], n - 2));
-  } else {  // MODE_UNIFORM: direct index on the (hinted) uniform grid
-    lo = max(0, min((int)r_mul(r_sub(qc, hd.x0), hd.s), n - 2));
-    if (K[lo].x > qc) {  // the guess overshot (rounding, or a wrong hint)
-      hi = lo - 1;
-      lo = 0;
-    } else {
-      hi = n - 2;
+  int lo;
+  if (MODE == MODE_BISECT) {
+    lo = 0;
+    for (int step = P >> 1; step > 0; step >>= 1) lo = (Xs[lo + step] <= qc) ? lo + step : lo;
+    lo = min(lo, n - 2);
+  } else {
+    int hi;
+    if (MODE == MODE_TABLE) {
+      const int b = bucket_of(qc, hd.x0, hd.s, nb);
+      lo = min((int)Tb[b], n - 2);  // clamps keep invalid (non-monotone) knots memory-safe
+      hi = max(lo, min((int)Tb[b + 1], n - 2));
+    } else {  // MODE_UNIFORM
+      lo = max(0, min((int)r_mul(r_sub(qc, hd.x0), hd.s), n - 2));
+      if (K[lo].x > qc) {  // the guess overshot (rounding, or a wrong hint)
+        hi = lo - 1;
+        lo = 0;
+      } else {
+        hi = n - 2;
+      }
     }
+    if (hi - lo > 2) {  // wide bracket (clustered knots or a wrong hint): bisect it down
+      do {
+        const int mid = (lo + hi + 1) >> 1;
+        if (K[mid].x <= qc) lo = mid;
+        else hi = mid - 1;
+      } while (hi - lo > 2);
+    }
+    while (lo < hi && K[lo + 1].x <= qc) ++lo;  // largest j in [lo, hi] with x_j <= q
   }
-  if (hi - lo > 4) {  // wide bracket (clustered knots or a wrong hint): bisect it down
-    do {
-      const int mid = (lo + hi + 1) >> 1;
-      if (K[mid].x <= qc) lo = mid;
-      else hi = mid - 1;
-    } while (hi - lo > 4);
-  }
-  Knot<T> a = K[lo], b = K[lo + 1];
-  while (lo < hi && b.x <= qc) {  // largest j in [lo, hi] with x_j <= q
-    ++lo;
-    a = b;
-    b = K[lo + 1];
-  }
+  const Knot<T> a = K[lo], b = K[lo + 1];
   const T v = interp_core(qc, a.x, b.x, a.y, b.y, a.z, b.z, a.ih);
   j = in ? lo : -1;
   val = in ? v : qnan<T>();
 }
 
 constexpr int kEvalThreads = 256;
-constexpr int kStageHeader = 16;  // mbarrier (8 B) + pad, ahead of the staged arrays
+constexpr int kStageHeader = 16;  // two mbarriers, ahead of the staged arrays
 
 __host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
+__host__ __device__ constexpr int pow2_at_least(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
 
 // Shared-memory layout of one CTA: two raw stages (x, y, y2 of cpb curves each, filled by
-// TMA bulk copies) + the packed knots / scales / bucket table of the item being evaluated.
+// TMA bulk copies) + the packed knots / headers / padded x / bucket table of the item
+// being evaluated.
 template <typename T> struct StageLayout {
-  size_t raw[2], knots, scale, table, total;
-  __host__ __device__ StageLayout(int cpb, int n, bool packed, bool table_) {
+  size_t raw0, rawstep, knots, hdr, xs, table, total;
+  int P;
+  __host__ __device__ StageLayout(int cpb, int n, int mode) {
+    const bool packed = mode != MODE_BSEARCH;
+    P = pow2_at_least(n - 1);
     const size_t rawb = 3 * sizeof(T) * (size_t)cpb * n;
-    raw[0] = kStageHeader;
-    raw[1] = align16(raw[0] + rawb);
-    size_t off = align16(raw[1] + rawb);
+    raw0 = kStageHeader;
+    rawstep = align16(rawb);
+    size_t off = raw0 + 2 * rawstep;
     knots = off;
     if (packed) off = align16(off + sizeof(Knot<T>) * (size_t)cpb * n);
-    scale = off;
+    hdr = off;
     if (packed) off = align16(off + sizeof(CurveHdr<T>) * (size_t)cpb);
+    xs = off;
+    if (mode == MODE_BISECT) off = align16(off + sizeof(T) * (size_t)cpb * P);
     table = off;
-    if (table_) off = align16(off + sizeof(uint16_t) * (size_t)cpb * (kBucketsPerKnot * n + 2));
+    if (mode == MODE_TABLE) off = align16(off + sizeof(uint16_t) * (size_t)cpb * (kBucketsPerKnot * n + 2));
     total = off;
   }
 };
 
-// Work item `it`: curves [c0, c0+nc) and queries [k0, k1) (flat indices into q).
-struct Item {
-  int64_t c0, k0, k1;
-  int nc;
-};
-__device__ __forceinline__ Item item_of(int64_t it, int64_t batch, int m, int cpb, int nchunks, int qchunk) {
-  Item r;
-  if (cpb > 1) {
-    r.c0 = it * cpb;
-    r.nc = (int)min64(cpb, batch - r.c0);
-    r.k0 = r.c0 * m;
-    r.k1 = (r.c0 + r.nc) * m;
-  } else {
-    r.c0 = it / nchunks;
-    const int ch = (int)(it - r.c0 * nchunks);
-    r.nc = 1;
-    r.k0 = r.c0 * m + (int64_t)ch * qchunk;
-    r.k1 = min64(r.c0 * m + m, r.k0 + qchunk);
-  }
-  return r;
-}
-
-// Persistent, double-buffered staged eval.  Grid = min(items, SMs x CTAs/SM); CTA b takes
-// items b, b+G, b+2G, ...  Pipeline per CTA:
-//   * raw stage s holds item i's x, y, y2 (cp.async.bulk -> mbarrier[s]); the copy for
-//     item i+1 is already in flight in stage s^1 while item i is evaluated, and stage s is
-//     refilled (item i+2) as soon as it has been consumed;
-//   * query batches are register double-buffered: batch b+1 (possibly the next item's
-//     first batch) is loaded before batch b is evaluated.
+// Persistent, double-buffered staged eval (unsorted queries).  Work item `it` = curves
+// [it*cpb, +cpb) with all their queries (cpb > 1), or queries [ch*qchunk, +qchunk) of curve
+// it/nchunks (cpb == 1).  Grid = min(items, SMs x CTAs/SM); CTA b takes items b, b+G, ...
+//   * raw stage s holds item i's x, y, y2 (cp.async.bulk -> mbarrier s); item i+1's copy is
+//     already in flight in stage s^1 while item i is evaluated, and stage s is refilled
+//     (item i+2) as soon as the packing pass has consumed it;
+//   * query batches are register double-buffered: batch b+1 (possibly the next item's first
+//     batch) is loaded before batch b is evaluated.
 // Each warp owns a contiguous run of an item's queries; lane l takes groups of V
 // consecutive queries (16-byte vectors when V > 1), U groups per batch.  A group's V
 // queries belong to one curve (m % V == 0 on the vector path).
 template <typename T, int MODE, int V, bool BULK>
-__global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3) k_eval_staged(const T *__restrict__ x, const T *__restrict__ y,
-                                                             const T *__restrict__ y2, int n, int64_t batch,
-                                                             const T *__restrict__ q, int m, T *__restrict__ out,
-                                                             int32_t *__restrict__ idx, int cpb, int nchunks,
-                                                             int qchunk, int64_t nitems, FastDiv divn,
-                                                             FastDiv divm) {
+__global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3)
+    k_eval_staged(const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ y2, int n, int64_t batch,
+                  const T *__restrict__ q, int m, T *__restrict__ out, int32_t *__restrict__ idx, int cpb,
+                  int nchunks, int qchunk, int64_t nitems, FastDiv divn, FastDiv divm) {
   constexpr int U = (V >= 4) ? 1 : 2;  // groups per lane per batch (x2 buffered)
-  constexpr bool PACKED = (MODE == MODE_TABLE || MODE == MODE_UNIFORM);
+  constexpr bool PACKED = (MODE != MODE_BSEARCH);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const StageLayout<T> L(cpb, n, PACKED, MODE == MODE_TABLE);
+  const StageLayout<T> L(cpb, n, MODE);
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);  // bar[0], bar[1]
   Knot<T> *K = reinterpret_cast<Knot<T> *>(smem_raw + L.knots);
-  CurveHdr<T> *Hd = reinterpret_cast<CurveHdr<T> *>(smem_raw + L.scale);
-  const int nb = kBucketsPerKnot * n;
+  CurveHdr<T> *Hd = reinterpret_cast<CurveHdr<T> *>(smem_raw + L.hdr);
+  T *Xs = reinterpret_cast<T *>(smem_raw + L.xs);
   uint16_t *Tb = reinterpret_cast<uint16_t *>(smem_raw + L.table);
+  const int P = L.P;
+  const int nb = kBucketsPerKnot * n;
   const int64_t G = gridDim.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const size_t cn = (size_t)cpb * n;
 
-  const size_t raw0 = L.raw[0], rawstep = L.raw[1] - L.raw[0];
-  auto raw = [&](int s) { return reinterpret_cast<T *>(smem_raw + raw0 + (size_t)s * rawstep); };
+  auto raw = [&](int s) { return reinterpret_cast<T *>(smem_raw + L.raw0 + (size_t)s * L.rawstep); };
+  auto item_of = [&](int64_t it, int64_t &c0, int64_t &k0, int &nc, int &cnt) {
+    if (cpb > 1) {
+      c0 = it * cpb;
+      nc = (int)min64(cpb, batch - c0);
+      k0 = c0 * m;
+      cnt = nc * m;
+    } else {
+      c0 = it / nchunks;
+      const int ch = (int)(it - c0 * nchunks);
+      nc = 1;
+      k0 = c0 * m + (int64_t)ch * qchunk;
+      cnt = (int)(min64(c0 * m + m, k0 + qchunk) - k0);
+    }
+  };
   auto issue = [&](int64_t it, int s) {  // thread 0 only
     if (!BULK || it >= nitems) return;
-    const Item I = item_of(it, batch, m, cpb, nchunks, qchunk);
-    const uint32_t bytes = (uint32_t)((size_t)I.nc * n * sizeof(T));
+    int64_t c0, k0;
+    int nc, cnt;
+    item_of(it, c0, k0, nc, cnt);
+    const uint32_t bytes = (uint32_t)((size_t)nc * n * sizeof(T));
     T *R = raw(s);
     mbar_expect_tx(bar + s, 3 * bytes);
-    bulk_g2s(R, x + I.c0 * n, bytes, bar + s);
-    bulk_g2s(R + (size_t)cpb * n, y + I.c0 * n, bytes, bar + s);
-    bulk_g2s(R + 2 * (size_t)cpb * n, y2 + I.c0 * n, bytes, bar + s);
+    bulk_g2s(R, x + c0 * n, bytes, bar + s);
+    bulk_g2s(R + cn, y + c0 * n, bytes, bar + s);
+    bulk_g2s(R + 2 * cn, y2 + c0 * n, bytes, bar + s);
   };
-  // The warp's group range of an item.
-  auto wrange = [&](const Item &I, int &wb, int &we) {
-    const int ng = (int)(I.k1 - I.k0) / V;
+  auto wrange = [&](int cnt, int &wb, int &we) {  // the warp's group range within an item
+    const int ng = cnt / V;
     const int per = (ng + nw - 1) / nw;
     wb = w * per;
     we = min(ng, wb + per);
   };
-  auto load_batch = [&](const Item &I, int gb, int we, T (&qv)[U][V]) {
+  auto load_batch = [&](int64_t k0, int gb, int we, T (&qv)[U][V]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int g = gb + u * 32 + lane;
-      if (g < we) VecIO<T, V>::load(q + I.k0 + (int64_t)g * V, qv[u]);
+      if (g < we) VecIO<T, V>::load(q + k0 + (int64_t)g * V, qv[u]);
     }
   };
 
@@ -260,33 +271,31 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3) k_eval_s
     issue(it + G, 1);
   }
   T qa[U][V], qn[U][V];
-  Item I = item_of(it < nitems ? it : 0, batch, m, cpb, nchunks, qchunk);
-  int wb, we;
-  wrange(I, wb, we);
-  if (it < nitems) load_batch(I, wb, we, qa);
+  int64_t c0, k0;
+  int nc, cnt, wb, we;
+  item_of(it < nitems ? it : 0, c0, k0, nc, cnt);
+  wrange(cnt, wb, we);
+  if (it < nitems) load_batch(k0, wb, we, qa);
   bool oor = false;
   uint32_t phases = 0u;  // bit s = parity to wait for on bar[s]
   int s = 0;
 
   for (; it < nitems; it += G) {
+    T *X = raw(s);
     if (BULK) {
       mbar_wait(bar + s, (phases >> s) & 1u);
       phases ^= 1u << s;
     } else {  // unaligned inputs: synchronous coalesced staging
-      T *R = raw(s);
-      const int tot = I.nc * n;
-      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        R[e] = x[I.c0 * n + e];
-        R[(size_t)cpb * n + e] = y[I.c0 * n + e];
-        R[2 * (size_t)cpb * n + e] = y2[I.c0 * n + e];
+      for (int e = threadIdx.x; e < nc * n; e += blockDim.x) {
+        X[e] = x[c0 * n + e];
+        X[cn + e] = y[c0 * n + e];
+        X[2 * cn + e] = y2[c0 * n + e];
       }
       __syncthreads();
     }
-    const T *X = raw(s);
-    const T *Y = X + (size_t)cpb * n;
-    const T *Z = Y + (size_t)cpb * n;
-    const int tot = I.nc * n;
+    const T *Y = X + cn, *Z = X + 2 * cn;
     if (PACKED) {
+      const int tot = nc * n;
       for (int e = threadIdx.x; e < tot; e += blockDim.x) {
         const int c = (int)divn.div((uint32_t)e);
         const int j = e - c * n;
@@ -297,59 +306,62 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3) k_eval_s
         kk.z = Z[e];
         kk.ih = (j < n - 1) ? r_rcp(r_sub(X[e + 1], xj)) : T(0);
         K[e] = kk;
-        const T x0 = X[c * n], xn = X[c * n + n - 1];
-        const T sc = (MODE == MODE_TABLE) ? (T)nb / (xn - x0) : (T)(n - 1) / (xn - x0);
-        if (j == 0) Hd[c] = CurveHdr<T>{x0, xn, sc, T(0)};
-        if (MODE == MODE_TABLE && j < n - 1) {
-          uint16_t *Tc = Tb + c * (nb + 2);
-          if (j == 0) Tc[0] = 0;
-          const int blo = bucket_of(xj, x0, sc, nb);
-          const int bhi = (j == n - 2) ? nb + 1 : bucket_of(X[e + 1], x0, sc, nb);
-          for (int b = blo + 1; b <= bhi; ++b) Tc[b] = (uint16_t)j;
+        if (MODE == MODE_BISECT) {
+          T *Xc = Xs + (size_t)c * P;
+          if (j < P) Xc[j] = xj;
+          for (int jj = n + j; jj < P; jj += n) Xc[jj] = (T)INFINITY;  // pad [n, P) with +inf
+        }
+        if (j == 0 || (MODE == MODE_TABLE && j < n - 1)) {
+          const T x0 = X[c * n], xn = X[c * n + n - 1];
+          const T sc = (MODE == MODE_TABLE) ? (T)nb / (xn - x0) : (T)(n - 1) / (xn - x0);
+          if (j == 0) Hd[c] = CurveHdr<T>{x0, xn, sc, T(0)};
+          if (MODE == MODE_TABLE) {
+            uint16_t *Tc = Tb + c * (nb + 2);
+            if (j == 0) Tc[0] = 0;
+            const int blo = bucket_of(xj, x0, sc, nb);
+            const int bhi = (j == n - 2) ? nb + 1 : bucket_of(X[e + 1], x0, sc, nb);
+            for (int b = blo + 1; b <= bhi; ++b) Tc[b] = (uint16_t)j;
+          }
         }
       }
-      __syncthreads();  // K/T built; raw stage s consumed
+      __syncthreads();  // packed data built; raw stage s consumed
       if (threadIdx.x == 0) issue(it + 2 * G, s);
     }
 
-    // next item's geometry (for the cross-item prefetch of its first batch)
+    // next item (its first batch is prefetched during this item's last batch)
     const int64_t itn = it + G;
-    Item In = I;
-    int wbn = 0, wen = 0;
+    int64_t c0n = 0, k0n = 0;
+    int ncn = 0, cntn = 0, wbn = 0, wen = 0;
     if (itn < nitems) {
-      In = item_of(itn, batch, m, cpb, nchunks, qchunk);
-      wrange(In, wbn, wen);
+      item_of(itn, c0n, k0n, ncn, cntn);
+      wrange(cntn, wbn, wen);
     }
+    const int kbase = (int)(k0 - c0 * m);  // item's first query, relative to its first curve
     for (int gb = wb; gb < we; gb += 32 * U) {
-      const bool last = gb + 32 * U >= we;
-      if (!last) load_batch(I, gb + 32 * U, we, qn);
-      else if (itn < nitems) load_batch(In, wbn, wen, qn);
+      if (gb + 32 * U < we) load_batch(k0, gb + 32 * U, we, qn);
+      else if (itn < nitems) load_batch(k0n, wbn, wen, qn);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int g = gb + u * 32 + lane;
         if (g < we) {
           T val[V];
           int jj[V];
-          // a group's V queries belong to one curve (m % V == 0 on the vector path)
-          const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(I.k0 - I.c0 * m + g * V)) : 0;
+          const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(kbase + g * V)) : 0;
           if (PACKED) {
             const CurveHdr<T> hd = Hd[cl];
             const Knot<T> *Kc = K + cl * n;
+            const T *Xc = Xs + (size_t)cl * P;
             const uint16_t *Tc = Tb + cl * (nb + 2);
 #pragma unroll
-            for (int i = 0; i < V; ++i) {
-              eval_packed<T, MODE>(Kc, Tc, hd, n, nb, qa[u][i], val[i], jj[i]);
-              oor |= (jj[i] < 0);
-            }
+            for (int i = 0; i < V; ++i) eval_packed<T, MODE>(Kc, Xc, P, Tc, hd, n, nb, qa[u][i], val[i], jj[i]);
           } else {
 #pragma unroll
-            for (int i = 0; i < V; ++i) {
-              eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qa[u][i], val[i], jj[i]);
-              oor |= (jj[i] < 0);
-            }
+            for (int i = 0; i < V; ++i) eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qa[u][i], val[i], jj[i]);
           }
-          VecIO<T, V>::store(out + I.k0 + (int64_t)g * V, val);
-          if (idx) VecIO<T, V>::store_idx(idx + I.k0 + (int64_t)g * V, jj);
+#pragma unroll
+          for (int i = 0; i < V; ++i) oor |= (jj[i] < 0);
+          VecIO<T, V>::store(out + k0 + (int64_t)g * V, val);
+          if (idx) VecIO<T, V>::store_idx(idx + k0 + (int64_t)g * V, jj);
         }
       }
 #pragma unroll
@@ -357,12 +369,10 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3) k_eval_s
 #pragma unroll
         for (int i = 0; i < V; ++i) qa[u][i] = qn[u][i];
     }
-    if (wb >= we && itn < nitems) load_batch(In, wbn, wen, qa);  // warp had no work in this item
-    __syncthreads();  // everyone is done with K/T (and raw stage s) of item `it`
+    if (wb >= we && itn < nitems) load_batch(k0n, wbn, wen, qa);  // warp had no work in this item
+    __syncthreads();  // everyone is done with this item's shared data
     if (!PACKED && threadIdx.x == 0) issue(it + 2 * G, s);
-    I = In;
-    wb = wbn;
-    we = wen;
+    c0 = c0n; k0 = k0n; nc = ncn; cnt = cntn; wb = wbn; we = wen;
     s ^= 1;
   }
   if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);

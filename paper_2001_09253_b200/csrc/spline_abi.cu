@@ -167,7 +167,7 @@ inline int num_sms() {
 template <typename T, int MODE, int V, bool BULK>
 int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
                     int32_t *idx, int cpb, int nchunks, int qchunk, int64_t nitems, cudaStream_t st) {
-  const StageLayout<T> L(cpb, n, MODE == MODE_TABLE || MODE == MODE_UNIFORM, MODE == MODE_TABLE);
+  const StageLayout<T> L(cpb, n, MODE);
   const size_t sm = L.total;
   auto kern = k_eval_staged<T, MODE, V, BULK>;
   if (int rc = set_smem(kern, sm)) return rc;
@@ -182,11 +182,9 @@ int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 constexpr size_t kSmemCap = 220 * 1024;   // per-CTA dynamic shared memory we allow ourselves
-constexpr size_t kItemSmem = 40 * 1024;   // target per-CTA footprint for multi-curve items
+constexpr size_t kItemSmem = 48 * 1024;   // target per-CTA footprint for multi-curve items
 
-template <typename T> size_t stage_total(int cpb, int n, int mode) {
-  return StageLayout<T>(cpb, n, mode == MODE_TABLE || mode == MODE_UNIFORM, mode == MODE_TABLE).total;
-}
+template <typename T> size_t stage_total(int cpb, int n, int mode) { return StageLayout<T>(cpb, n, mode).total; }
 
 template <typename T, int MODE>
 int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
@@ -203,7 +201,7 @@ int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, con
     nchunks = (int)((m + qchunk - 1) / qchunk);
     nitems = batch * nchunks;
   } else {
-    int64_t c = std::max<int64_t>(1, 2048 / m);
+    int64_t c = std::max<int64_t>(1, 8192 / m);
     c = std::min<int64_t>(c, batch);
     while (c > 1 && stage_total<T>((int)c, n, MODE) > kItemSmem) c >>= 1;
     while (c > 1 && (uint64_t)c * m * m >= (1ull << 32)) c >>= 1;  // FastDiv range
@@ -247,6 +245,10 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
     const int nn = (int)n;
     if ((flags & SPLINE_X_UNIFORM) && stage_total<T>(1, nn, MODE_UNIFORM) <= kSmemCap)
       return launch_staged<T, MODE_UNIFORM>(x, y, y2, nn, batch, q, m, out, idx, st);
+    // short curves: branch-free bisection; longer curves with many queries per knot: the
+    // bucket table (its O(n) build per item is amortised over the queries)
+    if (n <= 512 && stage_total<T>(1, nn, MODE_BISECT) <= kSmemCap)
+      return launch_staged<T, MODE_BISECT>(x, y, y2, nn, batch, q, m, out, idx, st);
     if (stage_total<T>(1, nn, MODE_TABLE) <= kSmemCap)
       return launch_staged<T, MODE_TABLE>(x, y, y2, nn, batch, q, m, out, idx, st);
     if (stage_total<T>(1, nn, MODE_BSEARCH) <= kSmemCap)
