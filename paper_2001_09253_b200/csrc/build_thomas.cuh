@@ -1,17 +1,23 @@
-// build_thomas.cuh -- K1: batched Thomas solve, one thread per curve (short curves, n <= 128).
+// build_thomas.cuh -- K1: batched Thomas solves for short curves (n <= 128).
 //
 // Method: the paper's new_second_derivative sweep -- forward elimination
-// c'_j, d'_j, d' stored where y2 goes, back-substitution
-// y2_j = d'_j - c'_j y2_{j+1} -- with the rows of Eq. init_val,
-// the clamped start row and the clamped end row of P:1017-1018.
+// c'_j, d'_j stored in place, back-substitution
+// y2_j = d'_j - c'_j y2_{j+1} -- on the rows of Eq. init_val, the
+// clamped start row and the clamped end row of P:1017-1018.
 //
-// Layout: global x/y/y2 are curve-major [B][n].  A CTA owns CPB consecutive curves: it
-// stages their x and y with coalesced loads into shared memory tiles whose per-curve
-// stride S = n|1 is odd, so that at sweep step j the 32 lanes (32 curves) read
-// 32 distinct banks -- the "interleaved SoA" access of the north star, realised
-// on-chip.  c' overwrites x and d' (then y2) overwrites y in place; the y2 tile is then
-// written back with coalesced stores.  Validation (strictly increasing, finite knots,
-// finite values and slopes) is fused into the sweep.
+// K1  (k1_thomas_babe, 3 <= n <= 128): two threads per curve run the same elimination
+//     from both ends ("burn at both ends"): the top thread eliminates rows 0..k-1 downward
+//     (c'_j, d'_j), the bottom thread rows n-1..k+1 upward (a''_j, d''_j), they meet at the
+//     middle row k = n/2 through one shuffle, y2_k = (d_k - a_k d'_{k-1} - c_k d''_{k+1}) /
+//     (b_k - a_k c'_{k-1} - c_k a''_{k+1}), and each back-substitutes outward.  Same flop
+//     count as Thomas, half the dependency chain.  The CTA stages its curves' x, y with
+//     coalesced loads into shared-memory tiles of odd stride S = n|1 (at a given step the
+//     lanes of a warp hit distinct banks -- the north star's interleaved SoA, realised
+//     on-chip); coefficients and y2 overwrite x, y in place; y2 leaves with coalesced stores.
+// K1r (k1_thomas_regs, n <= 16): one thread per curve, everything in registers, 16-byte
+//     vector loads/stores -- the few-control-point regime (BASELINE cfg3).
+// Validation (strictly increasing finite knots, finite values and slopes) is
+// fused: a bad curve's y2 is all NaN and SPLINE_STATUS_BAD_KNOTS is raised.
 #pragma once
 #include "common.cuh"
 
@@ -19,14 +25,13 @@ namespace fs {
 
 constexpr int kK1Threads = 256;
 
-// blockDim = 256 threads stage the tile (all loads in flight at once); the first CPB
-// threads (one per curve) run the sweeps.
 template <typename T>
-__global__ void __launch_bounds__(kK1Threads, 4) k1_thomas_batched(const T *__restrict__ x, const T *__restrict__ y,
-                                                                int n, int64_t batch, int bc,
-                                                                const T *__restrict__ yp1, const T *__restrict__ ypn,
-                                                                T *__restrict__ y2, int S, int CPB, FastDiv divn) {
+__global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict__ x, const T *__restrict__ y, int n,
+                                                             int64_t batch, int bc, const T *__restrict__ yp1,
+                                                             const T *__restrict__ ypn, T *__restrict__ y2, int S,
+                                                             FastDiv divn) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int CPB = blockDim.x / 2;  // blockDim = 2 x curves per CTA (<= 256)
   T *X = reinterpret_cast<T *>(smem_raw);
   T *Y = X + (size_t)CPB * S;
 
@@ -39,11 +44,12 @@ __global__ void __launch_bounds__(kK1Threads, 4) k1_thomas_batched(const T *__re
   // Stage: flat coalesced loads (UL per array per thread in flight), scattered into the
   // odd-stride tiles.
   constexpr int UL = sizeof(T) == 4 ? 16 : 8;
-  for (int base = threadIdx.x; base < tot; base += UL * kK1Threads) {
+  const int NT = blockDim.x;
+  for (int base = threadIdx.x; base < tot; base += UL * NT) {
     T vx[UL], vy[UL];
 #pragma unroll
     for (int u = 0; u < UL; ++u) {
-      const int e = base + u * kK1Threads;
+      const int e = base + u * NT;
       if (e < tot) {
         vx[u] = ld_stream(xb + e);
         vy[u] = ld_stream(yb + e);
@@ -51,7 +57,7 @@ __global__ void __launch_bounds__(kK1Threads, 4) k1_thomas_batched(const T *__re
     }
 #pragma unroll
     for (int u = 0; u < UL; ++u) {
-      const int e = base + u * kK1Threads;
+      const int e = base + u * NT;
       if (e < tot) {
         const int c = (int)divn.div((uint32_t)e);
         const int j = e - c * n;
@@ -62,76 +68,248 @@ __global__ void __launch_bounds__(kK1Threads, 4) k1_thomas_batched(const T *__re
   }
   __syncthreads();
 
-  const int t = threadIdx.x;
-  if (t < nc) {
-    T *Xc = X + t * S;
-    T *Yc = Y + t * S;
-    const int64_t cg = c0 + t;
-    bool ok = true;
-
-    T xo = Xc[0], yo = Yc[0];
-    T xn = Xc[1], yn = Yc[1];
-    ok = ok && finite(xo) && finite(yo) && finite(yn) && (xn > xo);
-    T hprev = xn - xo;
-    T ddprev = (yn - yo) / hprev;
-    T cp, dp;
-    if (bc & 1) {  // clamped start: c'_0 = 1/2, d'_0 = 3 (dd_0 - y'_0) / h_0
-      const T s = yp1[cg];
-      ok = ok && finite(s);
-      cp = T(0.5);
-      dp = T(3) * (ddprev - s) / hprev;
-    } else {  // natural start
-      cp = T(0);
-      dp = T(0);
-    }
-    Xc[0] = cp;
-    Yc[0] = dp;
-    // Forward substitution over the interior rows; two loads per step.
-    for (int j = 1; j < n - 1; ++j) {
-      xo = xn;
-      yo = yn;
-      xn = Xc[j + 1];
-      yn = Yc[j + 1];
-      ok = ok && (xn > xo) && finite(yn);
-      const T h = xn - xo;
-      const T dd = (yn - yo) / h;
-      const T inv = T(1) / (T(2) * (hprev + h) - hprev * cp);
-      dp = (T(6) * (dd - ddprev) - hprev * dp) * inv;
-      cp = h * inv;
-      Xc[j] = cp;
-      Yc[j] = dp;
-      hprev = h;
-      ddprev = dd;
-    }
-    ok = ok && finite(xn);
-    // End row.
-    if (bc & 2) {  // clamped end: a = h_{n-2}, b = 2 h_{n-2}, d = 6 (y'_{n-1} - dd_{n-2})
-      const T e = ypn[cg];
-      ok = ok && finite(e);
-      const T inv = T(1) / (T(2) * hprev - hprev * cp);
-      dp = (T(6) * (e - ddprev) - hprev * dp) * inv;
+  const int t = threadIdx.x >> 1;       // curve within the CTA
+  const bool top = (threadIdx.x & 1) == 0;
+  const bool act = t < nc;              // pairs are lane-adjacent, so shuffles stay in-warp
+  const int k = n >> 1;                 // meeting row, 1 <= k <= n-2
+  T *Xc = X + (act ? t : 0) * S;
+  T *Yc = Y + (act ? t : 0) * S;
+  const int64_t cg = c0 + t;
+  bool ok = true;
+  T hb = T(0), ddb = T(0), cpb = T(0), dpb = T(0);  // this side's values at the seam
+  if (act) {
+    if (top) {
+      // rows 0 .. k-1, downward
+      T xo = Xc[0], yo = Yc[0];
+      T xn = Xc[1], yn = Yc[1];
+      ok = finite(xo) && finite(yo) && finite(xn) && finite(yn) && (xn > xo);
+      T hprev = xn - xo;
+      T ddprev = (yn - yo) / hprev;
+      T cp, dp;
+      if (bc & 1) {  // clamped start: c'_0 = 1/2, d'_0 = 3 (dd_0 - y'_0) / h_0
+        const T s = yp1[cg];
+        ok = ok && finite(s);
+        cp = T(0.5);
+        dp = T(3) * (ddprev - s) / hprev;
+      } else {  // natural start
+        cp = T(0);
+        dp = T(0);
+      }
+      Xc[0] = cp;
+      Yc[0] = dp;
+      for (int j = 1; j < k; ++j) {
+        xo = xn;
+        yo = yn;
+        xn = Xc[j + 1];
+        yn = Yc[j + 1];
+        ok = ok && (xn > xo) && finite(xn) && finite(yn);
+        const T h = xn - xo;
+        const T dd = (yn - yo) / h;
+        const T inv = T(1) / (T(2) * (hprev + h) - hprev * cp);
+        dp = (T(6) * (dd - ddprev) - hprev * dp) * inv;
+        cp = h * inv;
+        Xc[j] = cp;
+        Yc[j] = dp;
+        hprev = h;
+        ddprev = dd;
+      }
+      hb = hprev;  // h_{k-1}
+      ddb = ddprev;
+      cpb = cp;    // c'_{k-1}
+      dpb = dp;    // d'_{k-1}
     } else {
-      dp = T(0);
+      // rows n-1 .. k+1, upward: y2_j = d''_j - a''_j y2_{j-1}
+      T xo = Xc[n - 1], yo = Yc[n - 1];
+      T xn = Xc[n - 2], yn = Yc[n - 2];
+      ok = finite(xo) && finite(yo) && finite(xn) && finite(yn) && (xo > xn);
+      T hnext = xo - xn;            // h_{n-2}
+      T ddnext = (yo - yn) / hnext; // dd_{n-2}
+      T ap, dp;
+      if (bc & 2) {  // clamped end: a = h, b = 2h, d = 6 (y'_{n-1} - dd_{n-2})
+        const T e = ypn[cg];
+        ok = ok && finite(e);
+        ap = T(0.5);
+        dp = T(3) * (e - ddnext) / hnext;
+      } else {  // natural end
+        ap = T(0);
+        dp = T(0);
+      }
+      Xc[n - 1] = ap;
+      Yc[n - 1] = dp;
+      for (int j = n - 2; j > k; --j) {
+        xo = xn;
+        yo = yn;
+        xn = Xc[j - 1];
+        yn = Yc[j - 1];
+        ok = ok && (xo > xn) && finite(xn) && finite(yn);
+        const T h = xo - xn;          // h_{j-1}
+        const T dd = (yo - yn) / h;   // dd_{j-1}
+        // row j: a = h_{j-1}, b = 2(h_{j-1} + h_j), c = h_j, d = 6(dd_j - dd_{j-1})
+        const T inv = T(1) / (T(2) * (h + hnext) - hnext * ap);
+        dp = (T(6) * (ddnext - dd) - hnext * dp) * inv;
+        ap = h * inv;
+        Xc[j] = ap;
+        Yc[j] = dp;
+        hnext = h;
+        ddnext = dd;
+      }
+      hb = hnext;   // h_k
+      ddb = ddnext; // dd_k
+      cpb = ap;     // a''_{k+1}
+      dpb = dp;     // d''_{k+1}
     }
-    Yc[n - 1] = dp;
-    // Backward substitution.
-    for (int j = n - 2; j >= 0; --j) {
-      dp = Yc[j] - Xc[j] * dp;
-      Yc[j] = dp;
-    }
-    if (!ok) {
-      const T nanv = qnan<T>();
-      for (int j = 0; j < n; ++j) Yc[j] = nanv;
-    }
-    raise_status_warp(!ok, kBadKnots);
   }
+  // meet at row k: a_k = h_{k-1}, b_k = 2(h_{k-1} + h_k), c_k = h_k, d_k = 6(dd_k - dd_{k-1})
+  const T o_h = __shfl_xor_sync(0xffffffffu, hb, 1);
+  const T o_dd = __shfl_xor_sync(0xffffffffu, ddb, 1);
+  const T o_cp = __shfl_xor_sync(0xffffffffu, cpb, 1);
+  const T o_dp = __shfl_xor_sync(0xffffffffu, dpb, 1);
+  const bool o_ok = __shfl_xor_sync(0xffffffffu, ok, 1);
+  if (act) {
+    ok = ok && o_ok;
+    const T hk1 = top ? hb : o_h, ddk1 = top ? ddb : o_dd, cT = top ? cpb : o_cp, dT = top ? dpb : o_dp;
+    const T hk = top ? o_h : hb, ddk = top ? o_dd : ddb, aB = top ? o_cp : cpb, dB = top ? o_dp : dpb;
+    const T yk = (T(6) * (ddk - ddk1) - hk1 * dT - hk * dB) / (T(2) * (hk1 + hk) - hk1 * cT - hk * aB);
+    T yv = yk;
+    if (top) {
+      Yc[k] = yk;
+      for (int j = k - 1; j >= 0; --j) {
+        yv = Yc[j] - Xc[j] * yv;
+        Yc[j] = yv;
+      }
+    } else {
+      for (int j = k + 1; j < n; ++j) {
+        yv = Yc[j] - Xc[j] * yv;
+        Yc[j] = yv;
+      }
+    }
+    if (!ok) {  // both threads of the pair see the same ok
+      const T nanv = qnan<T>();
+      for (int j = top ? 0 : k + 1; j < (top ? k + 1 : n); ++j) Yc[j] = nanv;
+    }
+  }
+  raise_status_warp(act && !ok && top, kBadKnots);
   __syncthreads();
 
   T *y2b = y2 + c0 * n;
-  for (int e = threadIdx.x; e < tot; e += kK1Threads) {
+  for (int e = threadIdx.x; e < tot; e += NT) {
     const int c = (int)divn.div((uint32_t)e);
     const int j = e - c * n;
     y2b[e] = Y[c * S + j];
+  }
+}
+
+// K1r: one thread per curve, n <= NMAX, all in registers.
+template <typename T, int NMAX>
+__global__ void __launch_bounds__(256) k1_thomas_regs(const T *__restrict__ x, const T *__restrict__ y, int n,
+                                                      int64_t batch, int bc, const T *__restrict__ yp1,
+                                                      const T *__restrict__ ypn, T *__restrict__ y2, int vec) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= batch) return;
+  T xv[NMAX], yv[NMAX];
+  const T *xc = x + c * n, *yc = y + c * n;
+  constexpr int VW = 16 / sizeof(T);
+  if (vec) {  // n % VW == 0 and 16-byte aligned rows
+    using VT = typename Vec16<T>::V;
+#pragma unroll
+    for (int j = 0; j < NMAX; j += VW) {
+      if (j < n) {
+        const VT a = __ldcs(reinterpret_cast<const VT *>(xc + j));
+        const VT b = __ldcs(reinterpret_cast<const VT *>(yc + j));
+#pragma unroll
+        for (int i = 0; i < VW; ++i) {
+          xv[j + i] = reinterpret_cast<const T *>(&a)[i];
+          yv[j + i] = reinterpret_cast<const T *>(&b)[i];
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+      if (j < n) {
+        xv[j] = ld_stream(xc + j);
+        yv[j] = ld_stream(yc + j);
+      } else {
+        xv[j] = T(0);
+        yv[j] = T(0);
+      }
+    }
+  }
+  bool ok = true;
+  T cpv[NMAX], dpv[NMAX];
+  T hprev = xv[1] - xv[0];
+  T ddprev = (yv[1] - yv[0]) / hprev;
+  if (bc & 1) {
+    const T s = yp1[c];
+    ok = ok && finite(s);
+    cpv[0] = T(0.5);
+    dpv[0] = T(3) * (ddprev - s) / hprev;
+  } else {
+    cpv[0] = T(0);
+    dpv[0] = T(0);
+  }
+  T cpp = cpv[0], dpp = dpv[0];
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) {
+    if (j < n) {
+      ok = ok && finite(xv[j]) && finite(yv[j]);
+      if (j + 1 < n) ok = ok && (xv[j + 1] > xv[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 1; j < NMAX - 1; ++j) {
+    if (j < n - 1) {
+      const T h = xv[j + 1] - xv[j];
+      const T dd = (yv[j + 1] - yv[j]) / h;
+      const T inv = T(1) / (T(2) * (hprev + h) - hprev * cpv[j - 1]);
+      dpv[j] = (T(6) * (dd - ddprev) - hprev * dpv[j - 1]) * inv;
+      cpv[j] = h * inv;
+      cpp = cpv[j];
+      dpp = dpv[j];
+      hprev = h;
+      ddprev = dd;
+    }
+  }
+  T z[NMAX];
+  T last = T(0);
+  if (bc & 2) {
+    const T e = ypn[c];
+    ok = ok && finite(e);
+    last = (T(6) * (e - ddprev) - hprev * dpp) / (T(2) * hprev - hprev * cpp);
+  }
+  T nxt = last;
+#pragma unroll
+  for (int j = NMAX - 1; j >= 0; --j) {
+    if (j == n - 1) {
+      z[j] = last;
+    } else if (j < n - 1) {
+      nxt = dpv[j] - cpv[j] * nxt;
+      z[j] = nxt;
+    } else {
+      z[j] = T(0);
+    }
+  }
+  if (!ok) {
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) z[j] = qnan<T>();
+  }
+  raise_status_warp(!ok, kBadKnots);
+  T *zc = y2 + c * n;
+  if (vec) {
+    using VT = typename Vec16<T>::V;
+#pragma unroll
+    for (int j = 0; j < NMAX; j += VW) {
+      if (j < n) {
+        VT a;
+#pragma unroll
+        for (int i = 0; i < VW; ++i) reinterpret_cast<T *>(&a)[i] = z[j + i];
+        *reinterpret_cast<VT *>(zc + j) = a;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j)
+      if (j < n) zc[j] = z[j];
   }
 }
 

@@ -111,6 +111,30 @@ template <typename T> __device__ __forceinline__ int bucket_of(T v, T x0, T s, i
   return (f >= T(0)) ? min((int)f, nb) : 0;  // (int) truncates; f >= 0 here
 }
 
+// Branch-free bisection over Xs[0 .. 2^L2) (largest j with Xs[j] <= q, Xs[0] <= q):
+// fully unrolled, 4 instructions per step (address, LDS, compare, select).
+template <typename T, int L2> __device__ __forceinline__ int bisect_pow2(const T *Xs, T q) {
+  int lo = 0;
+#pragma unroll
+  for (int t = L2 - 1; t >= 0; --t) lo = (Xs[lo + (1 << t)] <= q) ? lo + (1 << t) : lo;
+  return lo;
+}
+
+template <typename T> __device__ __forceinline__ int bisect_padded(const T *Xs, int l2, T q) {
+  switch (l2) {  // warp-uniform
+    case 0: return 0;
+    case 1: return bisect_pow2<T, 1>(Xs, q);
+    case 2: return bisect_pow2<T, 2>(Xs, q);
+    case 3: return bisect_pow2<T, 3>(Xs, q);
+    case 4: return bisect_pow2<T, 4>(Xs, q);
+    case 5: return bisect_pow2<T, 5>(Xs, q);
+    case 6: return bisect_pow2<T, 6>(Xs, q);
+    case 7: return bisect_pow2<T, 7>(Xs, q);
+    case 8: return bisect_pow2<T, 8>(Xs, q);
+    default: return bisect_pow2<T, 9>(Xs, q);
+  }
+}
+
 // Locate + evaluate one query against a packed curve.  Branch-light: out-of-range / NaN
 // queries run the same path on a clamped stand-in and are masked at the end.
 template <typename T, int MODE>
@@ -120,9 +144,7 @@ __device__ __forceinline__ void eval_packed(const Knot<T> *K, const T *Xs, int P
   const T qc = in ? q : hd.x0;
   int lo;
   if (MODE == MODE_BISECT) {
-    lo = 0;
-    for (int step = P >> 1; step > 0; step >>= 1) lo = (Xs[lo + step] <= qc) ? lo + step : lo;
-    lo = min(lo, n - 2);
+    lo = min(bisect_padded(Xs, P, qc), n - 2);  // P carries log2 of the padded length here
   } else {
     int hi;
     if (MODE == MODE_TABLE) {
@@ -214,6 +236,7 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3)
   T *Xs = reinterpret_cast<T *>(smem_raw + L.xs);
   uint16_t *Tb = reinterpret_cast<uint16_t *>(smem_raw + L.table);
   const int P = L.P;
+  const int l2P = 31 - __clz(P);
   const int nb = kBucketsPerKnot * n;
   const int64_t G = gridDim.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -353,7 +376,7 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3)
             const T *Xc = Xs + (size_t)cl * P;
             const uint16_t *Tc = Tb + cl * (nb + 2);
 #pragma unroll
-            for (int i = 0; i < V; ++i) eval_packed<T, MODE>(Kc, Xc, P, Tc, hd, n, nb, qa[u][i], val[i], jj[i]);
+            for (int i = 0; i < V; ++i) eval_packed<T, MODE>(Kc, Xc, l2P, Tc, hd, n, nb, qa[u][i], val[i], jj[i]);
           } else {
 #pragma unroll
             for (int i = 0; i < V; ++i) eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qa[u][i], val[i], jj[i]);

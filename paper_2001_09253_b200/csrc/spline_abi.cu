@@ -41,6 +41,7 @@ template <typename K> int set_smem(K kernel, size_t bytes) {
 }
 
 inline int launch_rc() { return cuda_rc(cudaGetLastError()); }
+inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 // ------------------------------------------------------------------------ build
 
@@ -136,16 +137,25 @@ int build_long(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T
 template <typename T>
 int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
             cudaStream_t st) {
-  if (n <= kK1MaxN) {
+  if (n <= 16) {  // K1r: registers only
+    constexpr int VW = 16 / sizeof(T);
+    const int vec = (n % VW == 0) && aligned16(x) && aligned16(y) && aligned16(y2);
+    const int64_t grid = (batch + 255) / 256;
+    if (n <= 8)
+      k1_thomas_regs<T, 8><<<(unsigned)grid, 256, 0, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, vec);
+    else
+      k1_thomas_regs<T, 16><<<(unsigned)grid, 256, 0, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, vec);
+    return launch_rc();
+  }
+  if (n <= kK1MaxN) {  // K1: two threads per curve, staged odd-stride tiles
     const int S = (int)(n | 1);
-    int cpb = 64;
-    if ((size_t)2 * cpb * S * sizeof(T) > 64 * 1024) cpb = 32;
+    int cpb = 128;
+    while (cpb > 16 && (size_t)2 * cpb * S * sizeof(T) > 100 * 1024) cpb -= 16;
     const size_t sm = (size_t)2 * cpb * S * sizeof(T);
-    auto kern = k1_thomas_batched<T>;
+    auto kern = k1_thomas_babe<T>;
     if (int rc = set_smem(kern, sm)) return rc;
     const int64_t grid = (batch + cpb - 1) / cpb;
-    kern<<<(unsigned)grid, kK1Threads, sm, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, S, cpb,
-                                                 FastDiv((uint32_t)n));
+    kern<<<(unsigned)grid, 2 * cpb, sm, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, S, FastDiv((uint32_t)n));
     return launch_rc();
   }
   if (n <= 256 * rmax<T>()) return build_mid<T>(x, y, n, batch, bc, yp1, ypn, y2, st);
@@ -179,7 +189,6 @@ int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
   return launch_rc();
 }
 
-inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 constexpr size_t kSmemCap = 220 * 1024;   // per-CTA dynamic shared memory we allow ourselves
 constexpr size_t kItemSmem = 48 * 1024;   // target per-CTA footprint for multi-curve items
