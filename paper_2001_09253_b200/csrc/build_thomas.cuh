@@ -25,49 +25,11 @@ namespace fs {
 
 constexpr int kK1Threads = 256;
 
+// The two-ended sweep of one CTA tile: curve t = threadIdx.x/2 of the tile lives at
+// Xc = X + t*S, Yc = Y + t*S (odd stride S); on return Yc holds y2 (or NaN).
 template <typename T>
-__global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict__ x, const T *__restrict__ y, int n,
-                                                             int64_t batch, int bc, const T *__restrict__ yp1,
-                                                             const T *__restrict__ ypn, T *__restrict__ y2, int S,
-                                                             FastDiv divn) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int CPB = blockDim.x / 2;  // blockDim = 2 x curves per CTA (<= 256)
-  T *X = reinterpret_cast<T *>(smem_raw);
-  T *Y = X + (size_t)CPB * S;
-
-  const int64_t c0 = (int64_t)blockIdx.x * CPB;
-  const int nc = (int)min64(CPB, batch - c0);
-  const int tot = nc * n;
-  const T *xb = x + c0 * n;
-  const T *yb = y + c0 * n;
-
-  // Stage: flat coalesced loads (UL per array per thread in flight), scattered into the
-  // odd-stride tiles.
-  constexpr int UL = sizeof(T) == 4 ? 16 : 8;
-  const int NT = blockDim.x;
-  for (int base = threadIdx.x; base < tot; base += UL * NT) {
-    T vx[UL], vy[UL];
-#pragma unroll
-    for (int u = 0; u < UL; ++u) {
-      const int e = base + u * NT;
-      if (e < tot) {
-        vx[u] = ld_stream(xb + e);
-        vy[u] = ld_stream(yb + e);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < UL; ++u) {
-      const int e = base + u * NT;
-      if (e < tot) {
-        const int c = (int)divn.div((uint32_t)e);
-        const int j = e - c * n;
-        X[c * S + j] = vx[u];
-        Y[c * S + j] = vy[u];
-      }
-    }
-  }
-  __syncthreads();
-
+__device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int64_t c0, int bc,
+                                          const T *__restrict__ yp1, const T *__restrict__ ypn) {
   const int t = threadIdx.x >> 1;       // curve within the CTA
   const bool top = (threadIdx.x & 1) == 0;
   const bool act = t < nc;              // pairs are lane-adjacent, so shuffles stay in-warp
@@ -189,6 +151,53 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict
     }
   }
   raise_status_warp(act && !ok && top, kBadKnots);
+
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict__ x, const T *__restrict__ y, int n,
+                                                             int64_t batch, int bc, const T *__restrict__ yp1,
+                                                             const T *__restrict__ ypn, T *__restrict__ y2, int S,
+                                                             FastDiv divn) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int CPB = blockDim.x / 2;  // blockDim = 2 x curves per CTA (<= 256)
+  T *X = reinterpret_cast<T *>(smem_raw);
+  T *Y = X + (size_t)CPB * S;
+
+  const int64_t c0 = (int64_t)blockIdx.x * CPB;
+  const int nc = (int)min64(CPB, batch - c0);
+  const int tot = nc * n;
+  const T *xb = x + c0 * n;
+  const T *yb = y + c0 * n;
+
+  // Stage: flat coalesced loads (UL per array per thread in flight), scattered into the
+  // odd-stride tiles.
+  constexpr int UL = sizeof(T) == 4 ? 16 : 8;
+  const int NT = blockDim.x;
+  for (int base = threadIdx.x; base < tot; base += UL * NT) {
+    T vx[UL], vy[UL];
+#pragma unroll
+    for (int u = 0; u < UL; ++u) {
+      const int e = base + u * NT;
+      if (e < tot) {
+        vx[u] = ld_stream(xb + e);
+        vy[u] = ld_stream(yb + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UL; ++u) {
+      const int e = base + u * NT;
+      if (e < tot) {
+        const int c = (int)divn.div((uint32_t)e);
+        const int j = e - c * n;
+        X[c * S + j] = vx[u];
+        Y[c * S + j] = vy[u];
+      }
+    }
+  }
+  __syncthreads();
+
+  babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn);
   __syncthreads();
 
   T *y2b = y2 + c0 * n;
@@ -196,6 +205,65 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict
     const int c = (int)divn.div((uint32_t)e);
     const int j = e - c * n;
     y2b[e] = Y[c * S + j];
+  }
+}
+
+
+// K1 pipelined: persistent CTAs.  One raw stage receives a tile's x, y by TMA bulk copy;
+// it is transposed into the odd-stride tiles at once, and the next tile's copy is issued
+// into it before the sweep starts, so the load of tile i+1 overlaps the sweep and the
+// stores of tile i.  Requires n*sizeof(T) % 16 == 0 and 16-byte aligned x, y (else
+// k1_thomas_babe).
+template <typename T>
+__global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(const T *__restrict__ x, const T *__restrict__ y, int n,
+                                                             int64_t batch, int bc, const T *__restrict__ yp1,
+                                                             const T *__restrict__ ypn, T *__restrict__ y2, int S,
+                                                             int64_t ntiles, FastDiv divn) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int CPB = blockDim.x / 2;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
+  T *Xr = reinterpret_cast<T *>(smem_raw + 16);
+  T *Yr = Xr + (size_t)CPB * n;
+  T *X = reinterpret_cast<T *>(smem_raw + 16 + ((2 * (size_t)CPB * n * sizeof(T) + 15) & ~(size_t)15));
+  T *Y = X + (size_t)CPB * S;
+  const int64_t G = gridDim.x;
+  auto issue = [&](int64_t it) {  // thread 0 only
+    if (it >= ntiles) return;
+    const int64_t c0 = it * CPB;
+    const int nc = (int)min64(CPB, batch - c0);
+    const uint32_t bytes = (uint32_t)((size_t)nc * n * sizeof(T));
+    mbar_expect_tx(bar, 2 * bytes);
+    bulk_g2s(Xr, x + c0 * n, bytes, bar);
+    bulk_g2s(Yr, y + c0 * n, bytes, bar);
+  };
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();
+  int64_t it = blockIdx.x;
+  if (threadIdx.x == 0) issue(it);
+  uint32_t phase = 0u;
+  for (; it < ntiles; it += G) {
+    const int64_t c0 = it * CPB;
+    const int nc = (int)min64(CPB, batch - c0);
+    const int tot = nc * n;
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {  // to the odd-stride tiles
+      const int c = (int)divn.div((uint32_t)e);
+      const int j = e - c * n;
+      X[c * S + j] = Xr[e];
+      Y[c * S + j] = Yr[e];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) issue(it + G);  // raw stage consumed: next tile in flight
+    babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn);
+    __syncthreads();
+    T *y2b = y2 + c0 * n;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int c = (int)divn.div((uint32_t)e);
+      const int j = e - c * n;
+      y2b[e] = Y[c * S + j];
+    }
+    __syncthreads();
   }
 }
 

@@ -113,10 +113,14 @@ template <typename T> __device__ __forceinline__ int bucket_of(T v, T x0, T s, i
 
 // Branch-free bisection over Xs[0 .. 2^L2) (largest j with Xs[j] <= q, Xs[0] <= q):
 // fully unrolled, 4 instructions per step (address, LDS, compare, select).
+// Xs is stored with one pad word per 32 entries (entry i at i + i/32) so that the probes of
+// one step (and the two halves of the curve) fall in distinct shared-memory banks.
+__host__ __device__ __forceinline__ int xs_slot(int i) { return i + (i >> 5); }
+
 template <typename T, int L2> __device__ __forceinline__ int bisect_pow2(const T *Xs, T q) {
   int lo = 0;
 #pragma unroll
-  for (int t = L2 - 1; t >= 0; --t) lo = (Xs[lo + (1 << t)] <= q) ? lo + (1 << t) : lo;
+  for (int t = L2 - 1; t >= 0; --t) lo = (Xs[xs_slot(lo + (1 << t))] <= q) ? lo + (1 << t) : lo;
   return lo;
 }
 
@@ -203,7 +207,7 @@ template <typename T> struct StageLayout {
     hdr = off;
     if (packed) off = align16(off + sizeof(CurveHdr<T>) * (size_t)cpb);
     xs = off;
-    if (mode == MODE_BISECT) off = align16(off + sizeof(T) * (size_t)cpb * P);
+    if (mode == MODE_BISECT) off = align16(off + sizeof(T) * (size_t)cpb * xs_slot(P));
     table = off;
     if (mode == MODE_TABLE) off = align16(off + sizeof(uint16_t) * (size_t)cpb * (kBucketsPerKnot * n + 2));
     total = off;
@@ -330,9 +334,9 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3)
         kk.ih = (j < n - 1) ? r_rcp(r_sub(X[e + 1], xj)) : T(0);
         K[e] = kk;
         if (MODE == MODE_BISECT) {
-          T *Xc = Xs + (size_t)c * P;
-          if (j < P) Xc[j] = xj;
-          for (int jj = n + j; jj < P; jj += n) Xc[jj] = (T)INFINITY;  // pad [n, P) with +inf
+          T *Xc = Xs + (size_t)c * xs_slot(P);
+          if (j < P) Xc[xs_slot(j)] = xj;
+          for (int jj = n + j; jj < P; jj += n) Xc[xs_slot(jj)] = (T)INFINITY;  // pad [n, P) with +inf
         }
         if (j == 0 || (MODE == MODE_TABLE && j < n - 1)) {
           const T x0 = X[c * n], xn = X[c * n + n - 1];
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3)
           if (PACKED) {
             const CurveHdr<T> hd = Hd[cl];
             const Knot<T> *Kc = K + cl * n;
-            const T *Xc = Xs + (size_t)cl * P;
+            const T *Xc = Xs + (size_t)cl * xs_slot(P);
             const uint16_t *Tc = Tb + cl * (nb + 2);
 #pragma unroll
             for (int i = 0; i < V; ++i) eval_packed<T, MODE>(Kc, Xc, l2P, Tc, hd, n, nb, qa[u][i], val[i], jj[i]);

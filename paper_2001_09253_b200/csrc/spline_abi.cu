@@ -42,6 +42,17 @@ template <typename K> int set_smem(K kernel, size_t bytes) {
 
 inline int launch_rc() { return cuda_rc(cudaGetLastError()); }
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+inline int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+
 
 // ------------------------------------------------------------------------ build
 
@@ -149,6 +160,24 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
   }
   if (n <= kK1MaxN) {  // K1: two threads per curve, staged odd-stride tiles
     const int S = (int)(n | 1);
+    if ((n * sizeof(T)) % 16 == 0 && aligned16(x) && aligned16(y)) {
+      // persistent + TMA-pipelined; CPB curves per tile (2 threads each)
+      int cpb = 64;
+      const auto smem_of = [&](int c) {
+        return 16 + ((2 * (size_t)c * n * sizeof(T) + 15) & ~(size_t)15) + 2 * (size_t)c * S * sizeof(T);
+      };
+      while (cpb > 16 && smem_of(cpb) > 64 * 1024) cpb -= 16;
+      const size_t sm = smem_of(cpb);
+      auto kern = k1_thomas_pipe<T>;
+      if (int rc = set_smem(kern, sm)) return rc;
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 2 * cpb, sm) != cudaSuccess || occ < 1) occ = 1;
+      const int64_t ntiles = (batch + cpb - 1) / cpb;
+      const int64_t grid = std::min<int64_t>(ntiles, (int64_t)occ * num_sms());
+      kern<<<(unsigned)grid, 2 * cpb, sm, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, S, ntiles,
+                                                 FastDiv((uint32_t)n));
+      return launch_rc();
+    }
     int cpb = 128;
     while (cpb > 16 && (size_t)2 * cpb * S * sizeof(T) > 100 * 1024) cpb -= 16;
     const size_t sm = (size_t)2 * cpb * S * sizeof(T);
@@ -163,16 +192,6 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
 }
 
 // ------------------------------------------------------------------------- eval
-
-inline int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-  }
-  return sms;
-}
 
 template <typename T, int MODE, int V, bool BULK>
 int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,

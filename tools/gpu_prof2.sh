@@ -4,6 +4,6 @@ for C in $1; do
   python tools/prof.py $C 2 > gpurun_out/prof_plain_$C.log 2>&1 || { echo "plain run failed $C"; cat gpurun_out/prof_plain_$C.log; exit 1; }
 done
 for C in $1; do
-  ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 -o gpurun_out/prof_cfg${C}_$2 -f python tools/prof.py $C 2 > gpurun_out/ncu_cfg$C.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:$2 -s 2 -c 2 -o gpurun_out/prof_cfg${C} -f python tools/prof.py $C 2 > gpurun_out/ncu_cfg$C.log 2>&1
   echo "ncu $C rc=$?"
 done
