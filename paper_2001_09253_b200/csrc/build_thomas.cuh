@@ -27,131 +27,96 @@ constexpr int kK1Threads = 256;
 
 // The two-ended sweep of one CTA tile: curve t = threadIdx.x/2 of the tile lives at
 // Xc = X + t*S, Yc = Y + t*S (odd stride S); on return Yc holds y2 (or NaN).
+// Both threads of a pair run the SAME instruction stream with a direction dir = +1 (top:
+// rows 0, 1, .., k-1) or -1 (bottom: rows n-1, n-2, .., k+1), so a warp never diverges:
+//   g_i  = (y_{j+dir} - y_j) / (x_{j+dir} - x_j)      (the divided difference of the step)
+//   h_i  = dir (x_{j+dir} - x_j) > 0
+//   row  : den = 2(h_c + h) - h_c c'_prev,  c' = h/den,  d' = (6 dir (g - g_c) - h_c d'_prev)/den
+// where (h_c, g_c) belong to the interval already eliminated.  For dir = +1 this is the
+// paper's forward sweep verbatim; for dir = -1 it is the same recurrence read
+// from the other end.  Divisions are a correctly rounded reciprocal then a multiply.
 template <typename T>
 __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int64_t c0, int bc,
                                           const T *__restrict__ yp1, const T *__restrict__ ypn) {
-  const int t = threadIdx.x >> 1;       // curve within the CTA
+  const int t = threadIdx.x >> 1;  // curve within the CTA
   const bool top = (threadIdx.x & 1) == 0;
-  const bool act = t < nc;              // pairs are lane-adjacent, so shuffles stay in-warp
-  const int k = n >> 1;                 // meeting row, 1 <= k <= n-2
+  const bool act = t < nc;         // pairs are lane-adjacent, so shuffles stay in-warp
+  const int k = n >> 1;            // meeting row, 1 <= k <= n-2
+  const int dir = top ? 1 : -1;
+  const int j0 = top ? 0 : n - 1;
+  const int nsteps = top ? k - 1 : n - 2 - k;  // interior rows on this side
   T *Xc = X + (act ? t : 0) * S;
   T *Yc = Y + (act ? t : 0) * S;
-  const int64_t cg = c0 + t;
-  bool ok = true;
-  T hb = T(0), ddb = T(0), cpb = T(0), dpb = T(0);  // this side's values at the seam
+  const int64_t cg = c0 + (act ? t : 0);
+  // end row
+  T xo = Xc[j0], yo = Yc[j0];
+  T xn = Xc[j0 + dir], yn = Yc[j0 + dir];
+  bool ok = finite(xo) && finite(yo) && finite(xn) && finite(yn) && (T(dir) * (xn - xo) > T(0));
+  T hc = T(dir) * (xn - xo);
+  T gc = (yn - yo) * r_rcp(xn - xo);
+  const bool clamped = top ? (bc & 1) : (bc & 2);
+  T cp = T(0), dp = T(0);
+  if (clamped) {  // P:966-971 (start) / P:1017-1018 (end): c' = 1/2, d' = 3 dir (g - y') / h
+    const T sl = top ? yp1[cg] : ypn[cg];
+    ok = ok && finite(sl);
+    cp = T(0.5);
+    dp = T(3 * dir) * (gc - sl) * r_rcp(hc);
+  }
   if (act) {
-    if (top) {
-      // rows 0 .. k-1, downward
-      T xo = Xc[0], yo = Yc[0];
-      T xn = Xc[1], yn = Yc[1];
-      ok = finite(xo) && finite(yo) && finite(xn) && finite(yn) && (xn > xo);
-      T hprev = xn - xo;
-      T ddprev = (yn - yo) / hprev;
-      T cp, dp;
-      if (bc & 1) {  // clamped start: c'_0 = 1/2, d'_0 = 3 (dd_0 - y'_0) / h_0
-        const T s = yp1[cg];
-        ok = ok && finite(s);
-        cp = T(0.5);
-        dp = T(3) * (ddprev - s) / hprev;
-      } else {  // natural start
-        cp = T(0);
-        dp = T(0);
-      }
-      Xc[0] = cp;
-      Yc[0] = dp;
-      for (int j = 1; j < k; ++j) {
-        xo = xn;
-        yo = yn;
-        xn = Xc[j + 1];
-        yn = Yc[j + 1];
-        ok = ok && (xn > xo) && finite(xn) && finite(yn);
-        const T h = xn - xo;
-        const T dd = (yn - yo) / h;
-        const T inv = T(1) / (T(2) * (hprev + h) - hprev * cp);
-        dp = (T(6) * (dd - ddprev) - hprev * dp) * inv;
-        cp = h * inv;
+    Xc[j0] = cp;
+    Yc[j0] = dp;
+  }
+  int j = j0 + dir;
+  const int maxsteps = k - 1;  // >= nsteps on both sides: the bottom idles one step when n is even
+  for (int i = 0; i < maxsteps; ++i) {
+    if (i < nsteps) {
+      xo = xn;
+      yo = yn;
+      xn = Xc[j + dir];
+      yn = Yc[j + dir];
+      ok = ok && finite(xn) && finite(yn) && (T(dir) * (xn - xo) > T(0));
+      const T h = T(dir) * (xn - xo);
+      const T g = (yn - yo) * r_rcp(xn - xo);
+      const T inv = r_rcp(T(2) * (hc + h) - hc * cp);
+      dp = (T(6 * dir) * (g - gc) - hc * dp) * inv;
+      cp = h * inv;
+      if (act) {
         Xc[j] = cp;
         Yc[j] = dp;
-        hprev = h;
-        ddprev = dd;
       }
-      hb = hprev;  // h_{k-1}
-      ddb = ddprev;
-      cpb = cp;    // c'_{k-1}
-      dpb = dp;    // d'_{k-1}
-    } else {
-      // rows n-1 .. k+1, upward: y2_j = d''_j - a''_j y2_{j-1}
-      T xo = Xc[n - 1], yo = Yc[n - 1];
-      T xn = Xc[n - 2], yn = Yc[n - 2];
-      ok = finite(xo) && finite(yo) && finite(xn) && finite(yn) && (xo > xn);
-      T hnext = xo - xn;            // h_{n-2}
-      T ddnext = (yo - yn) / hnext; // dd_{n-2}
-      T ap, dp;
-      if (bc & 2) {  // clamped end: a = h, b = 2h, d = 6 (y'_{n-1} - dd_{n-2})
-        const T e = ypn[cg];
-        ok = ok && finite(e);
-        ap = T(0.5);
-        dp = T(3) * (e - ddnext) / hnext;
-      } else {  // natural end
-        ap = T(0);
-        dp = T(0);
-      }
-      Xc[n - 1] = ap;
-      Yc[n - 1] = dp;
-      for (int j = n - 2; j > k; --j) {
-        xo = xn;
-        yo = yn;
-        xn = Xc[j - 1];
-        yn = Yc[j - 1];
-        ok = ok && (xo > xn) && finite(xn) && finite(yn);
-        const T h = xo - xn;          // h_{j-1}
-        const T dd = (yo - yn) / h;   // dd_{j-1}
-        // row j: a = h_{j-1}, b = 2(h_{j-1} + h_j), c = h_j, d = 6(dd_j - dd_{j-1})
-        const T inv = T(1) / (T(2) * (h + hnext) - hnext * ap);
-        dp = (T(6) * (ddnext - dd) - hnext * dp) * inv;
-        ap = h * inv;
-        Xc[j] = ap;
-        Yc[j] = dp;
-        hnext = h;
-        ddnext = dd;
-      }
-      hb = hnext;   // h_k
-      ddb = ddnext; // dd_k
-      cpb = ap;     // a''_{k+1}
-      dpb = dp;     // d''_{k+1}
+      hc = h;
+      gc = g;
+      j += dir;
     }
   }
   // meet at row k: a_k = h_{k-1}, b_k = 2(h_{k-1} + h_k), c_k = h_k, d_k = 6(dd_k - dd_{k-1})
-  const T o_h = __shfl_xor_sync(0xffffffffu, hb, 1);
-  const T o_dd = __shfl_xor_sync(0xffffffffu, ddb, 1);
-  const T o_cp = __shfl_xor_sync(0xffffffffu, cpb, 1);
-  const T o_dp = __shfl_xor_sync(0xffffffffu, dpb, 1);
-  const bool o_ok = __shfl_xor_sync(0xffffffffu, ok, 1);
+  const T o_h = __shfl_xor_sync(0xffffffffu, hc, 1);
+  const T o_g = __shfl_xor_sync(0xffffffffu, gc, 1);
+  const T o_cp = __shfl_xor_sync(0xffffffffu, cp, 1);
+  const T o_dp = __shfl_xor_sync(0xffffffffu, dp, 1);
+  ok = ok && __shfl_xor_sync(0xffffffffu, (int)ok, 1);
+  const T hk1 = top ? hc : o_h, gk1 = top ? gc : o_g, cT = top ? cp : o_cp, dT = top ? dp : o_dp;
+  const T hk = top ? o_h : hc, gk = top ? o_g : gc, aB = top ? o_cp : cp, dB = top ? o_dp : dp;
+  const T yk = (T(6) * (gk - gk1) - hk1 * dT - hk * dB) / (T(2) * (hk1 + hk) - hk1 * cT - hk * aB);
   if (act) {
-    ok = ok && o_ok;
-    const T hk1 = top ? hb : o_h, ddk1 = top ? ddb : o_dd, cT = top ? cpb : o_cp, dT = top ? dpb : o_dp;
-    const T hk = top ? o_h : hb, ddk = top ? o_dd : ddb, aB = top ? o_cp : cpb, dB = top ? o_dp : dpb;
-    const T yk = (T(6) * (ddk - ddk1) - hk1 * dT - hk * dB) / (T(2) * (hk1 + hk) - hk1 * cT - hk * aB);
+    if (top) Yc[k] = yk;
+    // back-substitution outward from the seam: y_j = d'_j - c'_j y_{j+dir}
     T yv = yk;
-    if (top) {
-      Yc[k] = yk;
-      for (int j = k - 1; j >= 0; --j) {
-        yv = Yc[j] - Xc[j] * yv;
-        Yc[j] = yv;
-      }
-    } else {
-      for (int j = k + 1; j < n; ++j) {
-        yv = Yc[j] - Xc[j] * yv;
-        Yc[j] = yv;
+    int jj = k - dir;
+    const int cnt = top ? k : n - 1 - k;
+    for (int i = 0; i < k; ++i) {
+      if (i < cnt) {
+        yv = Yc[jj] - Xc[jj] * yv;
+        Yc[jj] = yv;
+        jj -= dir;
       }
     }
     if (!ok) {  // both threads of the pair see the same ok
       const T nanv = qnan<T>();
-      for (int j = top ? 0 : k + 1; j < (top ? k + 1 : n); ++j) Yc[j] = nanv;
+      for (int r = top ? 0 : k + 1; r < (top ? k + 1 : n); ++r) Yc[r] = nanv;
     }
   }
   raise_status_warp(act && !ok && top, kBadKnots);
-
 }
 
 template <typename T>
