@@ -94,7 +94,8 @@ __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int6
   const T o_g = __shfl_xor_sync(0xffffffffu, gc, 1);
   const T o_cp = __shfl_xor_sync(0xffffffffu, cp, 1);
   const T o_dp = __shfl_xor_sync(0xffffffffu, dp, 1);
-  ok = ok && __shfl_xor_sync(0xffffffffu, (int)ok, 1);
+  const int o_ok = __shfl_xor_sync(0xffffffffu, (int)ok, 1);  // unconditional: every lane joins
+  ok = ok && o_ok;
   const T hk1 = top ? hc : o_h, gk1 = top ? gc : o_g, cT = top ? cp : o_cp, dT = top ? dp : o_dp;
   const T hk = top ? o_h : hc, gk = top ? o_g : gc, aB = top ? o_cp : cp, dB = top ? o_dp : dp;
   const T yk = (T(6) * (gk - gk1) - hk1 * dT - hk * dB) / (T(2) * (hk1 + hk) - hk1 * cT - hk * aB);

@@ -161,3 +161,25 @@ def test_linear_and_cubic_closed_forms_gpu(api):
         y2 = api.build(parity.to_dev(xx), parity.to_dev(f(xx)), 3, fp(-2.0), fp(2.0)).cpu().numpy()
         # conditioning: rounding of dd_j is amplified by 1/h^2 (the oracle has the same error)
         assert np.max(np.abs(y2 - (1 + 1.5 * xx))) <= 1e-14 * 4 * (n / 4.0) ** 2
+
+
+@pytest.mark.parametrize("cid,kw", [(2, dict(batch=40000, m=64)), (2, dict(batch=40000, m=256)),
+                                    (3, dict(batch=300000, m=8)), (4, dict(batch=700, n=64, m=512))])
+def test_persistent_multi_item(api, cid, kw):
+    """Enough curves that every persistent CTA (K1 pipeline, staged eval) runs several items."""
+    parity.check_case(api, workloads.generate(cid, **kw))
+
+
+def test_bad_knots_in_multi_tile_pipeline(api):
+    rng = np.random.default_rng(77)
+    B, n = 30000, 64
+    x = np.cumsum(rng.uniform(0.5, 1.5, (B, n)), axis=1).astype(np.float32)
+    y = rng.normal(size=(B, n)).astype(np.float32)
+    bad = rng.choice(B, 50, replace=False)
+    x[bad, 10] = x[bad, 9]
+    api.status()
+    y2 = api.build(parity.to_dev(x), parity.to_dev(y), 0).cpu().numpy()
+    assert api.status() & api.STATUS_BAD_KNOTS
+    assert np.all(np.isnan(y2[bad]))
+    good = np.setdiff1d(np.arange(B), bad)
+    assert np.all(np.isfinite(y2[good]))
