@@ -37,85 +37,85 @@ constexpr int kK1Threads = 256;
 // from the other end.  Divisions are a correctly rounded reciprocal then a multiply.
 template <typename T>
 __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int64_t c0, int bc,
-                                          const T *__restrict__ yp1, const T *__restrict__ ypn) {
+                                          const T *__restrict__ yp1, const T *__restrict__ ypn, T *dummy) {
   const int t = threadIdx.x >> 1;  // curve within the CTA
   const bool top = (threadIdx.x & 1) == 0;
   const bool act = t < nc;         // pairs are lane-adjacent, so shuffles stay in-warp
   const int k = n >> 1;            // meeting row, 1 <= k <= n-2
   const int dir = top ? 1 : -1;
   const int j0 = top ? 0 : n - 1;
-  const int nsteps = top ? k - 1 : n - 2 - k;  // interior rows on this side
-  T *Xc = X + (act ? t : 0) * S;
-  T *Yc = Y + (act ? t : 0) * S;
+  // inactive pairs (ragged last tile) run on a private scratch row, so no store is predicated
+  T *Xc = act ? X + t * S : dummy;
+  T *Yc = act ? Y + t * S : dummy + S;
+  if (!act) {
+    Xc[j0] = T(j0);
+    Xc[j0 + dir] = T(j0 + dir);
+  }
   const int64_t cg = c0 + (act ? t : 0);
   // end row
   T xo = Xc[j0], yo = Yc[j0];
   T xn = Xc[j0 + dir], yn = Yc[j0 + dir];
-  bool ok = finite(xo) && finite(yo) && finite(xn) && finite(yn) && (T(dir) * (xn - xo) > T(0));
+  bool ok = finite(xo) & finite(yo) & finite(xn) & finite(yn) & (T(dir) * (xn - xo) > T(0));
   T hc = T(dir) * (xn - xo);
-  T gc = (yn - yo) * r_rcp(xn - xo);
+  T gc = (yn - yo) * nr_rcp(xn - xo);
   const bool clamped = top ? (bc & 1) : (bc & 2);
   T cp = T(0), dp = T(0);
   if (clamped) {  // P:966-971 (start) / P:1017-1018 (end): c' = 1/2, d' = 3 dir (g - y') / h
     const T sl = top ? yp1[cg] : ypn[cg];
-    ok = ok && finite(sl);
+    ok &= finite(sl);
     cp = T(0.5);
-    dp = T(3 * dir) * (gc - sl) * r_rcp(hc);
+    dp = T(3 * dir) * (gc - sl) * nr_rcp(hc);
   }
-  if (act) {
-    Xc[j0] = cp;
-    Yc[j0] = dp;
-  }
+  Xc[j0] = cp;
+  Yc[j0] = dp;
   int j = j0 + dir;
-  const int maxsteps = k - 1;  // >= nsteps on both sides: the bottom idles one step when n is even
-  for (int i = 0; i < maxsteps; ++i) {
-    if (i < nsteps) {
-      xo = xn;
-      yo = yn;
-      xn = Xc[j + dir];
-      yn = Yc[j + dir];
-      ok = ok && finite(xn) && finite(yn) && (T(dir) * (xn - xo) > T(0));
-      const T h = T(dir) * (xn - xo);
-      const T g = (yn - yo) * r_rcp(xn - xo);
-      const T inv = r_rcp(T(2) * (hc + h) - hc * cp);
-      dp = (T(6 * dir) * (g - gc) - hc * dp) * inv;
-      cp = h * inv;
-      if (act) {
-        Xc[j] = cp;
-        Yc[j] = dp;
-      }
-      hc = h;
-      gc = g;
-      j += dir;
-    }
-  }
+  auto step = [&]() {
+    xo = xn;
+    yo = yn;
+    xn = Xc[j + dir];
+    yn = Yc[j + dir];
+    const T h = T(dir) * (xn - xo);
+    ok &= finite(xn) & finite(yn) & (h > T(0));
+    const T g = (yn - yo) * nr_rcp(xn - xo);
+    const T inv = nr_rcp(T(2) * (hc + h) - hc * cp);
+    dp = (T(6 * dir) * (g - gc) - hc * dp) * inv;
+    cp = h * inv;
+    Xc[j] = cp;
+    Yc[j] = dp;
+    hc = h;
+    gc = g;
+    j += dir;
+  };
+  const int common = n - 2 - k;  // bottom's interior rows; the top has one more when n is even
+#pragma unroll 2
+  for (int i = 0; i < common; ++i) step();
+  if (top && (k - 1 > common)) step();
   // meet at row k: a_k = h_{k-1}, b_k = 2(h_{k-1} + h_k), c_k = h_k, d_k = 6(dd_k - dd_{k-1})
   const T o_h = __shfl_xor_sync(0xffffffffu, hc, 1);
   const T o_g = __shfl_xor_sync(0xffffffffu, gc, 1);
   const T o_cp = __shfl_xor_sync(0xffffffffu, cp, 1);
   const T o_dp = __shfl_xor_sync(0xffffffffu, dp, 1);
   const int o_ok = __shfl_xor_sync(0xffffffffu, (int)ok, 1);  // unconditional: every lane joins
-  ok = ok && o_ok;
+  ok = ok & (o_ok != 0);
   const T hk1 = top ? hc : o_h, gk1 = top ? gc : o_g, cT = top ? cp : o_cp, dT = top ? dp : o_dp;
   const T hk = top ? o_h : hc, gk = top ? o_g : gc, aB = top ? o_cp : cp, dB = top ? o_dp : dp;
-  const T yk = (T(6) * (gk - gk1) - hk1 * dT - hk * dB) / (T(2) * (hk1 + hk) - hk1 * cT - hk * aB);
-  if (act) {
-    if (top) Yc[k] = yk;
-    // back-substitution outward from the seam: y_j = d'_j - c'_j y_{j+dir}
-    T yv = yk;
-    int jj = k - dir;
-    const int cnt = top ? k : n - 1 - k;
-    for (int i = 0; i < k; ++i) {
-      if (i < cnt) {
-        yv = Yc[jj] - Xc[jj] * yv;
-        Yc[jj] = yv;
-        jj -= dir;
-      }
-    }
-    if (!ok) {  // both threads of the pair see the same ok
-      const T nanv = qnan<T>();
-      for (int r = top ? 0 : k + 1; r < (top ? k + 1 : n); ++r) Yc[r] = nanv;
-    }
+  const T yk = (T(6) * (gk - gk1) - hk1 * dT - hk * dB) * nr_rcp(T(2) * (hk1 + hk) - hk1 * cT - hk * aB);
+  if (top) Yc[k] = yk;
+  // back-substitution outward from the seam: y_j = d'_j - c'_j y_{j+dir}
+  T yv = yk;
+  int jj = k - dir;
+  auto back = [&]() {
+    yv = Yc[jj] - Xc[jj] * yv;
+    Yc[jj] = yv;
+    jj -= dir;
+  };
+  const int bcommon = n - 1 - k;  // bottom's count; the top has k (one more when n is even)
+#pragma unroll 2
+  for (int i = 0; i < bcommon; ++i) back();
+  if (top && (k > bcommon)) back();
+  if (!ok) {  // both threads of the pair see the same ok
+    const T nanv = qnan<T>();
+    for (int r = top ? 0 : k + 1; r < (top ? k + 1 : n); ++r) Yc[r] = nanv;
   }
   raise_status_warp(act && !ok && top, kBadKnots);
 }
@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict
   const int CPB = blockDim.x / 2;  // blockDim = 2 x curves per CTA (<= 256)
   T *X = reinterpret_cast<T *>(smem_raw);
   T *Y = X + (size_t)CPB * S;
+  T *dummy = Y + (size_t)CPB * S;  // 2S scratch for inactive pairs
 
   const int64_t c0 = (int64_t)blockIdx.x * CPB;
   const int nc = (int)min64(CPB, batch - c0);
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict
   }
   __syncthreads();
 
-  babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn);
+  babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn, dummy);
   __syncthreads();
 
   T *y2b = y2 + c0 * n;
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(const T *__restrict
   T *Yr = Xr + (size_t)CPB * n;
   T *X = reinterpret_cast<T *>(smem_raw + 16 + ((2 * (size_t)CPB * n * sizeof(T) + 15) & ~(size_t)15));
   T *Y = X + (size_t)CPB * S;
+  T *dummy = Y + (size_t)CPB * S;  // 2S scratch for inactive pairs
   const int64_t G = gridDim.x;
   auto issue = [&](int64_t it) {  // thread 0 only
     if (it >= ntiles) return;
@@ -213,21 +215,35 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(const T *__restrict
     const int tot = nc * n;
     mbar_wait(bar, phase);
     phase ^= 1u;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {  // to the odd-stride tiles
+    // to the odd-stride tiles: 16-byte reads of the raw stage (n*sizeof(T) % 16 == 0, so a
+    // vector never straddles two curves)
+    constexpr int VW = 16 / sizeof(T);
+    using VT = typename Vec16<T>::V;
+    for (int e = threadIdx.x * VW; e < tot; e += blockDim.x * VW) {
       const int c = (int)divn.div((uint32_t)e);
       const int j = e - c * n;
-      X[c * S + j] = Xr[e];
-      Y[c * S + j] = Yr[e];
+      const VT a = *reinterpret_cast<const VT *>(Xr + e);
+      const VT b = *reinterpret_cast<const VT *>(Yr + e);
+      T *xd = X + c * S + j, *yd = Y + c * S + j;
+#pragma unroll
+      for (int i = 0; i < VW; ++i) {
+        xd[i] = reinterpret_cast<const T *>(&a)[i];
+        yd[i] = reinterpret_cast<const T *>(&b)[i];
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) issue(it + G);  // raw stage consumed: next tile in flight
-    babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn);
+    babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn, dummy);
     __syncthreads();
     T *y2b = y2 + c0 * n;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    for (int e = threadIdx.x * VW; e < tot; e += blockDim.x * VW) {
       const int c = (int)divn.div((uint32_t)e);
       const int j = e - c * n;
-      y2b[e] = Y[c * S + j];
+      const T *ys = Y + c * S + j;
+      VT a;
+#pragma unroll
+      for (int i = 0; i < VW; ++i) reinterpret_cast<T *>(&a)[i] = ys[i];
+      *reinterpret_cast<VT *>(y2b + e) = a;
     }
     __syncthreads();
   }

@@ -59,6 +59,25 @@ __device__ __forceinline__ double r_fma(double a, double b, double c) { return _
 __device__ __forceinline__ float r_rcp(float a) { return __frcp_rn(a); }   // correctly rounded 1/a
 __device__ __forceinline__ double r_rcp(double a) { return __drcp_rn(a); }
 
+// Reciprocal for the solver sweeps: hardware approximation refined by Newton-Raphson
+// (fp32: one step; fp64: two steps after the 23-bit MUFU seed), |relative error| <= ~1 ulp
+// of the correctly rounded value, no special-case branch.  Only used on finite, normal,
+// nonzero arguments (interval widths and pivots of a strictly diagonally dominant system).
+__device__ __forceinline__ float nr_rcp(float a) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+  const float e = __fmaf_rn(-a, r, 1.0f);
+  return __fmaf_rn(r, e, r);
+}
+__device__ __forceinline__ double nr_rcp(double a) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = __fma_rn(-a, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-a, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
 // Eq. nr_formula on one interval, given ih = 1/h (the paper's inv_ba):
 //   A = (x1 - q) ih, B = (q - x0) ih,
 //   out = A y0 + B y1 + ((A^3 - A) y2_0 + (B^3 - B) y2_1) h^2 / 6.

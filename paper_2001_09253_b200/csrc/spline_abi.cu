@@ -164,7 +164,7 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
       // persistent + TMA-pipelined; CPB curves per tile (2 threads each)
       int cpb = 64;
       const auto smem_of = [&](int c) {
-        return 16 + ((2 * (size_t)c * n * sizeof(T) + 15) & ~(size_t)15) + 2 * (size_t)c * S * sizeof(T);
+        return 16 + ((2 * (size_t)c * n * sizeof(T) + 15) & ~(size_t)15) + 2 * (size_t)(c + 1) * S * sizeof(T);
       };
       while (cpb > 16 && smem_of(cpb) > 64 * 1024) cpb -= 16;
       const size_t sm = smem_of(cpb);
@@ -179,8 +179,8 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
       return launch_rc();
     }
     int cpb = 128;
-    while (cpb > 16 && (size_t)2 * cpb * S * sizeof(T) > 100 * 1024) cpb -= 16;
-    const size_t sm = (size_t)2 * cpb * S * sizeof(T);
+    while (cpb > 16 && (size_t)2 * (cpb + 1) * S * sizeof(T) > 100 * 1024) cpb -= 16;
+    const size_t sm = (size_t)2 * (cpb + 1) * S * sizeof(T);
     auto kern = k1_thomas_babe<T>;
     if (int rc = set_smem(kern, sm)) return rc;
     const int64_t grid = (batch + cpb - 1) / cpb;
