@@ -183,3 +183,53 @@ def test_bad_knots_in_multi_tile_pipeline(api):
     assert np.all(np.isnan(y2[bad]))
     good = np.setdiff1d(np.arange(B), bad)
     assert np.all(np.isfinite(y2[good]))
+
+
+@pytest.mark.parametrize("world,n,bc", [(2, 20000, 0), (3, 50001, 3), (8, 1 << 18, 0), (4, 9000, 1)])
+def test_spike_seam_emulated_ranks(api, world, n, bc):
+    """The multi-GPU SPIKE seam with G ranks emulated on one GPU (the kernels of different
+    ranks never wait on one another, so running them one after another is exact): every
+    rank's reduce, an all-gather by concatenation, every rank's finish -> the oracle's y2."""
+    from paper_2001_09253_b200 import dist as sdist
+    wl = workloads.generate(5, n=n, m=16)
+    x, y = parity.to_dev(wl.x[0]), parity.to_dev(wl.y[0])
+    s0 = torch.full((1,), 0.3, dtype=x.dtype, device=x.device)
+    s1 = torch.full((1,), -0.2, dtype=x.dtype, device=x.device)
+    recs, wss = [], []
+    for r in range(world):
+        rb, re = sdist.shard_rows(n, world, r)
+        ws = api.spike_workspace(n, rb, re, x.dtype, x.device)
+        rec = torch.empty(6, dtype=x.dtype, device=x.device)
+        api.spike_reduce(x, y, rb, re, bc, s0, s1, rec, ws)
+        recs.append(rec)
+        wss.append(ws)
+    allr = torch.cat(recs)
+    parts = []
+    for r in range(world):
+        rb, re = sdist.shard_rows(n, world, r)
+        y2s = torch.empty(re - rb, dtype=x.dtype, device=x.device)
+        api.spike_finish(x, y, rb, re, bc, s0, s1, allr, world, r, y2s, wss[r])
+        parts.append(y2s)
+    y2 = torch.cat(parts).cpu().numpy()
+    ref, _ = oracle.build_y2(wl.x[0], wl.y[0], bc, [0.3], [-0.2])
+    assert parity.y2_rel_err(y2[None], ref[None]).max() <= 1e-12
+
+
+def test_spike_record_matches_dense_block(api):
+    """The CUDA block record equals the dense-solve record of the same rows (seam contract)."""
+    import seam_ref
+    wl = workloads.generate(5, n=3000, m=16)
+    ops = seam_ref.SeamRefOps(wl.x[0], wl.y[0], 3, 0.5, 0.25)
+    x, y = parity.to_dev(wl.x[0]), parity.to_dev(wl.y[0])
+    s0 = torch.full((1,), 0.5, dtype=x.dtype, device=x.device)
+    s1 = torch.full((1,), 0.25, dtype=x.dtype, device=x.device)
+    for rb, re in [(0, 1200), (1200, 3000), (700, 2900)]:
+        ws = api.spike_workspace(3000, rb, re, x.dtype, x.device)
+        rec = torch.empty(6, dtype=x.dtype, device=x.device)
+        api.spike_reduce(x, y, rb, re, 3, s0, s1, rec, ws)
+        ref = torch.empty(6, dtype=torch.float64)
+        ops.reduce(None, None, rb, re, 3, None, None, ref, None)
+        g, r = rec.cpu().numpy(), ref.numpy()
+        scale = np.array([abs(r[0]) + abs(r[3])] * 6)
+        scale[[1, 2, 4, 5]] = 1.0
+        assert np.all(np.abs(g - r) <= 1e-12 * scale), (g, r)
