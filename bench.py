@@ -185,6 +185,72 @@ def cpu_baseline(args, wl_full):
                       f"{t:.2f} s", "knots_per_s": wl.batch * wl.n / t}
 
 
+def run_long_curve_dist(args, world, rank, local, dev):
+    """cfg5 on G GPUs (strong scaling): the one long curve's rows are partitioned (SPIKE:
+    per-rank block record -> NCCL all_gather of 6 scalars per rank -> redundant reduced solve
+    -> per-rank finish), the y2 shards are all-gathered (NCCL), and each rank evaluates its
+    shard of the 2^28 queries.  All of it is inside the timed step."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2001_09253_b200 import api, workloads
+    from paper_2001_09253_b200 import dist as sdist
+
+    spec = workloads.CONFIGS[5]
+    wl = workloads.generate(5, m=1)  # x, y identical on every rank (drawn before q)
+    n, M = wl.n, spec.m
+    qb, qe = sdist.shard_batch(M, world, rank)
+    rng = np.random.default_rng([spec.seed, 1000 + rank])
+    q = torch.from_numpy(rng.random(qe - qb)[None]).to(dev)
+    x = torch.from_numpy(wl.x[0]).to(dev)
+    y = torch.from_numpy(wl.y[0]).to(dev)
+    rb, re = sdist.shard_rows(n, world, rank)
+    ws = api.spike_workspace(n, rb, re, x.dtype, dev)
+    out = torch.empty_like(q)
+    idx = torch.empty(q.shape, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        y2s, _ = sdist.build_long_curve(x, y, wl.bc, workspace=ws)
+        y2 = sdist.gather_curve(y2s, n)
+        api.evaluate(x[None], y[None], y2[None], q, 0, out=out, idx=idx)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(K):
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([statistics.mean(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    if rank == 0:
+        build_bytes, eval_bytes = algorithmic_bytes(1, n, M, 8)
+        peak, peak_src = peaks()
+        line = {"metric": METRIC, "value": M / (ms * 1e-3), "unit": "queries/s", "n_gpus": world, "steps": K,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded PCG64, BASELINE.json cfg5 recipe; per-rank query shards)",
+                "config": {"workload": spec.name, "n": n, "m_total": M,
+                           "parallelism": f"rows sharded over {world} GPUs (SPIKE, NCCL record all_gather), "
+                                          "y2 all_gather, queries sharded",
+                           "l2": "inputs (1.5 GiB curve, 2 GiB queries) exceed L2"},
+                "knots_per_s": n / (ms * 1e-3),
+                "hbm_gbs_step_per_gpu": (build_bytes / world + eval_bytes / world) / (ms * 1e-3) / 1e9,
+                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": 7 * K,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -203,6 +269,11 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+
+    if args.config == 5 and world > 1:
+        run_long_curve_dist(args, world, rank, local, dev)
+        dist.destroy_process_group()
+        return
 
     spec = workloads.CONFIGS[args.config]
     wl = workloads.generate(args.config, shard=rank)
