@@ -90,8 +90,8 @@ __device__ __forceinline__ void eval_one(const T *X, const T *Y, const T *Z, int
 // Per staged curve: K[j] = {x_j, y_j, y2_j, 1/h_j} (one 16/32-byte record per knot, so the
 // gather is two vector loads and the per-query division becomes a multiply by the
 // interval's precomputed reciprocal -- the paper's inv_ba).
-//   MODE_BISECT : branch-free bisection over Xs, the knots padded with +inf to P = 2^k >=
-//                 n-1 entries: log2(P) uniform steps, no divergence (short curves).
+//   MODE_BISECT : branch-free bisection over the knots in Eytzinger order (see eytz_count):
+//                 ceil(log2 n) uniform steps, no divergence, conflict-free (short curves).
 //   MODE_TABLE  : bucket table over nb = 2n equal-width buckets of [x_0, x_{n-1}]:
 //                   bucket(v) = min(nb, (int)((v - x_0) * s)),   s = nb / (x_{n-1} - x_0)
 //                   Tb[b]     = max{ j in [0, n-2] : bucket(x_j) < b }   (Tb[0] = 0).
@@ -111,44 +111,34 @@ template <typename T> __device__ __forceinline__ int bucket_of(T v, T x0, T s, i
   return (f >= T(0)) ? min((int)f, nb) : 0;  // (int) truncates; f >= 0 here
 }
 
-// Branch-free bisection over Xs[0 .. 2^L2) (largest j with Xs[j] <= q, Xs[0] <= q):
-// fully unrolled, 4 instructions per step (address, LDS, compare, select).
-// Xs is stored with one pad word per 32 entries (entry i at i + i/32) so that the probes of
-// one step (and the two halves of the curve) fall in distinct shared-memory banks.
-__host__ __device__ __forceinline__ int xs_slot(int i) { return i + (i >> 5); }
-
-template <typename T, int L2> __device__ __forceinline__ int bisect_pow2(const T *Xs, T q) {
-  int lo = 0;
+// MODE_BISECT search structure: the keys x_1 .. x_{n-1} (padded with +inf to 2^L2 - 1 keys)
+// in Eytzinger (breadth-first) order, E[1 .. 2^L2 - 1], E[i]'s children at 2i, 2i+1.  A
+// branch-free descent i <- 2i + (E[i] <= q) of exactly L2 steps ends at i = 2^L2 + c with
+// c = #{keys <= q}, which is the locate rule's answer (clamped to n-2 for q = x_{n-1}).
+// Level t of the tree is 2^t consecutive words, so the probes of a warp hit distinct banks.
+template <typename T, int L2> __device__ __forceinline__ int eytz_count(const T *E, T q) {
+  int i = 1;
 #pragma unroll
-  for (int t = L2 - 1; t >= 0; --t) lo = (Xs[xs_slot(lo + (1 << t))] <= q) ? lo + (1 << t) : lo;
-  return lo;
+  for (int t = 0; t < L2; ++t) i = 2 * i + (E[i] <= q ? 1 : 0);
+  return i - (1 << L2);
 }
 
-template <typename T> __device__ __forceinline__ int bisect_padded(const T *Xs, int l2, T q) {
-  switch (l2) {  // warp-uniform
-    case 0: return 0;
-    case 1: return bisect_pow2<T, 1>(Xs, q);
-    case 2: return bisect_pow2<T, 2>(Xs, q);
-    case 3: return bisect_pow2<T, 3>(Xs, q);
-    case 4: return bisect_pow2<T, 4>(Xs, q);
-    case 5: return bisect_pow2<T, 5>(Xs, q);
-    case 6: return bisect_pow2<T, 6>(Xs, q);
-    case 7: return bisect_pow2<T, 7>(Xs, q);
-    case 8: return bisect_pow2<T, 8>(Xs, q);
-    default: return bisect_pow2<T, 9>(Xs, q);
-  }
+// in-order rank (0-based) of breadth-first node i (1-based) in a complete tree of depth L2
+__device__ __forceinline__ int eytz_rank(int i, int L2) {
+  int d = 31 - __clz(i);  // depth
+  return ((2 * (i - (1 << d)) + 1) << (L2 - 1 - d)) - 1;
 }
 
 // Locate + evaluate one query against a packed curve.  Branch-light: out-of-range / NaN
 // queries run the same path on a clamped stand-in and are masked at the end.
-template <typename T, int MODE>
-__device__ __forceinline__ void eval_packed(const Knot<T> *K, const T *Xs, int P, const uint16_t *Tb,
+template <typename T, int MODE, int L2>
+__device__ __forceinline__ void eval_packed(const Knot<T> *K, const T *E, const uint16_t *Tb,
                                             const CurveHdr<T> &hd, int n, int nb, T q, T &val, int &j) {
   const bool in = (q >= hd.x0) && (q <= hd.xn);  // false for NaN
   const T qc = in ? q : hd.x0;
   int lo;
   if (MODE == MODE_BISECT) {
-    lo = min(bisect_padded(Xs, P, qc), n - 2);  // P carries log2 of the padded length here
+    lo = min(eytz_count<T, L2>(E, qc), n - 2);
   } else {
     int hi;
     if (MODE == MODE_TABLE) {
@@ -194,10 +184,10 @@ __host__ __device__ constexpr int pow2_at_least(int v) {
 // being evaluated.
 template <typename T> struct StageLayout {
   size_t raw0, rawstep, knots, hdr, xs, table, total;
-  int P;
+  int P;  // Eytzinger array stride per curve (MODE_BISECT): 2^L2 >= n
   __host__ __device__ StageLayout(int cpb, int n, int mode) {
     const bool packed = mode != MODE_BSEARCH;
-    P = pow2_at_least(n - 1);
+    P = pow2_at_least(n);
     const size_t rawb = 3 * sizeof(T) * (size_t)cpb * n;
     raw0 = kStageHeader;
     rawstep = align16(rawb);
@@ -207,7 +197,7 @@ template <typename T> struct StageLayout {
     hdr = off;
     if (packed) off = align16(off + sizeof(CurveHdr<T>) * (size_t)cpb);
     xs = off;
-    if (mode == MODE_BISECT) off = align16(off + sizeof(T) * (size_t)cpb * xs_slot(P));
+    if (mode == MODE_BISECT) off = align16(off + sizeof(T) * (size_t)cpb * P);
     table = off;
     if (mode == MODE_TABLE) off = align16(off + sizeof(uint16_t) * (size_t)cpb * (kBucketsPerKnot * n + 2));
     total = off;
@@ -225,8 +215,8 @@ template <typename T> struct StageLayout {
 // Each warp owns a contiguous run of an item's queries; lane l takes groups of V
 // consecutive queries (16-byte vectors when V > 1), U groups per batch.  A group's V
 // queries belong to one curve (m % V == 0 on the vector path).
-template <typename T, int MODE, int V, bool BULK>
-__global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3)
+template <typename T, int MODE, int V, bool BULK, int L2>
+__global__ void __launch_bounds__(kEvalThreads, 3)
     k_eval_staged(const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ y2, int n, int64_t batch,
                   const T *__restrict__ q, int m, T *__restrict__ out, int32_t *__restrict__ idx, int cpb,
                   int nchunks, int qchunk, int64_t nitems, FastDiv divn, FastDiv divm) {
@@ -240,7 +230,6 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3)
   T *Xs = reinterpret_cast<T *>(smem_raw + L.xs);
   uint16_t *Tb = reinterpret_cast<uint16_t *>(smem_raw + L.table);
   const int P = L.P;
-  const int l2P = 31 - __clz(P);
   const int nb = kBucketsPerKnot * n;
   const int64_t G = gridDim.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -333,11 +322,6 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3)
         kk.z = Z[e];
         kk.ih = (j < n - 1) ? r_rcp(r_sub(X[e + 1], xj)) : T(0);
         K[e] = kk;
-        if (MODE == MODE_BISECT) {
-          T *Xc = Xs + (size_t)c * xs_slot(P);
-          if (j < P) Xc[xs_slot(j)] = xj;
-          for (int jj = n + j; jj < P; jj += n) Xc[xs_slot(jj)] = (T)INFINITY;  // pad [n, P) with +inf
-        }
         if (j == 0 || (MODE == MODE_TABLE && j < n - 1)) {
           const T x0 = X[c * n], xn = X[c * n + n - 1];
           const T sc = (MODE == MODE_TABLE) ? (T)nb / (xn - x0) : (T)(n - 1) / (xn - x0);
@@ -349,6 +333,16 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3)
             const int bhi = (j == n - 2) ? nb + 1 : bucket_of(X[e + 1], x0, sc, nb);
             for (int b = blo + 1; b <= bhi; ++b) Tc[b] = (uint16_t)j;
           }
+        }
+      }
+      if (MODE == MODE_BISECT) {  // Eytzinger keys x_1 .. x_{n-1}, +inf padded
+        const int te = nc * P;
+        for (int e = threadIdx.x; e < te; e += blockDim.x) {
+          const int c = e >> L2;
+          const int i = e & (P - 1);
+          if (i == 0) continue;
+          const int r = eytz_rank(i, L2) + 1;  // knot index
+          Xs[e] = (r < n) ? X[c * n + r] : (T)INFINITY;
         }
       }
       __syncthreads();  // packed data built; raw stage s consumed
@@ -377,10 +371,10 @@ __global__ void __launch_bounds__(kEvalThreads, sizeof(T) == 4 ? 4 : 3)
           if (PACKED) {
             const CurveHdr<T> hd = Hd[cl];
             const Knot<T> *Kc = K + cl * n;
-            const T *Xc = Xs + (size_t)cl * xs_slot(P);
+            const T *Ec = Xs + (size_t)cl * P;
             const uint16_t *Tc = Tb + cl * (nb + 2);
 #pragma unroll
-            for (int i = 0; i < V; ++i) eval_packed<T, MODE>(Kc, Xc, l2P, Tc, hd, n, nb, qa[u][i], val[i], jj[i]);
+            for (int i = 0; i < V; ++i) eval_packed<T, MODE, L2>(Kc, Ec, Tc, hd, n, nb, qa[u][i], val[i], jj[i]);
           } else {
 #pragma unroll
             for (int i = 0; i < V; ++i) eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qa[u][i], val[i], jj[i]);

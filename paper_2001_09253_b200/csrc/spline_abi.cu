@@ -193,12 +193,27 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
 
 // ------------------------------------------------------------------------- eval
 
-template <typename T, int MODE, int V, bool BULK>
+template <typename T, int MODE, int V, bool BULK, int L2 = 0>
 int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
                     int32_t *idx, int cpb, int nchunks, int qchunk, int64_t nitems, cudaStream_t st) {
+  if constexpr (MODE == MODE_BISECT && L2 == 0) {
+    // pick the compile-time search depth: 2^L2 >= n
+    int l2 = 0;
+    while ((1 << l2) < n) ++l2;
+    switch (l2 < 2 ? 2 : l2) {
+      case 2: return launch_staged_k<T, MODE, V, BULK, 2>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 3: return launch_staged_k<T, MODE, V, BULK, 3>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 4: return launch_staged_k<T, MODE, V, BULK, 4>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 5: return launch_staged_k<T, MODE, V, BULK, 5>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 6: return launch_staged_k<T, MODE, V, BULK, 6>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 7: return launch_staged_k<T, MODE, V, BULK, 7>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 8: return launch_staged_k<T, MODE, V, BULK, 8>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      default: return launch_staged_k<T, MODE, V, BULK, 9>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+    }
+  }
   const StageLayout<T> L(cpb, n, MODE);
   const size_t sm = L.total;
-  auto kern = k_eval_staged<T, MODE, V, BULK>;
+  auto kern = k_eval_staged<T, MODE, V, BULK, L2>;
   if (int rc = set_smem(kern, sm)) return rc;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, sm) != cudaSuccess || occ < 1) occ = 1;
