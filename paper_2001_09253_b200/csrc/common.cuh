@@ -157,6 +157,17 @@ template <typename T, int V> struct VecIO {
       for (int i = 0; i < V; ++i) v[i] = tt[i];
     }
   }
+  static __device__ __forceinline__ void load_shared(const T *p, T *v) {
+    if constexpr (V == 1) {
+      v[0] = p[0];
+    } else {
+      using VT = typename Vec16<T>::V;
+      const VT t = *reinterpret_cast<const VT *>(p);
+      const T *tt = reinterpret_cast<const T *>(&t);
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = tt[i];
+    }
+  }
   static __device__ __forceinline__ void store(T *p, const T *v) {
     if constexpr (V == 1) {
       st_stream(p, v[0]);

@@ -116,11 +116,30 @@ template <typename T> __device__ __forceinline__ int bucket_of(T v, T x0, T s, i
 // branch-free descent i <- 2i + (E[i] <= q) of exactly L2 steps ends at i = 2^L2 + c with
 // c = #{keys <= q}, which is the locate rule's answer (clamped to n-2 for q = x_{n-1}).
 // Level t of the tree is 2^t consecutive words, so the probes of a warp hit distinct banks.
+__device__ __forceinline__ float lds_f(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f(uint32_t a, double) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+// The descent on shared-memory byte addresses: a_{t+1} = 2 a_t + (E[i] <= q ? s - base : -base)
+// (a = base + s*i), i.e. one load, one compare, one select and one multiply-add per level.
 template <typename T, int L2> __device__ __forceinline__ int eytz_count(const T *E, T q) {
-  int i = 1;
+  const uint32_t base = smem_u32(E);
+  const uint32_t k0 = 0u - base, k1 = (uint32_t)sizeof(T) - base;
+  uint32_t a = base + (uint32_t)sizeof(T);
 #pragma unroll
-  for (int t = 0; t < L2; ++t) i = 2 * i + (E[i] <= q ? 1 : 0);
-  return i - (1 << L2);
+  for (int t = 0; t < L2; ++t) {
+    T v;
+    if constexpr (sizeof(T) == 4) v = lds_f(a);
+    else v = lds_f(a, 0.0);
+    a = 2u * a + (v <= q ? k1 : k0);
+  }
+  return (int)((a - base) / (uint32_t)sizeof(T)) - (1 << L2);
 }
 
 // in-order rank (0-based) of breadth-first node i (1-based) in a complete tree of depth L2
@@ -179,18 +198,20 @@ __host__ __device__ constexpr int pow2_at_least(int v) {
   return p;
 }
 
-// Shared-memory layout of one CTA: two raw stages (x, y, y2 of cpb curves each, filled by
-// TMA bulk copies) + the packed knots / headers / padded x / bucket table of the item
-// being evaluated.
+// Shared-memory layout of one CTA: two stages, each holding an item's raw x, y, y2 (cpb
+// curves) and -- when queries are staged too -- its up to qmax queries, all filled by TMA bulk
+// copies; plus the packed knots / headers / Eytzinger keys / bucket table of the item being
+// evaluated.
 template <typename T> struct StageLayout {
-  size_t raw0, rawstep, knots, hdr, xs, table, total;
+  size_t raw0, rawstep, qoff, knots, hdr, xs, table, total;
   int P;  // Eytzinger array stride per curve (MODE_BISECT): 2^L2 >= n
-  __host__ __device__ StageLayout(int cpb, int n, int mode) {
+  __host__ __device__ StageLayout(int cpb, int n, int mode, int qmax) {
     const bool packed = mode != MODE_BSEARCH;
     P = pow2_at_least(n);
     const size_t rawb = 3 * sizeof(T) * (size_t)cpb * n;
     raw0 = kStageHeader;
-    rawstep = align16(rawb);
+    qoff = align16(rawb);
+    rawstep = align16(qoff + sizeof(T) * (size_t)qmax);
     size_t off = raw0 + 2 * rawstep;
     knots = off;
     if (packed) off = align16(off + sizeof(Knot<T>) * (size_t)cpb * n);
@@ -206,24 +227,24 @@ template <typename T> struct StageLayout {
 
 // Persistent, double-buffered staged eval (unsorted queries).  Work item `it` = curves
 // [it*cpb, +cpb) with all their queries (cpb > 1), or queries [ch*qchunk, +qchunk) of curve
-// it/nchunks (cpb == 1).  Grid = min(items, SMs x CTAs/SM); CTA b takes items b, b+G, ...
-//   * raw stage s holds item i's x, y, y2 (cp.async.bulk -> mbarrier s); item i+1's copy is
-//     already in flight in stage s^1 while item i is evaluated, and stage s is refilled
-//     (item i+2) as soon as the packing pass has consumed it;
-//   * query batches are register double-buffered: batch b+1 (possibly the next item's first
-//     batch) is loaded before batch b is evaluated.
-// Each warp owns a contiguous run of an item's queries; lane l takes groups of V
-// consecutive queries (16-byte vectors when V > 1), U groups per batch.  A group's V
-// queries belong to one curve (m % V == 0 on the vector path).
+// it/nchunks (cpb == 1); an item's queries are contiguous in HBM.  Grid = min(items,
+// SMs x CTAs/SM); CTA b takes items b, b+G, ...
+//   BULK (aligned inputs, V = 16/sizeof(T)): stage s receives item i's x, y, y2 AND its
+//     queries through cp.async.bulk (mbarrier s); item i+1 is already in flight in stage s^1
+//     while item i is evaluated; stage s is refilled (item i+2) once item i is done.  Every
+//     input byte arrives asynchronously; outputs leave as 16-byte streaming stores.
+//   !BULK (unaligned or ragged m): coalesced synchronous staging, queries from registers.
+// A packing pass then builds {x, y, y2, 1/h} records (+ the mode's search structure).  Each
+// warp owns a contiguous run of the item's queries; lane l takes groups of V consecutive
+// queries (one curve per group: m % V == 0 when V > 1).
 template <typename T, int MODE, int V, bool BULK, int L2>
 __global__ void __launch_bounds__(kEvalThreads, 3)
     k_eval_staged(const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ y2, int n, int64_t batch,
                   const T *__restrict__ q, int m, T *__restrict__ out, int32_t *__restrict__ idx, int cpb,
-                  int nchunks, int qchunk, int64_t nitems, FastDiv divn, FastDiv divm) {
-  constexpr int U = (V >= 4) ? 1 : 2;  // groups per lane per batch (x2 buffered)
+                  int nchunks, int qchunk, int qmax, int64_t nitems, FastDiv divn, FastDiv divm) {
   constexpr bool PACKED = (MODE != MODE_BSEARCH);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const StageLayout<T> L(cpb, n, MODE);
+  const StageLayout<T> L(cpb, n, MODE, BULK ? qmax : 0);
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);  // bar[0], bar[1]
   Knot<T> *K = reinterpret_cast<Knot<T> *>(smem_raw + L.knots);
   CurveHdr<T> *Hd = reinterpret_cast<CurveHdr<T> *>(smem_raw + L.hdr);
@@ -235,7 +256,7 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const size_t cn = (size_t)cpb * n;
 
-  auto raw = [&](int s) { return reinterpret_cast<T *>(smem_raw + L.raw0 + (size_t)s * L.rawstep); };
+  auto stage = [&](int s) { return smem_raw + L.raw0 + (size_t)s * L.rawstep; };
   auto item_of = [&](int64_t it, int64_t &c0, int64_t &k0, int &nc, int &cnt) {
     if (cpb > 1) {
       c0 = it * cpb;
@@ -256,24 +277,13 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
     int nc, cnt;
     item_of(it, c0, k0, nc, cnt);
     const uint32_t bytes = (uint32_t)((size_t)nc * n * sizeof(T));
-    T *R = raw(s);
-    mbar_expect_tx(bar + s, 3 * bytes);
+    const uint32_t qbytes = (uint32_t)((size_t)cnt * sizeof(T));
+    T *R = reinterpret_cast<T *>(stage(s));
+    mbar_expect_tx(bar + s, 3 * bytes + qbytes);
     bulk_g2s(R, x + c0 * n, bytes, bar + s);
     bulk_g2s(R + cn, y + c0 * n, bytes, bar + s);
     bulk_g2s(R + 2 * cn, y2 + c0 * n, bytes, bar + s);
-  };
-  auto wrange = [&](int cnt, int &wb, int &we) {  // the warp's group range within an item
-    const int ng = cnt / V;
-    const int per = (ng + nw - 1) / nw;
-    wb = w * per;
-    we = min(ng, wb + per);
-  };
-  auto load_batch = [&](int64_t k0, int gb, int we, T (&qv)[U][V]) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int g = gb + u * 32 + lane;
-      if (g < we) VecIO<T, V>::load(q + k0 + (int64_t)g * V, qv[u]);
-    }
+    bulk_g2s(stage(s) + L.qoff, q + k0, qbytes, bar + s);
   };
 
   if (threadIdx.x == 0) {
@@ -286,18 +296,16 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
     issue(it, 0);
     issue(it + G, 1);
   }
-  T qa[U][V], qn[U][V];
-  int64_t c0, k0;
-  int nc, cnt, wb, we;
-  item_of(it < nitems ? it : 0, c0, k0, nc, cnt);
-  wrange(cnt, wb, we);
-  if (it < nitems) load_batch(k0, wb, we, qa);
   bool oor = false;
   uint32_t phases = 0u;  // bit s = parity to wait for on bar[s]
   int s = 0;
 
   for (; it < nitems; it += G) {
-    T *X = raw(s);
+    int64_t c0, k0;
+    int nc, cnt;
+    item_of(it, c0, k0, nc, cnt);
+    T *X = reinterpret_cast<T *>(stage(s));
+    const T *Qs = reinterpret_cast<const T *>(stage(s) + L.qoff);
     if (BULK) {
       mbar_wait(bar + s, (phases >> s) & 1u);
       phases ^= 1u << s;
@@ -345,55 +353,41 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
           Xs[e] = (r < n) ? X[c * n + r] : (T)INFINITY;
         }
       }
-      __syncthreads();  // packed data built; raw stage s consumed
-      if (threadIdx.x == 0) issue(it + 2 * G, s);
+      __syncthreads();  // packed data built
     }
 
-    // next item (its first batch is prefetched during this item's last batch)
-    const int64_t itn = it + G;
-    int64_t c0n = 0, k0n = 0;
-    int ncn = 0, cntn = 0, wbn = 0, wen = 0;
-    if (itn < nitems) {
-      item_of(itn, c0n, k0n, ncn, cntn);
-      wrange(cntn, wbn, wen);
-    }
+    // the warp's contiguous run of groups within the item
+    const int ng = cnt / V;
+    const int per = (ng + nw - 1) / nw;
+    const int wb = w * per, we = min(ng, wb + per);
     const int kbase = (int)(k0 - c0 * m);  // item's first query, relative to its first curve
-    for (int gb = wb; gb < we; gb += 32 * U) {
-      if (gb + 32 * U < we) load_batch(k0, gb + 32 * U, we, qn);
-      else if (itn < nitems) load_batch(k0n, wbn, wen, qn);
+    for (int g = wb + lane; g < we; g += 32) {
+      T qv[V], val[V];
+      int jj[V];
+      if (BULK) {
+        VecIO<T, V>::load_shared(Qs + g * V, qv);
+      } else {
+        VecIO<T, V>::load(q + k0 + (int64_t)g * V, qv);
+      }
+      const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(kbase + g * V)) : 0;
+      if (PACKED) {
+        const CurveHdr<T> hd = Hd[cl];
+        const Knot<T> *Kc = K + cl * n;
+        const T *Ec = Xs + (size_t)cl * P;
+        const uint16_t *Tc = Tb + cl * (nb + 2);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int g = gb + u * 32 + lane;
-        if (g < we) {
-          T val[V];
-          int jj[V];
-          const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(kbase + g * V)) : 0;
-          if (PACKED) {
-            const CurveHdr<T> hd = Hd[cl];
-            const Knot<T> *Kc = K + cl * n;
-            const T *Ec = Xs + (size_t)cl * P;
-            const uint16_t *Tc = Tb + cl * (nb + 2);
+        for (int i = 0; i < V; ++i) eval_packed<T, MODE, L2>(Kc, Ec, Tc, hd, n, nb, qv[i], val[i], jj[i]);
+      } else {
 #pragma unroll
-            for (int i = 0; i < V; ++i) eval_packed<T, MODE, L2>(Kc, Ec, Tc, hd, n, nb, qa[u][i], val[i], jj[i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < V; ++i) eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qa[u][i], val[i], jj[i]);
-          }
-#pragma unroll
-          for (int i = 0; i < V; ++i) oor |= (jj[i] < 0);
-          VecIO<T, V>::store(out + k0 + (int64_t)g * V, val);
-          if (idx) VecIO<T, V>::store_idx(idx + k0 + (int64_t)g * V, jj);
-        }
+        for (int i = 0; i < V; ++i) eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qv[i], val[i], jj[i]);
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int i = 0; i < V; ++i) qa[u][i] = qn[u][i];
+      for (int i = 0; i < V; ++i) oor |= (jj[i] < 0);
+      VecIO<T, V>::store(out + k0 + (int64_t)g * V, val);
+      if (idx) VecIO<T, V>::store_idx(idx + k0 + (int64_t)g * V, jj);
     }
-    if (wb >= we && itn < nitems) load_batch(k0n, wbn, wen, qa);  // warp had no work in this item
-    __syncthreads();  // everyone is done with this item's shared data
-    if (!PACKED && threadIdx.x == 0) issue(it + 2 * G, s);
-    c0 = c0n; k0 = k0n; nc = ncn; cnt = cntn; wb = wbn; we = wen;
+    __syncthreads();  // everyone is done with this item's stage and packed data
+    if (threadIdx.x == 0) issue(it + 2 * G, s);
     s ^= 1;
   }
   if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);

@@ -196,6 +196,7 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
 template <typename T, int MODE, int V, bool BULK, int L2 = 0>
 int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
                     int32_t *idx, int cpb, int nchunks, int qchunk, int64_t nitems, cudaStream_t st) {
+  static_assert(!BULK || V > 1, "query staging needs 16-byte query groups");
   if constexpr (MODE == MODE_BISECT && L2 == 0) {
     // pick the compile-time search depth: 2^L2 >= n
     int l2 = 0;
@@ -211,7 +212,8 @@ int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
       default: return launch_staged_k<T, MODE, V, BULK, 9>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
     }
   }
-  const StageLayout<T> L(cpb, n, MODE);
+  const int qmax = (cpb > 1) ? cpb * (int)m : qchunk;
+  const StageLayout<T> L(cpb, n, MODE, BULK ? qmax : 0);
   const size_t sm = L.total;
   auto kern = k_eval_staged<T, MODE, V, BULK, L2>;
   if (int rc = set_smem(kern, sm)) return rc;
@@ -219,15 +221,18 @@ int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, sm) != cudaSuccess || occ < 1) occ = 1;
   const int64_t grid = std::min<int64_t>(nitems, (int64_t)occ * num_sms());
   kern<<<(unsigned)grid, kEvalThreads, sm, st>>>(x, y, y2, n, batch, q, (int)m, out, idx, cpb, nchunks, qchunk,
-                                                 nitems, FastDiv((uint32_t)n), FastDiv((uint32_t)m));
+                                                 qmax, nitems, FastDiv((uint32_t)n), FastDiv((uint32_t)m));
   return launch_rc();
 }
 
 
 constexpr size_t kSmemCap = 220 * 1024;   // per-CTA dynamic shared memory we allow ourselves
-constexpr size_t kItemSmem = 48 * 1024;   // target per-CTA footprint for multi-curve items
+constexpr size_t kItemSmem = 72 * 1024;   // target per-CTA footprint for multi-curve items
 
-template <typename T> size_t stage_total(int cpb, int n, int mode) { return StageLayout<T>(cpb, n, mode).total; }
+constexpr int kQMax = 4096;  // queries per staged work item (BULK path)
+template <typename T> size_t stage_total(int cpb, int n, int mode, int qmax = 0) {
+  return StageLayout<T>(cpb, n, mode, qmax).total;
+}
 
 template <typename T, int MODE>
 int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
@@ -236,28 +241,29 @@ int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, con
   int cpb = 1, nchunks = 1, qchunk = (int)m;
   int64_t nitems;
   if (m >= 2048 || batch == 1) {
-    // One curve per item; split a curve's queries if there are too few curves to fill the GPU.
+    // One curve per item; split a curve's queries into chunks of <= kQMax (and enough items
+    // to fill the GPU when there are few curves).
     const int64_t want = (4 * 148 + batch - 1) / batch;
-    nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (m + 1023) / 1024));
+    nchunks = (int)std::max<int64_t>({(int64_t)1, std::min<int64_t>(want, (m + 1023) / 1024),
+                                      (m + kQMax - 1) / kQMax});
     qchunk = (int)((m + nchunks - 1) / nchunks);
     qchunk = (qchunk + VW - 1) / VW * VW;
     nchunks = (int)((m + qchunk - 1) / qchunk);
     nitems = batch * nchunks;
   } else {
-    int64_t c = std::max<int64_t>(1, 8192 / m);
+    int64_t c = std::max<int64_t>(1, kQMax / m);
     c = std::min<int64_t>(c, batch);
-    while (c > 1 && stage_total<T>((int)c, n, MODE) > kItemSmem) c >>= 1;
+    while (c > 1 && stage_total<T>((int)c, n, MODE, (int)(c * m)) > kItemSmem) c >>= 1;
     while (c > 1 && (uint64_t)c * m * m >= (1ull << 32)) c >>= 1;  // FastDiv range
     cpb = (int)std::max<int64_t>(1, c);
     nitems = (batch + cpb - 1) / cpb;
   }
-  // 16-byte vector query I/O when every curve's query run is whole vectors and aligned.
+  // 16-byte vector query I/O when every curve's query run is whole vectors and aligned;
+  // TMA bulk staging of knots + queries when, in addition, curve blocks are whole 16-byte units.
   const bool vec = (m % VW == 0) && aligned16(q) && aligned16(out) && (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0));
-  // TMA bulk staging when every curve block is a whole number of 16-byte units and aligned.
-  const bool bulk = ((n * sizeof(T)) % 16 == 0) && aligned16(x) && aligned16(y) && aligned16(y2);
-  if (vec && bulk) return launch_staged_k<T, MODE, VW, true>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+  const bool bulk = vec && ((n * sizeof(T)) % 16 == 0) && aligned16(x) && aligned16(y) && aligned16(y2);
+  if (bulk) return launch_staged_k<T, MODE, VW, true>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
   if (vec) return launch_staged_k<T, MODE, VW, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
-  if (bulk) return launch_staged_k<T, MODE, 1, true>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
   return launch_staged_k<T, MODE, 1, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
 }
 
@@ -286,15 +292,15 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
   }
   if (n < 65535) {
     const int nn = (int)n;
-    if ((flags & SPLINE_X_UNIFORM) && stage_total<T>(1, nn, MODE_UNIFORM) <= kSmemCap)
+    if ((flags & SPLINE_X_UNIFORM) && stage_total<T>(1, nn, MODE_UNIFORM, kQMax) <= kSmemCap)
       return launch_staged<T, MODE_UNIFORM>(x, y, y2, nn, batch, q, m, out, idx, st);
     // short curves: branch-free bisection; longer curves with many queries per knot: the
     // bucket table (its O(n) build per item is amortised over the queries)
-    if (n <= 512 && stage_total<T>(1, nn, MODE_BISECT) <= kSmemCap)
+    if (n <= 512 && stage_total<T>(1, nn, MODE_BISECT, kQMax) <= kSmemCap)
       return launch_staged<T, MODE_BISECT>(x, y, y2, nn, batch, q, m, out, idx, st);
-    if (stage_total<T>(1, nn, MODE_TABLE) <= kSmemCap)
+    if (stage_total<T>(1, nn, MODE_TABLE, kQMax) <= kSmemCap)
       return launch_staged<T, MODE_TABLE>(x, y, y2, nn, batch, q, m, out, idx, st);
-    if (stage_total<T>(1, nn, MODE_BSEARCH) <= kSmemCap)
+    if (stage_total<T>(1, nn, MODE_BSEARCH, kQMax) <= kSmemCap)
       return launch_staged<T, MODE_BSEARCH>(x, y, y2, nn, batch, q, m, out, idx, st);
   }
   const int64_t total = batch * m;
