@@ -93,6 +93,25 @@ int spline_build(const void *x, const void *y, int64_t n, int64_t batch, int bc,
 int spline_eval(const void *x, const void *y, const void *y2, int64_t n, int64_t batch, const void *q,
                 int64_t m, void *out, int32_t *idx, int flags, int dtype, spline_stream_t stream);
 
+/*
+ * spline_build_eval -- construction and evaluation in one call: the same y2, out and
+ * idx (bitwise) as spline_build followed by spline_eval on the same stream.
+ *   x, y, bc, yp1, ypn   as spline_build.
+ *   y2                   [batch][n] output, NULLABLE: NULL = do not write y2 (it then never
+ *                        leaves the chip on the fused path).
+ *   q, m, out, idx       as spline_eval (q and out required when m > 0; idx nullable).
+ *   flags                SPLINE_Q_SORTED | SPLINE_X_UNIFORM hints (speed only).
+ * The fused kernel (one launch; x, y read once from HBM, y2 produced and consumed on chip:
+ * SURVEY.md §8(f) row 1, the paper evaluating right after the build) runs when
+ * 3 <= n <= 128, n*sizeof(T) % 16 == 0, m % (16/sizeof(T)) == 0 and x, y, y2, q, out are
+ * 16-byte aligned (idx 16-byte aligned for f32, 8-byte for f64); otherwise the two kernels run
+ * back to back (with stream-ordered scratch for y2 when y2 is NULL).  m == 0 builds only.
+ * Errors: the union of spline_build's and spline_eval's.
+ */
+int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1,
+                      const void *ypn, void *y2, const void *q, int64_t m, void *out, int32_t *idx, int flags,
+                      int dtype, spline_stream_t stream);
+
 /* Typed thin wrappers (same semantics). */
 int spline_build_f32(const float *x, const float *y, int64_t n, int64_t batch, int bc, const float *yp1,
                      const float *ypn, float *y2, spline_stream_t stream);

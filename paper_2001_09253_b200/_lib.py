@@ -24,6 +24,7 @@ _vp, _i64, _i32, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_s
 SIGNATURES = {
     "spline_build": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _vp]),
     "spline_eval": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i32, _i32, _vp]),
+    "spline_build_eval": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _vp]),
     "spline_build_f32": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "spline_build_f64": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "spline_eval_f32": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i32, _vp]),

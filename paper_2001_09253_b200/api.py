@@ -85,6 +85,39 @@ def evaluate(x, y, y2, q, flags: int = 0, out=None, idx=None, want_idx: bool = T
     return o, i
 
 
+def build_eval(x, y, q, bc: int = BC_NATURAL, yp1=None, ypn=None, flags: int = 0, want_y2: bool = True,
+               y2=None, out=None, idx=None, want_idx: bool = True, stream=None):
+    """Build + evaluate in one call (spline_build_eval; one fused kernel for n <= 128).
+    Returns (y2 or None, out, idx or None); bitwise equal to build() then evaluate()."""
+    squeeze = x.dim() == 1
+    x, y, q = _as2d(x), _as2d(y), _as2d(q)
+    B, n = x.shape
+    m = q.shape[1]
+    if yp1 is not None and not isinstance(yp1, torch.Tensor):
+        yp1 = torch.full((B,), float(yp1), dtype=x.dtype, device=x.device)
+    if ypn is not None and not isinstance(ypn, torch.Tensor):
+        ypn = torch.full((B,), float(ypn), dtype=x.dtype, device=x.device)
+    _check_curves(x, y, q, yp1, ypn)
+    if y.shape != x.shape or q.shape[0] != B:
+        raise ValueError("x, y must be (B, n) and q (B, m)")
+    z = None
+    if want_y2:
+        z = torch.empty_like(x) if y2 is None else _as2d(y2)
+        _check_curves(x, z)
+    o = torch.empty_like(q) if out is None else _as2d(out)
+    i = None
+    if want_idx:
+        i = torch.empty(q.shape, dtype=torch.int32, device=q.device) if idx is None else _as2d(idx)
+        if i.dtype != torch.int32 or not i.is_contiguous():
+            raise ValueError("idx must be contiguous int32")
+    rc = _lib.load().spline_build_eval(_p(x), _p(y), n, B, bc, _p(yp1), _p(ypn), _p(z), _p(q), m, _p(o), _p(i),
+                                       flags, _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_build_eval")
+    if squeeze:
+        return (None if z is None else z[0]), o[0], (None if i is None else i[0])
+    return z, o, i
+
+
 def status(stream=None) -> int:
     """Synchronise the stream, return and clear the data-error bits (STATUS_*)."""
     bits = ctypes.c_uint(0)

@@ -37,9 +37,10 @@ constexpr int kK1Threads = 256;
 // from the other end.  Divisions are a correctly rounded reciprocal then a multiply.
 template <typename T>
 __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int64_t c0, int bc,
-                                          const T *__restrict__ yp1, const T *__restrict__ ypn, T *dummy) {
-  const int t = threadIdx.x >> 1;  // curve within the CTA
-  const bool top = (threadIdx.x & 1) == 0;
+                                          const T *__restrict__ yp1, const T *__restrict__ ypn, T *dummy,
+                                          int tid) {
+  const int t = tid >> 1;  // curve within the tile (tid = thread index within the solving group)
+  const bool top = (tid & 1) == 0;
   const bool act = t < nc;         // pairs are lane-adjacent, so shuffles stay in-warp
   const int k = n >> 1;            // meeting row, 1 <= k <= n-2
   const int dir = top ? 1 : -1;
@@ -66,14 +67,21 @@ __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int6
     cp = T(0.5);
     dp = T(3 * dir) * (gc - sl) * nr_rcp(hc);
   }
+  // the row after next is loaded one step ahead (register rotation), so the shared-memory
+  // latency is off the dependency chain; near the meeting row the look-ahead may read a row
+  // of the other thread's half, a value that is never used
+  T xnn = Xc[j0 + 2 * dir], ynn = Yc[j0 + 2 * dir];  // n >= 3
   Xc[j0] = cp;
   Yc[j0] = dp;
   int j = j0 + dir;
   auto step = [&]() {
     xo = xn;
     yo = yn;
-    xn = Xc[j + dir];
-    yn = Yc[j + dir];
+    xn = xnn;
+    yn = ynn;
+    const int jp = min(max(j + 2 * dir, 0), n - 1);
+    xnn = Xc[jp];
+    ynn = Yc[jp];
     const T h = T(dir) * (xn - xo);
     ok &= finite(xn) & finite(yn) & (h > T(0));
     const T g = (yn - yo) * nr_rcp(xn - xo);
@@ -104,9 +112,14 @@ __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int6
   // back-substitution outward from the seam: y_j = d'_j - c'_j y_{j+dir}
   T yv = yk;
   int jj = k - dir;
+  T cb = Xc[jj], db = Yc[jj];
   auto back = [&]() {
-    yv = Yc[jj] - Xc[jj] * yv;
+    const int jn = min(max(jj - dir, 0), n - 1);  // next row loaded ahead of this row's store
+    const T cb2 = Xc[jn], db2 = Yc[jn];
+    yv = db - cb * yv;
     Yc[jj] = yv;
+    cb = cb2;
+    db = db2;
     jj -= dir;
   };
   const int bcommon = n - 1 - k;  // bottom's count; the top has k (one more when n is even)
@@ -164,7 +177,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict
   }
   __syncthreads();
 
-  babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn, dummy);
+  babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn, dummy, threadIdx.x);
   __syncthreads();
 
   T *y2b = y2 + c0 * n;
@@ -233,7 +246,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(const T *__restrict
     }
     __syncthreads();
     if (threadIdx.x == 0) issue(it + G);  // raw stage consumed: next tile in flight
-    babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn, dummy);
+    babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn, dummy, threadIdx.x);
     __syncthreads();
     T *y2b = y2 + c0 * n;
     for (int e = threadIdx.x * VW; e < tot; e += blockDim.x * VW) {
@@ -247,6 +260,71 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(const T *__restrict
     }
     __syncthreads();
   }
+}
+
+// The paper's sweep for one curve held in registers, n <= NMAX: forward
+// elimination c'_j, d'_j, back-substitution.  s1 / sn are the
+// clamped end slopes (read only when that bc bit is set).  z = y2, all NaN when the curve
+// is invalid; returns validity.
+template <typename T, int NMAX>
+__device__ __forceinline__ bool thomas_regs(const T (&xv)[NMAX], const T (&yv)[NMAX], int n, int bc, T s1, T sn,
+                                            T (&z)[NMAX]) {
+  bool ok = true;
+  T cpv[NMAX], dpv[NMAX];
+  T hprev = xv[1] - xv[0];
+  T ddprev = (yv[1] - yv[0]) / hprev;
+  if (bc & 1) {  // P:966-971
+    ok = ok && finite(s1);
+    cpv[0] = T(0.5);
+    dpv[0] = T(3) * (ddprev - s1) / hprev;
+  } else {
+    cpv[0] = T(0);
+    dpv[0] = T(0);
+  }
+  T cpp = cpv[0], dpp = dpv[0];
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) {
+    if (j < n) {
+      ok = ok && finite(xv[j]) && finite(yv[j]);
+      if (j + 1 < n) ok = ok && (xv[j + 1] > xv[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 1; j < NMAX - 1; ++j) {
+    if (j < n - 1) {
+      const T h = xv[j + 1] - xv[j];
+      const T dd = (yv[j + 1] - yv[j]) / h;
+      const T inv = T(1) / (T(2) * (hprev + h) - hprev * cpv[j - 1]);
+      dpv[j] = (T(6) * (dd - ddprev) - hprev * dpv[j - 1]) * inv;
+      cpv[j] = h * inv;
+      cpp = cpv[j];
+      dpp = dpv[j];
+      hprev = h;
+      ddprev = dd;
+    }
+  }
+  T last = T(0);
+  if (bc & 2) {  // P:1017-1018
+    ok = ok && finite(sn);
+    last = (T(6) * (sn - ddprev) - hprev * dpp) / (T(2) * hprev - hprev * cpp);
+  }
+  T nxt = last;
+#pragma unroll
+  for (int j = NMAX - 1; j >= 0; --j) {
+    if (j == n - 1) {
+      z[j] = last;
+    } else if (j < n - 1) {
+      nxt = dpv[j] - cpv[j] * nxt;
+      z[j] = nxt;
+    } else {
+      z[j] = T(0);
+    }
+  }
+  if (!ok) {
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) z[j] = qnan<T>();
+  }
+  return ok;
 }
 
 // K1r: one thread per curve, n <= NMAX, all in registers.
@@ -285,64 +363,8 @@ __global__ void __launch_bounds__(256) k1_thomas_regs(const T *__restrict__ x, c
       }
     }
   }
-  bool ok = true;
-  T cpv[NMAX], dpv[NMAX];
-  T hprev = xv[1] - xv[0];
-  T ddprev = (yv[1] - yv[0]) / hprev;
-  if (bc & 1) {  // P:966-971
-    const T s = yp1[c];
-    ok = ok && finite(s);
-    cpv[0] = T(0.5);
-    dpv[0] = T(3) * (ddprev - s) / hprev;
-  } else {
-    cpv[0] = T(0);
-    dpv[0] = T(0);
-  }
-  T cpp = cpv[0], dpp = dpv[0];
-#pragma unroll
-  for (int j = 0; j < NMAX; ++j) {
-    if (j < n) {
-      ok = ok && finite(xv[j]) && finite(yv[j]);
-      if (j + 1 < n) ok = ok && (xv[j + 1] > xv[j]);
-    }
-  }
-#pragma unroll
-  for (int j = 1; j < NMAX - 1; ++j) {
-    if (j < n - 1) {
-      const T h = xv[j + 1] - xv[j];
-      const T dd = (yv[j + 1] - yv[j]) / h;
-      const T inv = T(1) / (T(2) * (hprev + h) - hprev * cpv[j - 1]);
-      dpv[j] = (T(6) * (dd - ddprev) - hprev * dpv[j - 1]) * inv;
-      cpv[j] = h * inv;
-      cpp = cpv[j];
-      dpp = dpv[j];
-      hprev = h;
-      ddprev = dd;
-    }
-  }
   T z[NMAX];
-  T last = T(0);
-  if (bc & 2) {  // P:1017-1018
-    const T e = ypn[c];
-    ok = ok && finite(e);
-    last = (T(6) * (e - ddprev) - hprev * dpp) / (T(2) * hprev - hprev * cpp);
-  }
-  T nxt = last;
-#pragma unroll
-  for (int j = NMAX - 1; j >= 0; --j) {
-    if (j == n - 1) {
-      z[j] = last;
-    } else if (j < n - 1) {
-      nxt = dpv[j] - cpv[j] * nxt;
-      z[j] = nxt;
-    } else {
-      z[j] = T(0);
-    }
-  }
-  if (!ok) {
-#pragma unroll
-    for (int j = 0; j < NMAX; ++j) z[j] = qnan<T>();
-  }
+  const bool ok = thomas_regs<T, NMAX>(xv, yv, n, bc, (bc & 1) ? yp1[c] : T(0), (bc & 2) ? ypn[c] : T(0), z);
   raise_status_warp(!ok, kBadKnots);
   T *zc = y2 + c * n;
   if (vec) {

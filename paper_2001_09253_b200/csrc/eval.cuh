@@ -156,33 +156,46 @@ __device__ __forceinline__ void eval_packed(const Knot<T> *K, const T *E, const 
   const bool in = (q >= hd.x0) && (q <= hd.xn);  // false for NaN
   const T qc = in ? q : hd.x0;
   int lo;
-  if (MODE == MODE_BISECT) {
-    lo = min(eytz_count<T, L2>(E, qc), n - 2);
+  Knot<T> a, b;
+  if (MODE == MODE_UNIFORM) {
+    // direct index on the hinted grid; accepted only if x_g <= q < x_{g+1} (or g = n-2), so
+    // rounding or a wrong hint costs a (rare) bisection, never a wrong idx
+    lo = max(0, min((int)r_mul(r_sub(qc, hd.x0), hd.s), n - 2));
+    a = K[lo];
+    b = K[lo + 1];
+    if (!(a.x <= qc && (qc < b.x || lo == n - 2))) {
+      int l = 0, h = n - 1;
+      while (h - l > 1) {
+        const int mid = (l + h) >> 1;
+        if (K[mid].x <= qc) l = mid;
+        else h = mid;
+      }
+      lo = l;
+      a = K[lo];
+      b = K[lo + 1];
+    }
   } else {
-    int hi;
-    if (MODE == MODE_TABLE) {
-      const int b = bucket_of(qc, hd.x0, hd.s, nb);
-      lo = min((int)Tb[b], n - 2);  // clamps keep invalid (non-monotone) knots memory-safe
-      hi = max(lo, min((int)Tb[b + 1], n - 2));
-    } else {  // MODE_UNIFORM
-      lo = max(0, min((int)r_mul(r_sub(qc, hd.x0), hd.s), n - 2));
-      if (K[lo].x > qc) {  // the guess overshot (rounding, or a wrong hint)
-        hi = lo - 1;
-        lo = 0;
+    if (MODE == MODE_BISECT) {
+      lo = min(eytz_count<T, L2>(E, qc), n - 2);
+    } else {  // MODE_TABLE
+      const int bk = bucket_of(qc, hd.x0, hd.s, nb);
+      lo = min((int)Tb[bk], n - 2);  // clamps keep invalid (non-monotone) knots memory-safe
+      const int hi = max(lo, min((int)Tb[bk + 1], n - 2));
+      if (hi - lo > 2) {  // wide bracket (clustered knots): bisect it down
+        int h = hi;
+        do {
+          const int mid = (lo + h + 1) >> 1;
+          if (K[mid].x <= qc) lo = mid;
+          else h = mid - 1;
+        } while (h - lo > 2);
+        while (lo < h && K[lo + 1].x <= qc) ++lo;
       } else {
-        hi = n - 2;
+        while (lo < hi && K[lo + 1].x <= qc) ++lo;  // largest j in [lo, hi] with x_j <= q
       }
     }
-    if (hi - lo > 2) {  // wide bracket (clustered knots or a wrong hint): bisect it down
-      do {
-        const int mid = (lo + hi + 1) >> 1;
-        if (K[mid].x <= qc) lo = mid;
-        else hi = mid - 1;
-      } while (hi - lo > 2);
-    }
-    while (lo < hi && K[lo + 1].x <= qc) ++lo;  // largest j in [lo, hi] with x_j <= q
+    a = K[lo];
+    b = K[lo + 1];
   }
-  const Knot<T> a = K[lo], b = K[lo + 1];
   const T v = interp_core(qc, a.x, b.x, a.y, b.y, a.z, b.z, a.ih);
   j = in ? lo : -1;
   val = in ? v : qnan<T>();
@@ -224,6 +237,95 @@ template <typename T> struct StageLayout {
     total = off;
   }
 };
+
+// Packing pass of one staged item: nc curves with raw knots X, Y (curve-major, stride n) and
+// second derivatives Z (row stride zs) become {x, y, y2, 1/h} records K, headers Hd and the
+// mode's search structure (Eytzinger keys Xs with stride P, or the bucket table Tb).
+// Threads tid = 0 .. nt-1 of the caller's group share the work.
+template <typename T, int MODE, int L2>
+__device__ __forceinline__ void pack_item(const T *X, const T *Y, const T *Z, int zs, int nc, int n, int nb,
+                                          FastDiv divn, Knot<T> *K, CurveHdr<T> *Hd, T *Xs, uint16_t *Tb, int P,
+                                          int tid, int nt) {
+  const int tot = nc * n;
+  for (int e = tid; e < tot; e += nt) {
+    const int c = (int)divn.div((uint32_t)e);
+    const int j = e - c * n;
+    const T xj = X[e];
+    Knot<T> kk;
+    kk.x = xj;
+    kk.y = Y[e];
+    kk.z = Z[c * zs + j];
+    kk.ih = (j < n - 1) ? r_rcp(r_sub(X[e + 1], xj)) : T(0);
+    K[e] = kk;
+    if (j == 0 || (MODE == MODE_TABLE && j < n - 1)) {
+      const T x0 = X[c * n], xn = X[c * n + n - 1];
+      const T sc = (MODE == MODE_TABLE) ? (T)nb / (xn - x0) : (T)(n - 1) / (xn - x0);
+      if (j == 0) Hd[c] = CurveHdr<T>{x0, xn, sc, T(0)};
+      if (MODE == MODE_TABLE) {
+        uint16_t *Tc = Tb + c * (nb + 2);
+        if (j == 0) Tc[0] = 0;
+        const int blo = bucket_of(xj, x0, sc, nb);
+        const int bhi = (j == n - 2) ? nb + 1 : bucket_of(X[e + 1], x0, sc, nb);
+        for (int b = blo + 1; b <= bhi; ++b) Tc[b] = (uint16_t)j;
+      }
+    }
+  }
+  if (MODE == MODE_BISECT) {  // Eytzinger keys x_1 .. x_{n-1}, +inf padded
+    const int te = nc * P;
+    for (int e = tid; e < te; e += nt) {
+      const int c = e >> L2;
+      const int i = e & (P - 1);
+      if (i == 0) continue;
+      const int r = eytz_rank(i, L2) + 1;  // knot index
+      Xs[e] = (r < n) ? X[c * n + r] : (T)INFINITY;
+    }
+  }
+}
+
+// Locate + evaluate the cnt queries of one staged item (first query k0 of HBM; first curve
+// c0; the queries staged at Qs when BULK, else read from q).  Warp w of nw owns a contiguous
+// run of V-query groups; lane l takes groups wb+l, wb+l+32, ...  Returns "some query was
+// out of range".
+template <typename T, int MODE, int V, bool BULK, int L2>
+__device__ __forceinline__ bool eval_item_queries(const T *Qs, const T *__restrict__ q, int64_t k0, int64_t c0,
+                                                  int m, int cnt, int cpb, FastDiv divm, const Knot<T> *K,
+                                                  const CurveHdr<T> *Hd, const T *Xs, const uint16_t *Tb,
+                                                  const T *X, const T *Y, const T *Z, int n, int nb, int P,
+                                                  T *__restrict__ out, int32_t *__restrict__ idx, int w, int nw,
+                                                  int lane) {
+  constexpr bool PACKED = (MODE != MODE_BSEARCH);
+  bool oor = false;
+  const int ng = cnt / V;
+  const int per = (ng + nw - 1) / nw;
+  const int wb = w * per, we = min(ng, wb + per);
+  const int kbase = (int)(k0 - c0 * m);  // item's first query, relative to its first curve
+  for (int g = wb + lane; g < we; g += 32) {
+    T qv[V], val[V];
+    int jj[V];
+    if (BULK) {
+      VecIO<T, V>::load_shared(Qs + g * V, qv);
+    } else {
+      VecIO<T, V>::load(q + k0 + (int64_t)g * V, qv);
+    }
+    const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(kbase + g * V)) : 0;
+    if (PACKED) {
+      const CurveHdr<T> hd = Hd[cl];
+      const Knot<T> *Kc = K + cl * n;
+      const T *Ec = Xs + (size_t)cl * P;
+      const uint16_t *Tc = Tb + cl * (nb + 2);
+#pragma unroll
+      for (int i = 0; i < V; ++i) eval_packed<T, MODE, L2>(Kc, Ec, Tc, hd, n, nb, qv[i], val[i], jj[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qv[i], val[i], jj[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) oor |= (jj[i] < 0);
+    VecIO<T, V>::store(out + k0 + (int64_t)g * V, val);
+    if (idx) VecIO<T, V>::store_idx(idx + k0 + (int64_t)g * V, jj);
+  }
+  return oor;
+}
 
 // Persistent, double-buffered staged eval (unsorted queries).  Work item `it` = curves
 // [it*cpb, +cpb) with all their queries (cpb > 1), or queries [ch*qchunk, +qchunk) of curve
@@ -319,73 +421,11 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
     }
     const T *Y = X + cn, *Z = X + 2 * cn;
     if (PACKED) {
-      const int tot = nc * n;
-      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int c = (int)divn.div((uint32_t)e);
-        const int j = e - c * n;
-        const T xj = X[e];
-        Knot<T> kk;
-        kk.x = xj;
-        kk.y = Y[e];
-        kk.z = Z[e];
-        kk.ih = (j < n - 1) ? r_rcp(r_sub(X[e + 1], xj)) : T(0);
-        K[e] = kk;
-        if (j == 0 || (MODE == MODE_TABLE && j < n - 1)) {
-          const T x0 = X[c * n], xn = X[c * n + n - 1];
-          const T sc = (MODE == MODE_TABLE) ? (T)nb / (xn - x0) : (T)(n - 1) / (xn - x0);
-          if (j == 0) Hd[c] = CurveHdr<T>{x0, xn, sc, T(0)};
-          if (MODE == MODE_TABLE) {
-            uint16_t *Tc = Tb + c * (nb + 2);
-            if (j == 0) Tc[0] = 0;
-            const int blo = bucket_of(xj, x0, sc, nb);
-            const int bhi = (j == n - 2) ? nb + 1 : bucket_of(X[e + 1], x0, sc, nb);
-            for (int b = blo + 1; b <= bhi; ++b) Tc[b] = (uint16_t)j;
-          }
-        }
-      }
-      if (MODE == MODE_BISECT) {  // Eytzinger keys x_1 .. x_{n-1}, +inf padded
-        const int te = nc * P;
-        for (int e = threadIdx.x; e < te; e += blockDim.x) {
-          const int c = e >> L2;
-          const int i = e & (P - 1);
-          if (i == 0) continue;
-          const int r = eytz_rank(i, L2) + 1;  // knot index
-          Xs[e] = (r < n) ? X[c * n + r] : (T)INFINITY;
-        }
-      }
+      pack_item<T, MODE, L2>(X, Y, Z, n, nc, n, nb, divn, K, Hd, Xs, Tb, P, threadIdx.x, blockDim.x);
       __syncthreads();  // packed data built
     }
-
-    // the warp's contiguous run of groups within the item
-    const int ng = cnt / V;
-    const int per = (ng + nw - 1) / nw;
-    const int wb = w * per, we = min(ng, wb + per);
-    const int kbase = (int)(k0 - c0 * m);  // item's first query, relative to its first curve
-    for (int g = wb + lane; g < we; g += 32) {
-      T qv[V], val[V];
-      int jj[V];
-      if (BULK) {
-        VecIO<T, V>::load_shared(Qs + g * V, qv);
-      } else {
-        VecIO<T, V>::load(q + k0 + (int64_t)g * V, qv);
-      }
-      const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(kbase + g * V)) : 0;
-      if (PACKED) {
-        const CurveHdr<T> hd = Hd[cl];
-        const Knot<T> *Kc = K + cl * n;
-        const T *Ec = Xs + (size_t)cl * P;
-        const uint16_t *Tc = Tb + cl * (nb + 2);
-#pragma unroll
-        for (int i = 0; i < V; ++i) eval_packed<T, MODE, L2>(Kc, Ec, Tc, hd, n, nb, qv[i], val[i], jj[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < V; ++i) eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qv[i], val[i], jj[i]);
-      }
-#pragma unroll
-      for (int i = 0; i < V; ++i) oor |= (jj[i] < 0);
-      VecIO<T, V>::store(out + k0 + (int64_t)g * V, val);
-      if (idx) VecIO<T, V>::store_idx(idx + k0 + (int64_t)g * V, jj);
-    }
+    oor |= eval_item_queries<T, MODE, V, BULK, L2>(Qs, q, k0, c0, m, cnt, cpb, divm, K, Hd, Xs, Tb, X, Y, Z, n, nb,
+                                                   P, out, idx, w, nw, lane);
     __syncthreads();  // everyone is done with this item's stage and packed data
     if (threadIdx.x == 0) issue(it + 2 * G, s);
     s ^= 1;

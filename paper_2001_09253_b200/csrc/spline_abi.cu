@@ -1,7 +1,8 @@
 // spline_abi.cu -- the C ABI of include/spline.h: argument checks, kernel dispatch, launches.
 //
 // Dispatch (build, by n and dtype):
-//   n <= 128                      K1 k1_thomas_batched   one thread per curve
+//   n <= 8                        K1r k1_thomas_regs     one thread per curve, registers
+//   n <= 128                      K1 k1_thomas_pipe      two threads per curve, sweep from both ends
 //   n <= 256*RMAX (4096 f64,      K2 k_tile<FULL>        one CTA per curve: 256 leaves x R rows,
 //                  8192 f32)                              merge tree in shared memory
 //   longer                        K3 k_tile<REDUCE> -> K4 k4_top -> K5 k_tile<FINISH>   (tiled SPIKE)
@@ -20,6 +21,7 @@
 #include "build_tile.cuh"
 #include "common.cuh"
 #include "eval.cuh"
+#include "fused.cuh"
 
 using namespace fs;
 
@@ -148,14 +150,11 @@ int build_long(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T
 template <typename T>
 int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
             cudaStream_t st) {
-  if (n <= 16) {  // K1r: registers only
+  if (n <= kRegsNMax) {  // K1r: registers only (the fused kernel's SOLVE_REGS takes the same n)
     constexpr int VW = 16 / sizeof(T);
     const int vec = (n % VW == 0) && aligned16(x) && aligned16(y) && aligned16(y2);
     const int64_t grid = (batch + 255) / 256;
-    if (n <= 8)
-      k1_thomas_regs<T, 8><<<(unsigned)grid, 256, 0, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, vec);
-    else
-      k1_thomas_regs<T, 16><<<(unsigned)grid, 256, 0, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, vec);
+    k1_thomas_regs<T, kRegsNMax><<<(unsigned)grid, 256, 0, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, vec);
     return launch_rc();
   }
   if (n <= kK1MaxN) {  // K1: two threads per curve, staged odd-stride tiles
@@ -309,6 +308,108 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
   return launch_rc();
 }
 
+// ------------------------------------------------------------------ fused build + eval
+
+template <typename T, int MODE, int L2, int SOLVE>
+int launch_fused_k(const T *x, const T *y, int n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+                   const T *q, int64_t m, T *out, int32_t *idx, int cpb, int nchunks, int qchunk, int64_t nitems,
+                   cudaStream_t st) {
+  if constexpr (MODE == MODE_BISECT && L2 == 0) {
+    int l2 = 0;
+    while ((1 << l2) < n) ++l2;
+    if constexpr (SOLVE == SOLVE_REGS) {  // n <= 8
+      if (l2 <= 2) return launch_fused_k<T, MODE, 2, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      return launch_fused_k<T, MODE, 3, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+    } else {
+    switch (l2 < 2 ? 2 : l2) {
+      case 2: return launch_fused_k<T, MODE, 2, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 3: return launch_fused_k<T, MODE, 3, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 4: return launch_fused_k<T, MODE, 4, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 5: return launch_fused_k<T, MODE, 5, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 6: return launch_fused_k<T, MODE, 6, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      default: return launch_fused_k<T, MODE, 7, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+    }
+    }
+  } else {
+    const int qmax = (cpb > 1) ? cpb * (int)m : qchunk;
+    const FusedLayout<T> L(cpb, n, qmax, SOLVE, MODE);
+    const size_t sm = L.total;
+    auto kern = k_fused_staged<T, MODE, L2, SOLVE>;
+    if (int rc = set_smem(kern, sm)) return rc;
+    int occ = 0;
+    constexpr int NT = fused_threads(SOLVE);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, sm) != cudaSuccess || occ < 1) occ = 1;
+    const int64_t grid = std::min<int64_t>(nitems, (int64_t)occ * num_sms());
+    kern<<<(unsigned)grid, NT, sm, st>>>(x, y, n, batch, bc, yp1, ypn, y2, q, (int)m, out, idx, cpb, nchunks,
+                                                   qchunk, qmax, nitems, FastDiv((uint32_t)n), FastDiv((uint32_t)m));
+    return launch_rc();
+  }
+}
+
+constexpr size_t kFusedItemSmem = 72 * 1024;  // per-CTA target (3 CTAs per SM)
+constexpr int kFusedMaxN = 128;
+
+template <typename T> bool fused_eligible(const T *x, const T *y, int64_t n, const T *q, int64_t m, const T *out,
+                                          const int32_t *idx, const T *y2) {
+  constexpr int VW = 16 / sizeof(T);
+  if (n > kFusedMaxN || (n * sizeof(T)) % 16 != 0 || m % VW != 0) return false;
+  if (!aligned16(x) || !aligned16(y) || !aligned16(q) || !aligned16(out) || (y2 && !aligned16(y2))) return false;
+  if (idx && ((uintptr_t)idx & (4 * VW - 1)) != 0) return false;
+  const int mode = MODE_BISECT;  // the larger footprint of the two modes
+  const int solve = n <= kRegsNMax ? SOLVE_REGS : SOLVE_BABE;
+  return FusedLayout<T>(1, (int)n, kQMax, solve, mode).total <= kSmemCap;
+}
+
+template <typename T, int MODE>
+int launch_fused(const T *x, const T *y, int n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2, const T *q,
+                 int64_t m, T *out, int32_t *idx, cudaStream_t st) {
+  constexpr int VW = 16 / sizeof(T);
+  const int solve = n <= kRegsNMax ? SOLVE_REGS : SOLVE_BABE;
+  int cpb = 1, nchunks = 1, qchunk = (int)m;
+  int64_t nitems;
+  if (m >= 2048 || batch == 1) {
+    const int64_t want = (4 * 148 + batch - 1) / batch;
+    nchunks = (int)std::max<int64_t>({(int64_t)1, std::min<int64_t>(want, (m + 1023) / 1024),
+                                      (m + kQMax - 1) / kQMax});
+    qchunk = (int)((m + nchunks - 1) / nchunks);
+    qchunk = (qchunk + VW - 1) / VW * VW;
+    nchunks = (int)((m + qchunk - 1) / qchunk);
+    nitems = batch * nchunks;
+  } else {
+    int64_t c = std::max<int64_t>(1, kQMax / m);
+    c = std::min<int64_t>(c, batch);
+    while (c > 1 && FusedLayout<T>((int)c, n, (int)(c * m), solve, MODE).total > kFusedItemSmem) --c;
+    while (c > 1 && (uint64_t)c * m * m >= (1ull << 32)) c >>= 1;  // FastDiv range
+    cpb = (int)std::max<int64_t>(1, c);
+    nitems = (batch + cpb - 1) / cpb;
+  }
+  if (solve == SOLVE_REGS)
+    return launch_fused_k<T, MODE, 0, SOLVE_REGS>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks,
+                                                  qchunk, nitems, st);
+  return launch_fused_k<T, MODE, 0, SOLVE_BABE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks,
+                                                qchunk, nitems, st);
+}
+
+template <typename T>
+int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+                 const T *q, int64_t m, T *out, int32_t *idx, int flags, cudaStream_t st) {
+  if (m == 0) return y2 ? build_t<T>(x, y, n, batch, bc, yp1, ypn, y2, st) : SPLINE_OK;
+  if (fused_eligible<T>(x, y, n, q, m, out, idx, y2)) {
+    if (flags & SPLINE_X_UNIFORM)
+      return launch_fused<T, MODE_UNIFORM>(x, y, (int)n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+    return launch_fused<T, MODE_BISECT>(x, y, (int)n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  }
+  // not fusable (long curves, unaligned or ragged arrays): the two kernels back to back
+  T *yy = y2;
+  if (!yy) {
+    if (int rc = cuda_rc(cudaMallocAsync((void **)&yy, sizeof(T) * (size_t)n * batch, st))) return rc;
+  }
+  int rc = build_t<T>(x, y, n, batch, bc, yp1, ypn, yy, st);
+  if (!rc) rc = eval_t<T>(x, y, yy, n, batch, q, m, out, idx, flags, st);
+  if (!y2) cudaFreeAsync(yy, st);
+  return rc;
+}
+
 int check_build(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1, const void *ypn,
                 const void *y2, int dtype) {
   if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
@@ -390,6 +491,24 @@ int spline_eval(const void *x, const void *y, const void *y2, int64_t n, int64_t
                          (float *)out, idx, flags, st);
   return eval_t<double>((const double *)x, (const double *)y, (const double *)y2, n, batch, (const double *)q, m,
                         (double *)out, idx, flags, st);
+}
+
+int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1,
+                      const void *ypn, void *y2, const void *q, int64_t m, void *out, int32_t *idx, int flags,
+                      int dtype, spline_stream_t stream) {
+  if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
+  if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
+  if (m < 0 || m >= (int64_t(1) << 31) || bc < 0 || bc > 3) return SPLINE_EINVAL;
+  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM)) return SPLINE_EINVAL;
+  if (batch == 0) return SPLINE_OK;
+  if (!x || !y || ((bc & 1) && !yp1) || ((bc & 2) && !ypn)) return SPLINE_EINVAL;
+  if (m > 0 && (!q || !out)) return SPLINE_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SPLINE_F32)
+    return build_eval_t<float>((const float *)x, (const float *)y, n, batch, bc, (const float *)yp1,
+                               (const float *)ypn, (float *)y2, (const float *)q, m, (float *)out, idx, flags, st);
+  return build_eval_t<double>((const double *)x, (const double *)y, n, batch, bc, (const double *)yp1,
+                              (const double *)ypn, (double *)y2, (const double *)q, m, (double *)out, idx, flags, st);
 }
 
 int spline_build_f32(const float *x, const float *y, int64_t n, int64_t batch, int bc, const float *yp1,

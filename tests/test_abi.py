@@ -92,3 +92,19 @@ def test_api_rejects_cpu_tensors():
     from paper_2001_09253_b200 import api
     with pytest.raises(ValueError):
         api.build(torch.zeros(8, dtype=torch.float64), torch.zeros(8, dtype=torch.float64))
+
+
+def test_einval_build_eval():
+    lib = _lib.load()
+    p = ctypes.c_void_p(16)
+    F32, E = _lib.SPLINE_F32, _lib.SPLINE_EINVAL
+    f = lib.spline_build_eval
+    assert f(p, p, 2, 1, 0, None, None, p, p, 4, p, None, 0, F32, None) == E      # n < 3
+    assert f(p, p, 8, 1, 0, None, None, p, p, -1, p, None, 0, F32, None) == E     # m < 0
+    assert f(p, p, 8, 1, 1, None, None, p, p, 4, p, None, 0, F32, None) == E      # clamped, no yp1
+    assert f(p, p, 8, 1, 0, None, None, p, None, 4, p, None, 0, F32, None) == E   # NULL q with m > 0
+    assert f(p, p, 8, 1, 0, None, None, p, p, 4, None, None, 0, F32, None) == E   # NULL out
+    assert f(p, p, 8, 1, 0, None, None, p, p, 4, p, None, 4, F32, None) == E      # unknown flag
+    assert f(p, p, 8, 1, 5, None, None, p, p, 4, p, None, 0, F32, None) == E      # bad bc
+    assert f(None, p, 8, 1, 0, None, None, p, p, 4, p, None, 0, F32, None) == E   # NULL x
+    assert f(None, None, 8, 0, 0, None, None, None, None, 4, None, None, 0, F32, None) == _lib.SPLINE_OK

@@ -1,0 +1,151 @@
+"""GPU parity of spline_build_eval (build and evaluate in one call).
+
+Two bars: (1) the oracle, element by element (bit-exact idx; y2 and out within the north-star
+tolerances, reading c2) and (2) bitwise identity with spline_build followed by
+spline_eval on the same inputs -- the fused kernel runs the same arithmetic on chip.
+Cases span several work items and CTAs, ragged last items, chunked single curves, both solver
+kinds (registers for n <= 8, two-ended sweep otherwise), both search modes, the fallback for
+shapes the fused kernel does not take, bad knots and out-of-range / NaN queries.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import parity
+from paper_2001_09253_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2001_09253_b200 import api as a
+    a.status()
+    return a
+
+
+def _dev(wl):
+    t = parity.to_dev
+    return (t(wl.x), t(wl.y), t(wl.q), t(wl.yp1) if wl.yp1 is not None else None,
+            t(wl.ypn) if wl.ypn is not None else None)
+
+
+def check_fused(api, wl, flags=None, nthreads=8):
+    flags = wl.flags if flags is None else flags
+    dt = wl.np_dtype
+    tol = parity.tol_for(dt)
+    x, y, q, yp1, ypn = _dev(wl)
+    api.status()
+    y2, out, idx = api.build_eval(x, y, q, wl.bc, yp1, ypn, flags)
+    bits = api.status()
+    # (1) the oracle
+    y2_ref = parity.oracle_build(wl, nthreads)
+    out_ref, idx_ref, nbad = oracle.evaluate(wl.x, wl.y, y2_ref, wl.q, nthreads=nthreads)
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_ref)
+    e2 = parity.y2_rel_err(y2.cpu().numpy(), y2_ref, wl.x, wl.y)
+    eo = parity.out_rel_err(out.cpu().numpy(), out_ref, wl.y)
+    assert np.all(e2 <= tol), f"y2 max rel err {e2.max():.3e}"
+    assert np.all(eo <= tol), f"out max rel err {eo.max():.3e}"
+    assert (bits & api.STATUS_Q_OUT_OF_RANGE) == (api.STATUS_Q_OUT_OF_RANGE if nbad else 0)
+    # (2) bitwise the separate path
+    y2s = api.build(x, y, wl.bc, yp1, ypn)
+    outs, idxs = api.evaluate(x, y, y2s, q, flags)
+    assert torch.equal(y2.view(torch.int8), y2s.view(torch.int8)), "y2 differs from spline_build"
+    assert torch.equal(idx, idxs)
+    assert torch.equal(out.view(torch.int8), outs.view(torch.int8)), "out differs from build -> eval"
+    # (3) without y2 / without idx: same out
+    none, out2, idx2 = api.build_eval(x, y, q, wl.bc, yp1, ypn, flags, want_y2=False)
+    assert none is None and torch.equal(out2.view(torch.int8), out.view(torch.int8)) and torch.equal(idx2, idx)
+    _, out3, none3 = api.build_eval(x, y, q, wl.bc, yp1, ypn, flags, want_idx=False)
+    assert none3 is None and torch.equal(out3.view(torch.int8), out.view(torch.int8))
+    return float(e2.max()), float(eo.max())
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(batch=3), dict(m=4000), dict(m=100000)])
+def test_fused_cfg1_babe_f64(api, kw):
+    check_fused(api, workloads.generate(1, **kw))
+
+
+@pytest.mark.parametrize("kw", [dict(batch=4096), dict(batch=1001, m=252), dict(batch=77, n=64, m=4),
+                                dict(batch=33, n=128, m=64), dict(batch=5, n=24, m=2048),
+                                dict(batch=1, n=64, m=10000)])
+def test_fused_cfg2_babe_f32(api, kw):
+    check_fused(api, workloads.generate(2, **kw))
+
+
+@pytest.mark.parametrize("kw", [dict(batch=20000), dict(batch=4099, m=36), dict(batch=50, n=4, m=8),
+                                dict(batch=129, n=8, m=4096)])
+def test_fused_cfg3_regs_f32(api, kw):
+    wl = workloads.generate(3, **kw)
+    check_fused(api, wl)
+    check_fused(api, wl, flags=0)  # bisection instead of the uniform-grid index: same answer
+
+
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
+@pytest.mark.parametrize("dt,n", [(np.float32, 8), (np.float32, 12), (np.float64, 6), (np.float64, 10),
+                                  (np.float64, 128), (np.float32, 100)])
+def test_fused_bc_dtype_grid(api, bc, dt, n):
+    rng = np.random.default_rng(1000 * n + bc)
+    B, m = 300, 40
+    x = np.cumsum(rng.exponential(1.0, (B, n)) + 0.05, axis=1).astype(dt)
+    y = np.cumsum(rng.normal(size=(B, n)), axis=1).astype(dt)
+    q = rng.uniform(x[:, :1], x[:, -1:], (B, m)).astype(dt)
+    q[:, :5] = x[:, [0, n - 1, n // 2, 1, n - 2]]  # exact knots: ties, both ends
+    yp1 = rng.normal(size=B).astype(dt)
+    ypn = rng.normal(size=B).astype(dt)
+    spec = workloads.ConfigSpec(0, "t", B, n, m, "f32" if dt == np.float32 else "f64", bc, 0, 0)
+    check_fused(api, workloads.Workload(spec, x, y, q, yp1, ypn, bc, 0))
+
+
+@pytest.mark.parametrize("kw", [dict(n=63, m=255), dict(n=200, m=64), dict(n=5, m=33)])
+def test_fused_fallback_shapes(api, kw):
+    """Shapes the fused kernel does not take still give the oracle's answer (two kernels)."""
+    check_fused(api, workloads.generate(2, batch=300, **kw))
+
+
+def test_fused_unaligned_views(api):
+    wl = workloads.generate(2, batch=200)
+    x, y, q, yp1, ypn = _dev(wl)
+    # offset by one element: not 16-byte aligned -> the separate kernels
+    xs = torch.empty(x.numel() + 1, dtype=x.dtype, device=x.device)[1:].view_as(x).copy_(x)
+    y2, out, idx = api.build_eval(xs, y, q, wl.bc, yp1, ypn)
+    y2r, outr, idxr = api.build_eval(x, y, q, wl.bc, yp1, ypn)
+    assert torch.equal(idx, idxr) and torch.equal(out.view(torch.int8), outr.view(torch.int8))
+    assert torch.equal(y2.view(torch.int8), y2r.view(torch.int8))
+
+
+def test_fused_bad_knots_and_out_of_range(api):
+    wl = workloads.generate(2, batch=64)
+    wl.x[5, 10] = wl.x[5, 9]          # repeated knot
+    wl.y[9, 3] = np.nan                # non-finite value
+    wl.q[2, 7] = wl.x[2, 0] - 1.0      # below the range
+    wl.q[3, 8] = np.nan
+    x, y, q, yp1, ypn = _dev(wl)
+    api.status()
+    y2, out, idx = api.build_eval(x, y, q, wl.bc, yp1, ypn)
+    bits = api.status()
+    assert bits == api.STATUS_BAD_KNOTS | api.STATUS_Q_OUT_OF_RANGE
+    z = y2.cpu().numpy()
+    assert np.all(np.isnan(z[5])) and np.all(np.isnan(z[9]))
+    ok = [c for c in range(64) if c not in (5, 9)]
+    assert np.all(np.isfinite(z[ok]))
+    i = idx.cpu().numpy()
+    assert i[2, 7] == -1 and i[3, 8] == -1 and np.isnan(out[2, 7].item()) and np.isnan(out[3, 8].item())
+    y2s = api.build(x, y, wl.bc, yp1, ypn)
+    outs, idxs = api.evaluate(x, y, y2s, q, 0)
+    api.status()
+    assert torch.equal(idx, idxs)
+    assert torch.equal(out.view(torch.int8), outs.view(torch.int8))
+
+
+def test_fused_build_only_and_empty(api):
+    wl = workloads.generate(2, batch=10, m=4)
+    x, y, q, yp1, ypn = _dev(wl)
+    q0 = q[:, :0].contiguous()
+    y2, out, idx = api.build_eval(x, y, q0, wl.bc, yp1, ypn)
+    assert out.shape == (10, 0)
+    assert torch.equal(y2.view(torch.int8), api.build(x, y, wl.bc, yp1, ypn).view(torch.int8))
+    assert api.status() == 0
