@@ -20,8 +20,10 @@
  *   - Work is enqueued on `stream` (NULL = the legacy default stream) and the call
  *     returns without synchronising.  The library is re-entrant; the only shared
  *     mutable state is the device-wide data-error word read by spline_status().
- *   - Temporary workspace (long-curve SPIKE records only) comes from the
- *     stream-ordered allocator (cudaMallocAsync on `stream`).
+ *   - Temporary workspace (long-curve SPIKE records; y2 scratch of an unfused
+ *     spline_build_eval called without y2) comes from a library-owned stream-ordered
+ *     memory pool per device (cudaMallocFromPoolAsync on `stream`) that keeps its
+ *     memory between calls.
  *
  * Errors:
  *   - Argument errors are synchronous: the call returns SPLINE_EINVAL and enqueues

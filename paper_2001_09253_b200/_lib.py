@@ -41,7 +41,7 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    return os.environ.get("SPLINE_LIB_OVERRIDE", _build.LIB)  # tools/ experiments only
 
 
 def load() -> ctypes.CDLL:

@@ -78,25 +78,56 @@ __device__ __forceinline__ double nr_rcp(double a) {
   return __fma_rn(r, e, r);
 }
 
-// Eq. nr_formula on one interval, given ih = 1/h (the paper's inv_ba):
-//   A = (x1 - q) ih, B = (q - x0) ih,
-//   out = A y0 + B y1 + ((A^3 - A) y2_0 + (B^3 - B) y2_1) h^2 / 6.
-template <typename T>
-__device__ __forceinline__ T interp_core(T q, T x0, T x1, T y0, T y1, T z0, T z1, T ih) {
-  const T A = r_mul(r_sub(x1, q), ih);
-  const T B = r_mul(r_sub(q, x0), ih);
+// Eq. nr_formula on one interval [x0, x1] in the interval-record form every eval
+// kernel uses.  With h = x1 - x0, ih = 1/h (the paper's inv_ba), zs_k = y2_k h^2/6:
+//     A = (x1 - q) ih,  B = (q - x0) ih,  C = A (A^2 - 1),  D = B (B^2 - 1)
+//     out = A y0 + B y1 + (C y2_0 + D y2_1) h^2/6  =  (A y0 + C zs0) + (B y1 + D zs1)
+// computed as hi - lo with hi = A y0 + C zs0 and lo = (-B) y1 + (-D) zs1 from the pair
+// P = ((x0 - q) ih, (x1 - q) ih) = (-B, A): the two halves are the two lanes of one fp32x2
+// operation (FADD2 / FMUL2 / FFMA2, 7 instructions per query).  Every operation is explicitly
+// rounded, so the packed and the scalar forms -- and every kernel -- give identical bits.
+template <typename T> struct Ival { T x0, x1, y1, y0, zs1, zs0, ih, pad; };
+
+template <typename T> __device__ __forceinline__ Ival<T> make_ival(T x0, T x1, T y0, T y1, T z0, T z1) {
   const T h = r_sub(x1, x0);
   const T h26 = r_mul(r_mul(h, h), T(1) / T(6));
-  const T C = r_mul(A, r_fma(A, A, T(-1)));
-  const T D = r_mul(B, r_fma(B, B, T(-1)));
-  const T t = r_fma(C, z0, r_mul(D, z1));
-  const T r = r_fma(A, y0, r_mul(B, y1));
-  return r_fma(t, h26, r);
+  return Ival<T>{x0, x1, y1, y0, r_mul(z1, h26), r_mul(z0, h26), r_rcp(h), T(0)};
 }
 
+template <typename T> __device__ __forceinline__ T ival_interp(const Ival<T> &r, T q) {
+  const T nB = r_mul(r_sub(r.x0, q), r.ih), A = r_mul(r_sub(r.x1, q), r.ih);
+  const T nD = r_mul(nB, r_fma(nB, nB, T(-1))), C = r_mul(A, r_fma(A, A, T(-1)));
+  const T lo = r_fma(nD, r.zs1, r_mul(nB, r.y1));
+  const T hi = r_fma(C, r.zs0, r_mul(A, r.y0));
+  return r_sub(hi, lo);
+}
+
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+// fp32: the same operations on the lane pairs (x0, x1), (y1, y0), (zs1, zs0) -- bitwise the
+// scalar form (f32x2 arithmetic is lane-wise IEEE round-to-nearest).
+template <> __device__ __forceinline__ float ival_interp<float>(const Ival<float> &r, float q) {
+  const uint64_t X = pack2(r.x0, r.x1), Yp = pack2(r.y1, r.y0), Z = pack2(r.zs1, r.zs0);
+  const uint64_t I = pack2(r.ih, r.ih), Q = pack2(q, q), M1 = pack2(-1.0f, -1.0f);
+  uint64_t D, P, W, Pc, t, u;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(D) : "l"(X), "l"(Q));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(P) : "l"(D), "l"(I));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(W) : "l"(P), "l"(P), "l"(M1));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(Pc) : "l"(P), "l"(W));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(P), "l"(Yp));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(u) : "l"(Pc), "l"(Z), "l"(t));
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(u));
+  return __fsub_rn(hi, lo);
+}
+
+// From the raw arrays (kernels that do not stage the curve).
 template <typename T>
 __device__ __forceinline__ T nr_interp(T q, T x0, T x1, T y0, T y1, T z0, T z1) {
-  return interp_core(q, x0, x1, y0, y1, z0, z1, r_rcp(r_sub(x1, x0)));
+  return ival_interp<T>(make_ival<T>(x0, x1, y0, y1, z0, z1), q);
 }
 
 }  // namespace fs

@@ -5,11 +5,11 @@
 // Eq. nr_formula only holds for x_j <= x <= x_{j+1}.  Every search below ends in
 // comparisons against this rule, so guesses (bucket table, uniform-grid index, sorted-run
 // carry, interpolation guess) change speed, never idx.
-// Evaluate: Eq. nr_formula, interp_core in common.cuh (explicitly rounded, so
-// all kernels and hints give bitwise-identical out).
+// Evaluate: Eq. nr_formula in the interval-record form of common.cuh (Ival,
+// ival_interp; explicitly rounded, so all kernels and hints give bitwise-identical out).
 //
 //  k_eval_staged : unsorted queries on curves that fit in shared memory.  Persistent CTAs,
-//                  TMA bulk staging (double-buffered), packed knots {x, y, y2, 1/h}:
+//                  TMA bulk staging (double-buffered), packed interval records:
 //                    MODE_BISECT  -- branch-free bisection over +inf-padded knots (short curves)
 //                    MODE_TABLE   -- per-curve bucket table brackets each query
 //                    MODE_UNIFORM -- direct index (q-x_0)(n-1)/(x_{n-1}-x_0), corrected
@@ -86,12 +86,13 @@ __device__ __forceinline__ void eval_one(const T *X, const T *Y, const T *Z, int
   val = nr_interp(q, X[j], X[j + 1], Y[j], Y[j + 1], Z[j], Z[j + 1]);
 }
 
-// ---- packed knots (MODE_BISECT, MODE_TABLE, MODE_UNIFORM) -------------------------------
-// Per staged curve: K[j] = {x_j, y_j, y2_j, 1/h_j} (one 16/32-byte record per knot, so the
-// gather is two vector loads and the per-query division becomes a multiply by the
-// interval's precomputed reciprocal -- the paper's inv_ba).
-//   MODE_BISECT : branch-free bisection over the knots in Eytzinger order (see eytz_count):
-//                 ceil(log2 n) uniform steps, no divergence, conflict-free (short curves).
+// ---- packed curves (MODE_BISECT, MODE_TABLE, MODE_UNIFORM) ------------------------------
+// Per staged curve: the interval record of [x_j, x_{j+1}] (common.cuh Ival: x_j, x_{j+1},
+// y_{j+1}, y_j, y2_{j+1} h^2/6, y2_j h^2/6, 1/h -- the paper's inv_ba), so the
+// gather is one record (two 16-byte loads for fp32) and the evaluation 7 packed fp32x2
+// operations.  Record slots have stride n per curve (slot n-1 unused).
+//   MODE_BISECT : branch-free bisection over the knots in Eytzinger order (eytz_descend):
+//                 L2 = ceil(log2(n-1)) uniform steps, no divergence, conflict-free.
 //   MODE_TABLE  : bucket table over nb = 2n equal-width buckets of [x_0, x_{n-1}]:
 //                   bucket(v) = min(nb, (int)((v - x_0) * s)),   s = nb / (x_{n-1} - x_0)
 //                   Tb[b]     = max{ j in [0, n-2] : bucket(x_j) < b }   (Tb[0] = 0).
@@ -100,7 +101,16 @@ __device__ __forceinline__ void eval_one(const T *X, const T *Y, const T *Z, int
 //                 table only brackets the search (long curves, many queries per knot).
 //   MODE_UNIFORM: direct index (q - x_0)(n-1)/(x_{n-1} - x_0) on the hinted uniform grid.
 // Every search ends in comparisons x_j <= q, so idx is exact on any grid.
-template <typename T> struct Knot { T x, y, z, ih; };
+// The record is stored as two 16-byte (fp32) halves in separate arrays, so that each of the
+// two vector loads of a gather has a 16-byte stride across records (random record indices
+// then spread over all shared-memory bank groups; a 32-byte stride would use half of them).
+template <typename T> struct IvalA { T x0, x1, y1, y0; };
+template <typename T> struct IvalB { T zs1, zs0, ih, pad; };
+template <typename T> __device__ __forceinline__ Ival<T> load_ival(const IvalA<T> *A, const IvalB<T> *B, int j) {
+  const IvalA<T> a = A[j];
+  const IvalB<T> b = B[j];
+  return Ival<T>{a.x0, a.x1, a.y1, a.y0, b.zs1, b.zs0, b.ih, b.pad};
+}
 // Per staged curve: range and scale (one vector load per group of V queries).
 template <typename T> struct CurveHdr { T x0, xn, s, pad; };
 
@@ -111,11 +121,17 @@ template <typename T> __device__ __forceinline__ int bucket_of(T v, T x0, T s, i
   return (f >= T(0)) ? min((int)f, nb) : 0;  // (int) truncates; f >= 0 here
 }
 
-// MODE_BISECT search structure: the keys x_1 .. x_{n-1} (padded with +inf to 2^L2 - 1 keys)
-// in Eytzinger (breadth-first) order, E[1 .. 2^L2 - 1], E[i]'s children at 2i, 2i+1.  A
-// branch-free descent i <- 2i + (E[i] <= q) of exactly L2 steps ends at i = 2^L2 + c with
-// c = #{keys <= q}, which is the locate rule's answer (clamped to n-2 for q = x_{n-1}).
+// MODE_BISECT search structure: the keys x_1 .. x_{n-2} (padded with +inf to 2^L2 - 1 keys,
+// 2^L2 >= n-1) in Eytzinger (breadth-first) order, E[1 .. 2^L2 - 1], E[i]'s children at 2i,
+// 2i+1.  A branch-free descent i <- 2i + (E[i] <= q) of exactly L2 steps ends at
+// i = 2^L2 + c with c = #{keys <= q}: for x_0 <= q <= x_{n-1} that is the locate rule's
+// answer, the largest j in [0, n-2] with x_j <= q (x_{n-1} is deliberately not a key).
 // Level t of the tree is 2^t consecutive words, so the probes of a warp hit distinct banks.
+__host__ __device__ constexpr int eytz_levels(int n) {
+  int l = 2;
+  while ((1 << l) < n - 1) ++l;
+  return l;
+}
 __device__ __forceinline__ float lds_f(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -126,20 +142,20 @@ __device__ __forceinline__ double lds_f(uint32_t a, double) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
   return v;
 }
-// The descent on shared-memory byte addresses: a_{t+1} = 2 a_t + (E[i] <= q ? s - base : -base)
-// (a = base + s*i), i.e. one load, one compare, one select and one multiply-add per level.
-template <typename T, int L2> __device__ __forceinline__ int eytz_count(const T *E, T q) {
-  const uint32_t base = smem_u32(E);
-  const uint32_t k0 = 0u - base, k1 = (uint32_t)sizeof(T) - base;
-  uint32_t a = base + (uint32_t)sizeof(T);
+// The descent on shared-memory byte addresses a = ebase + s i: a <- 2a - ebase (+ s when
+// E[i] <= q), one load, one compare and two integer adds per level.  Returns the final a,
+// = ebase + s (2^L2 + c).
+template <typename T, int L2> __device__ __forceinline__ uint32_t eytz_descend(uint32_t ebase, T q) {
+  uint32_t a = ebase + (uint32_t)sizeof(T);
 #pragma unroll
   for (int t = 0; t < L2; ++t) {
     T v;
     if constexpr (sizeof(T) == 4) v = lds_f(a);
     else v = lds_f(a, 0.0);
-    a = 2u * a + (v <= q ? k1 : k0);
+    a = 2u * a - ebase;
+    if (v <= q) a += (uint32_t)sizeof(T);
   }
-  return (int)((a - base) / (uint32_t)sizeof(T)) - (1 << L2);
+  return a;
 }
 
 // in-order rank (0-based) of breadth-first node i (1-based) in a complete tree of depth L2
@@ -148,55 +164,48 @@ __device__ __forceinline__ int eytz_rank(int i, int L2) {
   return ((2 * (i - (1 << d)) + 1) << (L2 - 1 - d)) - 1;
 }
 
-// Locate + evaluate one query against a packed curve.  Branch-light: out-of-range / NaN
-// queries run the same path on a clamped stand-in and are masked at the end.
+// Locate + evaluate one query against a packed curve (record halves Rc / Sc, Eytzinger keys
+// at shared address ebase).  Branch-light: out-of-range / NaN queries run the same path on a
+// clamped stand-in (qc = x_0) and are masked at the end.
 template <typename T, int MODE, int L2>
-__device__ __forceinline__ void eval_packed(const Knot<T> *K, const T *E, const uint16_t *Tb,
-                                            const CurveHdr<T> &hd, int n, int nb, T q, T &val, int &j) {
-  const bool in = (q >= hd.x0) && (q <= hd.xn);  // false for NaN
-  const T qc = in ? q : hd.x0;
+__device__ __forceinline__ void eval_packed(const IvalA<T> *Rc, const IvalB<T> *Sc, uint32_t ebase,
+                                            const uint16_t *Tb, const CurveHdr<T> &hd, int n, int nb, T q, T &val,
+                                            int &j) {
+  const T qc = fmin(fmax(q, hd.x0), hd.xn);  // NaN -> x_0 (fmax returns the number)
+  const bool in = (qc == q);                 // false for NaN and for q outside [x_0, x_{n-1}]
   int lo;
-  Knot<T> a, b;
-  if (MODE == MODE_UNIFORM) {
-    // direct index on the hinted grid; accepted only if x_g <= q < x_{g+1} (or g = n-2), so
-    // rounding or a wrong hint costs a (rare) bisection, never a wrong idx
+  if (MODE == MODE_BISECT) {
+    const uint32_t a = eytz_descend<T, L2>(ebase, qc);
+    // (the clamp only matters for invalid knots, e.g. x_{n-1} = +inf: memory safety)
+    lo = min((int)((a - ebase) / (uint32_t)sizeof(T)) - (1 << L2), n - 2);
+  } else if (MODE == MODE_UNIFORM) {
+    // direct index on the hinted grid; accepted only if x_g <= q < x_{g+1} (or g = n-2, i.e.
+    // x_{g+1} = x_{n-1}), so rounding or a wrong hint costs a (rare) bisection, never a wrong idx
     lo = max(0, min((int)r_mul(r_sub(qc, hd.x0), hd.s), n - 2));
-    a = K[lo];
-    b = K[lo + 1];
-    if (!(a.x <= qc && (qc < b.x || lo == n - 2))) {
+    const T xa = Rc[lo].x0, xb = Rc[lo].x1;
+    if (!(xa <= qc && (qc < xb || xb == hd.xn))) {
       int l = 0, h = n - 1;
       while (h - l > 1) {
         const int mid = (l + h) >> 1;
-        if (K[mid].x <= qc) l = mid;
+        if (Rc[mid].x0 <= qc) l = mid;
         else h = mid;
       }
       lo = l;
-      a = K[lo];
-      b = K[lo + 1];
     }
-  } else {
-    if (MODE == MODE_BISECT) {
-      lo = min(eytz_count<T, L2>(E, qc), n - 2);
-    } else {  // MODE_TABLE
-      const int bk = bucket_of(qc, hd.x0, hd.s, nb);
-      lo = min((int)Tb[bk], n - 2);  // clamps keep invalid (non-monotone) knots memory-safe
-      const int hi = max(lo, min((int)Tb[bk + 1], n - 2));
-      if (hi - lo > 2) {  // wide bracket (clustered knots): bisect it down
-        int h = hi;
-        do {
-          const int mid = (lo + h + 1) >> 1;
-          if (K[mid].x <= qc) lo = mid;
-          else h = mid - 1;
-        } while (h - lo > 2);
-        while (lo < h && K[lo + 1].x <= qc) ++lo;
-      } else {
-        while (lo < hi && K[lo + 1].x <= qc) ++lo;  // largest j in [lo, hi] with x_j <= q
-      }
+  } else {  // MODE_TABLE
+    const int bk = bucket_of(qc, hd.x0, hd.s, nb);
+    lo = min((int)Tb[bk], n - 2);  // clamps keep invalid (non-monotone) knots memory-safe
+    int hi = max(lo, min((int)Tb[bk + 1], n - 2));
+    if (hi - lo > 2) {  // wide bracket (clustered knots): bisect it down
+      do {
+        const int mid = (lo + hi + 1) >> 1;
+        if (Rc[mid].x0 <= qc) lo = mid;
+        else hi = mid - 1;
+      } while (hi - lo > 2);
     }
-    a = K[lo];
-    b = K[lo + 1];
+    while (lo < hi && Rc[lo + 1].x0 <= qc) ++lo;  // largest j in [lo, hi] with x_j <= q
   }
-  const T v = interp_core(qc, a.x, b.x, a.y, b.y, a.z, b.z, a.ih);
+  const T v = ival_interp<T>(load_ival(Rc, Sc, lo), qc);
   j = in ? lo : -1;
   val = in ? v : qnan<T>();
 }
@@ -217,17 +226,17 @@ __host__ __device__ constexpr int pow2_at_least(int v) {
 // evaluated.
 template <typename T> struct StageLayout {
   size_t raw0, rawstep, qoff, knots, hdr, xs, table, total;
-  int P;  // Eytzinger array stride per curve (MODE_BISECT): 2^L2 >= n
+  int P;  // Eytzinger array stride per curve (MODE_BISECT): 2^L2 >= n - 1
   __host__ __device__ StageLayout(int cpb, int n, int mode, int qmax) {
     const bool packed = mode != MODE_BSEARCH;
-    P = pow2_at_least(n);
+    P = 1 << eytz_levels(n);
     const size_t rawb = 3 * sizeof(T) * (size_t)cpb * n;
     raw0 = kStageHeader;
     qoff = align16(rawb);
     rawstep = align16(qoff + sizeof(T) * (size_t)qmax);
     size_t off = raw0 + 2 * rawstep;
     knots = off;
-    if (packed) off = align16(off + sizeof(Knot<T>) * (size_t)cpb * n);
+    if (packed) off = align16(off + sizeof(Ival<T>) * (size_t)cpb * n);
     hdr = off;
     if (packed) off = align16(off + sizeof(CurveHdr<T>) * (size_t)cpb);
     xs = off;
@@ -244,19 +253,19 @@ template <typename T> struct StageLayout {
 // Threads tid = 0 .. nt-1 of the caller's group share the work.
 template <typename T, int MODE, int L2>
 __device__ __forceinline__ void pack_item(const T *X, const T *Y, const T *Z, int zs, int nc, int n, int nb,
-                                          FastDiv divn, Knot<T> *K, CurveHdr<T> *Hd, T *Xs, uint16_t *Tb, int P,
-                                          int tid, int nt) {
+                                          FastDiv divn, IvalA<T> *RA, IvalB<T> *RB, CurveHdr<T> *Hd, T *Xs,
+                                          uint16_t *Tb, int P, int tid, int nt) {
   const int tot = nc * n;
   for (int e = tid; e < tot; e += nt) {
     const int c = (int)divn.div((uint32_t)e);
     const int j = e - c * n;
     const T xj = X[e];
-    Knot<T> kk;
-    kk.x = xj;
-    kk.y = Y[e];
-    kk.z = Z[c * zs + j];
-    kk.ih = (j < n - 1) ? r_rcp(r_sub(X[e + 1], xj)) : T(0);
-    K[e] = kk;
+    if (j < n - 1) {
+      const T *zc = Z + c * zs + j;
+      const Ival<T> r = make_ival<T>(xj, X[e + 1], Y[e], Y[e + 1], zc[0], zc[1]);
+      RA[e] = IvalA<T>{r.x0, r.x1, r.y1, r.y0};
+      RB[e] = IvalB<T>{r.zs1, r.zs0, r.ih, r.pad};
+    }
     if (j == 0 || (MODE == MODE_TABLE && j < n - 1)) {
       const T x0 = X[c * n], xn = X[c * n + n - 1];
       const T sc = (MODE == MODE_TABLE) ? (T)nb / (xn - x0) : (T)(n - 1) / (xn - x0);
@@ -270,14 +279,14 @@ __device__ __forceinline__ void pack_item(const T *X, const T *Y, const T *Z, in
       }
     }
   }
-  if (MODE == MODE_BISECT) {  // Eytzinger keys x_1 .. x_{n-1}, +inf padded
+  if (MODE == MODE_BISECT) {  // Eytzinger keys x_1 .. x_{n-2}, +inf padded
     const int te = nc * P;
     for (int e = tid; e < te; e += nt) {
       const int c = e >> L2;
       const int i = e & (P - 1);
       if (i == 0) continue;
       const int r = eytz_rank(i, L2) + 1;  // knot index
-      Xs[e] = (r < n) ? X[c * n + r] : (T)INFINITY;
+      Xs[e] = (r <= n - 2) ? X[c * n + r] : (T)INFINITY;
     }
   }
 }
@@ -288,7 +297,8 @@ __device__ __forceinline__ void pack_item(const T *X, const T *Y, const T *Z, in
 // out of range".
 template <typename T, int MODE, int V, bool BULK, int L2>
 __device__ __forceinline__ bool eval_item_queries(const T *Qs, const T *__restrict__ q, int64_t k0, int64_t c0,
-                                                  int m, int cnt, int cpb, FastDiv divm, const Knot<T> *K,
+                                                  int m, int cnt, int cpb, FastDiv divm, const IvalA<T> *RA,
+                                                  const IvalB<T> *RB,
                                                   const CurveHdr<T> *Hd, const T *Xs, const uint16_t *Tb,
                                                   const T *X, const T *Y, const T *Z, int n, int nb, int P,
                                                   T *__restrict__ out, int32_t *__restrict__ idx, int w, int nw,
@@ -310,11 +320,12 @@ __device__ __forceinline__ bool eval_item_queries(const T *Qs, const T *__restri
     const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(kbase + g * V)) : 0;
     if (PACKED) {
       const CurveHdr<T> hd = Hd[cl];
-      const Knot<T> *Kc = K + cl * n;
-      const T *Ec = Xs + (size_t)cl * P;
+      const IvalA<T> *Rc = RA + cl * n;
+      const IvalB<T> *Sc = RB + cl * n;
+      const uint32_t ebase = smem_u32(Xs + (size_t)cl * P);
       const uint16_t *Tc = Tb + cl * (nb + 2);
 #pragma unroll
-      for (int i = 0; i < V; ++i) eval_packed<T, MODE, L2>(Kc, Ec, Tc, hd, n, nb, qv[i], val[i], jj[i]);
+      for (int i = 0; i < V; ++i) eval_packed<T, MODE, L2>(Rc, Sc, ebase, Tc, hd, n, nb, qv[i], val[i], jj[i]);
     } else {
 #pragma unroll
       for (int i = 0; i < V; ++i) eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qv[i], val[i], jj[i]);
@@ -348,7 +359,8 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const StageLayout<T> L(cpb, n, MODE, BULK ? qmax : 0);
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);  // bar[0], bar[1]
-  Knot<T> *K = reinterpret_cast<Knot<T> *>(smem_raw + L.knots);
+  IvalA<T> *KA = reinterpret_cast<IvalA<T> *>(smem_raw + L.knots);
+  IvalB<T> *KB = reinterpret_cast<IvalB<T> *>(KA + (size_t)cpb * n);
   CurveHdr<T> *Hd = reinterpret_cast<CurveHdr<T> *>(smem_raw + L.hdr);
   T *Xs = reinterpret_cast<T *>(smem_raw + L.xs);
   uint16_t *Tb = reinterpret_cast<uint16_t *>(smem_raw + L.table);
@@ -421,11 +433,11 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
     }
     const T *Y = X + cn, *Z = X + 2 * cn;
     if (PACKED) {
-      pack_item<T, MODE, L2>(X, Y, Z, n, nc, n, nb, divn, K, Hd, Xs, Tb, P, threadIdx.x, blockDim.x);
+      pack_item<T, MODE, L2>(X, Y, Z, n, nc, n, nb, divn, KA, KB, Hd, Xs, Tb, P, threadIdx.x, blockDim.x);
       __syncthreads();  // packed data built
     }
-    oor |= eval_item_queries<T, MODE, V, BULK, L2>(Qs, q, k0, c0, m, cnt, cpb, divm, K, Hd, Xs, Tb, X, Y, Z, n, nb,
-                                                   P, out, idx, w, nw, lane);
+    oor |= eval_item_queries<T, MODE, V, BULK, L2>(Qs, q, k0, c0, m, cnt, cpb, divm, KA, KB, Hd, Xs, Tb, X, Y, Z, n,
+                                                   nb, P, out, idx, w, nw, lane);
     __syncthreads();  // everyone is done with this item's stage and packed data
     if (threadIdx.x == 0) issue(it + 2 * G, s);
     s ^= 1;

@@ -12,10 +12,11 @@
 //                           n >  8 : two lanes per curve, the sweep from both ends meeting in
 //                                    the middle (build_thomas.cuh babe_tile), on an
 //                                    odd-stride transposed copy (conflict-free)
-//   8 evaluator warps    pack {x, y, y2, 1/h} + search keys, locate + Eq. nr_formula for the
+//   8 evaluator warps    pack interval records + search keys, locate + Eq. nr_formula for the
 //                        item's queries, 16-byte streaming stores of out / idx
 //
-// Warp specialisation: the solver warps work up to two items ahead of the evaluator warps;
+// Warp specialisation: two solver warps take alternate items and work up to two items ahead of
+// the evaluator warps;
 // hand-offs are named barriers (bar.arrive / bar.sync): TFULL[s] "y2 tile s is ready",
 // TEMPTY[s] "y2 tile s has been packed, the solver may overwrite it".  The solve
 // (a serial chain of ~n/2 dependent steps per curve) is latency-bound; overlapping it with
@@ -45,7 +46,7 @@ constexpr int kRegsNMax = 8;     // SOLVE_REGS for n <= 8
 constexpr int kBabeCurves = 16;  // curves per solver-warp pass (2 lanes each)
 constexpr int kKnotStages = 3;   // x, y (+ y2 tile) stages
 constexpr int kQueryStages = 2;
-// solver warps per CTA: the register solve is short but covers 128+ curves per item
+// solver warps per CTA (each solves whole items, alternately)
 __host__ __device__ constexpr int fused_solver_warps(int solve) { return solve == SOLVE_REGS ? 2 : 1; }
 __host__ __device__ constexpr int fused_threads(int solve) { return kFusedEvalThreads + 32 * fused_solver_warps(solve); }
 // named barrier ids (0 is __syncthreads)
@@ -55,7 +56,7 @@ template <typename T> struct FusedLayout {
   size_t kst0, kststep, qst0, qststep, ytile, ytstep, scratch, scrstep, knots, hdr, xs, total;
   int P, S2;
   __host__ __device__ FusedLayout(int cpb, int n, int qmax, int solve, int mode) {
-    P = pow2_at_least(n);
+    P = 1 << eytz_levels(n);
     S2 = (solve == SOLVE_BABE) ? (n | 1) : n;
     size_t off = 64;  // mbarriers: knot stages, then query stages
     kst0 = off;
@@ -71,7 +72,7 @@ template <typename T> struct FusedLayout {
     scrstep = (solve == SOLVE_BABE) ? align16(sizeof(T) * (size_t)(kBabeCurves + 2) * S2) : 0;
     off += fused_solver_warps(solve) * scrstep;
     knots = off;
-    off = align16(off + sizeof(Knot<T>) * (size_t)cpb * n);
+    off = align16(off + sizeof(Ival<T>) * (size_t)cpb * n);
     hdr = off;
     off = align16(off + sizeof(CurveHdr<T>) * (size_t)cpb);
     xs = off;
@@ -179,12 +180,13 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
                    int64_t nitems, FastDiv divn, FastDiv divm) {
   constexpr int V = 16 / sizeof(T);
   constexpr int NSW = fused_solver_warps(SOLVE);
-  constexpr int NT = fused_threads(SOLVE);
+  constexpr int NB = kFusedEvalThreads + 32;  // named-barrier participants: evaluators + one solver warp
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const FusedLayout<T> L(cpb, n, qmax, SOLVE, MODE);
   uint64_t *kbar = reinterpret_cast<uint64_t *>(smem_raw);  // [kKnotStages]
   uint64_t *qbar = kbar + kKnotStages;                       // [kQueryStages]
-  Knot<T> *K = reinterpret_cast<Knot<T> *>(smem_raw + L.knots);
+  IvalA<T> *KA = reinterpret_cast<IvalA<T> *>(smem_raw + L.knots);
+  IvalB<T> *KB = reinterpret_cast<IvalB<T> *>(KA + (size_t)cpb * n);
   CurveHdr<T> *Hd = reinterpret_cast<CurveHdr<T> *>(smem_raw + L.hdr);
   T *Xs = reinterpret_cast<T *>(smem_raw + L.xs);
   const int P = L.P, S2 = L.S2;
@@ -243,26 +245,27 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
   bool oor = false;
 
   if (warp >= kFusedEvalWarps) {
-    // ---------------- solver warps
+    // ---------------- solver warps: warp sw takes the items k = sw, sw + NSW, ... whole, so
+    // NSW solves (latency-bound dependency chains) are in flight at once
     const int sw = warp - kFusedEvalWarps;
-    for (int k = 0; k < nmine; ++k) {
+    for (int k = sw; k < nmine; k += NSW) {
       const int ks = k % kKnotStages;
       const int64_t it = first + (int64_t)k * G;
       int64_t c0, k0;
       int nc, cnt;
       item_of(it, c0, k0, nc, cnt);
       mbar_wait(kbar + ks, (uint32_t)(k / kKnotStages) & 1u);
-      if (k >= kKnotStages) nbar_sync(BAR_TEMPTY + ks, NT);  // tile ks packed (item k-3)
+      if (k >= kKnotStages) nbar_sync(BAR_TEMPTY + ks, NB);  // tile ks packed (item k-3)
       const T *Xr = kstage(ks);
       const T *Yr = Xr + cn;
       T *y2o = (y2 && (cpb > 1 || it % nchunks == 0)) ? y2 : nullptr;  // chunk 0 writes y2
       if constexpr (SOLVE == SOLVE_BABE)
         fused_solve_babe<T>(Xr, Yr, ytile(ks), reinterpret_cast<T *>(smem_raw + L.scratch + sw * L.scrstep), S2, n,
-                            nc, c0, bc, yp1, ypn, y2o, divn, lane, sw, NSW);
+                            nc, c0, bc, yp1, ypn, y2o, divn, lane, 0, 1);
       else
-        fused_solve_regs<T>(Xr, Yr, ytile(ks), n, nc, c0, bc, yp1, ypn, y2o, lane, sw, NSW);
+        fused_solve_regs<T>(Xr, Yr, ytile(ks), n, nc, c0, bc, yp1, ypn, y2o, lane, 0, 1);
       __syncwarp();
-      nbar_arrive(BAR_TFULL + ks, NT);
+      nbar_arrive(BAR_TFULL + ks, NB);
     }
   } else {
     // ---------------- evaluator warps
@@ -272,17 +275,17 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
       int64_t c0, k0;
       int nc, cnt;
       item_of(it, c0, k0, nc, cnt);
-      nbar_sync(BAR_TFULL + ks, NT);                           // y2 tile ks ready (so the stage landed)
+      nbar_sync(BAR_TFULL + ks, NB);                           // y2 tile ks ready (so the stage landed)
       mbar_wait(kbar + ks, (uint32_t)(k / kKnotStages) & 1u);  // completes at once; orders the TMA writes
       const T *X = kstage(ks);
       const T *Y = X + cn;
-      pack_item<T, MODE, L2>(X, Y, ytile(ks), S2, nc, n, 0, divn, K, Hd, Xs, nullptr, P, threadIdx.x,
+      pack_item<T, MODE, L2>(X, Y, ytile(ks), S2, nc, n, 0, divn, KA, KB, Hd, Xs, nullptr, P, threadIdx.x,
                              kFusedEvalThreads);
-      if (k + kKnotStages < nmine) nbar_arrive(BAR_TEMPTY + ks, NT);  // this thread is done with tile ks
+      if (k + kKnotStages < nmine) nbar_arrive(BAR_TEMPTY + ks, NB);  // this thread is done with tile ks
       nbar_sync(BAR_EVAL, kFusedEvalThreads);                          // packed data built; stage ks free
       if (threadIdx.x == 0) issue_knots(it + kKnotStages * G, ks);
       mbar_wait(qbar + qs, (uint32_t)(k / kQueryStages) & 1u);
-      oor |= eval_item_queries<T, MODE, V, true, L2>(qstage(qs), q, k0, c0, m, cnt, cpb, divm, K, Hd, Xs, nullptr,
+      oor |= eval_item_queries<T, MODE, V, true, L2>(qstage(qs), q, k0, c0, m, cnt, cpb, divm, KA, KB, Hd, Xs, nullptr,
                                                      X, Y, ytile(ks), n, 0, P, out, idx, warp, kFusedEvalWarps,
                                                      lane);
       nbar_sync(BAR_EVAL, kFusedEvalThreads);  // done with query stage qs and the packed data

@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
 
 #include "../../include/spline.h"
 #include "build_thomas.cuh"
@@ -43,6 +45,30 @@ template <typename K> int set_smem(K kernel, size_t bytes) {
 }
 
 inline int launch_rc() { return cuda_rc(cudaGetLastError()); }
+
+// Stream-ordered scratch (SPIKE tile records; y2 for an unfused spline_build_eval without y2)
+// from a library-owned pool per device that keeps its memory between calls (release
+// threshold = max), so repeated calls do not map and unmap device memory.
+inline int ws_alloc(void **p, size_t bytes, cudaStream_t st) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[128] = {};
+  int dev = 0;
+  if (int rc = cuda_rc(cudaGetDevice(&dev))) return rc;
+  if (dev < 0 || dev >= 128) return SPLINE_ECUDA;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      if (int rc = cuda_rc(cudaMemPoolCreate(&pools[dev], &props))) return rc;
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  return cuda_rc(cudaMallocFromPoolAsync(p, bytes, pools[dev], st));
+}
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 inline int num_sms() {
   static int sms = 0;
@@ -135,7 +161,7 @@ int build_long(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T
   const int64_t ntiles = (n + 256 * R - 1) / (256 * R);
   const size_t bytes = spike_ws_layout<T>(ntiles, batch, nullptr, nullptr);
   void *base = nullptr;
-  if (int rc = cuda_rc(cudaMallocAsync(&base, bytes, st))) return rc;
+  if (int rc = ws_alloc(&base, bytes, st)) return rc;
   SpikeWs w;
   spike_ws_layout<T>(ntiles, batch, &w, (char *)base);
   int rc = cuda_rc(cudaMemsetAsync(w.badflag, 0, sizeof(int) * batch, st));
@@ -159,7 +185,7 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
   }
   if (n <= kK1MaxN) {  // K1: two threads per curve, staged odd-stride tiles
     const int S = (int)(n | 1);
-    if ((n * sizeof(T)) % 16 == 0 && aligned16(x) && aligned16(y)) {
+    if (!getenv("SPLINE_K1_BABE") && (n * sizeof(T)) % 16 == 0 && aligned16(x) && aligned16(y)) {
       // persistent + TMA-pipelined; CPB curves per tile (2 threads each)
       int cpb = 64;
       const auto smem_of = [&](int c) {
@@ -197,10 +223,8 @@ int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
                     int32_t *idx, int cpb, int nchunks, int qchunk, int64_t nitems, cudaStream_t st) {
   static_assert(!BULK || V > 1, "query staging needs 16-byte query groups");
   if constexpr (MODE == MODE_BISECT && L2 == 0) {
-    // pick the compile-time search depth: 2^L2 >= n
-    int l2 = 0;
-    while ((1 << l2) < n) ++l2;
-    switch (l2 < 2 ? 2 : l2) {
+    // the compile-time search depth: 2^L2 >= n - 1
+    switch (eytz_levels(n)) {
       case 2: return launch_staged_k<T, MODE, V, BULK, 2>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
       case 3: return launch_staged_k<T, MODE, V, BULK, 3>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
       case 4: return launch_staged_k<T, MODE, V, BULK, 4>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
@@ -315,13 +339,12 @@ int launch_fused_k(const T *x, const T *y, int n, int64_t batch, int bc, const T
                    const T *q, int64_t m, T *out, int32_t *idx, int cpb, int nchunks, int qchunk, int64_t nitems,
                    cudaStream_t st) {
   if constexpr (MODE == MODE_BISECT && L2 == 0) {
-    int l2 = 0;
-    while ((1 << l2) < n) ++l2;
+    const int l2 = eytz_levels(n);
     if constexpr (SOLVE == SOLVE_REGS) {  // n <= 8
       if (l2 <= 2) return launch_fused_k<T, MODE, 2, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
       return launch_fused_k<T, MODE, 3, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
     } else {
-    switch (l2 < 2 ? 2 : l2) {
+    switch (l2) {
       case 2: return launch_fused_k<T, MODE, 2, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
       case 3: return launch_fused_k<T, MODE, 3, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
       case 4: return launch_fused_k<T, MODE, 4, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
@@ -402,7 +425,7 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
   // not fusable (long curves, unaligned or ragged arrays): the two kernels back to back
   T *yy = y2;
   if (!yy) {
-    if (int rc = cuda_rc(cudaMallocAsync((void **)&yy, sizeof(T) * (size_t)n * batch, st))) return rc;
+    if (int rc = ws_alloc((void **)&yy, sizeof(T) * (size_t)n * batch, st)) return rc;
   }
   int rc = build_t<T>(x, y, n, batch, bc, yp1, ypn, yy, st);
   if (!rc) rc = eval_t<T>(x, y, yy, n, batch, q, m, out, idx, flags, st);
