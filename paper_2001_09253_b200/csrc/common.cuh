@@ -147,6 +147,29 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                : "memory");
 }
 
+// Plain arrival (release semantics) on an mbarrier.
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Orders this thread's earlier generic-proxy shared-memory accesses before later async-proxy
+// (TMA) accesses, e.g. before a bulk copy overwrites a stage that was read.
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// One lane per warp arrives on a shared counter of `nwarps` arrivals; returns true (to that
+// lane) for the last arrival, after resetting the counter.  Used to let the last warp done
+// with a stage issue its refill without any warp waiting for the others.
+__device__ __forceinline__ bool last_warp_arrival(int *counter, int nwarps) {
+  __threadfence_block();
+  const int old = atomicAdd(counter, 1);
+  __threadfence_block();
+  if (old == nwarps - 1) {
+    *counter = 0;
+    return true;
+  }
+  return false;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
   uint32_t done;
   do {

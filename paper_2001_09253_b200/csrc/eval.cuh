@@ -183,7 +183,8 @@ __device__ __forceinline__ void eval_packed(const IvalA<T> *Rc, const IvalB<T> *
     // x_{g+1} = x_{n-1}), so rounding or a wrong hint costs a (rare) bisection, never a wrong idx
     lo = max(0, min((int)r_mul(r_sub(qc, hd.x0), hd.s), n - 2));
     const T xa = Rc[lo].x0, xb = Rc[lo].x1;
-    if (!(xa <= qc && (qc < xb || xb == hd.xn))) {
+    const bool miss = !(xa <= qc && (qc < xb || xb == hd.xn));
+    if (__any_sync(__activemask(), miss) && miss) {  // warp-uniform test: no divergence bookkeeping
       int l = 0, h = n - 1;
       while (h - l > 1) {
         const int mid = (l + h) >> 1;
@@ -211,7 +212,7 @@ __device__ __forceinline__ void eval_packed(const IvalA<T> *Rc, const IvalB<T> *
 }
 
 constexpr int kEvalThreads = 256;
-constexpr int kStageHeader = 16;  // two mbarriers, ahead of the staged arrays
+constexpr int kStageHeader = 32;  // two mbarriers + two counters, ahead of the staged arrays
 
 __host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 __host__ __device__ constexpr int pow2_at_least(int v) {
@@ -309,13 +310,16 @@ __device__ __forceinline__ bool eval_item_queries(const T *Qs, const T *__restri
   const int per = (ng + nw - 1) / nw;
   const int wb = w * per, we = min(ng, wb + per);
   const int kbase = (int)(k0 - c0 * m);  // item's first query, relative to its first curve
+  T *const ob = out + k0;
+  int32_t *const ib = idx ? idx + k0 : nullptr;
+  const T *const qb = q + k0;
   for (int g = wb + lane; g < we; g += 32) {
     T qv[V], val[V];
     int jj[V];
     if (BULK) {
       VecIO<T, V>::load_shared(Qs + g * V, qv);
     } else {
-      VecIO<T, V>::load(q + k0 + (int64_t)g * V, qv);
+      VecIO<T, V>::load(qb + g * V, qv);
     }
     const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(kbase + g * V)) : 0;
     if (PACKED) {
@@ -332,8 +336,8 @@ __device__ __forceinline__ bool eval_item_queries(const T *Qs, const T *__restri
     }
 #pragma unroll
     for (int i = 0; i < V; ++i) oor |= (jj[i] < 0);
-    VecIO<T, V>::store(out + k0 + (int64_t)g * V, val);
-    if (idx) VecIO<T, V>::store_idx(idx + k0 + (int64_t)g * V, jj);
+    VecIO<T, V>::store(ob + g * V, val);
+    if (ib) VecIO<T, V>::store_idx(ib + g * V, jj);
   }
   return oor;
 }
@@ -441,6 +445,90 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
     __syncthreads();  // everyone is done with this item's stage and packed data
     if (threadIdx.x == 0) issue(it + 2 * G, s);
     s ^= 1;
+  }
+  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
+}
+
+// Persistent staged eval with per-warp curve ownership (cpb a multiple of the warp count, 16-
+// byte aligned inputs): warp w of the CTA owns curves [w cpw, (w+1) cpw) of every item
+// (cpw = cpb / 8), packs them and evaluates their queries, so there is no CTA-wide barrier in
+// the loop.  Each warp waits on the stage's TMA mbarrier itself; the last warp to finish an
+// item (a shared counter) issues the refill of that stage (item + 2), so warps drift freely
+// by up to one item and the pack of one warp overlaps the evaluation of another.
+template <typename T, int MODE, int L2>
+__global__ void __launch_bounds__(kEvalThreads, 3)
+    k_eval_warps(const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ y2, int n, int64_t batch,
+                 const T *__restrict__ q, int m, T *__restrict__ out, int32_t *__restrict__ idx, int cpb,
+                 int64_t nitems, FastDiv divn, FastDiv divm) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int NW = kEvalThreads / 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const StageLayout<T> L(cpb, n, MODE, cpb * m);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);  // bar[0], bar[1]
+  int *cnt = reinterpret_cast<int *>(smem_raw + 16);       // cnt[0], cnt[1]
+  IvalA<T> *KA = reinterpret_cast<IvalA<T> *>(smem_raw + L.knots);
+  IvalB<T> *KB = reinterpret_cast<IvalB<T> *>(KA + (size_t)cpb * n);
+  CurveHdr<T> *Hd = reinterpret_cast<CurveHdr<T> *>(smem_raw + L.hdr);
+  T *Xs = reinterpret_cast<T *>(smem_raw + L.xs);
+  uint16_t *Tb = reinterpret_cast<uint16_t *>(smem_raw + L.table);
+  const int P = L.P;
+  const int nb = kBucketsPerKnot * n;
+  const int64_t G = gridDim.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const size_t cn = (size_t)cpb * n;
+  const int cpw = cpb / NW;
+
+  auto stage = [&](int s) { return smem_raw + L.raw0 + (size_t)s * L.rawstep; };
+  auto issue = [&](int64_t it, int s) {  // one thread
+    if (it >= nitems) return;
+    const int64_t c0 = it * cpb;
+    const int nc = (int)min64(cpb, batch - c0);
+    const uint32_t bytes = (uint32_t)((size_t)nc * n * sizeof(T));
+    const uint32_t qbytes = (uint32_t)((size_t)nc * m * sizeof(T));
+    T *R = reinterpret_cast<T *>(stage(s));
+    mbar_expect_tx(bar + s, 3 * bytes + qbytes);
+    bulk_g2s(R, x + c0 * n, bytes, bar + s);
+    bulk_g2s(R + cn, y + c0 * n, bytes, bar + s);
+    bulk_g2s(R + 2 * cn, y2 + c0 * n, bytes, bar + s);
+    bulk_g2s(stage(s) + L.qoff, q + c0 * m, qbytes, bar + s);
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    cnt[0] = cnt[1] = 0;
+  }
+  __syncthreads();
+  const int64_t first = blockIdx.x;
+  const int nmine = first < nitems ? (int)((nitems - 1 - first) / G + 1) : 0;
+  if (threadIdx.x == 0) {
+    issue(first, 0);
+    issue(first + G, 1);
+  }
+  bool oor = false;
+  for (int k = 0; k < nmine; ++k) {
+    const int s = k & 1;
+    const int64_t it = first + (int64_t)k * G;
+    const int64_t c0 = it * cpb;
+    const int nc = (int)min64(cpb, batch - c0);
+    mbar_wait(bar + s, (uint32_t)(k >> 1) & 1u);
+    const int cw0 = w * cpw, nmy = min(cpw, nc - cw0);
+    if (nmy > 0) {
+      const T *X = reinterpret_cast<const T *>(stage(s)) + (size_t)cw0 * n;
+      const T *Y = X + cn, *Z = X + 2 * cn;
+      const T *Qs = reinterpret_cast<const T *>(stage(s) + L.qoff) + (size_t)cw0 * m;
+      pack_item<T, MODE, L2>(X, Y, Z, n, nmy, n, nb, divn, KA + cw0 * n, KB + cw0 * n, Hd + cw0, Xs + cw0 * P,
+                             Tb + cw0 * (nb + 2), P, lane, 32);
+      __syncwarp();
+      oor |= eval_item_queries<T, MODE, V, true, L2>(Qs, q, (c0 + cw0) * m, c0 + cw0, m, nmy * m, cpb, divm,
+                                                     KA + cw0 * n, KB + cw0 * n, Hd + cw0, Xs + cw0 * P,
+                                                     Tb + cw0 * (nb + 2), X, Y, Z, n, nb, P, out, idx, 0, 1, lane);
+    }
+    __syncwarp();
+    if (lane == 0 && last_warp_arrival(cnt + s, NW)) {
+      fence_proxy_async();
+      issue(it + 2 * G, s);
+    }
   }
   if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
 }

@@ -249,6 +249,34 @@ int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
 }
 
 
+template <typename T, int MODE, int L2 = 0>
+int launch_warps_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
+                   int32_t *idx, int cpb, int64_t nitems, cudaStream_t st) {
+  if constexpr (MODE == MODE_BISECT && L2 == 0) {
+    switch (eytz_levels(n)) {
+      case 2: return launch_warps_k<T, MODE, 2>(x, y, y2, n, batch, q, m, out, idx, cpb, nitems, st);
+      case 3: return launch_warps_k<T, MODE, 3>(x, y, y2, n, batch, q, m, out, idx, cpb, nitems, st);
+      case 4: return launch_warps_k<T, MODE, 4>(x, y, y2, n, batch, q, m, out, idx, cpb, nitems, st);
+      case 5: return launch_warps_k<T, MODE, 5>(x, y, y2, n, batch, q, m, out, idx, cpb, nitems, st);
+      case 6: return launch_warps_k<T, MODE, 6>(x, y, y2, n, batch, q, m, out, idx, cpb, nitems, st);
+      case 7: return launch_warps_k<T, MODE, 7>(x, y, y2, n, batch, q, m, out, idx, cpb, nitems, st);
+      case 8: return launch_warps_k<T, MODE, 8>(x, y, y2, n, batch, q, m, out, idx, cpb, nitems, st);
+      default: return launch_warps_k<T, MODE, 9>(x, y, y2, n, batch, q, m, out, idx, cpb, nitems, st);
+    }
+  } else {
+    const StageLayout<T> L(cpb, n, MODE, cpb * (int)m);
+    const size_t sm = L.total;
+    auto kern = k_eval_warps<T, MODE, L2>;
+    if (int rc = set_smem(kern, sm)) return rc;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, sm) != cudaSuccess || occ < 1) occ = 1;
+    const int64_t grid = std::min<int64_t>(nitems, (int64_t)occ * num_sms());
+    kern<<<(unsigned)grid, kEvalThreads, sm, st>>>(x, y, y2, n, batch, q, (int)m, out, idx, cpb, nitems,
+                                                  FastDiv((uint32_t)n), FastDiv((uint32_t)m));
+    return launch_rc();
+  }
+}
+
 constexpr size_t kSmemCap = 220 * 1024;   // per-CTA dynamic shared memory we allow ourselves
 constexpr size_t kItemSmem = 72 * 1024;   // target per-CTA footprint for multi-curve items
 
@@ -285,6 +313,10 @@ int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, con
   // TMA bulk staging of knots + queries when, in addition, curve blocks are whole 16-byte units.
   const bool vec = (m % VW == 0) && aligned16(q) && aligned16(out) && (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0));
   const bool bulk = vec && ((n * sizeof(T)) % 16 == 0) && aligned16(x) && aligned16(y) && aligned16(y2);
+  // per-warp curve ownership for the bisection mode (measured faster there; the uniform-grid
+  // mode, whose per-query work is small, keeps the CTA-wide pack)
+  if (bulk && cpb >= 8 && cpb % 8 == 0 && MODE == MODE_BISECT)
+    return launch_warps_k<T, MODE>(x, y, y2, n, batch, q, m, out, idx, cpb, nitems, st);
   if (bulk) return launch_staged_k<T, MODE, VW, true>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
   if (vec) return launch_staged_k<T, MODE, VW, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
   return launch_staged_k<T, MODE, 1, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
