@@ -321,11 +321,31 @@ def main():
     build_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
     eval_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
     step_ms = statistics.mean(b + e for b, e in zip(build_ms, eval_ms))
-    t = torch.tensor([step_ms, statistics.mean(build_ms), statistics.mean(eval_ms)], dtype=torch.float64,
+
+    # ---- the fused single-kernel path (spline_build_eval, SPLINE_PATH_FUSED), same protocol
+    fused_ms = 0.0
+    fusable = n <= 128 and (n * s) % 16 == 0 and m % (16 // s) == 0
+    if fusable:
+        ff = wl.flags | api.PATH_FUSED
+
+        def fstep():
+            api.build_eval(x, y, q, wl.bc, yp1, ypn, ff, y2=y2, out=out, idx=idx)
+
+        for _ in range(3):
+            fstep()
+        fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for k in range(K):
+            flush.zero_()
+            fev[k][0].record(stream)
+            fstep()
+            fev[k][1].record(stream)
+        torch.cuda.synchronize()
+        fused_ms = statistics.mean(a.elapsed_time(b) for a, b in fev)
+    t = torch.tensor([step_ms, statistics.mean(build_ms), statistics.mean(eval_ms), fused_ms], dtype=torch.float64,
                      device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    step_ms, bms, ems = t.tolist()
+    step_ms, bms, ems, fused_ms = t.tolist()
 
     # ---- end to end through the public API with host buffers (pinned), copies timed
     e2e = None
@@ -345,8 +365,7 @@ def main():
             for d, h in zip(d_s, h_sl):
                 if d is not None:
                     d.copy_(h, non_blocking=True)
-            api.build(d_x, d_y, wl.bc, d_s[0], d_s[1], out=y2)
-            api.evaluate(d_x, d_y, y2, d_q, wl.flags, out=out, idx=idx)
+            api.build_eval(d_x, d_y, d_q, wl.bc, d_s[0], d_s[1], wl.flags, y2=y2, out=out, idx=idx)
             h_y2.copy_(y2, non_blocking=True)
             h_out.copy_(out, non_blocking=True)
             h_idx.copy_(idx, non_blocking=True)
@@ -369,7 +388,8 @@ def main():
         d2h = x.numel() * s + q.numel() * s + q.numel() * 4
         e2e = {"value": world * B * m / (te.item() * 1e-3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": te.item(), "pinned": True,
-               "path": "api.build/api.evaluate (C ABI) with pinned host in/out, copies on the same stream"}
+               "path": "api.build_eval (C ABI spline_build_eval, library-chosen kernels) with pinned host in/out, "
+                       "copies on the same stream"}
 
     if rank != 0:
         if world > 1:
@@ -380,9 +400,20 @@ def main():
     peak, peak_src = peaks()
     ach = ebytes / (ems * 1e-3) / 1e9
     wkey = f"cfg{args.config}"
+    long_curve = n > 256 * (16 if s == 8 else 32)
     launches = 2 * K  # 1 build kernel + 1 eval kernel per step for configs 1-4
-    if n > 256 * (16 if s == 8 else 32):
-        launches = 4 * K  # tiled SPIKE: reduce + top + finish, then eval
+    if long_curve:
+        launches = 5 * K  # tiled SPIKE: reduce + top + finish; eval: pack records + gather
+    if wl.flags & workloads.FLAG_Q_SORTED:
+        ekern = "k_eval_sorted"
+    elif long_curve or 3 * n * s > 200 * 1024:
+        ekern = "k_pack_records + k_eval_records"
+    elif n <= 512 and not (wl.flags & workloads.FLAG_X_UNIFORM) and B >= 8 and m < 2048:
+        ekern = "k_eval_warps"
+    else:
+        ekern = "k_eval_staged"
+    bkern = ("k1_thomas_regs" if n <= 8 else "k1_thomas_pipe" if n <= 128 else
+             "k_tile<FULL>" if not long_curve else "k_tile<REDUCE> + k4_top + k_tile<FINISH>")
     line = {
         "metric": METRIC,
         "value": world * B * m / (step_ms * 1e-3),
@@ -405,12 +436,18 @@ def main():
         "build_ms": bms,
         "eval_ms": ems,
         "build_gbs": bbytes / (bms * 1e-3) / 1e9,
-        "roofline": {"kernel": "k_eval_staged" if 3 * n * s <= 96 * 1024 else "k_eval_global", "bound": "hbm",
+        "roofline": {"kernel": ekern, "bound": "hbm",
                      "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": traffic_for(wkey, "eval"), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": ebytes,
-                     "build": {"achieved": bbytes / (bms * 1e-3) / 1e9, "frac": bbytes / (bms * 1e-3) / 1e9 / peak,
+                     "build": {"kernel": bkern, "achieved": bbytes / (bms * 1e-3) / 1e9,
+                               "frac": bbytes / (bms * 1e-3) / 1e9 / peak,
                                "algorithmic_bytes_per_launch": bbytes, "traffic": traffic_for(wkey, "build")}},
+        "fused": ({"kernel": "k_fused_staged", "ms_per_step": fused_ms, "value": world * B * m / (fused_ms * 1e-3),
+                   "unit": "queries/s", "algorithmic_bytes": (2 * s + 4) * B * m + 3 * s * B * n,
+                   "hbm_gbs": ((2 * s + 4) * B * m + 3 * s * B * n) / (fused_ms * 1e-3) / 1e9,
+                   "note": "spline_build_eval with SPLINE_PATH_FUSED (one launch; x, y read once, y2 written once)"}
+                  if fusable else None),
         "cpu_baseline": None,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -63,8 +63,10 @@ enum {
   SPLINE_BC_CLAMPED = 3
 };
 /* Evaluation hints: may change speed, never results (every guess is corrected by
- * comparisons against the same locate rule). */
-enum { SPLINE_Q_SORTED = 1, SPLINE_X_UNIFORM = 2 };
+ * comparisons against the same locate rule).  SPLINE_PATH_* (spline_build_eval only) pick
+ * the fused single kernel or the two kernels instead of the library's choice; both give
+ * bitwise the same y2, out and idx. */
+enum { SPLINE_Q_SORTED = 1, SPLINE_X_UNIFORM = 2, SPLINE_PATH_FUSED = 4, SPLINE_PATH_SPLIT = 8 };
 /* Asynchronous data-error bits (spline_status). */
 enum { SPLINE_STATUS_BAD_KNOTS = 1, SPLINE_STATUS_Q_OUT_OF_RANGE = 2 };
 
@@ -102,12 +104,15 @@ int spline_eval(const void *x, const void *y, const void *y2, int64_t n, int64_t
  *   y2                   [batch][n] output, NULLABLE: NULL = do not write y2 (it then never
  *                        leaves the chip on the fused path).
  *   q, m, out, idx       as spline_eval (q and out required when m > 0; idx nullable).
- *   flags                SPLINE_Q_SORTED | SPLINE_X_UNIFORM hints (speed only).
+ *   flags                SPLINE_Q_SORTED | SPLINE_X_UNIFORM | SPLINE_PATH_* hints (speed only).
  * The fused kernel (one launch; x, y read once from HBM, y2 produced and consumed on chip:
  * SURVEY.md §8(f) row 1, the paper evaluating right after the build) runs when
  * 3 <= n <= 128, n*sizeof(T) % 16 == 0, m % (16/sizeof(T)) == 0 and x, y, y2, q, out are
  * 16-byte aligned (idx 16-byte aligned for f32, 8-byte for f64); otherwise the two kernels run
- * back to back (with stream-ordered scratch for y2 when y2 is NULL).  m == 0 builds only.
+ * back to back (with stream-ordered scratch for y2 when y2 is NULL).  Without a PATH hint the
+ * library fuses only launch-latency-bound problems (batch*m <= 2^19): on B200 the larger
+ * staged evaluations are bound by shared-memory bandwidth, which fusion does not relieve
+ * (measured: DESIGN.md).  m == 0 builds only.
  * Errors: the union of spline_build's and spline_eval's.
  */
 int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1,

@@ -13,7 +13,7 @@ from . import _build
 SPLINE_F32, SPLINE_F64 = 0, 1
 SPLINE_OK, SPLINE_EINVAL, SPLINE_ECUDA, SPLINE_ENOMEM = 0, -1, -2, -3
 BC_NATURAL, BC_CLAMP_START, BC_CLAMP_END, BC_CLAMPED = 0, 1, 2, 3
-Q_SORTED, X_UNIFORM = 1, 2
+Q_SORTED, X_UNIFORM, PATH_FUSED, PATH_SPLIT = 1, 2, 4, 8
 STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE = 1, 2
 
 _ERR = {SPLINE_EINVAL: "SPLINE_EINVAL (invalid argument)", SPLINE_ECUDA: "SPLINE_ECUDA (CUDA error)",

@@ -11,8 +11,8 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import (BC_CLAMP_END, BC_CLAMP_START, BC_CLAMPED, BC_NATURAL, Q_SORTED,  # noqa: F401
-                   STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE, X_UNIFORM)
+from ._lib import (BC_CLAMP_END, BC_CLAMP_START, BC_CLAMPED, BC_NATURAL, PATH_FUSED, PATH_SPLIT,  # noqa: F401
+                   Q_SORTED, STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE, X_UNIFORM)
 
 _DT = {torch.float32: _lib.SPLINE_F32, torch.float64: _lib.SPLINE_F64}
 

@@ -17,8 +17,10 @@
 //  k_eval_sorted : SPLINE_Q_SORTED.  A warp walks a contiguous run of queries with a
 //                  carried bracket (the paper's forward scan, made
 //                  warp-cooperative); knots are read through L1 (no staging), any n.
-//  k_eval_global : unsorted queries on long curves: interpolation guess in HBM, corrected
-//                  by galloping + bisection; gathers x, y, y2.
+//  k_pack_records + k_eval_records : unsorted queries on long curves: interval records in
+//                  an HBM workspace, one gather per query at the interpolation guess.
+//  k_eval_global : the same without workspace (gathers x, y, y2; used if the workspace
+//                  cannot be allocated).
 #pragma once
 #include "common.cuh"
 
@@ -631,6 +633,157 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x,
     for (int i = 0; i < V; ++i) qa[i] = qn[i];
   }
   raise_status_warp(oor, kOutOfRange);
+}
+
+// ---- long curves through interval records in HBM ---------------------------------------
+// k_pack_records writes, per curve c, the interval records R[c n + j] (j < n-1; the full
+// common.cuh Ival, 32 B fp32 / 64 B fp64, one aligned DRAM burst) and a header
+// {x_0, x_{n-1}, (n-1)/(x_{n-1} - x_0)}; k_eval_records then needs ONE gather round trip per
+// query on near-uniform grids (the interpolation guess g, checked against the record's own
+// x_g, x_{g+1}) instead of the two dependent trips and 4-5 scattered sectors of x, y, y2.
+// Algorithmic cost of the pack: read 3 s B and write sizeof(Ival) B per knot (workspace).
+// 256-bit global accesses (LDG.256 / STG.256 on sm_100a): one instruction per full 32-byte
+// sector, so a record is requested from L2 exactly once per sector.
+__device__ __forceinline__ void ld256(const void *p, double (&v)[4]) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld256(const void *p, float (&v)[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st256(void *p, const double (&v)[4]) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void st256(void *p, const float (&v)[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
+template <typename T> __device__ __forceinline__ Ival<T> ld_ival(const Ival<T> *p) {
+  constexpr int W = 32 / sizeof(T);  // elements per 256-bit access
+  Ival<T> r;
+  T *d = reinterpret_cast<T *>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Ival<T>) / 32); ++i) {
+    T v[W];
+    ld256(reinterpret_cast<const char *>(p) + 32 * i, v);
+#pragma unroll
+    for (int k = 0; k < W; ++k) d[i * W + k] = v[k];
+  }
+  return r;
+}
+template <typename T> __device__ __forceinline__ void st_ival(Ival<T> *p, const Ival<T> &r) {
+  constexpr int W = 32 / sizeof(T);
+  const T *d = reinterpret_cast<const T *>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Ival<T>) / 32); ++i) {
+    T v[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) v[k] = d[i * W + k];
+    st256(reinterpret_cast<char *>(p) + 32 * i, v);
+  }
+}
+
+// KP consecutive knots per thread (one curve-aligned run), each loaded once: the run's x, y,
+// y2 plus the first knot of the next run, then KP records stored with 256-bit stores.
+template <typename T>
+__global__ void __launch_bounds__(256) k_pack_records(const T *__restrict__ x, const T *__restrict__ y,
+                                                      const T *__restrict__ y2, int n, int64_t batch,
+                                                      Ival<T> *__restrict__ R, CurveHdr<T> *__restrict__ H) {
+  constexpr int KP = 4;
+  const int runs = (n + KP - 1) / KP;  // runs per curve
+  const int64_t total = batch * runs;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = (batch == 1) ? 0 : e / runs;
+    const int j0 = (int)(e - c * runs) * KP;
+    const int64_t b = c * n + j0;
+    const int cnt = min(KP + 1, n - j0);  // knots of the run, + the next run's first
+    T xv[KP + 1], yv[KP + 1], zv[KP + 1];
+#pragma unroll
+    for (int i = 0; i < KP + 1; ++i) {
+      if (i < cnt) {
+        xv[i] = __ldg(x + b + i);
+        yv[i] = __ldg(y + b + i);
+        zv[i] = __ldg(y2 + b + i);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < KP; ++i)
+      if (i + 1 < cnt) st_ival(R + b + i, make_ival<T>(xv[i], xv[i + 1], yv[i], yv[i + 1], zv[i], zv[i + 1]));
+    if (j0 + cnt == n) {  // the run holding the curve's last knot writes the header
+      const T x0 = __ldg(x + c * n), xn = xv[cnt - 1];
+      H[c] = CurveHdr<T>{x0, xn, (T)(n - 1) / (xn - x0), T(0)};
+    }
+  }
+}
+
+// U independent queries per thread; per query: the guess g = (q - x_0)(n-1)/(x_{n-1} - x_0),
+// one record; if x_g <= q < x_{g+1} fails (jitter, or a non-uniform grid) the neighbour on the
+// indicated side, then a bisection over the records' x_j (any grid: never a wrong idx).
+template <typename T>
+__global__ void __launch_bounds__(256) k_eval_records(const Ival<T> *__restrict__ R, const CurveHdr<T> *__restrict__ H,
+                                                      int n, int64_t batch, const T *__restrict__ q, int64_t m,
+                                                      T *__restrict__ out, int32_t *__restrict__ idx) {
+  constexpr int U = 4;
+  const int64_t total = batch * m;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool oor = false;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += U * stride) {
+    T qc[U];
+    int g[U];
+    int64_t off[U];
+    bool act[U], in[U];
+    Ival<T> r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = base + u * stride;
+      act[u] = k < total;
+      const T qq = act[u] ? ld_stream(q + k) : T(0);
+      const int64_t c = (batch == 1) ? 0 : (act[u] ? k / m : 0);
+      off[u] = c * n;
+      const CurveHdr<T> hd = H[c];
+      qc[u] = fmin(fmax(qq, hd.x0), hd.xn);
+      in[u] = act[u] && (qc[u] == qq);
+      g[u] = max(0, min((int)r_mul(r_sub(qc[u], hd.x0), hd.s), n - 2));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = ld_ival(R + off[u] + g[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool below = qc[u] < r[u].x0;
+      const bool above = !(qc[u] < r[u].x1) && g[u] < n - 2;
+      if (below || above) {
+        const Ival<T> *Rc = R + off[u];
+        int j = below ? g[u] - 1 : g[u] + 1;
+        Ival<T> t = ld_ival(Rc + j);
+        if (!(t.x0 <= qc[u] && (qc[u] < t.x1 || j == n - 2))) {
+          int lo = 0, hi = n - 1;  // bisection on x_j = R[j].x0
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(&Rc[mid].x0) <= qc[u]) lo = mid;
+            else hi = mid;
+          }
+          j = lo;
+          t = ld_ival(Rc + j);
+        }
+        g[u] = j;
+        r[u] = t;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!act[u]) continue;
+      const int64_t k = base + u * stride;
+      const T v = ival_interp<T>(r[u], qc[u]);
+      st_stream(out + k, in[u] ? v : qnan<T>());
+      if (idx) st_stream(idx + k, in[u] ? (int32_t)g[u] : -1);
+      oor |= !in[u];
+    }
+  }
+  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
 }
 
 // Long curves (not stageable): locate in HBM.  Each thread carries U independent queries

@@ -359,6 +359,24 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
       return launch_staged<T, MODE_BSEARCH>(x, y, y2, nn, batch, q, m, out, idx, st);
   }
   const int64_t total = batch * m;
+  // interval records in a pooled workspace: one gather round trip per query
+  const size_t rec_bytes = sizeof(Ival<T>) * (size_t)n * batch, hdr_bytes = sizeof(CurveHdr<T>) * (size_t)batch;
+  void *ws = nullptr;
+  if (ws_alloc(&ws, rec_bytes + hdr_bytes, st) == SPLINE_OK) {
+    Ival<T> *R = reinterpret_cast<Ival<T> *>(ws);
+    CurveHdr<T> *H = reinterpret_cast<CurveHdr<T> *>(reinterpret_cast<char *>(ws) + rec_bytes);
+    const int64_t pg = std::min<int64_t>(((n + 3) / 4 * batch + 255) / 256, (int64_t)num_sms() * 16);
+    k_pack_records<T><<<(unsigned)pg, 256, 0, st>>>(x, y, y2, (int)n, batch, R, H);
+    int rc = launch_rc();
+    if (!rc) {
+      const int64_t grid = std::min<int64_t>((total + 1023) / 1024, (int64_t)num_sms() * 16);
+      k_eval_records<T><<<(unsigned)grid, 256, 0, st>>>(R, H, (int)n, batch, q, m, out, idx);
+      rc = launch_rc();
+    }
+    cudaFreeAsync(ws, st);
+    return rc;
+  }
+  cudaGetLastError();  // clear the failed allocation
   const int64_t grid = std::min<int64_t>((total + 1023) / 1024, 148 * 16);
   k_eval_global<T><<<(unsigned)grid, 256, 0, st>>>(x, y, y2, (int)n, batch, q, m, out, idx);
   return launch_rc();
@@ -449,7 +467,10 @@ template <typename T>
 int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
                  const T *q, int64_t m, T *out, int32_t *idx, int flags, cudaStream_t st) {
   if (m == 0) return y2 ? build_t<T>(x, y, n, batch, bc, yp1, ypn, y2, st) : SPLINE_OK;
-  if (fused_eligible<T>(x, y, n, q, m, out, idx, y2)) {
+  const bool want_fused =
+      (flags & SPLINE_PATH_FUSED) || (!(flags & SPLINE_PATH_SPLIT) && batch * m <= (int64_t(1) << 19));
+  flags &= (SPLINE_Q_SORTED | SPLINE_X_UNIFORM);
+  if (want_fused && fused_eligible<T>(x, y, n, q, m, out, idx, y2)) {
     if (flags & SPLINE_X_UNIFORM)
       return launch_fused<T, MODE_UNIFORM>(x, y, (int)n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
     return launch_fused<T, MODE_BISECT>(x, y, (int)n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
@@ -554,7 +575,8 @@ int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, in
   if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
   if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
   if (m < 0 || m >= (int64_t(1) << 31) || bc < 0 || bc > 3) return SPLINE_EINVAL;
-  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM)) return SPLINE_EINVAL;
+  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM | SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT)) return SPLINE_EINVAL;
+  if ((flags & SPLINE_PATH_FUSED) && (flags & SPLINE_PATH_SPLIT)) return SPLINE_EINVAL;
   if (batch == 0) return SPLINE_OK;
   if (!x || !y || ((bc & 1) && !yp1) || ((bc & 2) && !ypn)) return SPLINE_EINVAL;
   if (m > 0 && (!q || !out)) return SPLINE_EINVAL;

@@ -62,6 +62,7 @@ def test_einval_eval():
     assert lib.spline_eval(p, p, p, 2, 1, p, 4, p, None, 0, F32, None) == _lib.SPLINE_EINVAL   # n < 3
     assert lib.spline_eval(p, p, p, 8, 1, p, -1, p, None, 0, F32, None) == _lib.SPLINE_EINVAL  # m < 0
     assert lib.spline_eval(p, p, p, 8, 1, p, 4, p, None, 8, F32, None) == _lib.SPLINE_EINVAL   # unknown flag
+    assert lib.spline_eval(p, p, p, 8, 1, p, 4, p, None, 16, F32, None) == _lib.SPLINE_EINVAL  # unknown flag
     assert lib.spline_eval(p, None, p, 8, 1, p, 4, p, None, 0, F32, None) == _lib.SPLINE_EINVAL  # NULL y
     assert lib.spline_eval(None, None, None, 8, 1, None, 0, None, None, 0, F32, None) == _lib.SPLINE_OK  # m == 0
     assert lib.spline_eval(None, None, None, 8, 0, None, 9, None, None, 0, F32, None) == _lib.SPLINE_OK  # B == 0
@@ -104,7 +105,8 @@ def test_einval_build_eval():
     assert f(p, p, 8, 1, 1, None, None, p, p, 4, p, None, 0, F32, None) == E      # clamped, no yp1
     assert f(p, p, 8, 1, 0, None, None, p, None, 4, p, None, 0, F32, None) == E   # NULL q with m > 0
     assert f(p, p, 8, 1, 0, None, None, p, p, 4, None, None, 0, F32, None) == E   # NULL out
-    assert f(p, p, 8, 1, 0, None, None, p, p, 4, p, None, 4, F32, None) == E      # unknown flag
+    assert f(p, p, 8, 1, 0, None, None, p, p, 4, p, None, 16, F32, None) == E     # unknown flag
     assert f(p, p, 8, 1, 5, None, None, p, p, 4, p, None, 0, F32, None) == E      # bad bc
     assert f(None, p, 8, 1, 0, None, None, p, p, 4, p, None, 0, F32, None) == E   # NULL x
+    assert f(p, p, 8, 1, 0, None, None, p, p, 4, p, None, 12, F32, None) == E     # both path hints
     assert f(None, None, 8, 0, 0, None, None, None, None, 4, None, None, 0, F32, None) == _lib.SPLINE_OK

@@ -39,7 +39,7 @@ def check_fused(api, wl, flags=None, nthreads=8):
     tol = parity.tol_for(dt)
     x, y, q, yp1, ypn = _dev(wl)
     api.status()
-    y2, out, idx = api.build_eval(x, y, q, wl.bc, yp1, ypn, flags)
+    y2, out, idx = api.build_eval(x, y, q, wl.bc, yp1, ypn, flags | api.PATH_FUSED)
     bits = api.status()
     # (1) the oracle
     y2_ref = parity.oracle_build(wl, nthreads)
@@ -57,10 +57,16 @@ def check_fused(api, wl, flags=None, nthreads=8):
     assert torch.equal(idx, idxs)
     assert torch.equal(out.view(torch.int8), outs.view(torch.int8)), "out differs from build -> eval"
     # (3) without y2 / without idx: same out
-    none, out2, idx2 = api.build_eval(x, y, q, wl.bc, yp1, ypn, flags, want_y2=False)
+    F = flags | api.PATH_FUSED
+    none, out2, idx2 = api.build_eval(x, y, q, wl.bc, yp1, ypn, F, want_y2=False)
     assert none is None and torch.equal(out2.view(torch.int8), out.view(torch.int8)) and torch.equal(idx2, idx)
-    _, out3, none3 = api.build_eval(x, y, q, wl.bc, yp1, ypn, flags, want_idx=False)
+    _, out3, none3 = api.build_eval(x, y, q, wl.bc, yp1, ypn, F, want_idx=False)
     assert none3 is None and torch.equal(out3.view(torch.int8), out.view(torch.int8))
+    # (4) the other path choices give the same bits
+    for pf in (0, api.PATH_SPLIT):
+        y2b, outb, idxb = api.build_eval(x, y, q, wl.bc, yp1, ypn, flags | pf)
+        assert torch.equal(y2b.view(torch.int8), y2.view(torch.int8)) and torch.equal(idxb, idx)
+        assert torch.equal(outb.view(torch.int8), out.view(torch.int8))
     return float(e2.max()), float(eo.max())
 
 
@@ -111,8 +117,8 @@ def test_fused_unaligned_views(api):
     x, y, q, yp1, ypn = _dev(wl)
     # offset by one element: not 16-byte aligned -> the separate kernels
     xs = torch.empty(x.numel() + 1, dtype=x.dtype, device=x.device)[1:].view_as(x).copy_(x)
-    y2, out, idx = api.build_eval(xs, y, q, wl.bc, yp1, ypn)
-    y2r, outr, idxr = api.build_eval(x, y, q, wl.bc, yp1, ypn)
+    y2, out, idx = api.build_eval(xs, y, q, wl.bc, yp1, ypn, api.PATH_FUSED)
+    y2r, outr, idxr = api.build_eval(x, y, q, wl.bc, yp1, ypn, api.PATH_FUSED)
     assert torch.equal(idx, idxr) and torch.equal(out.view(torch.int8), outr.view(torch.int8))
     assert torch.equal(y2.view(torch.int8), y2r.view(torch.int8))
 
@@ -125,7 +131,7 @@ def test_fused_bad_knots_and_out_of_range(api):
     wl.q[3, 8] = np.nan
     x, y, q, yp1, ypn = _dev(wl)
     api.status()
-    y2, out, idx = api.build_eval(x, y, q, wl.bc, yp1, ypn)
+    y2, out, idx = api.build_eval(x, y, q, wl.bc, yp1, ypn, api.PATH_FUSED)
     bits = api.status()
     assert bits == api.STATUS_BAD_KNOTS | api.STATUS_Q_OUT_OF_RANGE
     z = y2.cpu().numpy()
