@@ -43,6 +43,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--ablation", action="store_true",
+                    help="SURVEY §8(f) rows 2-3: the paper's control-point sweep (n = 4 .. 2^20) with its "
+                         "interpolation variants and no-op loop, ns/point p16/p50/p84 (one JSON line)")
+    ap.add_argument("--sweep-points", type=int, default=14)
+    ap.add_argument("--reps", type=int, default=7)
     return ap.parse_args()
 
 
@@ -251,8 +256,73 @@ def run_long_curve_dist(args, world, rank, local, dev):
         print(json.dumps(line), flush=True)
 
 
+def run_ablation(args):
+    """The paper's timing experiment on one B200: control-point counts from the
+    biased schedule, random curves (y = eps, x_i = x_{i-1} + eps), n uniformly spaced points
+    per curve, fp64; every (n, variant) pair in a freshly shuffled order per repetition, L2
+    flushed before each timed launch (CUDA events).  Each launch evaluates B = max(1, 2^22 / n)
+    curves so that the GPU is filled; reported per point.  Variants: the product form, the
+    paper's splint div/mul and newint orig/noinv, and the no-op (locate-only) loop."""
+    import random
+
+    import torch
+
+    from paper_2001_09253_b200 import _lib, api, workloads
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    # the paper's schedule, plus powers of two below 4096 (its coarse steps skip the short curves)
+    sched = sorted(set(workloads.sweep_schedule(args.sweep_points)) | {1 << k for k in range(2, 12)})
+    data = {}
+    for n in sched:
+        B = max(1, (1 << 22) // n)
+        x, y, q = workloads.sweep_curves(n, B, seed=11)
+        X, Y, Q = (torch.from_numpy(a).to(dev) for a in (x, y, q))
+        Z = api.build(X, Y, api.BC_NATURAL)
+        data[n] = (X, Y, Z, Q, torch.empty_like(Q), torch.empty(Q.shape, dtype=torch.int32, device=dev), B)
+    forms = list(_lib.FORMS)
+    times = {(n, f): [] for n in sched for f in forms}
+    rng = random.Random(0)
+    for _ in range(2):  # warm-up
+        for n in sched:
+            X, Y, Z, Q, O, I, B = data[n]
+            for f in forms:
+                api.evaluate_ablation(X, Y, Z, Q, f, out=O, idx=I)
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        for _ in range(args.reps):
+            order = [(n, f) for n in sched for f in forms]
+            rng.shuffle(order)
+            for n, f in order:
+                X, Y, Z, Q, O, I, B = data[n]
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                api.evaluate_ablation(X, Y, Z, Q, f, out=O, idx=I)
+                b.record()
+                b.synchronize()
+                times[(n, f)].append(a.elapsed_time(b) * 1e6 / (B * n))  # ns per point
+    if api.status() != 0:
+        raise RuntimeError("data-error status raised in the ablation sweep")
+    rows = []
+    for n in sched:
+        row = {"n": n, "curves": data[n][6], "points": data[n][6] * n}
+        for f in forms:
+            p16, p50, p84 = np.percentile(times[(n, f)], [16, 50, 84])
+            row[f] = {"p16": p16, "p50": p50, "p84": p84}
+        rows.append(row)
+    line = {"mode": "ablation", "metric": "ns per interpolated point (GPU-wide, B curves per launch)",
+            "unit": "ns/point", "dtype": "f64", "kernel": "k_eval_sorted<FORM> (spline_eval_ablation)",
+            "forms": forms, "reps": args.reps, "schedule": sched, "rows": rows, "clocks": clk.summary(),
+            "data": "synthetic: the paper's random curves (y = eps, x_i = x_{i-1} + eps, eps ~ U(0,1)), "
+                    "n uniformly spaced points per curve"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.ablation:
+        run_ablation(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return

@@ -119,6 +119,25 @@ int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, in
                       const void *ypn, void *y2, const void *q, int64_t m, void *out, int32_t *idx, int flags,
                       int dtype, spline_stream_t stream);
 
+/*
+ * spline_eval_ablation -- the paper's evaluation-variant experiment on the GPU (SURVEY.md
+ * §8(f) row 2): spline_eval's sorted-run kernel (every
+ * query located by the carried-bracket scan, valid for any query order) with
+ * the interpolation arithmetic replaced by
+ *   SPLINE_FORM_RECORD       the product's form (1/h per interval, records; = spline_eval bits)
+ *   SPLINE_FORM_SPLINT_DIV   Eq. nr_formula literally: A, B divided by h, C, D divided by 6
+ *   SPLINE_FORM_SPLINT_MUL   the same with the /6 replaced by *(1/6)
+ *   SPLINE_FORM_NEWINT_ORIG  the paper's newint: one 1/h, multiplied last
+ *   SPLINE_FORM_NEWINT_NOINV newint dividing by h last instead
+ *   SPLINE_FORM_NOOP         locate only, out = y_j (the paper's no-op loop)
+ * Arguments and errors as spline_eval (flags are implied: sorted runs).  idx is exact for
+ * every form; out meets the north-star tolerance for forms 0-4.
+ */
+enum { SPLINE_FORM_RECORD = 0, SPLINE_FORM_SPLINT_DIV = 1, SPLINE_FORM_SPLINT_MUL = 2, SPLINE_FORM_NEWINT_ORIG = 3,
+       SPLINE_FORM_NEWINT_NOINV = 4, SPLINE_FORM_NOOP = 5 };
+int spline_eval_ablation(const void *x, const void *y, const void *y2, int64_t n, int64_t batch, const void *q,
+                         int64_t m, void *out, int32_t *idx, int form, int dtype, spline_stream_t stream);
+
 /* Typed thin wrappers (same semantics). */
 int spline_build_f32(const float *x, const float *y, int64_t n, int64_t batch, int bc, const float *yp1,
                      const float *ypn, float *y2, spline_stream_t stream);

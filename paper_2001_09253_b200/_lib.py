@@ -15,6 +15,7 @@ SPLINE_OK, SPLINE_EINVAL, SPLINE_ECUDA, SPLINE_ENOMEM = 0, -1, -2, -3
 BC_NATURAL, BC_CLAMP_START, BC_CLAMP_END, BC_CLAMPED = 0, 1, 2, 3
 Q_SORTED, X_UNIFORM, PATH_FUSED, PATH_SPLIT = 1, 2, 4, 8
 STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE = 1, 2
+FORMS = {"record": 0, "splint_div": 1, "splint_mul": 2, "newint_orig": 3, "newint_noinv": 4, "noop": 5}
 
 _ERR = {SPLINE_EINVAL: "SPLINE_EINVAL (invalid argument)", SPLINE_ECUDA: "SPLINE_ECUDA (CUDA error)",
         SPLINE_ENOMEM: "SPLINE_ENOMEM (out of device memory)"}
@@ -25,6 +26,7 @@ SIGNATURES = {
     "spline_build": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _vp]),
     "spline_eval": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i32, _i32, _vp]),
     "spline_build_eval": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _vp]),
+    "spline_eval_ablation": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i32, _i32, _vp]),
     "spline_build_f32": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "spline_build_f64": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "spline_eval_f32": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i32, _vp]),

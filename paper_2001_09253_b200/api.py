@@ -118,6 +118,21 @@ def build_eval(x, y, q, bc: int = BC_NATURAL, yp1=None, ypn=None, flags: int = 0
     return z, o, i
 
 
+def evaluate_ablation(x, y, y2, q, form: str, out=None, idx=None, stream=None):
+    """spline_eval_ablation: the sorted-run eval kernel with one of the paper's interpolation
+    variants (_lib.FORMS: record, splint_div, splint_mul, newint_orig, newint_noinv, noop)."""
+    x, y, y2, q = _as2d(x), _as2d(y), _as2d(y2), _as2d(q)
+    B, n = x.shape
+    m = q.shape[1]
+    _check_curves(x, y, y2, q)
+    o = torch.empty_like(q) if out is None else out
+    i = torch.empty(q.shape, dtype=torch.int32, device=q.device) if idx is None else idx
+    rc = _lib.load().spline_eval_ablation(_p(x), _p(y), _p(y2), n, B, _p(q), m, _p(o), _p(i), _lib.FORMS[form],
+                                          _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_eval_ablation")
+    return o, i
+
+
 def status(stream=None) -> int:
     """Synchronise the stream, return and clear the data-error bits (STATUS_*)."""
     bits = ctypes.c_uint(0)

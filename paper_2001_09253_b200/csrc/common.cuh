@@ -124,6 +124,42 @@ template <> __device__ __forceinline__ float ival_interp<float>(const Ival<float
   return __fsub_rn(hi, lo);
 }
 
+// ---- the paper's evaluation variants (the division ablation) -------
+// All compute Eq. nr_formula on [x0, x1]; they differ only in where the
+// divisions are.  IEEE division (no -use_fast_math); contraction allowed.
+enum { FORM_RECORD = 0,        // the product: 1/h per interval, records form (ival_interp)
+       FORM_SPLINT_DIV = 1,    // NR splint: A, B divide by h, C, D divide by 6
+       FORM_SPLINT_MUL = 2,    // same, /6 replaced by *(1/6)
+       FORM_NEWINT_ORIG = 3,   // newint: one reciprocal inv_ba, multiplied at the end
+       FORM_NEWINT_NOINV = 4,  // newint with the final multiply replaced by / ba
+       FORM_NOOP = 5 };        // locate only, out = y_j (the paper's no-op loop)
+
+template <typename T, int FORM>
+__device__ __forceinline__ T interp_form(T q, T x0, T x1, T y0, T y1, T z0, T z1) {
+  if constexpr (FORM == FORM_RECORD) {
+    return ival_interp<T>(make_ival<T>(x0, x1, y0, y1, z0, z1), q);
+  } else if constexpr (FORM == FORM_SPLINT_DIV || FORM == FORM_SPLINT_MUL) {
+    const T h = x1 - x0;
+    const T A = (x1 - q) / h, B = (q - x0) / h;
+    const T cd = (A * A * A - A) * z0 + (B * B * B - B) * z1;
+    if constexpr (FORM == FORM_SPLINT_DIV) return A * y0 + B * y1 + cd * (h * h) / T(6);
+    else return A * y0 + B * y1 + cd * (h * h) * (T(1) / T(6));
+  } else if constexpr (FORM == FORM_NEWINT_ORIG || FORM == FORM_NEWINT_NOINV) {
+    const T ba = x1 - x0, xa = q - x0, bx = x1 - q, ba2 = ba * ba;
+    const T lower = xa * y1 + bx * y0;
+    const T C = (xa * xa - ba2) * xa * z1;
+    const T D = (bx * bx - ba2) * bx * z0;
+    if constexpr (FORM == FORM_NEWINT_ORIG) {
+      const T inv_ba = T(1) / ba;
+      return (lower + (T(1) / T(6)) * (C + D)) * inv_ba;
+    } else {
+      return (lower + (T(1) / T(6)) * (C + D)) / ba;
+    }
+  } else {
+    return y0;
+  }
+}
+
 // From the raw arrays (kernels that do not stage the curve).
 template <typename T>
 __device__ __forceinline__ T nr_interp(T q, T x0, T x1, T y0, T y1, T z0, T z1) {

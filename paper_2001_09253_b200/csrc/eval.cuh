@@ -564,7 +564,9 @@ template <typename T> __device__ __forceinline__ int warp_locate(const T *X, int
 // wrong hint) falls back to bisection; a long scan switches to galloping.  Knots are read
 // with read-only loads through L1: a warp's 32V queries touch a handful of knots, so almost
 // every gather is an L1 hit and each knot leaves HBM about once.
-template <typename T, int V>
+// FORM (common.cuh interp_form) selects the evaluation variant: FORM_RECORD for spline_eval,
+// the others for spline_eval_ablation (the paper's division variants and no-op loop).
+template <typename T, int V, int FORM = FORM_RECORD>
 __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x, const T *__restrict__ y,
                                                        const T *__restrict__ y2, int n, const T *__restrict__ q,
                                                        int64_t m, T *__restrict__ out, int32_t *__restrict__ idx,
@@ -618,7 +620,9 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x,
           }
         }
         const T xa = __ldg(X + j), xb = __ldg(X + j + 1);
-        const T v = nr_interp(qc, xa, xb, __ldg(Y + j), __ldg(Y + j + 1), __ldg(Z + j), __ldg(Z + j + 1));
+        T v;
+        if constexpr (FORM == FORM_NOOP) v = __ldg(Y + j);
+        else v = interp_form<T, FORM>(qc, xa, xb, __ldg(Y + j), __ldg(Y + j + 1), __ldg(Z + j), __ldg(Z + j + 1));
         val[i] = in ? v : qnan<T>();
         jj[i] = in ? j : -1;
         oor |= !in;

@@ -322,7 +322,7 @@ int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, con
   return launch_staged_k<T, MODE, 1, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
 }
 
-template <typename T, int V>
+template <typename T, int V, int FORM = FORM_RECORD>
 int launch_sorted_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
                     int32_t *idx, cudaStream_t st) {
   // runs of ~2048 queries per warp, but at least ~8 warps per SM of work
@@ -332,7 +332,7 @@ int launch_sorted_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
   const int64_t rpc = (m + qrun - 1) / qrun;
   const int64_t ntasks = batch * rpc;
   const int64_t grid = (ntasks + 7) / 8;
-  k_eval_sorted<T, V><<<(unsigned)grid, 256, 0, st>>>(x, y, y2, n, q, m, out, idx, qrun, rpc, ntasks);
+  k_eval_sorted<T, V, FORM><<<(unsigned)grid, 256, 0, st>>>(x, y, y2, n, q, m, out, idx, qrun, rpc, ntasks);
   return launch_rc();
 }
 
@@ -486,6 +486,29 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
   return rc;
 }
 
+template <typename T, int FORM>
+int ablation_form(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const T *q, int64_t m, T *out,
+                  int32_t *idx, cudaStream_t st) {
+  constexpr int VW = 16 / sizeof(T);
+  const bool vec = (m % VW == 0) && aligned16(q) && aligned16(out) && (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0));
+  if (vec) return launch_sorted_k<T, VW, FORM>(x, y, y2, (int)n, batch, q, m, out, idx, st);
+  return launch_sorted_k<T, 1, FORM>(x, y, y2, (int)n, batch, q, m, out, idx, st);
+}
+
+template <typename T>
+int ablation_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const T *q, int64_t m, T *out,
+               int32_t *idx, int form, cudaStream_t st) {
+  switch (form) {
+    case FORM_RECORD: return ablation_form<T, FORM_RECORD>(x, y, y2, n, batch, q, m, out, idx, st);
+    case FORM_SPLINT_DIV: return ablation_form<T, FORM_SPLINT_DIV>(x, y, y2, n, batch, q, m, out, idx, st);
+    case FORM_SPLINT_MUL: return ablation_form<T, FORM_SPLINT_MUL>(x, y, y2, n, batch, q, m, out, idx, st);
+    case FORM_NEWINT_ORIG: return ablation_form<T, FORM_NEWINT_ORIG>(x, y, y2, n, batch, q, m, out, idx, st);
+    case FORM_NEWINT_NOINV: return ablation_form<T, FORM_NEWINT_NOINV>(x, y, y2, n, batch, q, m, out, idx, st);
+    case FORM_NOOP: return ablation_form<T, FORM_NOOP>(x, y, y2, n, batch, q, m, out, idx, st);
+    default: return SPLINE_EINVAL;
+  }
+}
+
 int check_build(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1, const void *ypn,
                 const void *y2, int dtype) {
   if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
@@ -586,6 +609,21 @@ int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, in
                                (const float *)ypn, (float *)y2, (const float *)q, m, (float *)out, idx, flags, st);
   return build_eval_t<double>((const double *)x, (const double *)y, n, batch, bc, (const double *)yp1,
                               (const double *)ypn, (double *)y2, (const double *)q, m, (double *)out, idx, flags, st);
+}
+
+int spline_eval_ablation(const void *x, const void *y, const void *y2, int64_t n, int64_t batch, const void *q,
+                         int64_t m, void *out, int32_t *idx, int form, int dtype, spline_stream_t stream) {
+  if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
+  if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || m < 0 || m >= (int64_t(1) << 31)) return SPLINE_EINVAL;
+  if (form < SPLINE_FORM_RECORD || form > SPLINE_FORM_NOOP) return SPLINE_EINVAL;
+  if (batch == 0 || m == 0) return SPLINE_OK;
+  if (!x || !y || !y2 || !q || !out) return SPLINE_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SPLINE_F32)
+    return ablation_t<float>((const float *)x, (const float *)y, (const float *)y2, n, batch, (const float *)q, m,
+                             (float *)out, idx, form, st);
+  return ablation_t<double>((const double *)x, (const double *)y, (const double *)y2, n, batch, (const double *)q, m,
+                            (double *)out, idx, form, st);
 }
 
 int spline_build_f32(const float *x, const float *y, int64_t n, int64_t batch, int bc, const float *yp1,

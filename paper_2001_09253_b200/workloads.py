@@ -190,3 +190,26 @@ def generate(cid: int, batch: int | None = None, n: int | None = None, m: int | 
 # The hand-generated curve of the paper's quality checks.
 HAND_KNOTS = [0, 0.5, 1, 1.01, 1.25, 1.5, 1.58, 1.79, 2.12, 2.30, 2.402, 2.451, 2.5]
 HAND_VALUES = [1, 1.2, 2, 0.25, 0.25, 0.25, 0.63, 0.96, 1.17, 1.23, 1.245, 1.249, 1.25]
+
+
+def sweep_curves(n: int, batch: int, seed: int = 0, dtype=np.float64):
+    """The paper's randomised timing curves: y_i = eps, x_i = x_{i-1} + eps with
+    eps ~ U(0, 1) (eps == 0 -> 1e-4), and n uniformly spaced query points from x_0 to x_{n-1}
+    per curve (sorted).  Returns (x, y, q) as (batch, n) arrays; natural ends are implied."""
+    rng = np.random.default_rng([seed, n])
+    eps = rng.random((batch, n))
+    eps[eps == 0] = 1e-4
+    x = np.cumsum(eps, axis=1)
+    y = rng.random((batch, n))
+    y[y == 0] = 1e-4
+    t = np.linspace(0.0, 1.0, n)
+    q = x[:, :1] + t[None, :] * (x[:, -1:] - x[:, :1])
+    q = np.minimum(np.maximum(q, x[:, :1]), x[:, -1:])
+    return x.astype(dtype), y.astype(dtype), q.astype(dtype)
+
+
+def sweep_schedule(points: int, n_min: int = 4, n_max: int = 1 << 20):
+    """The paper's list of control-point counts: (r (sqrt(n_max) - sqrt(n_min))
+    + sqrt(n_min))^2 at `points` evenly spaced r in [0, 1] (biased towards short curves)."""
+    r = np.linspace(0.0, 1.0, points)
+    return [int(round((v * (np.sqrt(n_max) - np.sqrt(n_min)) + np.sqrt(n_min)) ** 2)) for v in r]
