@@ -78,56 +78,52 @@ __device__ __forceinline__ double nr_rcp(double a) {
   return __fma_rn(r, e, r);
 }
 
-// Eq. nr_formula on one interval [x0, x1] in the interval-record form every eval
-// kernel uses.  With h = x1 - x0, ih = 1/h (the paper's inv_ba), zs_k = y2_k h^2/6:
-//     A = (x1 - q) ih,  B = (q - x0) ih,  C = A (A^2 - 1),  D = B (B^2 - 1)
-//     out = A y0 + B y1 + (C y2_0 + D y2_1) h^2/6  =  (A y0 + C zs0) + (B y1 + D zs1)
-// computed as hi - lo with hi = A y0 + C zs0 and lo = (-B) y1 + (-D) zs1 from the pair
-// P = ((x0 - q) ih, (x1 - q) ih) = (-B, A): the two halves are the two lanes of one fp32x2
-// operation (FADD2 / FMUL2 / FFMA2, 7 instructions per query).  Every operation is explicitly
-// rounded, so the packed and the scalar forms -- and every kernel -- give identical bits.
-template <typename T> struct Ival { T x0, x1, y1, y0, zs1, zs0, ih, pad; };
+// Eq. nr_formula on one interval [x0, x1], in the factored form every eval kernel
+// uses.  With h = x1 - x0, B = (q - x0)/h, A = 1 - B and zs_k = y2_k h^2/6:
+//     A y0 + B y1 + (A^3 - A) zs0 + (B^3 - B) zs1
+//       = y0 + B dy - B (1 - B) (e1 + B e2),   dy = y1 - y0, e1 = 2 zs0 + zs1, e2 = zs1 - zs0
+// (A^3 - A = -B(1-B)(2-B), B^3 - B = -B(1-B)(1+B)).  Every factor is bounded like the NR
+// terms (B, 1-B in [0, 1]), so it is as well conditioned as Eq. nr_formula (an expansion in
+// powers of (q - x0) is not: its terms cancel catastrophically near x1 when y2 is large).
+// An interval carries Cub {1/h, y0, dy, e1} (16 B fp32: one shared-memory vector load) and e2;
+// x0 comes from the search.  1/h is the correctly rounded reciprocal (the paper's inv_ba,
+// P:386).  Every operation is explicitly rounded, so every kernel and hint gives the same bits.
+template <typename T> struct Cub { T ih, y0, dy, e1; };
 
-template <typename T> __device__ __forceinline__ Ival<T> make_ival(T x0, T x1, T y0, T y1, T z0, T z1) {
+template <typename T>
+__device__ __forceinline__ Cub<T> make_cub(T x0, T x1, T y0, T y1, T z0, T z1, T &e2) {
   const T h = r_sub(x1, x0);
   const T h26 = r_mul(r_mul(h, h), T(1) / T(6));
-  return Ival<T>{x0, x1, y1, y0, r_mul(z1, h26), r_mul(z0, h26), r_rcp(h), T(0)};
+  const T zs0 = r_mul(z0, h26), zs1 = r_mul(z1, h26);
+  e2 = r_sub(zs1, zs0);
+  return Cub<T>{r_rcp(h), y0, r_sub(y1, y0), r_fma(T(2), zs0, zs1)};
+}
+
+template <typename T> __device__ __forceinline__ T cub_eval(const Cub<T> &c, T e2, T x0, T q) {
+  const T B = r_mul(r_sub(q, x0), c.ih);
+  const T w = r_mul(B, r_sub(T(1), B));
+  const T lin = r_fma(B, c.dy, c.y0);
+  return r_fma(-w, r_fma(B, e2, c.e1), lin);
+}
+
+// Interval record of the long-curve path (HBM): the bracket [x0, x1] and the cubic
+// (32 B fp32 / 64 B fp64: one or two 256-bit accesses).
+template <typename T> struct Ival { T x0, x1, ih, y0, dy, e1, e2, pad; };
+
+template <typename T> __device__ __forceinline__ Ival<T> make_ival(T x0, T x1, T y0, T y1, T z0, T z1) {
+  T e2;
+  const Cub<T> c = make_cub<T>(x0, x1, y0, y1, z0, z1, e2);
+  return Ival<T>{x0, x1, c.ih, c.y0, c.dy, c.e1, e2, T(0)};
 }
 
 template <typename T> __device__ __forceinline__ T ival_interp(const Ival<T> &r, T q) {
-  const T nB = r_mul(r_sub(r.x0, q), r.ih), A = r_mul(r_sub(r.x1, q), r.ih);
-  const T nD = r_mul(nB, r_fma(nB, nB, T(-1))), C = r_mul(A, r_fma(A, A, T(-1)));
-  const T lo = r_fma(nD, r.zs1, r_mul(nB, r.y1));
-  const T hi = r_fma(C, r.zs0, r_mul(A, r.y0));
-  return r_sub(hi, lo);
-}
-
-__device__ __forceinline__ uint64_t pack2(float a, float b) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-// fp32: the same operations on the lane pairs (x0, x1), (y1, y0), (zs1, zs0) -- bitwise the
-// scalar form (f32x2 arithmetic is lane-wise IEEE round-to-nearest).
-template <> __device__ __forceinline__ float ival_interp<float>(const Ival<float> &r, float q) {
-  const uint64_t X = pack2(r.x0, r.x1), Yp = pack2(r.y1, r.y0), Z = pack2(r.zs1, r.zs0);
-  const uint64_t I = pack2(r.ih, r.ih), Q = pack2(q, q), M1 = pack2(-1.0f, -1.0f);
-  uint64_t D, P, W, Pc, t, u;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(D) : "l"(X), "l"(Q));
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(P) : "l"(D), "l"(I));
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(W) : "l"(P), "l"(P), "l"(M1));
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(Pc) : "l"(P), "l"(W));
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(P), "l"(Yp));
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(u) : "l"(Pc), "l"(Z), "l"(t));
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(u));
-  return __fsub_rn(hi, lo);
+  return cub_eval<T>(Cub<T>{r.ih, r.y0, r.dy, r.e1}, r.e2, r.x0, q);
 }
 
 // ---- the paper's evaluation variants (the division ablation) -------
 // All compute Eq. nr_formula on [x0, x1]; they differ only in where the
 // divisions are.  IEEE division (no -use_fast_math); contraction allowed.
-enum { FORM_RECORD = 0,        // the product: 1/h per interval, records form (ival_interp)
+enum { FORM_RECORD = 0,        // the product: the factored form of make_cub / cub_eval
        FORM_SPLINT_DIV = 1,    // NR splint: A, B divide by h, C, D divide by 6
        FORM_SPLINT_MUL = 2,    // same, /6 replaced by *(1/6)
        FORM_NEWINT_ORIG = 3,   // newint: one reciprocal inv_ba, multiplied at the end
@@ -137,7 +133,9 @@ enum { FORM_RECORD = 0,        // the product: 1/h per interval, records form (i
 template <typename T, int FORM>
 __device__ __forceinline__ T interp_form(T q, T x0, T x1, T y0, T y1, T z0, T z1) {
   if constexpr (FORM == FORM_RECORD) {
-    return ival_interp<T>(make_ival<T>(x0, x1, y0, y1, z0, z1), q);
+    T e2;
+    const Cub<T> c = make_cub<T>(x0, x1, y0, y1, z0, z1, e2);
+    return cub_eval<T>(c, e2, x0, q);
   } else if constexpr (FORM == FORM_SPLINT_DIV || FORM == FORM_SPLINT_MUL) {
     const T h = x1 - x0;
     const T A = (x1 - q) / h, B = (q - x0) / h;
@@ -163,7 +161,9 @@ __device__ __forceinline__ T interp_form(T q, T x0, T x1, T y0, T y1, T z0, T z1
 // From the raw arrays (kernels that do not stage the curve).
 template <typename T>
 __device__ __forceinline__ T nr_interp(T q, T x0, T x1, T y0, T y1, T z0, T z1) {
-  return ival_interp<T>(make_ival<T>(x0, x1, y0, y1, z0, z1), q);
+  T e2;
+  const Cub<T> c = make_cub<T>(x0, x1, y0, y1, z0, z1, e2);
+  return cub_eval<T>(c, e2, x0, q);
 }
 
 }  // namespace fs

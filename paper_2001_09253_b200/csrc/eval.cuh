@@ -5,8 +5,8 @@
 // Eq. nr_formula only holds for x_j <= x <= x_{j+1}.  Every search below ends in
 // comparisons against this rule, so guesses (bucket table, uniform-grid index, sorted-run
 // carry, interpolation guess) change speed, never idx.
-// Evaluate: Eq. nr_formula in the interval-record form of common.cuh (Ival,
-// ival_interp; explicitly rounded, so all kernels and hints give bitwise-identical out).
+// Evaluate: Eq. nr_formula in the factored form of common.cuh (Cub: make_cub,
+// cub_eval; explicitly rounded, so all kernels and hints give bitwise-identical out).
 //
 //  k_eval_staged : unsorted queries on curves that fit in shared memory.  Persistent CTAs,
 //                  TMA bulk staging (double-buffered), packed interval records:
@@ -89,12 +89,12 @@ __device__ __forceinline__ void eval_one(const T *X, const T *Y, const T *Z, int
 }
 
 // ---- packed curves (MODE_BISECT, MODE_TABLE, MODE_UNIFORM) ------------------------------
-// Per staged curve: the interval record of [x_j, x_{j+1}] (common.cuh Ival: x_j, x_{j+1},
-// y_{j+1}, y_j, y2_{j+1} h^2/6, y2_j h^2/6, 1/h -- the paper's inv_ba), so the
-// gather is one record (two 16-byte loads for fp32) and the evaluation 7 packed fp32x2
-// operations.  Record slots have stride n per curve (slot n-1 unused).
+// Per staged curve: interval j's Cub {1/h, y0, dy, e1} (common.cuh; 16 B fp32: ONE 16-byte
+// shared-memory load) and its e2 (one 4-byte load), and -- for the modes that check a bracket --
+// the plain knot array XK.  Slots have stride n per curve (slot n-1 unused).
 //   MODE_BISECT : branch-free bisection over the knots in Eytzinger order (eytz_descend):
-//                 L2 = ceil(log2(n-1)) uniform steps, no divergence, conflict-free.
+//                 L2 = ceil(log2(n-1)) uniform steps, no divergence, conflict-free; x_lo is
+//                 the last key the descent went right of (no extra load).
 //   MODE_TABLE  : bucket table over nb = 2n equal-width buckets of [x_0, x_{n-1}]:
 //                   bucket(v) = min(nb, (int)((v - x_0) * s)),   s = nb / (x_{n-1} - x_0)
 //                   Tb[b]     = max{ j in [0, n-2] : bucket(x_j) < b }   (Tb[0] = 0).
@@ -103,16 +103,6 @@ __device__ __forceinline__ void eval_one(const T *X, const T *Y, const T *Z, int
 //                 table only brackets the search (long curves, many queries per knot).
 //   MODE_UNIFORM: direct index (q - x_0)(n-1)/(x_{n-1} - x_0) on the hinted uniform grid.
 // Every search ends in comparisons x_j <= q, so idx is exact on any grid.
-// The record is stored as two 16-byte (fp32) halves in separate arrays, so that each of the
-// two vector loads of a gather has a 16-byte stride across records (random record indices
-// then spread over all shared-memory bank groups; a 32-byte stride would use half of them).
-template <typename T> struct IvalA { T x0, x1, y1, y0; };
-template <typename T> struct IvalB { T zs1, zs0, ih, pad; };
-template <typename T> __device__ __forceinline__ Ival<T> load_ival(const IvalA<T> *A, const IvalB<T> *B, int j) {
-  const IvalA<T> a = A[j];
-  const IvalB<T> b = B[j];
-  return Ival<T>{a.x0, a.x1, a.y1, a.y0, b.zs1, b.zs0, b.ih, b.pad};
-}
 // Per staged curve: range and scale (one vector load per group of V queries).
 template <typename T> struct CurveHdr { T x0, xn, s, pad; };
 
@@ -145,9 +135,10 @@ __device__ __forceinline__ double lds_f(uint32_t a, double) {
   return v;
 }
 // The descent on shared-memory byte addresses a = ebase + s i: a <- 2a - ebase (+ s when
-// E[i] <= q), one load, one compare and two integer adds per level.  Returns the final a,
-// = ebase + s (2^L2 + c).
-template <typename T, int L2> __device__ __forceinline__ uint32_t eytz_descend(uint32_t ebase, T q) {
+// E[i] <= q), one load, one compare and two integer adds per level (+ one select tracking the
+// last key <= q, which is x_c).  Returns the final a, = ebase + s (2^L2 + c); xl = x_c, or the
+// caller's x_0 when c = 0.
+template <typename T, int L2> __device__ __forceinline__ uint32_t eytz_descend(uint32_t ebase, T q, T &xl) {
   uint32_t a = ebase + (uint32_t)sizeof(T);
 #pragma unroll
   for (int t = 0; t < L2; ++t) {
@@ -155,7 +146,10 @@ template <typename T, int L2> __device__ __forceinline__ uint32_t eytz_descend(u
     if constexpr (sizeof(T) == 4) v = lds_f(a);
     else v = lds_f(a, 0.0);
     a = 2u * a - ebase;
-    if (v <= q) a += (uint32_t)sizeof(T);
+    if (v <= q) {
+      a += (uint32_t)sizeof(T);
+      xl = v;
+    }
   }
   return a;
 }
@@ -166,34 +160,38 @@ __device__ __forceinline__ int eytz_rank(int i, int L2) {
   return ((2 * (i - (1 << d)) + 1) << (L2 - 1 - d)) - 1;
 }
 
-// Locate + evaluate one query against a packed curve (record halves Rc / Sc, Eytzinger keys
-// at shared address ebase).  Branch-light: out-of-range / NaN queries run the same path on a
-// clamped stand-in (qc = x_0) and are masked at the end.
+// Locate + evaluate one query against a packed curve (cubics Pc + Ec2, knots Xc (not for
+// MODE_BISECT), Eytzinger keys at shared address ebase).  Branch-light: out-of-range / NaN
+// queries run the same path on a clamped stand-in (qc = x_0) and are masked at the end.
 template <typename T, int MODE, int L2>
-__device__ __forceinline__ void eval_packed(const IvalA<T> *Rc, const IvalB<T> *Sc, uint32_t ebase,
+__device__ __forceinline__ void eval_packed(const Cub<T> *Pc, const T *Ec2, const T *Xc, uint32_t ebase,
                                             const uint16_t *Tb, const CurveHdr<T> &hd, int n, int nb, T q, T &val,
                                             int &j) {
   const T qc = fmin(fmax(q, hd.x0), hd.xn);  // NaN -> x_0 (fmax returns the number)
   const bool in = (qc == q);                 // false for NaN and for q outside [x_0, x_{n-1}]
   int lo;
+  T xl;
   if (MODE == MODE_BISECT) {
-    const uint32_t a = eytz_descend<T, L2>(ebase, qc);
+    xl = hd.x0;
+    const uint32_t a = eytz_descend<T, L2>(ebase, qc, xl);
     // (the clamp only matters for invalid knots, e.g. x_{n-1} = +inf: memory safety)
     lo = min((int)((a - ebase) / (uint32_t)sizeof(T)) - (1 << L2), n - 2);
   } else if (MODE == MODE_UNIFORM) {
     // direct index on the hinted grid; accepted only if x_g <= q < x_{g+1} (or g = n-2, i.e.
     // x_{g+1} = x_{n-1}), so rounding or a wrong hint costs a (rare) bisection, never a wrong idx
     lo = max(0, min((int)r_mul(r_sub(qc, hd.x0), hd.s), n - 2));
-    const T xa = Rc[lo].x0, xb = Rc[lo].x1;
-    const bool miss = !(xa <= qc && (qc < xb || xb == hd.xn));
+    xl = Xc[lo];
+    const T xb = Xc[lo + 1];
+    const bool miss = !(xl <= qc && (qc < xb || xb == hd.xn));
     if (__any_sync(__activemask(), miss) && miss) {  // warp-uniform test: no divergence bookkeeping
       int l = 0, h = n - 1;
       while (h - l > 1) {
         const int mid = (l + h) >> 1;
-        if (Rc[mid].x0 <= qc) l = mid;
+        if (Xc[mid] <= qc) l = mid;
         else h = mid;
       }
       lo = l;
+      xl = Xc[lo];
     }
   } else {  // MODE_TABLE
     const int bk = bucket_of(qc, hd.x0, hd.s, nb);
@@ -202,13 +200,14 @@ __device__ __forceinline__ void eval_packed(const IvalA<T> *Rc, const IvalB<T> *
     if (hi - lo > 2) {  // wide bracket (clustered knots): bisect it down
       do {
         const int mid = (lo + hi + 1) >> 1;
-        if (Rc[mid].x0 <= qc) lo = mid;
+        if (Xc[mid] <= qc) lo = mid;
         else hi = mid - 1;
       } while (hi - lo > 2);
     }
-    while (lo < hi && Rc[lo + 1].x0 <= qc) ++lo;  // largest j in [lo, hi] with x_j <= q
+    while (lo < hi && Xc[lo + 1] <= qc) ++lo;  // largest j in [lo, hi] with x_j <= q
+    xl = Xc[lo];
   }
-  const T v = ival_interp<T>(load_ival(Rc, Sc, lo), qc);
+  const T v = cub_eval<T>(Pc[lo], Ec2[lo], xl, qc);
   j = in ? lo : -1;
   val = in ? v : qnan<T>();
 }
@@ -228,7 +227,7 @@ __host__ __device__ constexpr int pow2_at_least(int v) {
 // copies; plus the packed knots / headers / Eytzinger keys / bucket table of the item being
 // evaluated.
 template <typename T> struct StageLayout {
-  size_t raw0, rawstep, qoff, knots, hdr, xs, table, total;
+  size_t raw0, rawstep, qoff, knots, e2, xk, hdr, xs, table, total;
   int P;  // Eytzinger array stride per curve (MODE_BISECT): 2^L2 >= n - 1
   __host__ __device__ StageLayout(int cpb, int n, int mode, int qmax) {
     const bool packed = mode != MODE_BSEARCH;
@@ -239,7 +238,11 @@ template <typename T> struct StageLayout {
     rawstep = align16(qoff + sizeof(T) * (size_t)qmax);
     size_t off = raw0 + 2 * rawstep;
     knots = off;
-    if (packed) off = align16(off + sizeof(Ival<T>) * (size_t)cpb * n);
+    if (packed) off = align16(off + sizeof(Cub<T>) * (size_t)cpb * n);
+    e2 = off;
+    if (packed) off = align16(off + sizeof(T) * (size_t)cpb * n);
+    xk = off;
+    if (packed && mode != MODE_BISECT) off = align16(off + sizeof(T) * (size_t)cpb * n);
     hdr = off;
     if (packed) off = align16(off + sizeof(CurveHdr<T>) * (size_t)cpb);
     xs = off;
@@ -256,18 +259,17 @@ template <typename T> struct StageLayout {
 // Threads tid = 0 .. nt-1 of the caller's group share the work.
 template <typename T, int MODE, int L2>
 __device__ __forceinline__ void pack_item(const T *X, const T *Y, const T *Z, int zs, int nc, int n, int nb,
-                                          FastDiv divn, IvalA<T> *RA, IvalB<T> *RB, CurveHdr<T> *Hd, T *Xs,
+                                          FastDiv divn, Cub<T> *RP, T *RE, T *XK, CurveHdr<T> *Hd, T *Xs,
                                           uint16_t *Tb, int P, int tid, int nt) {
   const int tot = nc * n;
   for (int e = tid; e < tot; e += nt) {
     const int c = (int)divn.div((uint32_t)e);
     const int j = e - c * n;
     const T xj = X[e];
+    if (MODE != MODE_BISECT) XK[e] = xj;
     if (j < n - 1) {
       const T *zc = Z + c * zs + j;
-      const Ival<T> r = make_ival<T>(xj, X[e + 1], Y[e], Y[e + 1], zc[0], zc[1]);
-      RA[e] = IvalA<T>{r.x0, r.x1, r.y1, r.y0};
-      RB[e] = IvalB<T>{r.zs1, r.zs0, r.ih, r.pad};
+      RP[e] = make_cub<T>(xj, X[e + 1], Y[e], Y[e + 1], zc[0], zc[1], RE[e]);
     }
     if (j == 0 || (MODE == MODE_TABLE && j < n - 1)) {
       const T x0 = X[c * n], xn = X[c * n + n - 1];
@@ -300,8 +302,8 @@ __device__ __forceinline__ void pack_item(const T *X, const T *Y, const T *Z, in
 // out of range".
 template <typename T, int MODE, int V, bool BULK, int L2>
 __device__ __forceinline__ bool eval_item_queries(const T *Qs, const T *__restrict__ q, int64_t k0, int64_t c0,
-                                                  int m, int cnt, int cpb, FastDiv divm, const IvalA<T> *RA,
-                                                  const IvalB<T> *RB,
+                                                  int m, int cnt, int cpb, FastDiv divm, const Cub<T> *RP,
+                                                  const T *RE, const T *XK,
                                                   const CurveHdr<T> *Hd, const T *Xs, const uint16_t *Tb,
                                                   const T *X, const T *Y, const T *Z, int n, int nb, int P,
                                                   T *__restrict__ out, int32_t *__restrict__ idx, int w, int nw,
@@ -326,12 +328,13 @@ __device__ __forceinline__ bool eval_item_queries(const T *Qs, const T *__restri
     const int cl = (cpb > 1) ? (int)divm.div((uint32_t)(kbase + g * V)) : 0;
     if (PACKED) {
       const CurveHdr<T> hd = Hd[cl];
-      const IvalA<T> *Rc = RA + cl * n;
-      const IvalB<T> *Sc = RB + cl * n;
+      const Cub<T> *Pc = RP + cl * n;
+      const T *Ec2 = RE + cl * n;
+      const T *Xc = XK + cl * n;
       const uint32_t ebase = smem_u32(Xs + (size_t)cl * P);
       const uint16_t *Tc = Tb + cl * (nb + 2);
 #pragma unroll
-      for (int i = 0; i < V; ++i) eval_packed<T, MODE, L2>(Rc, Sc, ebase, Tc, hd, n, nb, qv[i], val[i], jj[i]);
+      for (int i = 0; i < V; ++i) eval_packed<T, MODE, L2>(Pc, Ec2, Xc, ebase, Tc, hd, n, nb, qv[i], val[i], jj[i]);
     } else {
 #pragma unroll
       for (int i = 0; i < V; ++i) eval_one<T>(X + cl * n, Y + cl * n, Z + cl * n, n, qv[i], val[i], jj[i]);
@@ -365,8 +368,9 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const StageLayout<T> L(cpb, n, MODE, BULK ? qmax : 0);
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);  // bar[0], bar[1]
-  IvalA<T> *KA = reinterpret_cast<IvalA<T> *>(smem_raw + L.knots);
-  IvalB<T> *KB = reinterpret_cast<IvalB<T> *>(KA + (size_t)cpb * n);
+  Cub<T> *KP = reinterpret_cast<Cub<T> *>(smem_raw + L.knots);
+  T *KE = reinterpret_cast<T *>(smem_raw + L.e2);
+  T *XK = reinterpret_cast<T *>(smem_raw + L.xk);
   CurveHdr<T> *Hd = reinterpret_cast<CurveHdr<T> *>(smem_raw + L.hdr);
   T *Xs = reinterpret_cast<T *>(smem_raw + L.xs);
   uint16_t *Tb = reinterpret_cast<uint16_t *>(smem_raw + L.table);
@@ -439,10 +443,10 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
     }
     const T *Y = X + cn, *Z = X + 2 * cn;
     if (PACKED) {
-      pack_item<T, MODE, L2>(X, Y, Z, n, nc, n, nb, divn, KA, KB, Hd, Xs, Tb, P, threadIdx.x, blockDim.x);
+      pack_item<T, MODE, L2>(X, Y, Z, n, nc, n, nb, divn, KP, KE, XK, Hd, Xs, Tb, P, threadIdx.x, blockDim.x);
       __syncthreads();  // packed data built
     }
-    oor |= eval_item_queries<T, MODE, V, BULK, L2>(Qs, q, k0, c0, m, cnt, cpb, divm, KA, KB, Hd, Xs, Tb, X, Y, Z, n,
+    oor |= eval_item_queries<T, MODE, V, BULK, L2>(Qs, q, k0, c0, m, cnt, cpb, divm, KP, KE, XK, Hd, Xs, Tb, X, Y, Z, n,
                                                    nb, P, out, idx, w, nw, lane);
     __syncthreads();  // everyone is done with this item's stage and packed data
     if (threadIdx.x == 0) issue(it + 2 * G, s);
@@ -468,8 +472,9 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
   const StageLayout<T> L(cpb, n, MODE, cpb * m);
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);  // bar[0], bar[1]
   int *cnt = reinterpret_cast<int *>(smem_raw + 16);       // cnt[0], cnt[1]
-  IvalA<T> *KA = reinterpret_cast<IvalA<T> *>(smem_raw + L.knots);
-  IvalB<T> *KB = reinterpret_cast<IvalB<T> *>(KA + (size_t)cpb * n);
+  Cub<T> *KP = reinterpret_cast<Cub<T> *>(smem_raw + L.knots);
+  T *KE = reinterpret_cast<T *>(smem_raw + L.e2);
+  T *XK = reinterpret_cast<T *>(smem_raw + L.xk);
   CurveHdr<T> *Hd = reinterpret_cast<CurveHdr<T> *>(smem_raw + L.hdr);
   T *Xs = reinterpret_cast<T *>(smem_raw + L.xs);
   uint16_t *Tb = reinterpret_cast<uint16_t *>(smem_raw + L.table);
@@ -519,11 +524,13 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
       const T *X = reinterpret_cast<const T *>(stage(s)) + (size_t)cw0 * n;
       const T *Y = X + cn, *Z = X + 2 * cn;
       const T *Qs = reinterpret_cast<const T *>(stage(s) + L.qoff) + (size_t)cw0 * m;
-      pack_item<T, MODE, L2>(X, Y, Z, n, nmy, n, nb, divn, KA + cw0 * n, KB + cw0 * n, Hd + cw0, Xs + cw0 * P,
+      pack_item<T, MODE, L2>(X, Y, Z, n, nmy, n, nb, divn, KP + cw0 * n, KE + cw0 * n, XK + cw0 * n, Hd + cw0,
+                             Xs + cw0 * P,
                              Tb + cw0 * (nb + 2), P, lane, 32);
       __syncwarp();
       oor |= eval_item_queries<T, MODE, V, true, L2>(Qs, q, (c0 + cw0) * m, c0 + cw0, m, nmy * m, cpb, divm,
-                                                     KA + cw0 * n, KB + cw0 * n, Hd + cw0, Xs + cw0 * P,
+                                                     KP + cw0 * n, KE + cw0 * n, XK + cw0 * n, Hd + cw0,
+                                                     Xs + cw0 * P,
                                                      Tb + cw0 * (nb + 2), X, Y, Z, n, nb, P, out, idx, 0, 1, lane);
     }
     __syncwarp();

@@ -12,7 +12,7 @@
 //                           n >  8 : two lanes per curve, the sweep from both ends meeting in
 //                                    the middle (build_thomas.cuh babe_tile), on an
 //                                    odd-stride transposed copy (conflict-free)
-//   8 evaluator warps    pack interval records + search keys, locate + Eq. nr_formula for the
+//   8 evaluator warps    pack the interval cubics + search keys, locate + Eq. nr_formula for the
 //                        item's queries, 16-byte streaming stores of out / idx
 //
 // Warp specialisation: two solver warps take alternate items and work up to two items ahead of
@@ -53,7 +53,7 @@ __host__ __device__ constexpr int fused_threads(int solve) { return kFusedEvalTh
 enum { BAR_EVAL = 1, BAR_TFULL = 2, BAR_TEMPTY = 2 + kKnotStages };
 
 template <typename T> struct FusedLayout {
-  size_t kst0, kststep, qst0, qststep, ytile, ytstep, scratch, scrstep, knots, hdr, xs, total;
+  size_t kst0, kststep, qst0, qststep, ytile, ytstep, scratch, scrstep, knots, e2, xk, hdr, xs, total;
   int P, S2;
   __host__ __device__ FusedLayout(int cpb, int n, int qmax, int solve, int mode) {
     P = 1 << eytz_levels(n);
@@ -72,7 +72,11 @@ template <typename T> struct FusedLayout {
     scrstep = (solve == SOLVE_BABE) ? align16(sizeof(T) * (size_t)(kBabeCurves + 2) * S2) : 0;
     off += fused_solver_warps(solve) * scrstep;
     knots = off;
-    off = align16(off + sizeof(Ival<T>) * (size_t)cpb * n);
+    off = align16(off + sizeof(Cub<T>) * (size_t)cpb * n);
+    e2 = off;
+    off = align16(off + sizeof(T) * (size_t)cpb * n);
+    xk = off;
+    if (mode != MODE_BISECT) off = align16(off + sizeof(T) * (size_t)cpb * n);
     hdr = off;
     off = align16(off + sizeof(CurveHdr<T>) * (size_t)cpb);
     xs = off;
@@ -185,8 +189,9 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
   const FusedLayout<T> L(cpb, n, qmax, SOLVE, MODE);
   uint64_t *kbar = reinterpret_cast<uint64_t *>(smem_raw);  // [kKnotStages]
   uint64_t *qbar = kbar + kKnotStages;                       // [kQueryStages]
-  IvalA<T> *KA = reinterpret_cast<IvalA<T> *>(smem_raw + L.knots);
-  IvalB<T> *KB = reinterpret_cast<IvalB<T> *>(KA + (size_t)cpb * n);
+  Cub<T> *KP = reinterpret_cast<Cub<T> *>(smem_raw + L.knots);
+  T *KE = reinterpret_cast<T *>(smem_raw + L.e2);
+  T *XK = reinterpret_cast<T *>(smem_raw + L.xk);
   CurveHdr<T> *Hd = reinterpret_cast<CurveHdr<T> *>(smem_raw + L.hdr);
   T *Xs = reinterpret_cast<T *>(smem_raw + L.xs);
   const int P = L.P, S2 = L.S2;
@@ -279,13 +284,13 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
       mbar_wait(kbar + ks, (uint32_t)(k / kKnotStages) & 1u);  // completes at once; orders the TMA writes
       const T *X = kstage(ks);
       const T *Y = X + cn;
-      pack_item<T, MODE, L2>(X, Y, ytile(ks), S2, nc, n, 0, divn, KA, KB, Hd, Xs, nullptr, P, threadIdx.x,
+      pack_item<T, MODE, L2>(X, Y, ytile(ks), S2, nc, n, 0, divn, KP, KE, XK, Hd, Xs, nullptr, P, threadIdx.x,
                              kFusedEvalThreads);
       if (k + kKnotStages < nmine) nbar_arrive(BAR_TEMPTY + ks, NB);  // this thread is done with tile ks
       nbar_sync(BAR_EVAL, kFusedEvalThreads);                          // packed data built; stage ks free
       if (threadIdx.x == 0) issue_knots(it + kKnotStages * G, ks);
       mbar_wait(qbar + qs, (uint32_t)(k / kQueryStages) & 1u);
-      oor |= eval_item_queries<T, MODE, V, true, L2>(qstage(qs), q, k0, c0, m, cnt, cpb, divm, KA, KB, Hd, Xs, nullptr,
+      oor |= eval_item_queries<T, MODE, V, true, L2>(qstage(qs), q, k0, c0, m, cnt, cpb, divm, KP, KE, XK, Hd, Xs, nullptr,
                                                      X, Y, ytile(ks), n, 0, P, out, idx, warp, kFusedEvalWarps,
                                                      lane);
       nbar_sync(BAR_EVAL, kFusedEvalThreads);  // done with query stage qs and the packed data

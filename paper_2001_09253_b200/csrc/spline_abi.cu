@@ -192,6 +192,7 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
         return 16 + ((2 * (size_t)c * n * sizeof(T) + 15) & ~(size_t)15) + 2 * (size_t)(c + 1) * S * sizeof(T);
       };
       while (cpb > 16 && smem_of(cpb) > 64 * 1024) cpb -= 16;
+      if (getenv("SPLINE_K1_CPB")) cpb = atoi(getenv("SPLINE_K1_CPB"));  // EXPERIMENT
       const size_t sm = smem_of(cpb);
       auto kern = k1_thomas_pipe<T>;
       if (int rc = set_smem(kern, sm)) return rc;
@@ -205,6 +206,7 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
     }
     int cpb = 128;
     while (cpb > 16 && (size_t)2 * (cpb + 1) * S * sizeof(T) > 100 * 1024) cpb -= 16;
+    if (getenv("SPLINE_K1_CPB")) cpb = atoi(getenv("SPLINE_K1_CPB"));  // EXPERIMENT
     const size_t sm = (size_t)2 * (cpb + 1) * S * sizeof(T);
     auto kern = k1_thomas_babe<T>;
     if (int rc = set_smem(kern, sm)) return rc;
