@@ -185,14 +185,13 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
   }
   if (n <= kK1MaxN) {  // K1: two threads per curve, staged odd-stride tiles
     const int S = (int)(n | 1);
-    if (!getenv("SPLINE_K1_BABE") && (n * sizeof(T)) % 16 == 0 && aligned16(x) && aligned16(y)) {
+    if ((n * sizeof(T)) % 16 == 0 && aligned16(x) && aligned16(y)) {
       // persistent + TMA-pipelined; CPB curves per tile (2 threads each)
       int cpb = 64;
       const auto smem_of = [&](int c) {
         return 16 + ((2 * (size_t)c * n * sizeof(T) + 15) & ~(size_t)15) + 2 * (size_t)(c + 1) * S * sizeof(T);
       };
       while (cpb > 16 && smem_of(cpb) > 64 * 1024) cpb -= 16;
-      if (getenv("SPLINE_K1_CPB")) cpb = atoi(getenv("SPLINE_K1_CPB"));  // EXPERIMENT
       const size_t sm = smem_of(cpb);
       auto kern = k1_thomas_pipe<T>;
       if (int rc = set_smem(kern, sm)) return rc;
@@ -206,7 +205,6 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
     }
     int cpb = 128;
     while (cpb > 16 && (size_t)2 * (cpb + 1) * S * sizeof(T) > 100 * 1024) cpb -= 16;
-    if (getenv("SPLINE_K1_CPB")) cpb = atoi(getenv("SPLINE_K1_CPB"));  // EXPERIMENT
     const size_t sm = (size_t)2 * (cpb + 1) * S * sizeof(T);
     auto kern = k1_thomas_babe<T>;
     if (int rc = set_smem(kern, sm)) return rc;
