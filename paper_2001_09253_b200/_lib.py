@@ -43,7 +43,7 @@ _lib = None
 
 
 def lib_path() -> str:
-    return os.environ.get("SPLINE_LIB_OVERRIDE", _build.LIB)  # tools/ experiments only
+    return _build.LIB
 
 
 def load() -> ctypes.CDLL:
