@@ -25,6 +25,14 @@ namespace fs {
 
 constexpr int kK1Threads = 256;
 
+// Row stride of the transposed tiles of babe_tile.  A warp holds 16 curves x (top, bottom):
+// at a step the top lanes touch row j and the bottom lanes row n-1-j of their curves.  With
+// S = 2 mod 4 the 16 curves of one end fall on 16 distinct banks of one parity class (S t mod 32
+// = 2 (u t mod 16), u odd), and for even n the two ends are n-1-2j (odd) banks apart, i.e. in the
+// other parity class: every step is conflict-free.  Odd n: an odd stride (16 distinct banks
+// per end; the two ends may share a bank).
+__host__ __device__ constexpr int babe_stride(int n) { return (n & 1) ? n : ((n % 4 == 2) ? n : n + 2); }
+
 // The two-ended sweep of one CTA tile: curve t = threadIdx.x/2 of the tile lives at
 // Xc = X + t*S, Yc = Y + t*S (odd stride S); on return Yc holds y2 (or NaN).
 // Both threads of a pair run the SAME instruction stream with a direction dir = +1 (top:

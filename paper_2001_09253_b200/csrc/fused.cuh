@@ -47,7 +47,7 @@ constexpr int kBabeCurves = 16;  // curves per solver-warp pass (2 lanes each)
 constexpr int kKnotStages = 3;   // x, y (+ y2 tile) stages
 constexpr int kQueryStages = 2;
 // solver warps per CTA (each solves whole items, alternately)
-__host__ __device__ constexpr int fused_solver_warps(int solve) { return solve == SOLVE_REGS ? 2 : 1; }
+__host__ __device__ constexpr int fused_solver_warps(int) { return 2; }
 __host__ __device__ constexpr int fused_threads(int solve) { return kFusedEvalThreads + 32 * fused_solver_warps(solve); }
 // named barrier ids (0 is __syncthreads)
 enum { BAR_EVAL = 1, BAR_TFULL = 2, BAR_TEMPTY = 2 + kKnotStages };
@@ -57,8 +57,8 @@ template <typename T> struct FusedLayout {
   int P, S2;
   __host__ __device__ FusedLayout(int cpb, int n, int qmax, int solve, int mode) {
     P = 1 << eytz_levels(n);
-    S2 = (solve == SOLVE_BABE) ? (n | 1) : n;
-    size_t off = 64;  // mbarriers: knot stages, then query stages
+    S2 = (solve == SOLVE_BABE) ? babe_stride(n) : n;
+    size_t off = 128;  // mbarriers (knot stages, query stages, tile full, tile empty) + counters
     kst0 = off;
     kststep = align16(2 * sizeof(T) * (size_t)cpb * n);
     off += kKnotStages * kststep;
@@ -176,7 +176,12 @@ __device__ __forceinline__ void fused_solve_regs(const T *Xr, const T *Yr, T *Yt
 
 // Requirements (checked by the host): x, y, q, out 16-byte aligned, idx 4V-byte aligned,
 // n * sizeof(T) % 16 == 0, m % V == 0 (V = 16 / sizeof(T)), 3 <= n <= 128.
-template <typename T, int MODE, int L2, int SOLVE>
+// WOWN (cpb a multiple of 8): evaluator warp w owns curves [w cpb/8, (w+1) cpb/8) of every item
+// -- it packs and evaluates them with no CTA-wide barrier; hand-offs are mbarriers (tile full:
+// solver -> warps; tile empty: 8 warp arrivals -> solver) and the last warp done with a stage
+// (shared counter) refills it.  Otherwise (chunked single curves) the CTA packs together and
+// the hand-offs are named barriers.
+template <typename T, int MODE, int L2, int SOLVE, bool WOWN>
 __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
     k_fused_staged(const T *__restrict__ x, const T *__restrict__ y, int n, int64_t batch, int bc,
                    const T *__restrict__ yp1, const T *__restrict__ ypn, T *__restrict__ y2, const T *__restrict__ q,
@@ -189,6 +194,10 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
   const FusedLayout<T> L(cpb, n, qmax, SOLVE, MODE);
   uint64_t *kbar = reinterpret_cast<uint64_t *>(smem_raw);  // [kKnotStages]
   uint64_t *qbar = kbar + kKnotStages;                       // [kQueryStages]
+  uint64_t *tfull = qbar + kQueryStages;                     // [kKnotStages]  (WOWN)
+  uint64_t *tempty = tfull + kKnotStages;                    // [kKnotStages]  (WOWN)
+  int *kcnt = reinterpret_cast<int *>(tempty + kKnotStages);  // [kKnotStages]  (WOWN)
+  int *qcnt = kcnt + kKnotStages;                            // [kQueryStages] (WOWN)
   Cub<T> *KP = reinterpret_cast<Cub<T> *>(smem_raw + L.knots);
   T *KE = reinterpret_cast<T *>(smem_raw + L.e2);
   T *XK = reinterpret_cast<T *>(smem_raw + L.xk);
@@ -237,8 +246,16 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kKnotStages; ++s) mbar_init(kbar + s, 1);
-    for (int s = 0; s < kQueryStages; ++s) mbar_init(qbar + s, 1);
+    for (int s = 0; s < kKnotStages; ++s) {
+      mbar_init(kbar + s, 1);
+      mbar_init(tfull + s, 1);
+      mbar_init(tempty + s, kFusedEvalWarps);
+      kcnt[s] = 0;
+    }
+    for (int s = 0; s < kQueryStages; ++s) {
+      mbar_init(qbar + s, 1);
+      qcnt[s] = 0;
+    }
   }
   __syncthreads();
   const int64_t first = blockIdx.x;
@@ -259,8 +276,13 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
       int64_t c0, k0;
       int nc, cnt;
       item_of(it, c0, k0, nc, cnt);
-      mbar_wait(kbar + ks, (uint32_t)(k / kKnotStages) & 1u);
-      if (k >= kKnotStages) nbar_sync(BAR_TEMPTY + ks, NB);  // tile ks packed (item k-3)
+      if constexpr (WOWN) {
+        if (k >= kKnotStages) mbar_wait(tempty + ks, (uint32_t)(k / kKnotStages - 1) & 1u);  // item k-3 packed
+        mbar_wait(kbar + ks, (uint32_t)(k / kKnotStages) & 1u);
+      } else {
+        mbar_wait(kbar + ks, (uint32_t)(k / kKnotStages) & 1u);
+        if (k >= kKnotStages) nbar_sync(BAR_TEMPTY + ks, NB);  // tile ks packed (item k-3)
+      }
       const T *Xr = kstage(ks);
       const T *Yr = Xr + cn;
       T *y2o = (y2 && (cpb > 1 || it % nchunks == 0)) ? y2 : nullptr;  // chunk 0 writes y2
@@ -270,7 +292,48 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
       else
         fused_solve_regs<T>(Xr, Yr, ytile(ks), n, nc, c0, bc, yp1, ypn, y2o, lane, 0, 1);
       __syncwarp();
-      nbar_arrive(BAR_TFULL + ks, NB);
+      if constexpr (WOWN) {
+        if (lane == 0) mbar_arrive(tfull + ks);
+      } else {
+        nbar_arrive(BAR_TFULL + ks, NB);
+      }
+    }
+  } else if constexpr (WOWN) {
+    // ---------------- evaluator warps, per-warp curve ownership
+    const int cpw = cpb / kFusedEvalWarps;
+    for (int k = 0; k < nmine; ++k) {
+      const int ks = k % kKnotStages, qs = k % kQueryStages;
+      const int64_t it = first + (int64_t)k * G;
+      const int64_t c0 = it * cpb;
+      const int nc = (int)min64(cpb, batch - c0);
+      mbar_wait(tfull + ks, (uint32_t)(k / kKnotStages) & 1u);  // y2 tile ks ready (so the stage landed)
+      mbar_wait(kbar + ks, (uint32_t)(k / kKnotStages) & 1u);   // completes at once; orders the TMA writes
+      const int cw0 = warp * cpw, nmy = min(cpw, nc - cw0);
+      const T *X = kstage(ks) + (size_t)cw0 * n;
+      const T *Y = X + cn;
+      const T *Z = ytile(ks) + (size_t)cw0 * S2;
+      if (nmy > 0)
+        pack_item<T, MODE, L2>(X, Y, Z, S2, nmy, n, 0, divn, KP + cw0 * n, KE + cw0 * n, XK + cw0 * n, Hd + cw0,
+                               Xs + cw0 * P, nullptr, P, lane, 32);
+      __syncwarp();
+      if (lane == 0) {
+        if (k + kKnotStages < nmine) mbar_arrive(tempty + ks);  // this warp is done with tile ks
+        if (last_warp_arrival(kcnt + ks, kFusedEvalWarps)) {     // every warp is: refill knot stage ks
+          fence_proxy_async();
+          issue_knots(it + kKnotStages * G, ks);
+        }
+      }
+      mbar_wait(qbar + qs, (uint32_t)(k / kQueryStages) & 1u);
+      if (nmy > 0)
+        oor |= eval_item_queries<T, MODE, V, true, L2>(qstage(qs) + (size_t)cw0 * m, q, (c0 + cw0) * m, c0 + cw0, m,
+                                                       nmy * m, cpb, divm, KP + cw0 * n, KE + cw0 * n, XK + cw0 * n,
+                                                       Hd + cw0, Xs + cw0 * P, nullptr, X, Y, Z, n, 0, P, out, idx,
+                                                       0, 1, lane);
+      __syncwarp();
+      if (lane == 0 && last_warp_arrival(qcnt + qs, kFusedEvalWarps)) {
+        fence_proxy_async();
+        issue_queries(it + kQueryStages * G, qs);
+      }
     }
   } else {
     // ---------------- evaluator warps

@@ -184,7 +184,7 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
     return launch_rc();
   }
   if (n <= kK1MaxN) {  // K1: two threads per curve, staged odd-stride tiles
-    const int S = (int)(n | 1);
+    const int S = babe_stride((int)n);
     if ((n * sizeof(T)) % 16 == 0 && aligned16(x) && aligned16(y)) {
       // persistent + TMA-pipelined; CPB curves per tile (2 threads each)
       int cpb = 64;
@@ -384,30 +384,30 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
 
 // ------------------------------------------------------------------ fused build + eval
 
-template <typename T, int MODE, int L2, int SOLVE>
+template <typename T, int MODE, int L2, int SOLVE, bool WOWN>
 int launch_fused_k(const T *x, const T *y, int n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
                    const T *q, int64_t m, T *out, int32_t *idx, int cpb, int nchunks, int qchunk, int64_t nitems,
                    cudaStream_t st) {
   if constexpr (MODE == MODE_BISECT && L2 == 0) {
     const int l2 = eytz_levels(n);
     if constexpr (SOLVE == SOLVE_REGS) {  // n <= 8
-      if (l2 <= 2) return launch_fused_k<T, MODE, 2, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
-      return launch_fused_k<T, MODE, 3, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      if (l2 <= 2) return launch_fused_k<T, MODE, 2, SOLVE, WOWN>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      return launch_fused_k<T, MODE, 3, SOLVE, WOWN>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
     } else {
     switch (l2) {
-      case 2: return launch_fused_k<T, MODE, 2, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
-      case 3: return launch_fused_k<T, MODE, 3, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
-      case 4: return launch_fused_k<T, MODE, 4, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
-      case 5: return launch_fused_k<T, MODE, 5, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
-      case 6: return launch_fused_k<T, MODE, 6, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
-      default: return launch_fused_k<T, MODE, 7, SOLVE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 2: return launch_fused_k<T, MODE, 2, SOLVE, WOWN>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 3: return launch_fused_k<T, MODE, 3, SOLVE, WOWN>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 4: return launch_fused_k<T, MODE, 4, SOLVE, WOWN>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 5: return launch_fused_k<T, MODE, 5, SOLVE, WOWN>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      case 6: return launch_fused_k<T, MODE, 6, SOLVE, WOWN>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
+      default: return launch_fused_k<T, MODE, 7, SOLVE, WOWN>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
     }
     }
   } else {
     const int qmax = (cpb > 1) ? cpb * (int)m : qchunk;
     const FusedLayout<T> L(cpb, n, qmax, SOLVE, MODE);
     const size_t sm = L.total;
-    auto kern = k_fused_staged<T, MODE, L2, SOLVE>;
+    auto kern = k_fused_staged<T, MODE, L2, SOLVE, WOWN>;
     if (int rc = set_smem(kern, sm)) return rc;
     int occ = 0;
     constexpr int NT = fused_threads(SOLVE);
@@ -456,11 +456,21 @@ int launch_fused(const T *x, const T *y, int n, int64_t batch, int bc, const T *
     cpb = (int)std::max<int64_t>(1, c);
     nitems = (batch + cpb - 1) / cpb;
   }
+  // per-warp curve ownership needs whole curves for each of the 8 evaluator warps
+  if (cpb >= 8) {
+    cpb = cpb / 8 * 8;
+    nitems = (batch + cpb - 1) / cpb;
+    if (solve == SOLVE_REGS)
+      return launch_fused_k<T, MODE, 0, SOLVE_REGS, true>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb,
+                                                          nchunks, qchunk, nitems, st);
+    return launch_fused_k<T, MODE, 0, SOLVE_BABE, true>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb,
+                                                        nchunks, qchunk, nitems, st);
+  }
   if (solve == SOLVE_REGS)
-    return launch_fused_k<T, MODE, 0, SOLVE_REGS>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks,
-                                                  qchunk, nitems, st);
-  return launch_fused_k<T, MODE, 0, SOLVE_BABE>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb, nchunks,
-                                                qchunk, nitems, st);
+    return launch_fused_k<T, MODE, 0, SOLVE_REGS, false>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb,
+                                                         nchunks, qchunk, nitems, st);
+  return launch_fused_k<T, MODE, 0, SOLVE_BABE, false>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb,
+                                                       nchunks, qchunk, nitems, st);
 }
 
 template <typename T>

@@ -16,7 +16,7 @@ y2 = torch.empty_like(x)
 out = torch.empty_like(q)
 idx = torch.empty(q.shape, dtype=torch.int32, device="cuda")
 for _ in range(iters):
-    api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags, y2=y2, out=out, idx=idx)
+    api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags | api.PATH_FUSED, y2=y2, out=out, idx=idx)
 torch.cuda.synchronize()
 assert api.status() == 0
 print("ok", cid)
