@@ -43,10 +43,20 @@ __host__ __device__ constexpr int babe_stride(int n) { return (n & 1) ? n : ((n 
 // where (h_c, g_c) belong to the interval already eliminated.  For dir = +1 this is the
 // paper's forward sweep verbatim; for dir = -1 it is the same recurrence read
 // from the other end.  Divisions are a correctly rounded reciprocal then a multiply.
+// The clamped end slope a thread of babe_tile needs (top: yp1, bottom: ypn; 0 when that end is
+// natural).  Callers issue this global load before staging the tile, so its latency is hidden.
 template <typename T>
-__device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int64_t c0, int bc,
-                                          const T *__restrict__ yp1, const T *__restrict__ ypn, T *dummy,
-                                          int tid) {
+__device__ __forceinline__ T babe_slope(int64_t c0, int nc, int bc, const T *__restrict__ yp1,
+                                        const T *__restrict__ ypn, int tid) {
+  const int t = tid >> 1;
+  const bool top = (tid & 1) == 0;
+  const int64_t cg = c0 + (t < nc ? t : 0);
+  if (top) return (bc & 1) ? yp1[cg] : T(0);
+  return (bc & 2) ? ypn[cg] : T(0);
+}
+
+template <typename T>
+__device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int bc, T sl, T *dummy, int tid) {
   const int t = tid >> 1;  // curve within the tile (tid = thread index within the solving group)
   const bool top = (tid & 1) == 0;
   const bool act = t < nc;         // pairs are lane-adjacent, so shuffles stay in-warp
@@ -60,7 +70,6 @@ __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int6
     Xc[j0] = T(j0);
     Xc[j0 + dir] = T(j0 + dir);
   }
-  const int64_t cg = c0 + (act ? t : 0);
   // end row
   T xo = Xc[j0], yo = Yc[j0];
   T xn = Xc[j0 + dir], yn = Yc[j0 + dir];
@@ -70,7 +79,6 @@ __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int6
   const bool clamped = top ? (bc & 1) : (bc & 2);
   T cp = T(0), dp = T(0);
   if (clamped) {  // P:966-971 (start) / P:1017-1018 (end): c' = 1/2, d' = 3 dir (g - y') / h
-    const T sl = top ? yp1[cg] : ypn[cg];
     ok &= finite(sl);
     cp = T(0.5);
     dp = T(3 * dir) * (gc - sl) * nr_rcp(hc);
@@ -155,6 +163,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict
   const int64_t c0 = (int64_t)blockIdx.x * CPB;
   const int nc = (int)min64(CPB, batch - c0);
   const int tot = nc * n;
+  const T sl = babe_slope(c0, nc, bc, yp1, ypn, threadIdx.x);  // in flight during the staging
   const T *xb = x + c0 * n;
   const T *yb = y + c0 * n;
 
@@ -185,7 +194,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict
   }
   __syncthreads();
 
-  babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn, dummy, threadIdx.x);
+  babe_tile(X, Y, S, n, nc, bc, sl, dummy, threadIdx.x);
   __syncthreads();
 
   T *y2b = y2 + c0 * n;
@@ -234,6 +243,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(const T *__restrict
     const int64_t c0 = it * CPB;
     const int nc = (int)min64(CPB, batch - c0);
     const int tot = nc * n;
+    const T sl = babe_slope(c0, nc, bc, yp1, ypn, threadIdx.x);  // in flight during the staging
     mbar_wait(bar, phase);
     phase ^= 1u;
     // to the odd-stride tiles: 16-byte reads of the raw stage (n*sizeof(T) % 16 == 0, so a
@@ -254,7 +264,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(const T *__restrict
     }
     __syncthreads();
     if (threadIdx.x == 0) issue(it + G);  // raw stage consumed: next tile in flight
-    babe_tile(X, Y, S, n, nc, c0, bc, yp1, ypn, dummy, threadIdx.x);
+    babe_tile(X, Y, S, n, nc, bc, sl, dummy, threadIdx.x);
     __syncthreads();
     T *y2b = y2 + c0 * n;
     for (int e = threadIdx.x * VW; e < tot; e += blockDim.x * VW) {

@@ -97,7 +97,8 @@ __device__ __forceinline__ void fused_solve_babe(const T *Xr, const T *Yr, T *Yt
   for (int p0 = sw * kBabeCurves; p0 < nc; p0 += nsw * kBabeCurves) {
     const int np = min(kBabeCurves, nc - p0);
     T *Yp = Yt + (size_t)p0 * S;
-    // transpose x, y of the pass into odd-stride rows (16-byte reads of the raw stage)
+    const T sl = babe_slope(c0 + p0, np, bc, yp1, ypn, lane);  // in flight during the transposition
+    // transpose x, y of the pass into the tiles (16-byte reads of the raw stage)
     const int tot = np * n;
     for (int e = lane * VW; e < tot; e += 32 * VW) {
       const int c = (int)divn.div((uint32_t)e);
@@ -111,7 +112,7 @@ __device__ __forceinline__ void fused_solve_babe(const T *Xr, const T *Yr, T *Yt
       }
     }
     __syncwarp();
-    babe_tile(Xs, Yp, S, n, np, c0 + p0, bc, yp1, ypn, dummy, lane);
+    babe_tile(Xs, Yp, S, n, np, bc, sl, dummy, lane);
     __syncwarp();
     if (y2) {
       T *yb = y2 + (c0 + p0) * n;
