@@ -30,7 +30,7 @@ template <typename T> struct Rec { T Gp, Vp, Wp, Gq, Vq, Wq; };
 
 // Merge adjacent block records A = [p, m], B = [m+1, q] into [p, q].
 template <typename T> __device__ __forceinline__ Rec<T> merge_rec(const Rec<T> &A, const Rec<T> &B) {
-  const T iD = T(1) / (T(1) - A.Wq * B.Vp);
+  const T iD = nr_rcp(T(1) - A.Wq * B.Vp);
   const T Gm = (A.Gq - A.Wq * B.Gp) * iD, Vm = A.Vq * iD, Wm = -(A.Wq * B.Wp) * iD;    // y_m
   const T Gm1 = (B.Gp - B.Vp * A.Gq) * iD, Vm1 = -(B.Vp * A.Vq) * iD, Wm1 = B.Wp * iD;  // y_{m+1}
   Rec<T> o;
@@ -49,7 +49,7 @@ template <typename T>
 __device__ __forceinline__ void split_seam(T AGq, T AVq, T AWq, T BGp, T BVp, T BWp, T L, T R, T &ym, T &ym1) {
   const T alpha = AGq - AVq * L;
   const T beta = BGp - BWp * R;
-  ym = (alpha - AWq * beta) / (T(1) - AWq * BVp);
+  ym = (alpha - AWq * beta) * nr_rcp(T(1) - AWq * BVp);
   ym1 = beta - BVp * ym;
 }
 
@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
   const T *yc = y + c * n;
   auto pad = [](int i) { return i + i / R; };
 
+  // coalesced staging with all of a thread's loads in flight before its first store
+#pragma unroll 8
   for (int e = threadIdx.x; e < nrows; e += NT) {
     X[pad(e)] = ld_stream(xc + P + e);
     Y[pad(e)] = ld_stream(yc + P + e);
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
     T hprev = T(0), ddprev = T(0);
     if (P + p > 0) {
       hprev = xi - xm1;
-      ddprev = (yi - ym1) / hprev;
+      ddprev = (yi - ym1) * nr_rcp(hprev);
     }
     T cprev = T(0), gprev = T(0), vprev = T(0);
 #pragma unroll
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
           else { xn = xq1; yn = yq1; }
           ok = ok && (xn > xi);
           h = xn - xi;
-          dd = (yn - yi) / h;
+          dd = (yn - yi) * nr_rcp(h);
         }
         T a, b, cc, d;
         if (gi == 0) {
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
         } else {  // Eq. init_val
           a = hprev; b = T(2) * (hprev + h); cc = h; d = T(6) * (dd - ddprev);
         }
-        const T inv = T(1) / (k == 0 ? b : b - a * cprev);
+        const T inv = nr_rcp(k == 0 ? b : b - a * cprev);
         const T cp = cc * inv;
         const T gp = (k == 0 ? d : d - a * gprev) * inv;
         const T vp = (k == 0 ? a : -(a * vprev)) * inv;
