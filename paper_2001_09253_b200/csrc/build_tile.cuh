@@ -285,10 +285,14 @@ template <typename T> __host__ __device__ constexpr size_t top_smem_bytes() {
   return sizeof(T) * (6 * kTopThreads + 6 * kTopThreads);
 }
 
+// Group c of the launch covers records [c ntiles, min((c+1) ntiles, ntot)) of the arrays (ntot <= 0:
+// every group has ntiles records -- one group per curve); so one long curve's tile records can
+// be merged by many CTAs (groups), their group records by one, and pushed back down by many.
 template <typename T>
 __global__ void __launch_bounds__(kTopThreads) k4_top(const T *__restrict__ recs, int ntiles, int up_only,
                                                       const T *__restrict__ root_ext, T *__restrict__ tile_ext,
-                                                      T *__restrict__ root_out, T *__restrict__ foldq) {
+                                                      T *__restrict__ root_out, T *__restrict__ foldq,
+                                                      int64_t ntot) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Rec<T> *rec = reinterpret_cast<Rec<T> *>(smem_raw);
   T *mi = reinterpret_cast<T *>(rec + kTopThreads);
@@ -296,6 +300,8 @@ __global__ void __launch_bounds__(kTopThreads) k4_top(const T *__restrict__ recs
   const int64_t c = blockIdx.x;
   const T *rc = recs + c * ntiles * 6;
   T *fq = foldq + c * ntiles * 3;
+  T *te = tile_ext + c * ntiles * 2;
+  if (ntot > 0) ntiles = (int)min64(ntiles, ntot - c * ntiles);
   const int chunk = (ntiles + kTopThreads - 1) / kTopThreads;
   const int nleaf = (ntiles + chunk - 1) / chunk;
   const int th = threadIdx.x;
@@ -331,7 +337,6 @@ __global__ void __launch_bounds__(kTopThreads) k4_top(const T *__restrict__ recs
   if (th < nleaf) {
     const T L = ext[2 * th];
     T Rv = ext[2 * th + 1];
-    T *te = tile_ext + c * ntiles * 2;
     for (int t = last; t > first; --t) {
       const Rec<T> B = load(t);
       T ym, ym1;

@@ -110,7 +110,7 @@ int build_mid(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T 
 }
 
 struct SpikeWs {
-  void *tile_rec, *tile_ext, *foldq, *badflag, *rank_ext, *rank_foldq;
+  void *tile_rec, *tile_ext, *foldq, *badflag, *rank_ext, *rank_foldq, *grp_rec;
 };
 constexpr int kMaxRanks = 1024;
 
@@ -128,17 +128,32 @@ template <typename T> size_t spike_ws_layout(int64_t ntiles, int64_t batch, Spik
   w.badflag = take(sizeof(int) * batch);
   w.rank_ext = take(sizeof(T) * 2 * kMaxRanks);
   w.rank_foldq = take(sizeof(T) * 3 * kMaxRanks);
+  w.grp_rec = take(sizeof(T) * 6 * kMaxRanks);
   if (ws) *ws = w;
   return off;
 }
 
 template <typename T> int launch_top(const T *recs, int ntiles, int64_t batch, int up_only, const T *root_ext,
-                                     T *tile_ext, T *root_out, T *foldq, cudaStream_t st) {
+                                     T *tile_ext, T *root_out, T *foldq, cudaStream_t st, int64_t ntot = 0) {
   auto kern = k4_top<T>;
   const size_t sm = top_smem_bytes<T>();
   if (int rc = set_smem(kern, sm)) return rc;
-  kern<<<(unsigned)batch, kTopThreads, sm, st>>>(recs, ntiles, up_only, root_ext, tile_ext, root_out, foldq);
+  kern<<<(unsigned)batch, kTopThreads, sm, st>>>(recs, ntiles, up_only, root_ext, tile_ext, root_out, foldq, ntot);
   return launch_rc();
+}
+
+// K4 for ONE long curve with many tiles: groups of kGroupTiles tiles are merged by one CTA each
+// (up), the group records by one CTA (up + down), and the outer values pushed back down the
+// groups (down) -- instead of one CTA folding every tile record.
+constexpr int kGroupTiles = 64;
+template <typename T>
+int launch_top_grouped(const T *recs, int ntiles, const SpikeWs &w, cudaStream_t st) {
+  const int G = (ntiles + kGroupTiles - 1) / kGroupTiles;
+  T *grp = (T *)w.grp_rec, *gext = (T *)w.rank_ext, *gfq = (T *)w.rank_foldq;
+  int rc = launch_top<T>(recs, kGroupTiles, G, 1, nullptr, nullptr, grp, (T *)w.foldq, st, ntiles);
+  if (!rc) rc = launch_top<T>(grp, G, 1, 0, nullptr, gext, nullptr, gfq, st);
+  if (!rc) rc = launch_top<T>(recs, kGroupTiles, G, 0, gext, (T *)w.tile_ext, nullptr, (T *)w.foldq, st, ntiles);
+  return rc;
 }
 
 template <typename T, int MODE>
@@ -166,8 +181,13 @@ int build_long(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T
   spike_ws_layout<T>(ntiles, batch, &w, (char *)base);
   int rc = cuda_rc(cudaMemsetAsync(w.badflag, 0, sizeof(int) * batch, st));
   if (!rc) rc = launch_tile_part<T, TILE_REDUCE>(x, y, n, 0, n, batch, bc, yp1, ypn, y2, w, st);
-  if (!rc) rc = launch_top<T>((const T *)w.tile_rec, (int)ntiles, batch, 0, nullptr, (T *)w.tile_ext, nullptr,
-                              (T *)w.foldq, st);
+  if (!rc) {
+    if (batch == 1 && ntiles > 2 * kGroupTiles && (ntiles + kGroupTiles - 1) / kGroupTiles <= kMaxRanks)
+      rc = launch_top_grouped<T>((const T *)w.tile_rec, (int)ntiles, w, st);
+    else
+      rc = launch_top<T>((const T *)w.tile_rec, (int)ntiles, batch, 0, nullptr, (T *)w.tile_ext, nullptr,
+                         (T *)w.foldq, st);
+  }
   if (!rc) rc = launch_tile_part<T, TILE_FINISH>(x, y, n, 0, n, batch, bc, yp1, ypn, y2, w, st);
   cudaFreeAsync(base, st);
   return rc;
