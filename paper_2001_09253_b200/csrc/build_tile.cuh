@@ -58,10 +58,11 @@ __device__ __forceinline__ void split_seam(T AGq, T AVq, T AWq, T BGp, T BVp, T 
 // every merge are saved in mi[] for the top-down pass.  Ends with __syncthreads().
 template <typename T> __device__ void tree_up(Rec<T> *rec, T *mi, int nleaf) {
   int off = 0;
-  for (int s = 1; s < nleaf; s <<= 1) {
-    const int nn = (nleaf + 2 * s - 1) / (2 * s);
+  for (int lg = 0; (1 << lg) < nleaf; ++lg) {  // s = 2^lg (shifts: the level sizes are powers of 2)
+    const int s = 1 << lg;
+    const int nn = (nleaf + 2 * s - 1) >> (lg + 1);
     for (int k = threadIdx.x; k < nn; k += blockDim.x) {
-      const int i = k * 2 * s, j = i + s;
+      const int i = k << (lg + 1), j = i + s;
       if (j < nleaf) {
         const Rec<T> A = rec[i], B = rec[j];
         T *o = mi + 6 * (off + k);
@@ -77,16 +78,20 @@ template <typename T> __device__ void tree_up(Rec<T> *rec, T *mi, int nleaf) {
 // Top-down: ext[i] = (L, R) of leaf i, given the root's (L, R).  Ends with __syncthreads().
 template <typename T> __device__ void tree_down(const T *mi, T *ext, int nleaf, T L, T R) {
   if (threadIdx.x == 0) { ext[0] = L; ext[1] = R; }
-  int smax = 1, total = 0;
-  for (int s = 1; s < nleaf; s <<= 1) { smax = s; total += (nleaf + 2 * s - 1) / (2 * s); }
+  int lgmax = 0, total = 0;
+  for (int lg = 0; (1 << lg) < nleaf; ++lg) {
+    lgmax = lg;
+    total += (nleaf + (2 << lg) - 1) >> (lg + 1);
+  }
   __syncthreads();
   if (nleaf == 1) return;
   int off = total;
-  for (int s = smax; s >= 1; s >>= 1) {
-    const int nn = (nleaf + 2 * s - 1) / (2 * s);
+  for (int lg = lgmax; lg >= 0; --lg) {
+    const int s = 1 << lg;
+    const int nn = (nleaf + 2 * s - 1) >> (lg + 1);
     off -= nn;
     for (int k = threadIdx.x; k < nn; k += blockDim.x) {
-      const int i = k * 2 * s, j = i + s;
+      const int i = k << (lg + 1), j = i + s;
       if (j < nleaf) {
         const T *o = mi + 6 * (off + k);
         const T Li = ext[2 * i], Ri = ext[2 * i + 1];
