@@ -142,9 +142,24 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
   const T *yc = y + c * n;
   auto pad = [](int i) { return i + i / R; };
 
-  // coalesced staging with all of a thread's loads in flight before its first store
+  // coalesced staging with all of a thread's loads in flight before its first store;
+  // 16-byte vectors when the tile's rows are 16-byte aligned
+  constexpr int VW = 16 / sizeof(T);
+  using VT = typename Vec16<T>::V;
+  const bool vec = ((((uintptr_t)(xc + P)) | ((uintptr_t)(yc + P))) & 15) == 0;
+  const int nvec = vec ? nrows / VW : 0;
+#pragma unroll 4
+  for (int v = threadIdx.x; v < nvec; v += NT) {
+    const VT a = __ldcs(reinterpret_cast<const VT *>(xc + P) + v);
+    const VT b = __ldcs(reinterpret_cast<const VT *>(yc + P) + v);
+#pragma unroll
+    for (int i = 0; i < VW; ++i) {
+      X[pad(v * VW + i)] = reinterpret_cast<const T *>(&a)[i];
+      Y[pad(v * VW + i)] = reinterpret_cast<const T *>(&b)[i];
+    }
+  }
 #pragma unroll 8
-  for (int e = threadIdx.x; e < nrows; e += NT) {
+  for (int e = nvec * VW + threadIdx.x; e < nrows; e += NT) {
     X[pad(e)] = ld_stream(xc + P + e);
     Y[pad(e)] = ld_stream(yc + P + e);
   }
@@ -277,7 +292,15 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < nrows; e += NT) y2o[e] = X[pad(e)];
+  const bool vo = (((uintptr_t)y2o) & 15) == 0;
+  const int novec = vo ? nrows / VW : 0;
+  for (int v = threadIdx.x; v < novec; v += NT) {
+    VT a;
+#pragma unroll
+    for (int i = 0; i < VW; ++i) reinterpret_cast<T *>(&a)[i] = X[pad(v * VW + i)];
+    __stcs(reinterpret_cast<VT *>(y2o) + v, a);
+  }
+  for (int e = novec * VW + threadIdx.x; e < nrows; e += NT) y2o[e] = X[pad(e)];
 }
 
 // K4: merge the per-tile records of each curve (grid = batch, one CTA per curve) and,
