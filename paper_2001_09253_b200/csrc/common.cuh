@@ -57,7 +57,7 @@ __device__ __forceinline__ double r_mul(double a, double b) { return __dmul_rn(a
 __device__ __forceinline__ float r_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double r_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float r_rcp(float a) { return __frcp_rn(a); }   // correctly rounded 1/a
-__device__ __forceinline__ double r_rcp(double a) { return __drcp_rn(a); }
+__device__ __forceinline__ double r_rcp(double a);  // fp64: rcp.approx + 2 Newton steps (below)
 
 // Reciprocal for the solver sweeps: hardware approximation refined by Newton-Raphson
 // (fp32: one step; fp64: two steps after the 23-bit MUFU seed), |relative error| <= ~1 ulp
@@ -77,6 +77,10 @@ __device__ __forceinline__ double nr_rcp(double a) {
   e = __fma_rn(-a, r, 1.0);
   return __fma_rn(r, e, r);
 }
+// The eval kernels' fp64 reciprocal: the correctly rounded __drcp_rn costs a slow-path
+// sequence per query in the sorted-run kernel; the Newton-refined seed is within ~1 ulp and is
+// what every eval kernel uses (so all of them still give identical bits).
+__device__ __forceinline__ double r_rcp(double a) { return nr_rcp(a); }
 
 // Eq. nr_formula on one interval [x0, x1], in the factored form every eval kernel
 // uses.  With h = x1 - x0, B = (q - x0)/h, A = 1 - B and zs_k = y2_k h^2/6:
