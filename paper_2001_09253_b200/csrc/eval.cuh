@@ -273,7 +273,8 @@ __device__ __forceinline__ void pack_item(const T *X, const T *Y, const T *Z, in
     }
     if (j == 0 || (MODE == MODE_TABLE && j < n - 1)) {
       const T x0 = X[c * n], xn = X[c * n + n - 1];
-      const T sc = (MODE == MODE_TABLE) ? (T)nb / (xn - x0) : (T)(n - 1) / (xn - x0);
+      // (the scale only steers a guess that is always verified: any positive value is exact)
+      const T sc = r_mul((MODE == MODE_TABLE) ? (T)nb : (T)(n - 1), nr_rcp(xn - x0));
       if (j == 0) Hd[c] = CurveHdr<T>{x0, xn, sc, T(0)};
       if (MODE == MODE_TABLE) {
         uint16_t *Tc = Tb + c * (nb + 2);
@@ -300,7 +301,7 @@ __device__ __forceinline__ void pack_item(const T *X, const T *Y, const T *Z, in
 // c0; the queries staged at Qs when BULK, else read from q).  Warp w of nw owns a contiguous
 // run of V-query groups; lane l takes groups wb+l, wb+l+32, ...  Returns "some query was
 // out of range".
-template <typename T, int MODE, int V, bool BULK, int L2>
+template <typename T, int MODE, int V, bool BULK, int L2, int NW>
 __device__ __forceinline__ bool eval_item_queries(const T *Qs, const T *__restrict__ q, int64_t k0, int64_t c0,
                                                   int m, int cnt, int cpb, FastDiv divm, const Cub<T> *RP,
                                                   const T *RE, const T *XK,
@@ -311,7 +312,7 @@ __device__ __forceinline__ bool eval_item_queries(const T *Qs, const T *__restri
   constexpr bool PACKED = (MODE != MODE_BSEARCH);
   bool oor = false;
   const int ng = cnt / V;
-  const int per = (ng + nw - 1) / nw;
+  const int per = (ng + NW - 1) / NW;  // NW (= nw) a compile-time warp count: a shift
   const int wb = w * per, we = min(ng, wb + per);
   const int kbase = (int)(k0 - c0 * m);  // item's first query, relative to its first curve
   T *const ob = out + k0;
@@ -446,7 +447,8 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
       pack_item<T, MODE, L2>(X, Y, Z, n, nc, n, nb, divn, KP, KE, XK, Hd, Xs, Tb, P, threadIdx.x, blockDim.x);
       __syncthreads();  // packed data built
     }
-    oor |= eval_item_queries<T, MODE, V, BULK, L2>(Qs, q, k0, c0, m, cnt, cpb, divm, KP, KE, XK, Hd, Xs, Tb, X, Y, Z, n,
+    oor |= eval_item_queries<T, MODE, V, BULK, L2, kEvalThreads / 32>(Qs, q, k0, c0, m, cnt, cpb, divm, KP, KE, XK, Hd,
+                                                                      Xs, Tb, X, Y, Z, n,
                                                    nb, P, out, idx, w, nw, lane);
     __syncthreads();  // everyone is done with this item's stage and packed data
     if (threadIdx.x == 0) issue(it + 2 * G, s);
@@ -528,7 +530,7 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
                              Xs + cw0 * P,
                              Tb + cw0 * (nb + 2), P, lane, 32);
       __syncwarp();
-      oor |= eval_item_queries<T, MODE, V, true, L2>(Qs, q, (c0 + cw0) * m, c0 + cw0, m, nmy * m, cpb, divm,
+      oor |= eval_item_queries<T, MODE, V, true, L2, 1>(Qs, q, (c0 + cw0) * m, c0 + cw0, m, nmy * m, cpb, divm,
                                                      KP + cw0 * n, KE + cw0 * n, XK + cw0 * n, Hd + cw0,
                                                      Xs + cw0 * P,
                                                      Tb + cw0 * (nb + 2), X, Y, Z, n, nb, P, out, idx, 0, 1, lane);

@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
       }
       mbar_wait(qbar + qs, (uint32_t)(k / kQueryStages) & 1u);
       if (nmy > 0)
-        oor |= eval_item_queries<T, MODE, V, true, L2>(qstage(qs) + (size_t)cw0 * m, q, (c0 + cw0) * m, c0 + cw0, m,
+        oor |= eval_item_queries<T, MODE, V, true, L2, 1>(qstage(qs) + (size_t)cw0 * m, q, (c0 + cw0) * m, c0 + cw0, m,
                                                        nmy * m, cpb, divm, KP + cw0 * n, KE + cw0 * n, XK + cw0 * n,
                                                        Hd + cw0, Xs + cw0 * P, nullptr, X, Y, Z, n, 0, P, out, idx,
                                                        0, 1, lane);
@@ -354,7 +354,8 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
       nbar_sync(BAR_EVAL, kFusedEvalThreads);                          // packed data built; stage ks free
       if (threadIdx.x == 0) issue_knots(it + kKnotStages * G, ks);
       mbar_wait(qbar + qs, (uint32_t)(k / kQueryStages) & 1u);
-      oor |= eval_item_queries<T, MODE, V, true, L2>(qstage(qs), q, k0, c0, m, cnt, cpb, divm, KP, KE, XK, Hd, Xs, nullptr,
+      oor |= eval_item_queries<T, MODE, V, true, L2, kFusedEvalWarps>(qstage(qs), q, k0, c0, m, cnt, cpb, divm, KP, KE, XK,
+                                                                      Hd, Xs, nullptr,
                                                      X, Y, ytile(ks), n, 0, P, out, idx, warp, kFusedEvalWarps,
                                                      lane);
       nbar_sync(BAR_EVAL, kFusedEvalThreads);  // done with query stage qs and the packed data
