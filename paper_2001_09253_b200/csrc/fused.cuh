@@ -46,16 +46,18 @@ constexpr int kRegsNMax = 8;     // SOLVE_REGS for n <= 8
 constexpr int kBabeCurves = 16;  // curves per solver-warp pass (2 lanes each)
 constexpr int kKnotStages = 3;   // x, y (+ y2 tile) stages
 constexpr int kQueryStages = 2;
-// solver warps per CTA (each solves whole items, alternately)
-__host__ __device__ constexpr int fused_solver_warps(int) { return 2; }
-__host__ __device__ constexpr int fused_threads(int solve) { return kFusedEvalThreads + 32 * fused_solver_warps(solve); }
+// solver warps per CTA, each solving whole items in turn: 4 with per-warp ownership (the
+// hand-offs are mbarriers, see the solver's tempty wait); 1 otherwise -- several solvers
+// would share a named barrier id for different items.
+__host__ __device__ constexpr int fused_solver_warps(bool wown) { return wown ? 4 : 1; }
+__host__ __device__ constexpr int fused_threads(bool wown) { return kFusedEvalThreads + 32 * fused_solver_warps(wown); }
 // named barrier ids (0 is __syncthreads)
 enum { BAR_EVAL = 1, BAR_TFULL = 2, BAR_TEMPTY = 2 + kKnotStages };
 
 template <typename T> struct FusedLayout {
   size_t kst0, kststep, qst0, qststep, ytile, ytstep, scratch, scrstep, knots, e2, xk, hdr, xs, total;
   int P, S2;
-  __host__ __device__ FusedLayout(int cpb, int n, int qmax, int solve, int mode) {
+  __host__ __device__ FusedLayout(int cpb, int n, int qmax, int solve, int mode, bool wown) {
     P = 1 << eytz_levels(n);
     S2 = (solve == SOLVE_BABE) ? babe_stride(n) : n;
     size_t off = 128;  // mbarriers (knot stages, query stages, tile full, tile empty) + counters
@@ -70,7 +72,7 @@ template <typename T> struct FusedLayout {
     off += kKnotStages * ytstep;
     scratch = off;  // per solver warp: c' rows of one babe pass + 2 rows for inactive pairs
     scrstep = (solve == SOLVE_BABE) ? align16(sizeof(T) * (size_t)(kBabeCurves + 2) * S2) : 0;
-    off += fused_solver_warps(solve) * scrstep;
+    off += fused_solver_warps(wown) * scrstep;
     knots = off;
     off = align16(off + sizeof(Cub<T>) * (size_t)cpb * n);
     e2 = off;
@@ -183,16 +185,16 @@ __device__ __forceinline__ void fused_solve_regs(const T *Xr, const T *Yr, T *Yt
 // (shared counter) refills it.  Otherwise (chunked single curves) the CTA packs together and
 // the hand-offs are named barriers.
 template <typename T, int MODE, int L2, int SOLVE, bool WOWN>
-__global__ void __launch_bounds__(fused_threads(SOLVE), 3)
+__global__ void __launch_bounds__(fused_threads(WOWN), WOWN ? 2 : 3)
     k_fused_staged(const T *__restrict__ x, const T *__restrict__ y, int n, int64_t batch, int bc,
                    const T *__restrict__ yp1, const T *__restrict__ ypn, T *__restrict__ y2, const T *__restrict__ q,
                    int m, T *__restrict__ out, int32_t *__restrict__ idx, int cpb, int nchunks, int qchunk, int qmax,
                    int64_t nitems, FastDiv divn, FastDiv divm) {
   constexpr int V = 16 / sizeof(T);
-  constexpr int NSW = fused_solver_warps(SOLVE);
+  constexpr int NSW = fused_solver_warps(WOWN);
   constexpr int NB = kFusedEvalThreads + 32;  // named-barrier participants: evaluators + one solver warp
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const FusedLayout<T> L(cpb, n, qmax, SOLVE, MODE);
+  const FusedLayout<T> L(cpb, n, qmax, SOLVE, MODE, WOWN);
   uint64_t *kbar = reinterpret_cast<uint64_t *>(smem_raw);  // [kKnotStages]
   uint64_t *qbar = kbar + kKnotStages;                       // [kQueryStages]
   uint64_t *tfull = qbar + kQueryStages;                     // [kKnotStages]  (WOWN)
@@ -278,7 +280,12 @@ __global__ void __launch_bounds__(fused_threads(SOLVE), 3)
       int nc, cnt;
       item_of(it, c0, k0, nc, cnt);
       if constexpr (WOWN) {
-        if (k >= kKnotStages) mbar_wait(tempty + ks, (uint32_t)(k / kKnotStages - 1) & 1u);  // item k-3 packed
+        // item k-3 packed.  A solver reaching item k has finished item k-NSW, so stage ks may be
+        // up to ceil(NSW/3) completions behind; a parity wait only tells phases one apart, so
+        // wait for each of them in order (one wait for NSW <= 2).
+#pragma unroll
+        for (int back = (NSW + kKnotStages - 1) / kKnotStages; back >= 1; --back)
+          if (k / kKnotStages - back >= 0) mbar_wait(tempty + ks, (uint32_t)(k / kKnotStages - back) & 1u);
         mbar_wait(kbar + ks, (uint32_t)(k / kKnotStages) & 1u);
       } else {
         mbar_wait(kbar + ks, (uint32_t)(k / kKnotStages) & 1u);

@@ -425,12 +425,12 @@ int launch_fused_k(const T *x, const T *y, int n, int64_t batch, int bc, const T
     }
   } else {
     const int qmax = (cpb > 1) ? cpb * (int)m : qchunk;
-    const FusedLayout<T> L(cpb, n, qmax, SOLVE, MODE);
+    const FusedLayout<T> L(cpb, n, qmax, SOLVE, MODE, WOWN);
     const size_t sm = L.total;
     auto kern = k_fused_staged<T, MODE, L2, SOLVE, WOWN>;
     if (int rc = set_smem(kern, sm)) return rc;
     int occ = 0;
-    constexpr int NT = fused_threads(SOLVE);
+    constexpr int NT = fused_threads(WOWN);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, sm) != cudaSuccess || occ < 1) occ = 1;
     const int64_t grid = std::min<int64_t>(nitems, (int64_t)occ * num_sms());
     kern<<<(unsigned)grid, NT, sm, st>>>(x, y, n, batch, bc, yp1, ypn, y2, q, (int)m, out, idx, cpb, nchunks,
@@ -450,7 +450,7 @@ template <typename T> bool fused_eligible(const T *x, const T *y, int64_t n, con
   if (idx && ((uintptr_t)idx & (4 * VW - 1)) != 0) return false;
   const int mode = MODE_BISECT;  // the larger footprint of the two modes
   const int solve = n <= kRegsNMax ? SOLVE_REGS : SOLVE_BABE;
-  return FusedLayout<T>(1, (int)n, kQMax, solve, mode).total <= kSmemCap;
+  return FusedLayout<T>(1, (int)n, kQMax, solve, mode, false).total <= kSmemCap;
 }
 
 template <typename T, int MODE>
@@ -471,7 +471,7 @@ int launch_fused(const T *x, const T *y, int n, int64_t batch, int bc, const T *
   } else {
     int64_t c = std::max<int64_t>(1, kQMax / m);
     c = std::min<int64_t>(c, batch);
-    while (c > 1 && FusedLayout<T>((int)c, n, (int)(c * m), solve, MODE).total > kFusedItemSmem) --c;
+    while (c > 1 && FusedLayout<T>((int)c, n, (int)(c * m), solve, MODE, c >= 8).total > kFusedItemSmem) --c;
     while (c > 1 && (uint64_t)c * m * m >= (1ull << 32)) c >>= 1;  // FastDiv range
     cpb = (int)std::max<int64_t>(1, c);
     nitems = (batch + cpb - 1) / cpb;
