@@ -60,3 +60,22 @@ def test_full_size_sampled(api, cid, curves, qs):
         eo = parity.out_rel_err(out[0, kt].cpu().numpy()[None], out_ref, wl.y)
         assert np.all(eo <= tol), eo.max()
     print(f"cfg{cid} full: y2 {e.max():.3e} out(sampled) {eo.max():.3e}")
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_full_size_fused_equals_split(api, cid):
+    """The fused kernel at full size (many items per persistent CTA: the hand-off protocol
+    runs its whole phase cycle many times) gives bitwise the split path's y2, out and idx."""
+    wl = workloads.generate(cid)
+    t = parity.to_dev
+    x, y, q = t(wl.x), t(wl.y), t(wl.q)
+    yp1 = t(wl.yp1) if wl.yp1 is not None else None
+    ypn = t(wl.ypn) if wl.ypn is not None else None
+    api.status()
+    y2f, outf, idxf = api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags | api.PATH_FUSED)
+    y2s, outs, idxs = api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags | api.PATH_SPLIT)
+    torch.cuda.synchronize()
+    assert api.status() == 0
+    assert torch.equal(y2f.view(torch.int8), y2s.view(torch.int8))
+    assert torch.equal(idxf, idxs)
+    assert torch.equal(outf.view(torch.int8), outs.view(torch.int8))
