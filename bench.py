@@ -129,6 +129,10 @@ class ClockSampler:
                 "reasons": rs, "samples": len(self.samples)}
 
 
+def long_curve_cfg(n, s):
+    return n > 256 * (16 if s == 8 else 32)
+
+
 def algorithmic_bytes(B, n, m, s):
     """SURVEY.md §8(d): build 3 s B/knot (read x, y; write y2) + 2 s per clamped curve;
     eval (2 s + 4) B/query (read q; write out, int32 idx) + 3 n s per curve (x, y, y2)."""
@@ -417,6 +421,25 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms, bms, ems, fused_ms = t.tolist()
 
+    # ---- cfg5: the random-gather ceiling: the same gathers at known intervals
+    gather = None
+    if long_curve_cfg(n, s):
+        def probe_ms(mode):
+            pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+            api.gather_probe(x, y, y2, q, idx, mode, out=pout, idx=pidx)
+            for kk in range(K):
+                flush.zero_()
+                pev[kk][0].record(stream)
+                api.gather_probe(x, y, y2, q, idx, mode, out=pout, idx=pidx)
+                pev[kk][1].record(stream)
+            torch.cuda.synchronize()
+            return statistics.mean(a.elapsed_time(b) for a, b in pev)
+        pout, pidx = torch.empty_like(out), torch.empty_like(idx)
+        raw_ms, rec_ms = probe_ms(0), probe_ms(1)
+        gather = {"raw_3array_ms": raw_ms, "records_ms": rec_ms, "eval_ms": None,
+                  "note": "spline_gather_probe: evaluation at the already known intervals (no search); "
+                          "records_ms includes building the records, like the eval path"}
+
     # ---- end to end through the public API with host buffers (pinned), copies timed
     e2e = None
     if not args.no_e2e:
@@ -520,6 +543,8 @@ def main():
                   if fusable else None),
         "cpu_baseline": None,
         "e2e": e2e,
+        "gather_ceiling": (dict(gather, eval_ms=ems, eval_over_records_ceiling=gather["records_ms"] / ems)
+                           if gather else None),
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

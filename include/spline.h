@@ -138,6 +138,20 @@ enum { SPLINE_FORM_RECORD = 0, SPLINE_FORM_SPLINT_DIV = 1, SPLINE_FORM_SPLINT_MU
 int spline_eval_ablation(const void *x, const void *y, const void *y2, int64_t n, int64_t batch, const void *q,
                          int64_t m, void *out, int32_t *idx, int form, int dtype, spline_stream_t stream);
 
+/*
+ * spline_gather_probe -- diagnostic: the random-gather ceiling of evaluation
+ * on long curves.  With the intervals ALREADY KNOWN (idx_in [batch][m], e.g. spline_eval's
+ * idx; -1 = out of range), evaluate without any search:
+ *   mode 0: gather x_j, x_{j+1}, y_j, y_{j+1}, y2_j, y2_{j+1} from the three arrays;
+ *   mode 1: build the interval records (as spline_eval does for long curves) and gather one
+ *           record per query.
+ * Writes out (the cubic; NaN where idx_in < 0) and idx (= idx_in).  Its time is what the
+ * access pattern itself costs; spline_eval's long-curve path is reported against it.
+ */
+int spline_gather_probe(const void *x, const void *y, const void *y2, int64_t n, int64_t batch, const void *q,
+                        int64_t m, const int32_t *idx_in, void *out, int32_t *idx, int mode, int dtype,
+                        spline_stream_t stream);
+
 /* Typed thin wrappers (same semantics). */
 int spline_build_f32(const float *x, const float *y, int64_t n, int64_t batch, int bc, const float *yp1,
                      const float *ypn, float *y2, spline_stream_t stream);

@@ -133,6 +133,21 @@ def evaluate_ablation(x, y, y2, q, form: str, out=None, idx=None, stream=None):
     return o, i
 
 
+def gather_probe(x, y, y2, q, idx_in, mode: int, out=None, idx=None, stream=None):
+    """spline_gather_probe (diagnostic): evaluate at the KNOWN intervals idx_in with no search --
+    mode 0 gathers from x, y, y2; mode 1 through interval records.  Returns (out, idx)."""
+    x, y, y2, q, idx_in = _as2d(x), _as2d(y), _as2d(y2), _as2d(q), _as2d(idx_in)
+    B, n = x.shape
+    m = q.shape[1]
+    _check_curves(x, y, y2, q)
+    o = torch.empty_like(q) if out is None else out
+    i = torch.empty(q.shape, dtype=torch.int32, device=q.device) if idx is None else idx
+    rc = _lib.load().spline_gather_probe(_p(x), _p(y), _p(y2), n, B, _p(q), m, _p(idx_in), _p(o), _p(i), mode,
+                                         _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_gather_probe")
+    return o, i
+
+
 def status(stream=None) -> int:
     """Synchronise the stream, return and clear the data-error bits (STATUS_*)."""
     bits = ctypes.c_uint(0)

@@ -799,6 +799,36 @@ __global__ void __launch_bounds__(256) k_eval_records(const Ival<T> *__restrict_
   if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
 }
 
+// ---- diagnostics: the random-gather ceiling of the long-curve evaluation ---
+// The access pattern alone, with the interval already known (idx_in, e.g. from spline_eval):
+//   k_probe_raw : q, then x_j, x_{j+1}, y_j, y_{j+1}, y2_j, y2_{j+1} from the three arrays
+//                 (the pattern of an evaluation without records), out = the cubic, idx copied;
+//   k_probe_rec : q, then the one record of interval j (the pattern of k_eval_records).
+// They do no search: their time is what the gathers themselves cost on this memory system.
+template <typename T>
+__global__ void __launch_bounds__(256) k_probe_raw(const T *__restrict__ x, const T *__restrict__ y,
+                                                   const T *__restrict__ y2, int n, int64_t batch,
+                                                   const T *__restrict__ q, int64_t m,
+                                                   const int32_t *__restrict__ idx_in, T *__restrict__ out,
+                                                   int32_t *__restrict__ idx) {
+  const int64_t total = batch * m;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int j = __ldcs(idx_in + k);
+    const int64_t off = (batch == 1) ? 0 : (k / m) * n;
+    const int jj = max(j, 0);
+    const T *X = x + off + jj, *Y = y + off + jj, *Z = y2 + off + jj;
+    const T v = nr_interp(ld_stream(q + k), __ldg(X), __ldg(X + 1), __ldg(Y), __ldg(Y + 1), __ldg(Z), __ldg(Z + 1));
+    st_stream(out + k, j >= 0 ? v : qnan<T>());
+    st_stream(idx + k, j);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_probe_rec(const Ival<T> *__restrict__ R, int n, int64_t batch,
+                                                   const T *__restrict__ q, int64_t m,
+                                                   const int32_t *__restrict__ idx_in, T *__restrict__ out,
+                                                   int32_t *__restrict__ idx);
+
 // Long curves (not stageable): locate in HBM.  Each thread carries U independent queries
 // through the three dependent round trips (q -> x pair at the interpolation guess -> y, y2
 // pairs) so that U x (threads per SM) gathers are in flight.  The guess
@@ -873,6 +903,22 @@ __global__ void __launch_bounds__(256) k_eval_global(const T *__restrict__ x, co
     }
   }
   if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_probe_rec(const Ival<T> *__restrict__ R, int n, int64_t batch,
+                                                   const T *__restrict__ q, int64_t m,
+                                                   const int32_t *__restrict__ idx_in, T *__restrict__ out,
+                                                   int32_t *__restrict__ idx) {
+  const int64_t total = batch * m;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int j = __ldcs(idx_in + k);
+    const int64_t off = (batch == 1) ? 0 : (k / m) * n;
+    const Ival<T> r = ld_ival(R + off + max(j, 0));
+    const T v = ival_interp<T>(r, ld_stream(q + k));
+    st_stream(out + k, j >= 0 ? v : qnan<T>());
+    st_stream(idx + k, j);
+  }
 }
 
 }  // namespace fs

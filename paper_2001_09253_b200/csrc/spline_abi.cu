@@ -539,6 +539,31 @@ int ablation_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, co
   }
 }
 
+template <typename T>
+int probe_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const T *q, int64_t m,
+            const int32_t *idx_in, T *out, int32_t *idx, int mode, cudaStream_t st) {
+  const int64_t total = batch * m;
+  const int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+  if (mode == 0) {
+    k_probe_raw<T><<<(unsigned)grid, 256, 0, st>>>(x, y, y2, (int)n, batch, q, m, idx_in, out, idx);
+    return launch_rc();
+  }
+  const size_t rec_bytes = sizeof(Ival<T>) * (size_t)n * batch, hdr_bytes = sizeof(CurveHdr<T>) * (size_t)batch;
+  void *ws = nullptr;
+  if (int rc = ws_alloc(&ws, rec_bytes + hdr_bytes, st)) return rc;
+  Ival<T> *R = reinterpret_cast<Ival<T> *>(ws);
+  CurveHdr<T> *H = reinterpret_cast<CurveHdr<T> *>(reinterpret_cast<char *>(ws) + rec_bytes);
+  const int64_t pg = std::min<int64_t>(((n + 3) / 4 * batch + 255) / 256, (int64_t)num_sms() * 16);
+  k_pack_records<T><<<(unsigned)pg, 256, 0, st>>>(x, y, y2, (int)n, batch, R, H);
+  int rc = launch_rc();
+  if (!rc) {
+    k_probe_rec<T><<<(unsigned)grid, 256, 0, st>>>(R, (int)n, batch, q, m, idx_in, out, idx);
+    rc = launch_rc();
+  }
+  cudaFreeAsync(ws, st);
+  return rc;
+}
+
 int check_build(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1, const void *ypn,
                 const void *y2, int dtype) {
   if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
@@ -654,6 +679,21 @@ int spline_eval_ablation(const void *x, const void *y, const void *y2, int64_t n
                              (float *)out, idx, form, st);
   return ablation_t<double>((const double *)x, (const double *)y, (const double *)y2, n, batch, (const double *)q, m,
                             (double *)out, idx, form, st);
+}
+
+int spline_gather_probe(const void *x, const void *y, const void *y2, int64_t n, int64_t batch, const void *q,
+                        int64_t m, const int32_t *idx_in, void *out, int32_t *idx, int mode, int dtype,
+                        spline_stream_t stream) {
+  if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
+  if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || m < 0 || (mode != 0 && mode != 1)) return SPLINE_EINVAL;
+  if (batch == 0 || m == 0) return SPLINE_OK;
+  if (!x || !y || !y2 || !q || !idx_in || !out || !idx) return SPLINE_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SPLINE_F32)
+    return probe_t<float>((const float *)x, (const float *)y, (const float *)y2, n, batch, (const float *)q, m,
+                          idx_in, (float *)out, idx, mode, st);
+  return probe_t<double>((const double *)x, (const double *)y, (const double *)y2, n, batch, (const double *)q, m,
+                         idx_in, (double *)out, idx, mode, st);
 }
 
 int spline_build_f32(const float *x, const float *y, int64_t n, int64_t batch, int bc, const float *yp1,

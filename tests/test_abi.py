@@ -110,3 +110,13 @@ def test_einval_build_eval():
     assert f(None, p, 8, 1, 0, None, None, p, p, 4, p, None, 0, F32, None) == E   # NULL x
     assert f(p, p, 8, 1, 0, None, None, p, p, 4, p, None, 12, F32, None) == E     # both path hints
     assert f(None, None, 8, 0, 0, None, None, None, None, 4, None, None, 0, F32, None) == _lib.SPLINE_OK
+
+
+def test_einval_gather_probe():
+    lib = _lib.load()
+    p = ctypes.c_void_p(16)
+    F64, E = _lib.SPLINE_F64, _lib.SPLINE_EINVAL
+    assert lib.spline_gather_probe(p, p, p, 8, 1, p, 4, p, p, p, 2, F64, None) == E    # bad mode
+    assert lib.spline_gather_probe(p, p, p, 2, 1, p, 4, p, p, p, 0, F64, None) == E    # n < 3
+    assert lib.spline_gather_probe(p, p, p, 8, 1, p, 4, None, p, p, 0, F64, None) == E  # NULL idx_in
+    assert lib.spline_gather_probe(None, None, None, 8, 0, None, 4, None, None, None, 0, F64, None) == _lib.SPLINE_OK

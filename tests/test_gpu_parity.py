@@ -233,3 +233,21 @@ def test_spike_record_matches_dense_block(api):
         scale = np.array([abs(r[0]) + abs(r[3])] * 6)
         scale[[1, 2, 4, 5]] = 1.0
         assert np.all(np.abs(g - r) <= 1e-12 * scale), (g, r)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_gather_probe_matches_eval(api, dt):
+    """The gather-ceiling probe evaluates at known intervals: with spline_eval's
+    idx it reproduces spline_eval's out bitwise through both access patterns."""
+    wl = workloads.generate(5, n=(1 << 17) + 5, m=50000)
+    x = parity.to_dev(wl.x.astype(dt))
+    y = parity.to_dev(wl.y.astype(dt))
+    q = parity.to_dev(wl.q.astype(dt))
+    q[0, :3] = float("nan")
+    y2 = api.build(x, y, 0)
+    out, idx = api.evaluate(x, y, y2, q, 0)
+    for mode in (0, 1):
+        o, i = api.gather_probe(x, y, y2, q, idx, mode)
+        assert torch.equal(i, idx)
+        assert torch.equal(o.view(torch.int8), out.view(torch.int8))
+    api.status()
