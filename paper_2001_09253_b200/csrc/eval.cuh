@@ -216,11 +216,6 @@ constexpr int kEvalThreads = 256;
 constexpr int kStageHeader = 32;  // two mbarriers + two counters, ahead of the staged arrays
 
 __host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
-__host__ __device__ constexpr int pow2_at_least(int v) {
-  int p = 1;
-  while (p < v) p <<= 1;
-  return p;
-}
 
 // Shared-memory layout of one CTA: two stages, each holding an item's raw x, y, y2 (cpb
 // curves) and -- when queries are staged too -- its up to qmax queries, all filled by TMA bulk
