@@ -377,7 +377,9 @@ def main():
         raise RuntimeError("data-error status raised on the benchmark inputs")
 
     K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    # the step: build then eval back to back (the eval launch may overlap the build's drain:
+    # programmatic dependent launch), CUDA events around the pair
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -386,15 +388,26 @@ def main():
             flush.zero_()  # evict L2 (126 MB) between steps, outside the timed events
             ev[k][0].record(stream)
             api.build(x, y, wl.bc, yp1, ypn, out=y2)
-            ev[k][1].record(stream)
             api.evaluate(x, y, y2, q, wl.flags, out=out, idx=idx)
-            ev[k][2].record(stream)
+            ev[k][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    build_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
-    eval_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
-    step_ms = statistics.mean(b + e for b, e in zip(build_ms, eval_ms))
+    step_ms = statistics.mean(ev[k][0].elapsed_time(ev[k][1]) for k in range(K))
+    # per-kernel breakdown (for the rooflines): each kernel timed alone, same flush protocol
+    bev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    for k in range(K):
+        flush.zero_()
+        bev[k][0].record(stream)
+        api.build(x, y, wl.bc, yp1, ypn, out=y2)
+        bev[k][1].record(stream)
+        flush.zero_()
+        bev[k][2].record(stream)
+        api.evaluate(x, y, y2, q, wl.flags, out=out, idx=idx)
+        bev[k][3].record(stream)
+    torch.cuda.synchronize()
+    build_ms = [bev[k][0].elapsed_time(bev[k][1]) for k in range(K)]
+    eval_ms = [bev[k][2].elapsed_time(bev[k][3]) for k in range(K)]
 
     # ---- the fused single-kernel path (spline_build_eval, SPLINE_PATH_FUSED), same protocol
     fused_ms = 0.0

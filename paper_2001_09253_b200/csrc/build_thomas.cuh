@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict
                                                              const T *__restrict__ ypn, T *__restrict__ y2, int S,
                                                              FastDiv divn) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  pdl_trigger();
   const int CPB = blockDim.x / 2;  // blockDim = 2 x curves per CTA (<= 256)
   T *X = reinterpret_cast<T *>(smem_raw);
   T *Y = X + (size_t)CPB * S;
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(const T *__restrict
                                                              const T *__restrict__ ypn, T *__restrict__ y2, int S,
                                                              int64_t ntiles, FastDiv divn) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  pdl_trigger();
   const int CPB = blockDim.x / 2;
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
   T *Xr = reinterpret_cast<T *>(smem_raw + 16);
@@ -350,6 +352,7 @@ template <typename T, int NMAX>
 __global__ void __launch_bounds__(256) k1_thomas_regs(const T *__restrict__ x, const T *__restrict__ y, int n,
                                                       int64_t batch, int bc, const T *__restrict__ yp1,
                                                       const T *__restrict__ ypn, T *__restrict__ y2, int vec) {
+  pdl_trigger();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= batch) return;
   T xv[NMAX], yv[NMAX];

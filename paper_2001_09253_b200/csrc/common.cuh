@@ -187,6 +187,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                : "memory");
 }
 
+// Programmatic dependent launch (PDL): a build kernel lets the next kernel of the stream be
+// scheduled before it finishes (pdl_trigger, at its start: the dependent's CTAs then launch as
+// the build's CTAs drain, all of which have started); an eval kernel waits for its predecessor
+// to complete -- with all memory visible -- before reading x, y, y2 (pdl_wait).  Both are
+// no-ops when the launch carries no programmatic dependency.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Plain arrival (release semantics) on an mbarrier.
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");

@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
     k_eval_staged(const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ y2, int n, int64_t batch,
                   const T *__restrict__ q, int m, T *__restrict__ out, int32_t *__restrict__ idx, int cpb,
                   int nchunks, int qchunk, int qmax, int64_t nitems, FastDiv divn, FastDiv divm) {
+  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
   constexpr bool PACKED = (MODE != MODE_BSEARCH);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const StageLayout<T> L(cpb, n, MODE, BULK ? qmax : 0);
@@ -463,6 +464,7 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
     k_eval_warps(const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ y2, int n, int64_t batch,
                  const T *__restrict__ q, int m, T *__restrict__ out, int32_t *__restrict__ idx, int cpb,
                  int64_t nitems, FastDiv divn, FastDiv divm) {
+  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
   constexpr int V = 16 / sizeof(T);
   constexpr int NW = kEvalThreads / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -575,6 +577,7 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x,
                                                        const T *__restrict__ y2, int n, const T *__restrict__ q,
                                                        int64_t m, T *__restrict__ out, int32_t *__restrict__ idx,
                                                        int64_t qrun, int64_t runs_per_curve, int64_t ntasks) {
+  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
   const int lane = threadIdx.x & 31;
   const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (task >= ntasks) return;  // whole warp; no block-level synchronisation below
@@ -701,6 +704,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_pack_records(const T *__restrict__ x, const T *__restrict__ y,
                                                       const T *__restrict__ y2, int n, int64_t batch,
                                                       Ival<T> *__restrict__ R, CurveHdr<T> *__restrict__ H) {
+  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
   constexpr int KP = 4;
   const int runs = (n + KP - 1) / KP;  // runs per curve
   const int64_t total = batch * runs;

@@ -46,6 +46,23 @@ template <typename K> int set_smem(K kernel, size_t bytes) {
 
 inline int launch_rc() { return cuda_rc(cudaGetLastError()); }
 
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
+// previous kernel of the stream is finishing; it must pdl_wait() before reading its inputs.
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_rc(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // Stream-ordered scratch (SPIKE tile records; y2 for an unfused spline_build_eval without y2)
 // from a library-owned pool per device that keeps its memory between calls (release
 // threshold = max), so repeated calls do not map and unmap device memory.
@@ -263,9 +280,8 @@ int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, sm) != cudaSuccess || occ < 1) occ = 1;
   const int64_t grid = std::min<int64_t>(nitems, (int64_t)occ * num_sms());
-  kern<<<(unsigned)grid, kEvalThreads, sm, st>>>(x, y, y2, n, batch, q, (int)m, out, idx, cpb, nchunks, qchunk,
-                                                 qmax, nitems, FastDiv((uint32_t)n), FastDiv((uint32_t)m));
-  return launch_rc();
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kEvalThreads), sm, st, x, y, y2, n, batch, q, (int)m, out, idx,
+                    cpb, nchunks, qchunk, qmax, nitems, FastDiv((uint32_t)n), FastDiv((uint32_t)m));
 }
 
 
@@ -291,9 +307,8 @@ int launch_warps_k(const T *x, const T *y, const T *y2, int n, int64_t batch, co
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, sm) != cudaSuccess || occ < 1) occ = 1;
     const int64_t grid = std::min<int64_t>(nitems, (int64_t)occ * num_sms());
-    kern<<<(unsigned)grid, kEvalThreads, sm, st>>>(x, y, y2, n, batch, q, (int)m, out, idx, cpb, nitems,
-                                                  FastDiv((uint32_t)n), FastDiv((uint32_t)m));
-    return launch_rc();
+    return launch_pdl(kern, dim3((unsigned)grid), dim3(kEvalThreads), sm, st, x, y, y2, n, batch, q, (int)m, out,
+                      idx, cpb, nitems, FastDiv((uint32_t)n), FastDiv((uint32_t)m));
   }
 }
 
@@ -352,8 +367,8 @@ int launch_sorted_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
   const int64_t rpc = (m + qrun - 1) / qrun;
   const int64_t ntasks = batch * rpc;
   const int64_t grid = (ntasks + 7) / 8;
-  k_eval_sorted<T, V, FORM><<<(unsigned)grid, 256, 0, st>>>(x, y, y2, n, q, m, out, idx, qrun, rpc, ntasks);
-  return launch_rc();
+  return launch_pdl(k_eval_sorted<T, V, FORM>, dim3((unsigned)grid), dim3(256), 0, st, x, y, y2, n, q, m, out, idx,
+                    qrun, rpc, ntasks);
 }
 
 template <typename T>
@@ -386,8 +401,7 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
     Ival<T> *R = reinterpret_cast<Ival<T> *>(ws);
     CurveHdr<T> *H = reinterpret_cast<CurveHdr<T> *>(reinterpret_cast<char *>(ws) + rec_bytes);
     const int64_t pg = std::min<int64_t>(((n + 3) / 4 * batch + 255) / 256, (int64_t)num_sms() * 16);
-    k_pack_records<T><<<(unsigned)pg, 256, 0, st>>>(x, y, y2, (int)n, batch, R, H);
-    int rc = launch_rc();
+    int rc = launch_pdl(k_pack_records<T>, dim3((unsigned)pg), dim3(256), 0, st, x, y, y2, (int)n, batch, R, H);
     if (!rc) {
       const int64_t grid = std::min<int64_t>((total + 1023) / 1024, (int64_t)num_sms() * 16);
       k_eval_records<T><<<(unsigned)grid, 256, 0, st>>>(R, H, (int)n, batch, q, m, out, idx);
