@@ -113,7 +113,8 @@ template <typename T, int R> __host__ __device__ constexpr size_t tile_smem_byte
   return sizeof(T) * (2 * (size_t)kTileThreads * (R + 1) + 6 * kTileThreads + 6 * kTileThreads);
 }
 
-// One CTA solves rows [P, Q] of curve blockIdx.y (P = row_begin + blockIdx.x * 256R).
+// One CTA solves rows [P, Q] of one curve: the linear block index is curve c times ntiles plus
+// tile t (a 1-D grid, so the batch is not capped at 65535), P = row_begin + t * 256R.
 //  FULL   : the tile is the whole curve (row_begin = 0, row_end = n <= 256R); writes y2.
 //  REDUCE : writes the tile's block record to tile_rec[(c*ntiles + t)*6].
 //  FINISH : reads the tile's outer (L, R) from tile_ext[(c*ntiles + t)*2]; writes y2 rows
@@ -123,7 +124,8 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
                                                       int64_t row_begin, int64_t row_end, int bc,
                                                       const T *__restrict__ yp1, const T *__restrict__ ypn,
                                                       T *__restrict__ y2, T *__restrict__ tile_rec,
-                                                      const T *__restrict__ tile_ext, int *__restrict__ badflag) {
+                                                      const T *__restrict__ tile_ext, int *__restrict__ badflag,
+                                                      int ntiles) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int NT = kTileThreads;
   constexpr int TR = NT * R;
@@ -133,9 +135,9 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
   T *mi = reinterpret_cast<T *>(rec + NT);
   T *ext = reinterpret_cast<T *>(rec);  // aliases rec: used only after tree_up
 
-  const int64_t c = blockIdx.y;
-  const int ntiles = gridDim.x;
-  const int64_t P = row_begin + (int64_t)blockIdx.x * TR;
+  const int64_t c = blockIdx.x / ntiles;
+  const int tile = (int)(blockIdx.x - c * ntiles);
+  const int64_t P = row_begin + (int64_t)tile * TR;
   const int nrows = (int)min64(TR, row_end - P);
   const int nleaf = (nrows + R - 1) / R;
   const T *xc = x + c * n;
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
   if (MODE == TILE_REDUCE) {
     if (threadIdx.x == 0) {
       const Rec<T> r = rec[0];
-      T *o = tile_rec + (c * ntiles + blockIdx.x) * 6;
+      T *o = tile_rec + (c * ntiles + tile) * 6;
       o[0] = r.Gp; o[1] = r.Vp; o[2] = r.Wp; o[3] = r.Gq; o[4] = r.Vq; o[5] = r.Wq;
       if (bad) { atomicOr(badflag + c, 1); raise_status(kBadKnots); }
     }
@@ -274,8 +276,8 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
   }
   T Lr = T(0), Rr = T(0);
   if (MODE == TILE_FINISH) {
-    Lr = tile_ext[(c * ntiles + blockIdx.x) * 2];
-    Rr = tile_ext[(c * ntiles + blockIdx.x) * 2 + 1];
+    Lr = tile_ext[(c * ntiles + tile) * 2];
+    Rr = tile_ext[(c * ntiles + tile) * 2 + 1];
   }
   tree_down(mi, ext, nleaf, Lr, Rr);
   if (l < nleaf) {

@@ -107,8 +107,7 @@ int launch_tile_full(const T *x, const T *y, int64_t n, int64_t batch, int bc, c
   auto kern = k_tile<T, R, TILE_FULL>;
   const size_t sm = tile_smem_bytes<T, R>();
   if (int rc = set_smem(kern, sm)) return rc;
-  kern<<<dim3(1, (unsigned)batch), kTileThreads, sm, st>>>(x, y, n, 0, n, bc, yp1, ypn, y2, nullptr, nullptr,
-                                                           nullptr);
+  kern<<<(unsigned)batch, kTileThreads, sm, st>>>(x, y, n, 0, n, bc, yp1, ypn, y2, nullptr, nullptr, nullptr, 1);
   return launch_rc();
 }
 
@@ -181,8 +180,9 @@ int launch_tile_part(const T *x, const T *y, int64_t n, int64_t rb, int64_t re, 
   auto kern = k_tile<T, R, MODE>;
   const size_t sm = tile_smem_bytes<T, R>();
   if (int rc = set_smem(kern, sm)) return rc;
-  kern<<<dim3((unsigned)ntiles, (unsigned)batch), kTileThreads, sm, st>>>(
-      x, y, n, rb, re, bc, yp1, ypn, y2, (T *)w.tile_rec, (const T *)w.tile_ext, (int *)w.badflag);
+  if (ntiles * batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
+  kern<<<(unsigned)(ntiles * batch), kTileThreads, sm, st>>>(x, y, n, rb, re, bc, yp1, ypn, y2, (T *)w.tile_rec,
+                                                             (const T *)w.tile_ext, (int *)w.badflag, (int)ntiles);
   return launch_rc();
 }
 

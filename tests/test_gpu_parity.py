@@ -251,3 +251,14 @@ def test_gather_probe_matches_eval(api, dt):
         assert torch.equal(i, idx)
         assert torch.equal(o.view(torch.int8), out.view(torch.int8))
     api.status()
+
+
+def test_tile_solve_batch_beyond_grid_y(api):
+    """K2 (one CTA per curve) with more than 65535 curves: the 1-D launch covers any batch."""
+    rng = np.random.default_rng(99)
+    B, n = 70000, 200
+    x = np.cumsum(rng.exponential(1.0, (B, n)) + 0.05, axis=1).astype(np.float32)
+    y = np.cumsum(rng.normal(size=(B, n)), axis=1).astype(np.float32)
+    spec = workloads.ConfigSpec(0, "t", B, n, 4, "f32", 0, 0, 0)
+    wl = workloads.Workload(spec, x, y, x[:, :4].copy(), None, None, 0, 0)
+    parity.check_case(api, wl, y2_only=True)
