@@ -262,3 +262,48 @@ def test_tile_solve_batch_beyond_grid_y(api):
     spec = workloads.ConfigSpec(0, "t", B, n, 4, "f32", 0, 0, 0)
     wl = workloads.Workload(spec, x, y, x[:, :4].copy(), None, None, 0, 0)
     parity.check_case(api, wl, y2_only=True)
+
+
+def _sorted_case(rng, dt, B, n, m, kind):
+    x = np.cumsum(rng.exponential(1.0, (B, n)) + 0.01, axis=1).astype(dt)
+    y = rng.normal(size=(B, n)).astype(dt)
+    y2 = rng.normal(size=(B, n)).astype(dt)
+    if kind == "clustered":  # 90% of the queries in 1% of the range; the sparse rest gives
+        lo, hi = x[:, :1], x[:, -1:]  # tiles whose window overflows shared memory
+        q = np.concatenate([rng.uniform(lo, hi, (B, m // 10)),
+                            rng.uniform(lo, lo + 0.01 * (hi - lo), (B, m - m // 10))], axis=1)
+    else:
+        q = rng.uniform(x[:, :1], x[:, -1:], (B, m))
+    q = q.astype(dt)
+    k = min(m // 8, n)
+    q[:, :k] = x[:, rng.integers(0, n, k)][0]  # exact knot hits
+    q[:, k], q[:, k + 1], q[:, k + 2], q[:, k + 3] = x[:, 0], x[:, -1], x[:, 0] - 1, x[:, -1] + 1
+    if kind == "nan":
+        q[:, k + 4] = np.nan
+    if kind != "unsorted":
+        q = np.sort(q, axis=1)  # NaN sorts to the end
+    return x, y, y2, q
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("B,n,m,kind", [(3, 4096, 65536, "dense"), (2, 129, 8 * 1024 + 8, "nan"),
+                                        (5, 3, 64, "dense"), (2, 2000, 40000, "clustered"), (3, 100, 3000, "dense"),
+                                        (2, 500, 8192, "unsorted"), (1, 257, 4100, "dense")])
+def test_sorted_edge_cases(api, dt, B, n, m, kind):
+    """SPLINE_Q_SORTED (k_eval_sorted): ties, both ends, out of range, NaN, ragged runs, dense
+    and clustered query densities and a wrong hint all match the oracle, idx bit-exact; out is
+    bitwise the unsorted path's (same make_cub / cub_eval arithmetic)."""
+    rng = np.random.default_rng(n * 7 + m)
+    x, y, y2, q = _sorted_case(rng, dt, B, n, m, kind)
+    out_ref, idx_ref, nbad = oracle.evaluate(x, y, y2, q)
+    t = parity.to_dev
+    api.status()
+    out, idx = api.evaluate(t(x), t(y), t(y2), t(q), 1)
+    bits = api.status()
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_ref)
+    e = parity.out_rel_err(out.cpu().numpy(), out_ref, y)
+    assert np.all(e <= parity.tol_for(dt))
+    assert (bits & api.STATUS_Q_OUT_OF_RANGE) == (api.STATUS_Q_OUT_OF_RANGE if nbad else 0)
+    out_u, idx_u = api.evaluate(t(x), t(y), t(y2), t(q), 0)
+    assert torch.equal(idx, idx_u)
+    assert torch.equal(torch.nan_to_num(out, 7.0).view(torch.int8), torch.nan_to_num(out_u, 7.0).view(torch.int8))
