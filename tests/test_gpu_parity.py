@@ -305,5 +305,6 @@ def test_sorted_edge_cases(api, dt, B, n, m, kind):
     assert np.all(e <= parity.tol_for(dt))
     assert (bits & api.STATUS_Q_OUT_OF_RANGE) == (api.STATUS_Q_OUT_OF_RANGE if nbad else 0)
     out_u, idx_u = api.evaluate(t(x), t(y), t(y2), t(q), 0)
+    assert (api.status() & api.STATUS_Q_OUT_OF_RANGE) == (api.STATUS_Q_OUT_OF_RANGE if nbad else 0)
     assert torch.equal(idx, idx_u)
     assert torch.equal(torch.nan_to_num(out, 7.0).view(torch.int8), torch.nan_to_num(out_u, 7.0).view(torch.int8))
