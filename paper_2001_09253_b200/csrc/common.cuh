@@ -218,13 +218,16 @@ __device__ __forceinline__ bool last_warp_arrival(int *counter, int nwarps) {
   return false;
 }
 
+// try_wait suspends the thread until the phase completes or this many ns pass, so waiting
+// warps do not spin through the issue slots of the working ones
+constexpr uint32_t kMbarSuspendNs = 1000000;
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
   uint32_t done;
   do {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
+        : "r"(smem_u32(bar)), "r"(phase), "r"(kMbarSuspendNs)
         : "memory");
   } while (!done);
 }
