@@ -518,7 +518,8 @@ def main():
         ekern = "k_eval_warps"
     else:
         ekern = "k_eval_staged"
-    bkern = ("k1_thomas_regs" if n <= 8 else "k1_thomas_pipe" if n <= 128 else
+    half = n == 16 or (s == 4 and n in (32, 64))  # K1h: half curves in registers
+    bkern = ("k1_thomas_regs" if n <= 8 else "k1_thomas_half" if half else "k1_thomas_pipe" if n <= 128 else
              "k_tile<FULL>" if not long_curve else "k_tile<REDUCE> + k4_top + k_tile<FINISH>")
     line = {
         "metric": METRIC,

@@ -55,6 +55,62 @@ __device__ __forceinline__ T babe_slope(int64_t c0, int nc, int bc, const T *__r
   return (bc & 2) ? ypn[cg] : T(0);
 }
 
+// The arithmetic of the two-ended sweep, shared by every kernel that runs it, with every
+// rounding explicit (no compiler-chosen contraction), so all of them agree bitwise: the end
+// row, one eliminated row, the meeting row and one back-substitution row.  dir = +1 (top) or
+// -1 (bottom); d = x_{j+dir} - x_j, h = dir d > 0.
+// End row: g = the divided difference; natural: c' = d' = 0; clamped (P:966-971 start,
+// P:1017-1018 end): c' = 1/2, d' = 3 dir (g - y') / h.
+template <typename T>
+__device__ __forceinline__ bool babe_first(T xo, T yo, T xn, T yn, int dir, bool clamped, T sl, T &hc, T &gc, T &cp,
+                                           T &dp) {
+  const T d = r_sub(xn, xo);
+  hc = (dir > 0) ? d : -d;
+  bool ok = finite(xo) & finite(yo) & finite(xn) & finite(yn) & (hc > T(0));
+  gc = r_mul(r_sub(yn, yo), nr_rcp(d));
+  cp = T(0);
+  dp = T(0);
+  if (clamped) {
+    ok &= finite(sl);
+    cp = T(0.5);
+    dp = r_mul(r_mul(T(3 * dir), r_sub(gc, sl)), nr_rcp(hc));
+  }
+  return ok;
+}
+// One row: den = 2(h_c + h) - h_c c'_prev, c' = h/den, d' = (6 dir (g - g_c) - h_c d'_prev)/den
+// (P:714-718 read from either end); returns the row's validity (finite, strictly increasing).
+template <typename T>
+__device__ __forceinline__ bool babe_row(T xo, T yo, T xn, T yn, int dir, T &hc, T &gc, T &cp, T &dp) {
+  const T d = r_sub(xn, xo);
+  const T h = (dir > 0) ? d : -d;
+  const bool ok = finite(xn) & finite(yn) & (h > T(0));
+  const T g = r_mul(r_sub(yn, yo), nr_rcp(d));
+  const T inv = nr_rcp(r_fma(-hc, cp, r_mul(T(2), r_add(hc, h))));
+  dp = r_mul(r_fma(-hc, dp, r_mul(T(6 * dir), r_sub(g, gc))), inv);
+  cp = r_mul(h, inv);
+  hc = h;
+  gc = g;
+  return ok;
+}
+// Meet at row k (lanes 2t, 2t+1 hold the top and bottom sweeps of one curve): a_k = h_{k-1},
+// b_k = 2(h_{k-1} + h_k), c_k = h_k, d_k = 6(dd_k - dd_{k-1}); both lanes return y2_k, and ok
+// becomes the pair's.  Every lane of the warp must call it.
+template <typename T> __device__ __forceinline__ T babe_meet(bool top, T hc, T gc, T cp, T dp, bool &ok) {
+  const T o_h = __shfl_xor_sync(0xffffffffu, hc, 1);
+  const T o_g = __shfl_xor_sync(0xffffffffu, gc, 1);
+  const T o_cp = __shfl_xor_sync(0xffffffffu, cp, 1);
+  const T o_dp = __shfl_xor_sync(0xffffffffu, dp, 1);
+  const int o_ok = __shfl_xor_sync(0xffffffffu, (int)ok, 1);
+  ok = ok & (o_ok != 0);
+  const T hk1 = top ? hc : o_h, gk1 = top ? gc : o_g, cT = top ? cp : o_cp, dT = top ? dp : o_dp;
+  const T hk = top ? o_h : hc, gk = top ? o_g : gc, aB = top ? o_cp : cp, dB = top ? o_dp : dp;
+  const T num = r_fma(-hk, dB, r_fma(-hk1, dT, r_mul(T(6), r_sub(gk, gk1))));
+  const T den = r_fma(-hk, aB, r_fma(-hk1, cT, r_mul(T(2), r_add(hk1, hk))));
+  return r_mul(num, nr_rcp(den));
+}
+// Back-substitution: y_j = d'_j - c'_j y_{j+dir}
+template <typename T> __device__ __forceinline__ T babe_back(T cb, T db, T yv) { return r_fma(-cb, yv, db); }
+
 template <typename T>
 __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int bc, T sl, T *dummy, int tid) {
   const int t = tid >> 1;  // curve within the tile (tid = thread index within the solving group)
@@ -73,16 +129,8 @@ __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int 
   // end row
   T xo = Xc[j0], yo = Yc[j0];
   T xn = Xc[j0 + dir], yn = Yc[j0 + dir];
-  bool ok = finite(xo) & finite(yo) & finite(xn) & finite(yn) & (T(dir) * (xn - xo) > T(0));
-  T hc = T(dir) * (xn - xo);
-  T gc = (yn - yo) * nr_rcp(xn - xo);
-  const bool clamped = top ? (bc & 1) : (bc & 2);
-  T cp = T(0), dp = T(0);
-  if (clamped) {  // P:966-971 (start) / P:1017-1018 (end): c' = 1/2, d' = 3 dir (g - y') / h
-    ok &= finite(sl);
-    cp = T(0.5);
-    dp = T(3 * dir) * (gc - sl) * nr_rcp(hc);
-  }
+  T hc, gc, cp, dp;
+  bool ok = babe_first(xo, yo, xn, yn, dir, top ? (bc & 1) : (bc & 2), sl, hc, gc, cp, dp);
   // the row after next is loaded one step ahead (register rotation), so the shared-memory
   // latency is off the dependency chain; near the meeting row the look-ahead may read a row
   // of the other thread's half, a value that is never used
@@ -98,32 +146,16 @@ __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int 
     const int jp = min(max(j + 2 * dir, 0), n - 1);
     xnn = Xc[jp];
     ynn = Yc[jp];
-    const T h = T(dir) * (xn - xo);
-    ok &= finite(xn) & finite(yn) & (h > T(0));
-    const T g = (yn - yo) * nr_rcp(xn - xo);
-    const T inv = nr_rcp(T(2) * (hc + h) - hc * cp);
-    dp = (T(6 * dir) * (g - gc) - hc * dp) * inv;
-    cp = h * inv;
+    ok &= babe_row(xo, yo, xn, yn, dir, hc, gc, cp, dp);
     Xc[j] = cp;
     Yc[j] = dp;
-    hc = h;
-    gc = g;
     j += dir;
   };
   const int common = n - 2 - k;  // bottom's interior rows; the top has one more when n is even
 #pragma unroll 2
   for (int i = 0; i < common; ++i) step();
   if (top && (k - 1 > common)) step();
-  // meet at row k: a_k = h_{k-1}, b_k = 2(h_{k-1} + h_k), c_k = h_k, d_k = 6(dd_k - dd_{k-1})
-  const T o_h = __shfl_xor_sync(0xffffffffu, hc, 1);
-  const T o_g = __shfl_xor_sync(0xffffffffu, gc, 1);
-  const T o_cp = __shfl_xor_sync(0xffffffffu, cp, 1);
-  const T o_dp = __shfl_xor_sync(0xffffffffu, dp, 1);
-  const int o_ok = __shfl_xor_sync(0xffffffffu, (int)ok, 1);  // unconditional: every lane joins
-  ok = ok & (o_ok != 0);
-  const T hk1 = top ? hc : o_h, gk1 = top ? gc : o_g, cT = top ? cp : o_cp, dT = top ? dp : o_dp;
-  const T hk = top ? o_h : hc, gk = top ? o_g : gc, aB = top ? o_cp : cp, dB = top ? o_dp : dp;
-  const T yk = (T(6) * (gk - gk1) - hk1 * dT - hk * dB) * nr_rcp(T(2) * (hk1 + hk) - hk1 * cT - hk * aB);
+  const T yk = babe_meet(top, hc, gc, cp, dp, ok);
   if (top) Yc[k] = yk;
   // back-substitution outward from the seam: y_j = d'_j - c'_j y_{j+dir}
   T yv = yk;
@@ -132,7 +164,7 @@ __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int 
   auto back = [&]() {
     const int jn = min(max(jj - dir, 0), n - 1);  // next row loaded ahead of this row's store
     const T cb2 = Xc[jn], db2 = Yc[jn];
-    yv = db - cb * yv;
+    yv = babe_back(cb, db, yv);
     Yc[jj] = yv;
     cb = cb2;
     db = db2;
@@ -403,6 +435,104 @@ __global__ void __launch_bounds__(256) k1_thomas_regs(const T *__restrict__ x, c
 #pragma unroll
     for (int j = 0; j < NMAX; ++j)
       if (j < n) zc[j] = z[j];
+  }
+}
+
+
+// K1h (k1_thomas_half, n = N in {16, 32, 64}, 16-byte-aligned curve rows): the two-ended sweep
+// with each thread's half curve in REGISTERS -- no shared-memory tile, no transposition, no
+// staging barrier.  Lane 2t (top) owns rows 0 .. K-1 of curve t, lane 2t+1 (bottom) rows
+// N-1 .. K (K = N/2); "step s" is row s for the top and row N-1-s for the bottom, so both run
+// one instruction stream.  Each thread loads / stores its half with 16-byte vectors (the bottom
+// reverses the element order).  The arithmetic is babe_first/babe_row/babe_meet/babe_back, so
+// y2 is bitwise the shared-memory K1's (and the fused kernel's).
+constexpr int kK1hThreads = 128;
+template <typename T, int N>
+__global__ void __launch_bounds__(kK1hThreads) k1_thomas_half(const T *__restrict__ x, const T *__restrict__ y,
+                                                              int64_t batch, int bc, const T *__restrict__ yp1,
+                                                              const T *__restrict__ ypn, T *__restrict__ y2) {
+  pdl_trigger();
+  constexpr int K = N / 2;
+  constexpr int VW = 16 / sizeof(T);
+  static_assert(K % VW == 0 && K >= 2 * VW, "each half is whole 16-byte vectors");
+  using VT = typename Vec16<T>::V;
+  const int64_t cv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 1;
+  const bool top = (threadIdx.x & 1) == 0;
+  const bool act = cv < batch;
+  const int64_t c = act ? cv : batch - 1;  // a ragged last warp shadows the last curve, stores nothing
+  const int dir = top ? 1 : -1;
+  const int hoff = top ? 0 : K;            // this thread's half of the row
+  const T sl = top ? ((bc & 1) ? yp1[c] : T(0)) : ((bc & 2) ? ypn[c] : T(0));
+  T xs[K], ys[K];
+  {
+    const T *xh = x + c * N + hoff, *yh = y + c * N + hoff;
+#pragma unroll
+    for (int g = 0; g < K; g += VW) {
+      const int o = top ? g : K - g - VW;
+      const VT a = __ldg(reinterpret_cast<const VT *>(xh + o));
+      const VT b = __ldg(reinterpret_cast<const VT *>(yh + o));
+      const T *pa = reinterpret_cast<const T *>(&a), *pb = reinterpret_cast<const T *>(&b);
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        xs[g + e] = top ? pa[e] : pa[VW - 1 - e];
+        ys[g + e] = top ? pb[e] : pb[VW - 1 - e];
+      }
+    }
+  }
+  // row K (the top's last neighbour) is the bottom thread's last step
+  const T xK = __shfl_xor_sync(0xffffffffu, xs[K - 1], 1), yK = __shfl_xor_sync(0xffffffffu, ys[K - 1], 1);
+  T hc, gc, cp, dp;
+  T cpr[K], dpr[K];
+  bool ok = babe_first(xs[0], ys[0], xs[1], ys[1], dir, top ? (bc & 1) : (bc & 2), sl, hc, gc, cp, dp);
+  cpr[0] = cp;
+  dpr[0] = dp;
+#pragma unroll
+  for (int s = 1; s < K - 1; ++s) {  // rows both threads eliminate
+    ok &= babe_row(xs[s], ys[s], xs[s + 1], ys[s + 1], dir, hc, gc, cp, dp);
+    cpr[s] = cp;
+    dpr[s] = dp;
+  }
+  {  // the top's extra row K-1 (the bottom's step K-1 is the meeting row itself)
+    T h2 = hc, g2 = gc, c2 = cp, d2 = dp;
+    const bool ok2 = babe_row(xs[K - 1], ys[K - 1], xK, yK, dir, h2, g2, c2, d2);
+    if (top) {
+      ok &= ok2;
+      hc = h2;
+      gc = g2;
+      cp = c2;
+      dp = d2;
+    }
+    cpr[K - 1] = c2;
+    dpr[K - 1] = d2;
+  }
+  const T yk = babe_meet(top, hc, gc, cp, dp, ok);
+  // back-substitution outward from the seam; yo[s] = y2 of step s's row (dpr reused)
+  T yv = yk;
+  {
+    const T yt = babe_back(cpr[K - 1], dpr[K - 1], yv);
+    yv = top ? yt : yk;
+    dpr[K - 1] = yv;  // top: row K-1; bottom: row K = the seam
+  }
+#pragma unroll
+  for (int s = K - 2; s >= 0; --s) {
+    yv = babe_back(cpr[s], dpr[s], yv);
+    dpr[s] = yv;
+  }
+  if (!ok) {  // both threads of the pair see the same ok
+#pragma unroll
+    for (int s = 0; s < K; ++s) dpr[s] = qnan<T>();
+  }
+  raise_status_warp(act && !ok && top, kBadKnots);
+  if (act) {
+    T *zh = y2 + c * N + hoff;
+#pragma unroll
+    for (int g = 0; g < K; g += VW) {
+      VT a;
+      T *pa = reinterpret_cast<T *>(&a);
+#pragma unroll
+      for (int e = 0; e < VW; ++e) pa[e] = top ? dpr[g + e] : dpr[g + VW - 1 - e];
+      *reinterpret_cast<VT *>(zh + (top ? g : K - g - VW)) = a;
+    }
   }
 }
 

@@ -221,6 +221,22 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
     return launch_rc();
   }
   if (n <= kK1MaxN) {  // K1: two threads per curve, staged odd-stride tiles
+    // K1h: the same sweep with each half curve in registers (16-byte-aligned rows)
+    // (fp32 n = 16, 32, 64; fp64 n = 16: 2n values per thread stay within ~90 registers)
+    if (aligned16(x) && aligned16(y) && aligned16(y2)) {
+      const unsigned grid = (unsigned)((2 * batch + kK1hThreads - 1) / kK1hThreads);
+      if constexpr (sizeof(T) == 4) {
+        if (n == 64 || n == 32) {
+          if (n == 64) k1_thomas_half<T, 64><<<grid, kK1hThreads, 0, st>>>(x, y, batch, bc, yp1, ypn, y2);
+          else k1_thomas_half<T, 32><<<grid, kK1hThreads, 0, st>>>(x, y, batch, bc, yp1, ypn, y2);
+          return launch_rc();
+        }
+      }
+      if (n == 16) {
+        k1_thomas_half<T, 16><<<grid, kK1hThreads, 0, st>>>(x, y, batch, bc, yp1, ypn, y2);
+        return launch_rc();
+      }
+    }
     const int S = babe_stride((int)n);
     if ((n * sizeof(T)) % 16 == 0 && aligned16(x) && aligned16(y)) {
       // persistent + TMA-pipelined; CPB curves per tile (2 threads each)
