@@ -56,7 +56,14 @@ __device__ __forceinline__ float r_mul(float a, float b) { return __fmul_rn(a, b
 __device__ __forceinline__ double r_mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float r_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double r_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
-__device__ __forceinline__ float r_rcp(float a) { return __frcp_rn(a); }   // correctly rounded 1/a
+// The interval records' 1/h (make_cub): fp32 rcp.approx (subnormal-preserving) + one Newton
+// step, within ~1 ulp of 1/h -- the correctly rounded __frcp_rn costs a multi-instruction path
+// per knot on the eval pack
+__device__ __forceinline__ float r_rcp(float a) {
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return __fmaf_rn(r, __fmaf_rn(-a, r, 1.0f), r);
+}
 __device__ __forceinline__ double r_rcp(double a);  // fp64: rcp.approx + 2 Newton steps (below)
 
 // Reciprocal for the solver sweeps: hardware approximation refined by Newton-Raphson
@@ -90,8 +97,9 @@ __device__ __forceinline__ double r_rcp(double a) { return nr_rcp(a); }
 // terms (B, 1-B in [0, 1]), so it is as well conditioned as Eq. nr_formula (an expansion in
 // powers of (q - x0) is not: its terms cancel catastrophically near x1 when y2 is large).
 // An interval carries Cub {1/h, y0, dy, e1} (16 B fp32: one shared-memory vector load) and e2;
-// x0 comes from the search.  1/h is the correctly rounded reciprocal (the paper's inv_ba,
-// P:386).  Every operation is explicitly rounded, so every kernel and hint gives the same bits.
+// x0 comes from the search.  1/h (the paper's inv_ba) is a Newton-refined reciprocal
+// within ~1 ulp (r_rcp).  Every operation is explicitly rounded, so every kernel and hint gives
+// the same bits.
 template <typename T> struct Cub { T ih, y0, dy, e1; };
 
 template <typename T>
