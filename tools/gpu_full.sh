@@ -1,5 +1,6 @@
 # usage: bash tools/gpu_full.sh -- round evidence: smoke, all GPU tests, bench (default + every config),
 # reference arm, ncu launch list of the default bench, ncu --set full of cfg2's build/eval/fused kernels
+# and of cfg3's / cfg4's build and eval kernels
 mkdir -p gpurun_out
 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 1200 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
@@ -13,3 +14,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 python tools/prof.py 2 3 > gpurun_out/pp_2.log 2>&1 && python tools/prof_fused.py 2 3 > gpurun_out/ppf_2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k "regex:k1_|k_eval" -s 2 -c 2 -o gpurun_out/prof_cfg2 -f python tools/prof.py 2 3 > gpurun_out/ncu_cfg2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k "regex:k_fused" -s 1 -c 1 -o gpurun_out/prof_fused_cfg2 -f python tools/prof_fused.py 2 3 > gpurun_out/ncu_fused_cfg2.log 2>&1; echo "ncu full rc=$?"
+for c in 3 4; do python tools/prof.py $c 3 > gpurun_out/pp_$c.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k "regex:k1_|k_tile|k_eval" -s 2 -c 2 -o gpurun_out/prof_cfg$c -f python tools/prof.py $c 3 > gpurun_out/ncu_cfg$c.log 2>&1; echo "ncu cfg$c rc=$?"; done

@@ -55,6 +55,7 @@ tp = os.path.join(ROOT, "profiles", "traffic.json")
 if os.path.exists(tp):
     traffic = json.load(open(tp))
 for rep, tag in [("prof_cfg2.ncu-rep", "ncu_full_cfg2"), ("prof_fused_cfg2.ncu-rep", "ncu_full_fused_cfg2"),
+                 ("prof_cfg3.ncu-rep", "ncu_full_cfg3"), ("prof_cfg4.ncu-rep", "ncu_full_cfg4"),
                  ("prof_cfg5r.ncu-rep", "ncu_full_cfg5_eval"), ("prof_cfg5.ncu-rep", "ncu_full_cfg5_build")]:
     p = os.path.join(src, rep)
     if not os.path.exists(p):
@@ -74,8 +75,8 @@ for rep, tag in [("prof_cfg2.ncu-rep", "ncu_full_cfg2"), ("prof_fused_cfg2.ncu-r
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         b = float(rd[0].replace(",", "")) * scale[rd[1]] + float(wr[0].replace(",", "")) * scale[wr[1]]
         k = d["kernel"]
-        if tag == "ncu_full_cfg2":
-            traffic.setdefault("cfg2", {})["build" if "k1_" in k else "eval"] = b
+        if tag in ("ncu_full_cfg2", "ncu_full_cfg3", "ncu_full_cfg4"):
+            traffic.setdefault(tag[-4:], {})["build" if ("k1_" in k or "k_tile" in k) else "eval"] = b
         elif tag == "ncu_full_fused_cfg2":
             traffic.setdefault("cfg2", {})["fused"] = b
         elif tag == "ncu_full_cfg5_eval" and "k_eval_records" in k:
