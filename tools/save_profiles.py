@@ -12,8 +12,11 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 import ncu_summary  # noqa: E402
 
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
+# optional second argument: an export root used instead of profiles/ (on the GPU box, so the
+# summaries travel back inside gpurun_out/ without the large .ncu-rep files)
+proot = os.path.abspath(sys.argv[2]) if len(sys.argv) > 2 else os.path.join(ROOT, "profiles")
 src = os.path.join(ROOT, "gpurun_out")
-dst = os.path.join(ROOT, "profiles", rnd)
+dst = os.path.join(proot, rnd)
 os.makedirs(dst, exist_ok=True)
 
 
@@ -51,9 +54,11 @@ if os.path.exists(lp):
             f.write(f"{100 * v / tot:6.2f}%  {v / 1e3:10.1f} us  {k}\n")
 
 traffic = {}
-tp = os.path.join(ROOT, "profiles", "traffic.json")
-if os.path.exists(tp):
-    traffic = json.load(open(tp))
+tp = os.path.join(proot, "traffic.json")
+for cand in (tp, os.path.join(ROOT, "profiles", "traffic.json")):
+    if os.path.exists(cand):
+        traffic = json.load(open(cand))
+        break
 for rep, tag in [("prof_cfg2.ncu-rep", "ncu_full_cfg2"), ("prof_fused_cfg2.ncu-rep", "ncu_full_fused_cfg2"),
                  ("prof_cfg3.ncu-rep", "ncu_full_cfg3"), ("prof_cfg4.ncu-rep", "ncu_full_cfg4"),
                  ("prof_cfg5r.ncu-rep", "ncu_full_cfg5_eval"), ("prof_cfg5.ncu-rep", "ncu_full_cfg5_build")]:
