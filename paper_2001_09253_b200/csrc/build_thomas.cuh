@@ -323,12 +323,13 @@ __device__ __forceinline__ bool thomas_regs(const T (&xv)[NMAX], const T (&yv)[N
                                             T (&z)[NMAX]) {
   bool ok = true;
   T cpv[NMAX], dpv[NMAX];
-  T hprev = xv[1] - xv[0];
-  T ddprev = (yv[1] - yv[0]) / hprev;
+  // (explicitly rounded, reciprocal + Newton then multiply, like the other solvers)
+  T hprev = r_sub(xv[1], xv[0]);
+  T ddprev = r_mul(r_sub(yv[1], yv[0]), nr_rcp(hprev));
   if (bc & 1) {
     ok = ok && finite(s1);
     cpv[0] = T(0.5);
-    dpv[0] = T(3) * (ddprev - s1) / hprev;
+    dpv[0] = r_mul(r_mul(T(3), r_sub(ddprev, s1)), nr_rcp(hprev));
   } else {
     cpv[0] = T(0);
     dpv[0] = T(0);
@@ -344,11 +345,11 @@ __device__ __forceinline__ bool thomas_regs(const T (&xv)[NMAX], const T (&yv)[N
 #pragma unroll
   for (int j = 1; j < NMAX - 1; ++j) {
     if (j < n - 1) {
-      const T h = xv[j + 1] - xv[j];
-      const T dd = (yv[j + 1] - yv[j]) / h;
-      const T inv = T(1) / (T(2) * (hprev + h) - hprev * cpv[j - 1]);
-      dpv[j] = (T(6) * (dd - ddprev) - hprev * dpv[j - 1]) * inv;
-      cpv[j] = h * inv;
+      const T h = r_sub(xv[j + 1], xv[j]);
+      const T dd = r_mul(r_sub(yv[j + 1], yv[j]), nr_rcp(h));
+      const T inv = nr_rcp(r_fma(-hprev, cpv[j - 1], r_mul(T(2), r_add(hprev, h))));
+      dpv[j] = r_mul(r_fma(-hprev, dpv[j - 1], r_mul(T(6), r_sub(dd, ddprev))), inv);
+      cpv[j] = r_mul(h, inv);
       cpp = cpv[j];
       dpp = dpv[j];
       hprev = h;
@@ -358,7 +359,7 @@ __device__ __forceinline__ bool thomas_regs(const T (&xv)[NMAX], const T (&yv)[N
   T last = T(0);
   if (bc & 2) {
     ok = ok && finite(sn);
-    last = (T(6) * (sn - ddprev) - hprev * dpp) / (T(2) * hprev - hprev * cpp);
+    last = r_mul(r_fma(-hprev, dpp, r_mul(T(6), r_sub(sn, ddprev))), nr_rcp(r_fma(-hprev, cpp, r_mul(T(2), hprev))));
   }
   T nxt = last;
 #pragma unroll
@@ -366,7 +367,7 @@ __device__ __forceinline__ bool thomas_regs(const T (&xv)[NMAX], const T (&yv)[N
     if (j == n - 1) {
       z[j] = last;
     } else if (j < n - 1) {
-      nxt = dpv[j] - cpv[j] * nxt;
+      nxt = r_fma(-cpv[j], nxt, dpv[j]);
       z[j] = nxt;
     } else {
       z[j] = T(0);
