@@ -564,14 +564,26 @@ template <typename T> __device__ __forceinline__ int warp_locate(const T *X, int
 
 // SPLINE_Q_SORTED: one warp per run of `qrun` consecutive queries of one curve.  Lane l
 // takes groups of V consecutive queries, 32V per warp step; every lane starts from the
-// warp's carried bracket jc (the largest interval found in the previous step) and scans
-// forward -- with sorted queries that is a few comparisons, generalising the paper's
-// "while x[i+1] < q: i += 1" sweep to 32 lanes.  A query below the carry (a
-// wrong hint) falls back to bisection; a long scan switches to galloping.  Knots are read
-// with read-only loads through L1: a warp's 32V queries touch a handful of knots, so almost
-// every gather is an L1 hit and each knot leaves HBM about once.
+// warp's carried bracket jc (the largest interval found in the previous step) and moves
+// forward -- generalising the paper's "while x[i+1] < q: i += 1" sweep to 32
+// lanes.  FORM_RECORD (spline_eval): the warp keeps a window of kSortWin interval records
+// in shared memory, built cooperatively (one make_cub per lane) at the carry and rebuilt when
+// the carry passes its middle; a query in the window is located by a short verified lift
+// from the carry (first query of the lane) or from the lane's previous query, so a step costs
+// a few shared-memory loads per query and no per-query record build.  Queries outside the
+// window, and the ablation FORMs, take the general path: a scan from the carry through L1
+// (bisection below the carry -- a wrong hint --, galloping for long jumps).
 // FORM (common.cuh interp_form) selects the evaluation variant: FORM_RECORD for spline_eval,
 // the others for spline_eval_ablation (the paper's division variants and no-op loop).
+// A warp's window of kSortWin interval records (FORM_RECORD): built cooperatively, one
+// interval per lane, at the carried bracket and reused while the carry stays in its first half.
+constexpr int kSortWin = 32;
+template <typename T> struct SortWin {
+  Cub<T> c[kSortWin];
+  T e2[kSortWin];
+  T x[kSortWin + 1];  // x[i] = x_{wb+i} (+inf past x_{n-2}); x[kSortWin] = x_{wb+kSortWin} or +inf
+};
+
 template <typename T, int V, int FORM = FORM_RECORD>
 __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x, const T *__restrict__ y,
                                                        const T *__restrict__ y2, int n, const T *__restrict__ q,
@@ -595,6 +607,9 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x,
   qf = (qf >= x0 && qf <= xn) ? qf : x0;
   int jc = warp_locate(X, n, qf, lane);
   bool oor = false;
+  __shared__ SortWin<T> wins[8];  // one per warp of the 256-thread CTA
+  SortWin<T> &sw = wins[threadIdx.x >> 5];
+  int wb = -(1 << 30);            // window base: none yet
 
   T qa[V], qn[V];
   int64_t kb = k0 + (int64_t)lane * V;
@@ -603,17 +618,71 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x,
     const int64_t k = base + (int64_t)lane * V;
     const int64_t kn = k + 32 * V;
     if (kn < k1) VecIO<T, V>::load(qb + kn, qn);  // next step in flight
-    if (lane < 3) prefetch_l1((lane == 0 ? X : lane == 1 ? Y : Z) + min(jc + 32, n - 1));
+    if constexpr (FORM != FORM_RECORD) {
+      if (lane < 3) prefetch_l1((lane == 0 ? X : lane == 1 ? Y : Z) + min(jc + 32, n - 1));
+    } else {
+      if (jc < wb || jc - wb > kSortWin / 2) {  // warp-uniform: rebuild the window at the carry
+        __syncwarp();
+        wb = jc;
+        const int jw = wb + lane;
+        if (jw <= n - 2) {
+          const T xa = __ldg(X + jw), xb = __ldg(X + jw + 1);
+          T e2;
+          sw.c[lane] = make_cub<T>(xa, xb, __ldg(Y + jw), __ldg(Y + jw + 1), __ldg(Z + jw), __ldg(Z + jw + 1), e2);
+          sw.e2[lane] = e2;
+          sw.x[lane] = xa;
+          if (lane == kSortWin - 1) sw.x[kSortWin] = xb;
+        } else {
+          sw.x[lane] = inf_of<T>();
+          if (lane == kSortWin - 1) sw.x[kSortWin] = inf_of<T>();
+        }
+        __syncwarp();
+      }
+    }
     int jl = -1;
     if (k < k1) {
       T val[V];
       int jj[V];
       int j = jc;
+      int lp = 0;  // this lane's previous window slot (FORM_RECORD)
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         const T qq = qa[i];
         const bool in = (qq >= x0) && (qq <= xn);
         const T qc = in ? qq : x0;
+        if constexpr (FORM == FORM_RECORD) {
+          // in the window at or after the carry: branch-free lifting over the window's knots
+          // (largest l < kSortWin with x_{wb+l} <= q; +inf past x_{n-2} keeps it <= n-2-wb)
+          const int l0 = jc - wb;
+          if (qc >= sw.x[l0] && qc < sw.x[kSortWin]) {
+            // a short lift from the carry (first query) or from this lane's previous query
+            // (sorted: at most a knot or two further), verified; a miss lifts the whole window
+            const int st = (i > 0 && qc >= sw.x[lp]) ? lp : l0;
+            int l = st;
+#pragma unroll
+            for (int d = (i == 0) ? 4 : 1; d >= 1; d >>= 1) {
+              const int p = min(l + d, kSortWin - 1);
+              l = (sw.x[p] <= qc) ? p : l;
+            }
+            if (sw.x[l + 1] <= qc && l < kSortWin - 1) {  // rare: a longer jump
+              l = l0;
+#pragma unroll
+              for (int d = kSortWin / 2; d >= 1; d >>= 1) {
+                const int p = min(l + d, kSortWin - 1);
+                l = (sw.x[p] <= qc) ? p : l;
+              }
+            }
+            lp = l;
+            const T v = cub_eval<T>(sw.c[l], sw.e2[l], sw.x[l], qc);
+            j = wb + l;
+            val[i] = in ? v : qnan<T>();
+            jj[i] = in ? j : -1;
+            oor |= !in;
+            if (in) jl = j;
+            continue;
+          }
+          j = jc;  // outside the window: the general path below
+        }
         if (__ldg(X + j) > qc) {
           j = bisect(X, n, qc);  // below the carry: unsorted input despite the hint
         } else {
