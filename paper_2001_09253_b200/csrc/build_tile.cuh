@@ -53,31 +53,36 @@ __device__ __forceinline__ void split_seam(T AGq, T AVq, T AWq, T BGp, T BVp, T 
   ym1 = beta - BVp * ym;
 }
 
-// Block-level merge tree over nleaf records held in shared memory.  Level s (1, 2, 4..)
-// merges rec[i] and rec[i+s] for i a multiple of 2s into rec[i]; the six seam values of
-// every merge are saved in mi[] for the top-down pass.  Ends with __syncthreads().
+// Block-level merge tree over nleaf <= blockDim.x records held in shared memory.  Level s
+// (1, 2, 4..) merges rec[i] and rec[i+s] for i a multiple of 2s into rec[i], done by thread i;
+// the six seam values of every merge are saved in mi[] for the top-down pass.  The levels
+// with 2s <= 32 stay inside one warp (both children and the next level's reader are lanes of
+// the same warp), so they need only __syncwarp; a CTA barrier separates the wider levels.
+// Ends with __syncthreads().
 template <typename T> __device__ void tree_up(Rec<T> *rec, T *mi, int nleaf) {
+  const int t = threadIdx.x;
   int off = 0;
   for (int lg = 0; (1 << lg) < nleaf; ++lg) {  // s = 2^lg (shifts: the level sizes are powers of 2)
     const int s = 1 << lg;
     const int nn = (nleaf + 2 * s - 1) >> (lg + 1);
-    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
-      const int i = k << (lg + 1), j = i + s;
-      if (j < nleaf) {
-        const Rec<T> A = rec[i], B = rec[j];
-        T *o = mi + 6 * (off + k);
-        o[0] = A.Gq; o[1] = A.Vq; o[2] = A.Wq; o[3] = B.Gp; o[4] = B.Vp; o[5] = B.Wp;
-        rec[i] = merge_rec(A, B);
-      }
+    if ((t & (2 * s - 1)) == 0 && t + s < nleaf) {
+      const Rec<T> A = rec[t], B = rec[t + s];
+      T *o = mi + 6 * (off + (t >> (lg + 1)));
+      o[0] = A.Gq; o[1] = A.Vq; o[2] = A.Wq; o[3] = B.Gp; o[4] = B.Vp; o[5] = B.Wp;
+      rec[t] = merge_rec(A, B);
     }
     off += nn;
-    __syncthreads();
+    if (4 * s <= 32) __syncwarp();  // the next level (children 2s apart) is warp-local too
+    else __syncthreads();
   }
+  __syncthreads();
 }
 
-// Top-down: ext[i] = (L, R) of leaf i, given the root's (L, R).  Ends with __syncthreads().
+// Top-down: ext[i] = (L, R) of leaf i, given the root's (L, R); thread i splits the merges it
+// made on the way up.  Ends with __syncthreads().
 template <typename T> __device__ void tree_down(const T *mi, T *ext, int nleaf, T L, T R) {
-  if (threadIdx.x == 0) { ext[0] = L; ext[1] = R; }
+  const int t = threadIdx.x;
+  if (t == 0) { ext[0] = L; ext[1] = R; }
   int lgmax = 0, total = 0;
   for (int lg = 0; (1 << lg) < nleaf; ++lg) {
     lgmax = lg;
@@ -90,20 +95,20 @@ template <typename T> __device__ void tree_down(const T *mi, T *ext, int nleaf, 
     const int s = 1 << lg;
     const int nn = (nleaf + 2 * s - 1) >> (lg + 1);
     off -= nn;
-    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
-      const int i = k << (lg + 1), j = i + s;
-      if (j < nleaf) {
-        const T *o = mi + 6 * (off + k);
-        const T Li = ext[2 * i], Ri = ext[2 * i + 1];
-        T ym, ym1;
-        split_seam(o[0], o[1], o[2], o[3], o[4], o[5], Li, Ri, ym, ym1);
-        ext[2 * i + 1] = ym1;
-        ext[2 * j] = ym;
-        ext[2 * j + 1] = Ri;
-      }
+    if ((t & (2 * s - 1)) == 0 && t + s < nleaf) {
+      const int j = t + s;
+      const T *o = mi + 6 * (off + (t >> (lg + 1)));
+      const T Li = ext[2 * t], Ri = ext[2 * t + 1];
+      T ym, ym1;
+      split_seam(o[0], o[1], o[2], o[3], o[4], o[5], Li, Ri, ym, ym1);
+      ext[2 * t + 1] = ym1;
+      ext[2 * j] = ym;
+      ext[2 * j + 1] = Ri;
     }
-    __syncthreads();
+    if (2 * s <= 32) __syncwarp();  // the next level's readers were written by their own warp
+    else __syncthreads();
   }
+  __syncthreads();
 }
 
 enum { TILE_FULL = 0, TILE_REDUCE = 1, TILE_FINISH = 2 };
