@@ -16,6 +16,11 @@ ncu --set full --clock-control none --import-source on -k "regex:k1_|k_eval" -s 
 ncu --set full --clock-control none --import-source on -k "regex:k_fused" -s 1 -c 1 -o gpurun_out/prof_fused_cfg2 -f python tools/prof_fused.py 2 3 > gpurun_out/ncu_fused_cfg2.log 2>&1; echo "ncu full rc=$?"
 for c in 3 4; do python tools/prof.py $c 3 > gpurun_out/pp_$c.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k "regex:k1_|k_tile|k_eval" -s 2 -c 2 -o gpurun_out/prof_cfg$c -f python tools/prof.py $c 3 > gpurun_out/ncu_cfg$c.log 2>&1; echo "ncu cfg$c rc=$?"; done
+# the paper's quality checks and the control-point / division sweep
+mkdir -p gpurun_out/export/r01
+timeout 600 python tools/precision_report.py gpurun_out/export/r01/precision_report.json > gpurun_out/precision.log 2>&1; echo "precision rc=$?"
+timeout 900 python bench.py --ablation > gpurun_out/ablation.log 2>&1; echo "ablation rc=$?"
+grep '^{' gpurun_out/ablation.log > gpurun_out/export/r01/ablation_sweep.jsonl
 # summaries + bench lines into gpurun_out/export (copied back); keep only cfg2's full report
 python tools/save_profiles.py r01 gpurun_out/export > gpurun_out/export.log 2>&1; echo "export rc=$?"
 rm -f gpurun_out/prof_fused_cfg2.ncu-rep gpurun_out/prof_cfg3.ncu-rep gpurun_out/prof_cfg4.ncu-rep
