@@ -57,7 +57,7 @@ def test_cfg5_spike_f64(api, kw):
 # ------------------------------------------------------------ every kernel x dtype
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
-@pytest.mark.parametrize("n", [3, 5, 64, 128, 129, 700, 4096, 4097, 9000, 70000])
+@pytest.mark.parametrize("n", [3, 5, 16, 32, 64, 128, 129, 700, 4096, 4097, 9000, 70000])
 @pytest.mark.parametrize("bc", [0, 1, 2, 3])
 def test_build_all_paths(api, dt, n, bc):
     rng = np.random.default_rng(n * 10 + bc)
@@ -118,11 +118,12 @@ def test_wrong_hints_do_not_change_results(api):
         assert torch.allclose(o, base[0], rtol=0, atol=0, equal_nan=True)
 
 
-@pytest.mark.parametrize("n", [6, 64, 1000, 20000])
-def test_bad_knots_status_and_nan(api, n):
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("n", [6, 16, 32, 64, 1000, 20000])
+def test_bad_knots_status_and_nan(api, n, dt):
     rng = np.random.default_rng(n)
-    x = np.cumsum(rng.uniform(0.5, 1.5, (4, n)), axis=1)
-    y = rng.normal(size=(4, n))
+    x = np.cumsum(rng.uniform(0.5, 1.5, (4, n)), axis=1).astype(dt)
+    y = rng.normal(size=(4, n)).astype(dt)
     x[1, n // 2] = x[1, n // 2 - 1]  # duplicate knot
     y[2, 1] = np.inf
     api.status()
@@ -131,7 +132,7 @@ def test_bad_knots_status_and_nan(api, n):
     assert bits & api.STATUS_BAD_KNOTS
     assert np.all(np.isnan(y2[1])) and np.all(np.isnan(y2[2]))
     ref, _ = oracle.build_y2(x[[0, 3]], y[[0, 3]], 0)
-    assert np.all(parity.y2_rel_err(y2[[0, 3]], ref) <= 1e-12)
+    assert np.all(parity.y2_rel_err(y2[[0, 3]], ref) <= parity.tol_for(dt))
 
 
 def test_idx_optional_and_empty(api):
