@@ -572,23 +572,27 @@ template <typename T> __device__ __forceinline__ int warp_locate(const T *X, int
 // from the carry (first query of the lane) or from the lane's previous query, so a step costs
 // a few shared-memory loads per query and no per-query record build.  Queries outside the
 // window, and the ablation FORMs, take the general path: a scan from the carry through L1
-// (bisection below the carry -- a wrong hint --, galloping for long jumps).
+// (bisection below the carry -- a wrong hint --, galloping for long jumps).  The host takes
+// the window (WIN) only for dense queries (at least kSortWinDensity per interval): for sparse
+// ones a rebuild would serve too few queries.
 // FORM (common.cuh interp_form) selects the evaluation variant: FORM_RECORD for spline_eval,
 // the others for spline_eval_ablation (the paper's division variants and no-op loop).
 // A warp's window of kSortWin interval records (FORM_RECORD): built cooperatively, one
 // interval per lane, at the carried bracket and reused while the carry stays in its first half.
 constexpr int kSortWin = 32;
+constexpr int kSortWinDensity = 8;  // queries per interval from which the window pays
 template <typename T> struct SortWin {
   Cub<T> c[kSortWin];
   T e2[kSortWin];
   T x[kSortWin + 1];  // x[i] = x_{wb+i} (+inf past x_{n-2}); x[kSortWin] = x_{wb+kSortWin} or +inf
 };
 
-template <typename T, int V, int FORM = FORM_RECORD>
+template <typename T, int V, int FORM = FORM_RECORD, bool WIN = false>
 __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x, const T *__restrict__ y,
                                                        const T *__restrict__ y2, int n, const T *__restrict__ q,
                                                        int64_t m, T *__restrict__ out, int32_t *__restrict__ idx,
                                                        int64_t qrun, int64_t runs_per_curve, int64_t ntasks) {
+  static_assert(!WIN || FORM == FORM_RECORD, "the record window serves the product form");
   pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
   const int lane = threadIdx.x & 31;
   const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -618,7 +622,7 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x,
     const int64_t k = base + (int64_t)lane * V;
     const int64_t kn = k + 32 * V;
     if (kn < k1) VecIO<T, V>::load(qb + kn, qn);  // next step in flight
-    if constexpr (FORM != FORM_RECORD) {
+    if constexpr (!WIN) {
       if (lane < 3) prefetch_l1((lane == 0 ? X : lane == 1 ? Y : Z) + min(jc + 32, n - 1));
     } else {
       if (jc < wb || jc - wb > kSortWin / 2) {  // warp-uniform: rebuild the window at the carry
@@ -650,7 +654,7 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x,
         const T qq = qa[i];
         const bool in = (qq >= x0) && (qq <= xn);
         const T qc = in ? qq : x0;
-        if constexpr (FORM == FORM_RECORD) {
+        if constexpr (WIN) {
           // in the window at or after the carry: branch-free lifting over the window's knots
           // (largest l < kSortWin with x_{wb+l} <= q; +inf past x_{n-2} keeps it <= n-2-wb)
           const int l0 = jc - wb;
@@ -681,8 +685,7 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x,
             if (in) jl = j;
             continue;
           }
-          j = jc;  // outside the window: the general path below
-        }
+        }  // outside the window: the general path, from this lane's previous interval
         if (__ldg(X + j) > qc) {
           j = bisect(X, n, qc);  // below the carry: unsorted input despite the hint
         } else {

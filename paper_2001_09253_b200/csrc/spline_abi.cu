@@ -383,6 +383,9 @@ int launch_sorted_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
   const int64_t rpc = (m + qrun - 1) / qrun;
   const int64_t ntasks = batch * rpc;
   const int64_t grid = (ntasks + 7) / 8;
+  if (FORM == FORM_RECORD && m >= (int64_t)kSortWinDensity * (n - 1))  // dense: the record window pays
+    return launch_pdl(k_eval_sorted<T, V, FORM_RECORD, true>, dim3((unsigned)grid), dim3(256), 0, st, x, y, y2, n, q,
+                      m, out, idx, qrun, rpc, ntasks);
   return launch_pdl(k_eval_sorted<T, V, FORM>, dim3((unsigned)grid), dim3(256), 0, st, x, y, y2, n, q, m, out, idx,
                     qrun, rpc, ntasks);
 }
