@@ -530,6 +530,8 @@ def main():
         launches = K
     if wl.flags & workloads.FLAG_Q_SORTED:
         ekern = "k_eval_sorted"
+    elif s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0:
+        ekern = "k_eval_small"
     elif long_curve or 3 * n * s > 200 * 1024:
         ekern = "k_pack_records + k_eval_records"
     elif n <= 512 and not (wl.flags & workloads.FLAG_X_UNIFORM) and B >= 8 and m < 2048:

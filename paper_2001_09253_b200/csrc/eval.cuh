@@ -541,6 +541,124 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
   if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
 }
 
+// ---- very short curves, few queries (fp32, n <= 8, m <= 32: BASELINE cfg3) -----------------
+// One warp per tile of 32 curves, no block-level synchronisation and no staging pass: lane l
+// builds the records of curve c0+l in registers straight from HBM (16-byte loads) into its
+// own slot of the warp's shared-memory table; the tile's m*32 queries (contiguous in HBM) are
+// then loaded as 16-byte vectors, lane l holding vectors l, l+32, ... (one curve each,
+// m % 4 == 0), all in flight at once.  A query is located by branch-free
+// binary lifting over its curve's n-1 left knots (3 steps for n <= 8; exact on any grid, so
+// the uniform-grid hint needs no separate path) and evaluated with the same make_cub /
+// cub_eval arithmetic as every other kernel.  Per query: ~35 instructions, no pack loop, no
+// division to find the curve.
+constexpr int kSmallN = 8, kSmallM = 32, kSmallWarps = 4;
+struct alignas(16) SmallCurve {  // 208 B: 52 words, so the 4 curves of a warp access hit distinct banks
+  Cub<float> c[kSmallN - 1];
+  float e2[kSmallN - 1];
+  float xk[kSmallN];
+  float x0, xn;
+  float pad[7];
+};
+
+__global__ void __launch_bounds__(kSmallWarps * 32, 6) k_eval_small(const float *__restrict__ x,
+                                                                 const float *__restrict__ y,
+                                                                 const float *__restrict__ y2, int n, int64_t batch,
+                                                                 const float *__restrict__ q, int m,
+                                                                 float *__restrict__ out, int32_t *__restrict__ idx,
+                                                                 int vecn) {
+  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
+  constexpr int MV = kSmallM;  // at most m vectors per lane (32 curves x m queries / (32 lanes x 4))
+  __shared__ SmallCurve tab[kSmallWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  SmallCurve *T = tab[w];
+  const int64_t ntiles = (batch + 31) >> 5;
+  bool oor = false;
+  for (int64_t tile = (int64_t)blockIdx.x * kSmallWarps + w; tile < ntiles; tile += (int64_t)gridDim.x * kSmallWarps) {
+    const int64_t c0 = tile << 5;
+    const int nc = (int)min64(32, batch - c0);
+    const int nq = nc * m;          // the tile's queries, contiguous from q + c0 m
+    const int nv = nq >> 2;         // 16-byte vectors
+    const float *qt = q + c0 * m;
+    // records of curve c0 + lane
+    if (lane < nc) {
+      const int64_t c = c0 + lane;
+      float xv[kSmallN], yv[kSmallN], zv[kSmallN];
+      if (vecn) {  // n == 8 with 16-byte aligned rows
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float4 a = __ldg(reinterpret_cast<const float4 *>(x + c * 8) + h);
+          const float4 b = __ldg(reinterpret_cast<const float4 *>(y + c * 8) + h);
+          const float4 d = __ldg(reinterpret_cast<const float4 *>(y2 + c * 8) + h);
+          xv[4 * h] = a.x; xv[4 * h + 1] = a.y; xv[4 * h + 2] = a.z; xv[4 * h + 3] = a.w;
+          yv[4 * h] = b.x; yv[4 * h + 1] = b.y; yv[4 * h + 2] = b.z; yv[4 * h + 3] = b.w;
+          zv[4 * h] = d.x; zv[4 * h + 1] = d.y; zv[4 * h + 2] = d.z; zv[4 * h + 3] = d.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kSmallN; ++j) {
+          const int jj = min(j, n - 1);
+          xv[j] = __ldg(x + c * n + jj);
+          yv[j] = __ldg(y + c * n + jj);
+          zv[j] = __ldg(y2 + c * n + jj);
+        }
+      }
+      SmallCurve &S = T[lane];
+#pragma unroll
+      for (int j = 0; j < kSmallN - 1; ++j) {
+        if (j < n - 1) {
+          float e2;
+          S.c[j] = make_cub<float>(xv[j], xv[j + 1], yv[j], yv[j + 1], zv[j], zv[j + 1], e2);
+          S.e2[j] = e2;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kSmallN; ++j) S.xk[j] = xv[j];  // (entries past n-1 repeat x_{n-1})
+      S.x0 = xv[0];
+      S.xn = xv[kSmallN - 1];  // = x_{n-1} (clamped index above)
+    }
+    float4 qv[MV / 4];  // (loaded after the record build: registers)
+#pragma unroll
+    for (int i = 0; i < MV / 4; ++i) {
+      const int v = lane + 32 * i;
+      if (v < nv) qv[i] = __ldcs(reinterpret_cast<const float4 *>(qt) + v);
+    }
+    __syncwarp();
+    // evaluate: vector v = lane + 32 i holds queries 4v .. 4v+3 of curve (4v) / m
+    const int top = n - 2;
+#pragma unroll
+    for (int i = 0; i < MV / 4; ++i) {
+      const int v = lane + 32 * i;
+      if (v < nv) {
+        const int cl = (4 * v) / m;
+        const SmallCurve &S = T[cl];
+        const float x0 = S.x0, xn = S.xn;
+        const float qq[4] = {qv[i].x, qv[i].y, qv[i].z, qv[i].w};
+        float r[4];
+        int jj[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool in = (qq[e] >= x0) && (qq[e] <= xn);
+          const float qc = in ? qq[e] : x0;
+          int j = 0;
+#pragma unroll
+          for (int d = kSmallN / 2; d >= 1; d >>= 1) {  // largest j <= n-2 with x_j <= q
+            const int p = min(j + d, top);
+            j = (S.xk[p] <= qc) ? p : j;
+          }
+          const float val = cub_eval<float>(S.c[j], S.e2[j], S.xk[j], qc);
+          r[e] = in ? val : qnan<float>();
+          jj[e] = in ? j : -1;
+          oor |= !in;
+        }
+        __stcs(reinterpret_cast<float4 *>(out + c0 * m) + v, make_float4(r[0], r[1], r[2], r[3]));
+        if (idx) __stcs(reinterpret_cast<int4 *>(idx + c0 * m) + v, make_int4(jj[0], jj[1], jj[2], jj[3]));
+      }
+    }
+    __syncwarp();  // the table is rebuilt for the next tile
+  }
+  raise_status_warp(oor, kOutOfRange);
+}
+
 // ---- sorted query runs ------------------------------------------------------------------
 
 // Warp-cooperative 32-ary search (all lanes hold the same q, X[0] <= q <= X[n-1]):

@@ -399,6 +399,20 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
     if (vec) return launch_sorted_k<T, VW>(x, y, y2, (int)n, batch, q, m, out, idx, st);
     return launch_sorted_k<T, 1>(x, y, y2, (int)n, batch, q, m, out, idx, st);
   }
+  if constexpr (sizeof(T) == 4) {  // very short curves with few queries (cfg3): k_eval_small
+    if (n <= kSmallN && m <= kSmallM && m % 4 == 0 && m > 0 && aligned16(q) && aligned16(out) &&
+        (!idx || aligned16(idx))) {
+      const int vecn = n == kSmallN && aligned16(x) && aligned16(y) && aligned16(y2);
+      const int64_t ntiles = (batch + 31) / 32;
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_small, kSmallWarps * 32, 0) != cudaSuccess ||
+          occ < 1)
+        occ = 1;
+      const int64_t grid = std::min<int64_t>((ntiles + kSmallWarps - 1) / kSmallWarps, (int64_t)occ * num_sms());
+      return launch_pdl(k_eval_small, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, x, y, y2, (int)n, batch, q,
+                        (int)m, out, idx, vecn);
+    }
+  }
   if (n < 65535) {
     const int nn = (int)n;
     if ((flags & SPLINE_X_UNIFORM) && stage_total<T>(1, nn, MODE_UNIFORM, kQMax) <= kSmemCap)

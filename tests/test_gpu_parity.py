@@ -35,7 +35,8 @@ def test_cfg2_k1_thomas_f32(api, kw):
     parity.check_case(api, workloads.generate(2, **kw))
 
 
-@pytest.mark.parametrize("kw", [dict(batch=20000), dict(batch=4099, m=33), dict(batch=50, n=3, m=7)])
+@pytest.mark.parametrize("kw", [dict(batch=20000), dict(batch=4099, m=33), dict(batch=50, n=3, m=7),
+                                dict(batch=1001, n=5, m=12), dict(batch=33, m=28), dict(batch=70001, n=4, m=4)])
 def test_cfg3_uniform_f32(api, kw):
     parity.check_case(api, workloads.generate(3, **kw))
     parity.check_case(api, workloads.generate(3, **kw), flags=0)  # same answer without the hint
