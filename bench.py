@@ -532,6 +532,8 @@ def main():
         ekern = "k_eval_sorted"
     elif s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0:
         ekern = "k_eval_small"
+    elif (n <= 64 and B >= 4 * 148 and m % (16 // s) == 0 and not (wl.flags & workloads.FLAG_X_UNIFORM)):
+        ekern = "k_eval_curvewarp"
     elif long_curve or 3 * n * s > 200 * 1024:
         ekern = "k_pack_records + k_eval_records"
     elif n <= 512 and not (wl.flags & workloads.FLAG_X_UNIFORM) and B >= 8 and m < 2048:

@@ -541,6 +541,98 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
   if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
 }
 
+// ---- one warp per curve, no staging pass (n <= 64, unsorted queries: BASELINE cfg2) -----
+// Each warp walks its own sequence of curves.  Per curve: lane l loads knots l and l+32 of x,
+// y, y2 straight from HBM (coalesced; the next curve's are already in flight), builds the
+// records of intervals l and l+32 into the warp's table, then the Eytzinger keys (the slot ->
+// knot rank of a lane's slots is the same for every curve: computed once), and evaluates the
+// curve's m queries as 16-byte vectors (lane l: vectors l, l+32, ...), with the same
+// eval_packed descent and make_cub / cub_eval arithmetic as the staged kernels.  No TMA ring,
+// no block barrier, no per-element division.
+constexpr int kCwMaxN = 64, kCwWarps = 8;
+template <typename T> struct CwTable {
+  Cub<T> c[kCwMaxN];
+  T e2[kCwMaxN];
+  T xk[kCwMaxN];
+  T ey[kCwMaxN];  // Eytzinger keys, slot 0 unused
+};
+
+template <typename T, int L2>
+__global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(const T *__restrict__ x, const T *__restrict__ y,
+                                                                     const T *__restrict__ y2, int n, int64_t batch,
+                                                                     const T *__restrict__ q, int m,
+                                                                     T *__restrict__ out, int32_t *__restrict__ idx) {
+  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
+  constexpr int VW = 16 / sizeof(T);
+  constexpr int P = 1 << L2;  // <= 64
+  using VT = typename Vec16<T>::V;
+  __shared__ CwTable<T> tabs[kCwWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  CwTable<T> &tb = tabs[w];
+  const uint32_t ebase = smem_u32(tb.ey);
+  // this lane's Eytzinger slots (lane, lane + 32 < P) and the knots they hold
+  const int r0 = (lane > 0 && lane < P) ? eytz_rank(lane, L2) + 1 : 0;
+  const int r1 = (lane + 32 < P) ? eytz_rank(lane + 32, L2) + 1 : 0;
+  const int nv = m / VW;  // query vectors per curve
+  const int64_t G = (int64_t)gridDim.x * kCwWarps;
+  int64_t c = (int64_t)blockIdx.x * kCwWarps + w;
+  bool oor = false;
+  // the current curve's knots (lane's two) in registers
+  T kx[2], ky[2], kz[2];
+  auto load_knots = [&](int64_t cc) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h;
+      if (cc < batch && j < n) {
+        kx[h] = __ldcs(x + cc * n + j);
+        ky[h] = __ldcs(y + cc * n + j);
+        kz[h] = __ldcs(y2 + cc * n + j);
+      }
+    }
+  };
+  load_knots(c);
+  for (; c < batch; c += G) {
+    // records of intervals lane, lane+32 (x_{j+1}, y_{j+1}, y2_{j+1} from the neighbour lane)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h;
+      const T xn1 = __shfl_down_sync(0xffffffffu, kx[h], 1), yn1 = __shfl_down_sync(0xffffffffu, ky[h], 1),
+              zn1 = __shfl_down_sync(0xffffffffu, kz[h], 1);
+      // lane 31's neighbour is lane 0 of the next half
+      const T xh = __shfl_sync(0xffffffffu, kx[1], 0), yh = __shfl_sync(0xffffffffu, ky[1], 0),
+              zh = __shfl_sync(0xffffffffu, kz[1], 0);
+      const T xb = (lane == 31) ? xh : xn1, yb = (lane == 31) ? yh : yn1, zb = (lane == 31) ? zh : zn1;
+      if (j < n) tb.xk[j] = kx[h];
+      if (j < n - 1) tb.c[j] = make_cub<T>(kx[h], xb, ky[h], yb, kz[h], zb, tb.e2[j]);
+    }
+    load_knots(c + G);  // the next curve's knots, in flight during this curve's queries
+    __syncwarp();
+    // Eytzinger keys x_1 .. x_{n-2}, +inf padded
+    if (lane > 0 && lane < P) tb.ey[lane] = (r0 <= n - 2) ? tb.xk[r0] : (T)INFINITY;
+    if (lane + 32 < P) tb.ey[lane + 32] = (r1 <= n - 2) ? tb.xk[r1] : (T)INFINITY;
+    __syncwarp();
+    const CurveHdr<T> hd{tb.xk[0], tb.xk[n - 1], T(0), T(0)};
+    const T *qc = q + c * m;
+    T *oc = out + c * m;
+    int32_t *ic = idx ? idx + c * m : nullptr;
+    for (int v = lane; v < nv; v += 32) {
+      const VT a = __ldcs(reinterpret_cast<const VT *>(qc) + v);
+      const T *qa = reinterpret_cast<const T *>(&a);
+      T val[VW];
+      int jj[VW];
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        eval_packed<T, MODE_BISECT, L2>(tb.c, tb.e2, tb.xk, ebase, nullptr, hd, n, 0, qa[e], val[e], jj[e]);
+        oor |= jj[e] < 0;
+      }
+      VecIO<T, VW>::store(oc + (size_t)v * VW, val);
+      if (ic) VecIO<T, VW>::store_idx(ic + (size_t)v * VW, jj);
+    }
+    __syncwarp();  // the table is rebuilt for the next curve
+  }
+  raise_status_warp(oor, kOutOfRange);
+}
+
 // ---- very short curves, few queries (fp32, n <= 8, m <= 32: BASELINE cfg3) -----------------
 // One warp per tile of 32 curves, no block-level synchronisation and no staging pass: lane l
 // builds the records of curve c0+l in registers straight from HBM (16-byte loads) into its

@@ -390,6 +390,27 @@ int launch_sorted_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
                     qrun, rpc, ntasks);
 }
 
+template <typename T, int L2>
+int launch_curvewarp_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int m, T *out,
+                       int32_t *idx, cudaStream_t st) {
+  auto kern = k_eval_curvewarp<T, L2>;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCwWarps * 32, 0) != cudaSuccess || occ < 1) occ = 1;
+  const int64_t grid = std::min<int64_t>((batch + kCwWarps - 1) / kCwWarps, (int64_t)occ * num_sms());
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kCwWarps * 32), 0, st, x, y, y2, n, batch, q, m, out, idx);
+}
+template <typename T>
+int launch_curvewarp(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int m, T *out,
+                     int32_t *idx, cudaStream_t st) {
+  switch (eytz_levels(n)) {
+    case 2: return launch_curvewarp_k<T, 2>(x, y, y2, n, batch, q, m, out, idx, st);
+    case 3: return launch_curvewarp_k<T, 3>(x, y, y2, n, batch, q, m, out, idx, st);
+    case 4: return launch_curvewarp_k<T, 4>(x, y, y2, n, batch, q, m, out, idx, st);
+    case 5: return launch_curvewarp_k<T, 5>(x, y, y2, n, batch, q, m, out, idx, st);
+    default: return launch_curvewarp_k<T, 6>(x, y, y2, n, batch, q, m, out, idx, st);
+  }
+}
+
 template <typename T>
 int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const T *q, int64_t m, T *out,
            int32_t *idx, int flags, cudaStream_t st) {
@@ -412,6 +433,14 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
       return launch_pdl(k_eval_small, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, x, y, y2, (int)n, batch, q,
                         (int)m, out, idx, vecn);
     }
+  }
+  {  // curves of up to 64 knots, unsorted queries: one warp per curve (k_eval_curvewarp)
+    constexpr int VW = 16 / sizeof(T);
+    // (enough curves to give every SM several warps; few long query runs are split by the staged path)
+    if (!(flags & SPLINE_X_UNIFORM) && n <= kCwMaxN && batch >= 4 * (int64_t)num_sms() && m > 0 && m % VW == 0 &&
+        aligned16(q) && aligned16(out) &&
+        (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0)))
+      return launch_curvewarp<T>(x, y, y2, (int)n, batch, q, (int)m, out, idx, st);
   }
   if (n < 65535) {
     const int nn = (int)n;
