@@ -592,6 +592,12 @@ __global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(const T *__
   };
   load_knots(c);
   for (; c < batch; c += G) {
+    const T *qc = q + c * m;
+    // the lane's first two query vectors of this curve: in flight during the table build
+    VT qpf[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      if (lane + 32 * i < nv) qpf[i] = __ldcs(reinterpret_cast<const VT *>(qc) + lane + 32 * i);
     // records of intervals lane, lane+32 (x_{j+1}, y_{j+1}, y2_{j+1} from the neighbour lane)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -612,11 +618,10 @@ __global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(const T *__
     if (lane + 32 < P) tb.ey[lane + 32] = (r1 <= n - 2) ? tb.xk[r1] : (T)INFINITY;
     __syncwarp();
     const CurveHdr<T> hd{tb.xk[0], tb.xk[n - 1], T(0), T(0)};
-    const T *qc = q + c * m;
     T *oc = out + c * m;
     int32_t *ic = idx ? idx + c * m : nullptr;
-    for (int v = lane; v < nv; v += 32) {
-      const VT a = __ldcs(reinterpret_cast<const VT *>(qc) + v);
+    for (int v = lane, i = 0; v < nv; v += 32, ++i) {
+      const VT a = (i == 0) ? qpf[0] : (i == 1) ? qpf[1] : __ldcs(reinterpret_cast<const VT *>(qc) + v);
       const T *qa = reinterpret_cast<const T *>(&a);
       T val[VW];
       int jj[VW];
