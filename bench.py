@@ -474,20 +474,10 @@ def main():
         h_y2 = torch.empty(x.shape, dtype=x.dtype).pin_memory()
         h_out = torch.empty(q.shape, dtype=q.dtype).pin_memory()
         h_idx = torch.empty(q.shape, dtype=torch.int32).pin_memory()
-        d_x, d_y, d_q = torch.empty_like(x), torch.empty_like(y), torch.empty_like(q)
-        d_s = [torch.empty_like(a) if a is not None else None for a in (yp1, ypn)]
 
-        def e2e_step():
-            d_x.copy_(h_in[0], non_blocking=True)
-            d_y.copy_(h_in[1], non_blocking=True)
-            d_q.copy_(h_in[2], non_blocking=True)
-            for d, h in zip(d_s, h_sl):
-                if d is not None:
-                    d.copy_(h, non_blocking=True)
-            api.build_eval(d_x, d_y, d_q, wl.bc, d_s[0], d_s[1], wl.flags, y2=y2, out=out, idx=idx)
-            h_y2.copy_(y2, non_blocking=True)
-            h_out.copy_(out, non_blocking=True)
-            h_idx.copy_(idx, non_blocking=True)
+        def e2e_step():  # spline_build_eval_host: chunks of curves, copies overlapped with kernels
+            api.build_eval_host(h_in[0], h_in[1], h_in[2], wl.bc, h_sl[0], h_sl[1], wl.flags, y2=h_y2, out=h_out,
+                                idx=h_idx, sync=False)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -507,8 +497,8 @@ def main():
         d2h = x.numel() * s + q.numel() * s + q.numel() * 4
         e2e = {"value": world * B * m / (te.item() * 1e-3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": te.item(), "pinned": True,
-               "path": "api.build_eval (C ABI spline_build_eval, library-chosen kernels) with pinned host in/out, "
-                       "copies on the same stream"}
+               "path": "api.build_eval_host (C ABI spline_build_eval_host): pinned host in/out, the batch in chunks "
+                       "whose H2D copies, kernels and D2H copies overlap on internal streams"}
 
     if rank != 0:
         if world > 1:

@@ -120,6 +120,20 @@ int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, in
                       int dtype, spline_stream_t stream);
 
 /*
+ * spline_build_eval_host -- spline_build_eval on HOST-resident arrays (same arguments, same
+ * results bitwise, every pointer a host pointer; y2 and idx nullable).  The batch is cut into
+ * chunks of whole curves that flow through internal streams: one chunk's host->device copy,
+ * another's kernels and a third's device->host copy overlap.  Pinned (page-locked) host memory
+ * gives the overlap; pageable memory works but serialises the copies.  Device scratch comes
+ * from the library pool.  Ordered after prior work on `stream`; `stream` waits for the whole
+ * call (synchronise it before reading the outputs).  The fused/split choice is the whole
+ * problem's.  Errors: as spline_build_eval.
+ */
+int spline_build_eval_host(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1,
+                           const void *ypn, void *y2, const void *q, int64_t m, void *out, int32_t *idx, int flags,
+                           int dtype, spline_stream_t stream);
+
+/*
  * spline_eval_ablation -- the paper's evaluation-variant experiment on the GPU (SURVEY.md
  * §8(f) row 2): spline_eval's sorted-run kernel (every
  * query located by the carried-bracket scan, valid for any query order) with

@@ -26,6 +26,7 @@ SIGNATURES = {
     "spline_build": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _vp]),
     "spline_eval": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i32, _i32, _vp]),
     "spline_build_eval": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _vp]),
+    "spline_build_eval_host": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i32, _i32, _vp]),
     "spline_eval_ablation": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _i32, _i32, _vp]),
     "spline_gather_probe": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp]),
     "spline_build_f32": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),

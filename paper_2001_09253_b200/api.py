@@ -118,6 +118,47 @@ def build_eval(x, y, q, bc: int = BC_NATURAL, yp1=None, ypn=None, flags: int = 0
     return z, o, i
 
 
+def build_eval_host(x, y, q, bc: int = BC_NATURAL, yp1=None, ypn=None, flags: int = 0, want_y2: bool = True,
+                    y2=None, out=None, idx=None, want_idx: bool = True, stream=None, sync: bool = True):
+    """spline_build_eval_host: build + evaluate on HOST tensors (pinned for copy/compute overlap),
+    chunked through the GPU.  Returns (y2 or None, out, idx or None) as CPU tensors; with
+    sync=False the caller synchronises `stream` before reading them."""
+    for t in (x, y, q):
+        if not isinstance(t, torch.Tensor) or t.device.type != "cpu" or not t.is_contiguous():
+            raise ValueError("build_eval_host takes contiguous CPU tensors (pinned for overlap)")
+    squeeze = x.dim() == 1
+    x, y, q = _as2d(x), _as2d(y), _as2d(q)
+    B, n = x.shape
+    m = q.shape[1]
+    if y.shape != x.shape or q.shape[0] != B or y.dtype != x.dtype or q.dtype != x.dtype:
+        raise ValueError("x, y must be (B, n) and q (B, m), one dtype")
+    if x.dtype not in _DT:
+        raise ValueError("dtype must be float32 or float64")
+    pin = x.is_pinned()
+
+    def host_like(shape, dtype):
+        t = torch.empty(shape, dtype=dtype)
+        return t.pin_memory() if pin else t
+
+    def slope(v):
+        if v is None or isinstance(v, torch.Tensor):
+            return v
+        return torch.full((B,), float(v), dtype=x.dtype)
+
+    yp1, ypn = slope(yp1), slope(ypn)
+    z = (host_like(x.shape, x.dtype) if y2 is None else _as2d(y2)) if want_y2 else None
+    o = host_like(q.shape, q.dtype) if out is None else _as2d(out)
+    i = (host_like(q.shape, torch.int32) if idx is None else _as2d(idx)) if want_idx else None
+    rc = _lib.load().spline_build_eval_host(_p(x), _p(y), n, B, bc, _p(yp1), _p(ypn), _p(z), _p(q), m, _p(o),
+                                            _p(i), flags, _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_build_eval_host")
+    if sync:
+        (torch.cuda.current_stream() if stream is None else stream).synchronize()
+    if squeeze:
+        return (None if z is None else z[0]), o[0], (None if i is None else i[0])
+    return z, o, i
+
+
 def evaluate_ablation(x, y, y2, q, form: str, out=None, idx=None, stream=None):
     """spline_eval_ablation: the sorted-run eval kernel with one of the paper's interpolation
     variants (_lib.FORMS: record, splint_div, splint_mul, newint_orig, newint_noinv, noop)."""

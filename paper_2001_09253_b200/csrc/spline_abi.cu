@@ -592,6 +592,94 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
   return rc;
 }
 
+// ---- host-resident arrays: chunked, copies overlapped with the kernels -------------------
+// spline_build_eval_host: the batch is cut into chunks of whole curves; chunk i runs on
+// internal stream i % kHostStreams: H2D of its x, y, q (and slopes), the device
+// build+eval, D2H of its y2, out, idx -- so one chunk's H2D, another's kernels and a third's
+// D2H overlap (PCIe is full duplex).  Device buffers come from the library pool; the call is
+// ordered after prior work on `stream`, and `stream` waits for all of it.  Pinned host memory
+// gives the overlap; pageable memory is correct but serialises the copies.
+constexpr int kHostStreams = 3;
+constexpr size_t kHostChunkBytes = 32u << 20;  // target copy traffic per chunk
+
+struct HostStreams {
+  cudaStream_t s[kHostStreams];
+  cudaEvent_t done[kHostStreams];
+  cudaEvent_t start;
+};
+inline int host_streams(HostStreams **out) {
+  static std::mutex mu;
+  static HostStreams *per_dev[128] = {};
+  int dev = 0;
+  if (int rc = cuda_rc(cudaGetDevice(&dev))) return rc;
+  if (dev < 0 || dev >= 128) return SPLINE_ECUDA;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!per_dev[dev]) {
+    auto *h = new HostStreams;
+    for (int i = 0; i < kHostStreams; ++i) {
+      if (int rc = cuda_rc(cudaStreamCreateWithFlags(&h->s[i], cudaStreamNonBlocking))) return rc;
+      if (int rc = cuda_rc(cudaEventCreateWithFlags(&h->done[i], cudaEventDisableTiming))) return rc;
+    }
+    if (int rc = cuda_rc(cudaEventCreateWithFlags(&h->start, cudaEventDisableTiming))) return rc;
+    per_dev[dev] = h;
+  }
+  *out = per_dev[dev];
+  return SPLINE_OK;
+}
+
+template <typename T>
+int build_eval_host_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+                      const T *q, int64_t m, T *out, int32_t *idx, int flags, cudaStream_t st) {
+  HostStreams *hs = nullptr;
+  if (int rc = host_streams(&hs)) return rc;
+  // the whole problem's fused/split choice, kept for every chunk
+  if (!(flags & (SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT)))
+    flags |= (batch * m <= (int64_t(1) << 19)) ? SPLINE_PATH_FUSED : SPLINE_PATH_SPLIT;
+  const size_t s = sizeof(T);
+  const size_t per_curve = s * (3 * (size_t)n + 2 * (size_t)m + 2) + 4 * (size_t)m;  // device bytes per curve
+  int64_t C = std::max<int64_t>(1, (int64_t)(kHostChunkBytes / per_curve));
+  C = std::max<int64_t>(C, 2 * (int64_t)num_sms());            // keep every chunk GPU-wide
+  C = std::min<int64_t>(C, (batch + kHostStreams - 1) / kHostStreams);  // and at least kHostStreams chunks
+  C = std::max<int64_t>(1, std::min<int64_t>(C, batch));
+  const int64_t nchunk = (batch + C - 1) / C;
+  const int nslot = (int)std::min<int64_t>(kHostStreams, nchunk);
+  // slot layout (16-byte aligned pieces)
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t bx = al(s * C * n), bq = al(s * C * m), bi = al(4 * (size_t)C * m), bs = al(s * C);
+  const size_t slot = 3 * bx + 2 * bq + bi + 2 * bs;
+  char *base = nullptr;
+  if (int rc = ws_alloc((void **)&base, slot * nslot, st)) return rc;
+  int rc = cuda_rc(cudaEventRecord(hs->start, st));
+  for (int k = 0; !rc && k < nslot; ++k) rc = cuda_rc(cudaStreamWaitEvent(hs->s[k], hs->start, 0));
+  for (int64_t i = 0; !rc && i < nchunk; ++i) {
+    const int k = (int)(i % nslot);
+    cudaStream_t ss = hs->s[k];
+    const int64_t c0 = i * C, nc = std::min<int64_t>(C, batch - c0);
+    char *b = base + slot * k;
+    T *dx = (T *)b, *dy = (T *)(b + bx), *dz = (T *)(b + 2 * bx), *dq = (T *)(b + 3 * bx), *dout = (T *)(b + 3 * bx + bq);
+    int32_t *didx = (int32_t *)(b + 3 * bx + 2 * bq);
+    T *ds1 = (T *)(b + 3 * bx + 2 * bq + bi), *ds2 = (T *)(b + 3 * bx + 2 * bq + bi + bs);
+    const size_t kn = s * nc * n, km = s * nc * m;
+    rc = cuda_rc(cudaMemcpyAsync(dx, x + c0 * n, kn, cudaMemcpyHostToDevice, ss));
+    if (!rc) rc = cuda_rc(cudaMemcpyAsync(dy, y + c0 * n, kn, cudaMemcpyHostToDevice, ss));
+    if (!rc && m) rc = cuda_rc(cudaMemcpyAsync(dq, q + c0 * m, km, cudaMemcpyHostToDevice, ss));
+    if (!rc && (bc & 1)) rc = cuda_rc(cudaMemcpyAsync(ds1, yp1 + c0, s * nc, cudaMemcpyHostToDevice, ss));
+    if (!rc && (bc & 2)) rc = cuda_rc(cudaMemcpyAsync(ds2, ypn + c0, s * nc, cudaMemcpyHostToDevice, ss));
+    if (!rc)
+      rc = build_eval_t<T>(dx, dy, n, nc, bc, (bc & 1) ? ds1 : nullptr, (bc & 2) ? ds2 : nullptr, dz, dq, m, dout,
+                           idx ? didx : nullptr, flags, ss);
+    if (!rc && y2) rc = cuda_rc(cudaMemcpyAsync(y2 + c0 * n, dz, kn, cudaMemcpyDeviceToHost, ss));
+    if (!rc && m) rc = cuda_rc(cudaMemcpyAsync(out + c0 * m, dout, km, cudaMemcpyDeviceToHost, ss));
+    if (!rc && m && idx) rc = cuda_rc(cudaMemcpyAsync(idx + c0 * m, didx, 4 * (size_t)nc * m, cudaMemcpyDeviceToHost, ss));
+  }
+  for (int k = 0; k < nslot; ++k) {
+    cudaEventRecord(hs->done[k], hs->s[k]);
+    cudaStreamWaitEvent(st, hs->done[k], 0);
+  }
+  cudaFreeAsync(base, st);
+  return rc;
+}
+
 template <typename T, int FORM>
 int ablation_form(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const T *q, int64_t m, T *out,
                   int32_t *idx, cudaStream_t st) {
@@ -740,6 +828,26 @@ int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, in
                                (const float *)ypn, (float *)y2, (const float *)q, m, (float *)out, idx, flags, st);
   return build_eval_t<double>((const double *)x, (const double *)y, n, batch, bc, (const double *)yp1,
                               (const double *)ypn, (double *)y2, (const double *)q, m, (double *)out, idx, flags, st);
+}
+
+int spline_build_eval_host(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1,
+                           const void *ypn, void *y2, const void *q, int64_t m, void *out, int32_t *idx, int flags,
+                           int dtype, spline_stream_t stream) {
+  if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
+  if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
+  if (m < 0 || m >= (int64_t(1) << 31) || bc < 0 || bc > 3) return SPLINE_EINVAL;
+  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM | SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT)) return SPLINE_EINVAL;
+  if ((flags & SPLINE_PATH_FUSED) && (flags & SPLINE_PATH_SPLIT)) return SPLINE_EINVAL;
+  if (batch == 0) return SPLINE_OK;
+  if (!x || !y || ((bc & 1) && !yp1) || ((bc & 2) && !ypn)) return SPLINE_EINVAL;
+  if (m > 0 && (!q || !out)) return SPLINE_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SPLINE_F32)
+    return build_eval_host_t<float>((const float *)x, (const float *)y, n, batch, bc, (const float *)yp1,
+                                    (const float *)ypn, (float *)y2, (const float *)q, m, (float *)out, idx, flags, st);
+  return build_eval_host_t<double>((const double *)x, (const double *)y, n, batch, bc, (const double *)yp1,
+                                   (const double *)ypn, (double *)y2, (const double *)q, m, (double *)out, idx, flags,
+                                   st);
 }
 
 int spline_eval_ablation(const void *x, const void *y, const void *y2, int64_t n, int64_t batch, const void *q,

@@ -95,11 +95,12 @@ def test_api_rejects_cpu_tensors():
         api.build(torch.zeros(8, dtype=torch.float64), torch.zeros(8, dtype=torch.float64))
 
 
-def test_einval_build_eval():
+@pytest.mark.parametrize("entry", ["spline_build_eval", "spline_build_eval_host"])
+def test_einval_build_eval(entry):
     lib = _lib.load()
     p = ctypes.c_void_p(16)
     F32, E = _lib.SPLINE_F32, _lib.SPLINE_EINVAL
-    f = lib.spline_build_eval
+    f = getattr(lib, entry)
     assert f(p, p, 2, 1, 0, None, None, p, p, 4, p, None, 0, F32, None) == E      # n < 3
     assert f(p, p, 8, 1, 0, None, None, p, p, -1, p, None, 0, F32, None) == E     # m < 0
     assert f(p, p, 8, 1, 1, None, None, p, p, 4, p, None, 0, F32, None) == E      # clamped, no yp1

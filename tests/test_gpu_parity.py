@@ -310,3 +310,27 @@ def test_sorted_edge_cases(api, dt, B, n, m, kind):
     assert (api.status() & api.STATUS_Q_OUT_OF_RANGE) == (api.STATUS_Q_OUT_OF_RANGE if nbad else 0)
     assert torch.equal(idx, idx_u)
     assert torch.equal(torch.nan_to_num(out, 7.0).view(torch.int8), torch.nan_to_num(out_u, 7.0).view(torch.int8))
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("cid,kw", [(2, dict(batch=5000)), (2, dict(batch=700, m=252)), (4, dict(batch=7, n=300, m=1000)),
+                                    (3, dict(batch=3000)), (5, dict(n=(1 << 15) + 3, m=4096))])
+def test_build_eval_host_equals_device(api, cid, kw, pinned):
+    """spline_build_eval_host (host arrays, chunked through internal streams) gives bitwise the
+    device call's y2, out, idx -- several chunks, ragged last chunk, pageable or pinned memory."""
+    wl = workloads.generate(cid, **kw)
+    t = parity.to_dev
+    h = lambda a: torch.from_numpy(a).pin_memory() if pinned else torch.from_numpy(a).clone()
+    s1 = wl.yp1 if wl.bc & 1 else None
+    s2 = wl.ypn if wl.bc & 2 else None
+    dv = lambda a: t(a) if a is not None else None
+    hv = lambda a: h(a) if a is not None else None
+    api.status()
+    y2d, od, idd = api.build_eval(t(wl.x), t(wl.y), t(wl.q), wl.bc, dv(s1), dv(s2), wl.flags)
+    bits_d = api.status()
+    y2h, oh, idh = api.build_eval_host(h(wl.x), h(wl.y), h(wl.q), wl.bc, hv(s1), hv(s2), wl.flags)
+    bits_h = api.status()
+    assert bits_h == bits_d
+    assert torch.equal(y2h.view(torch.int8), y2d.cpu().view(torch.int8))
+    assert torch.equal(idh, idd.cpu())
+    assert torch.equal(oh.view(torch.int8), od.cpu().view(torch.int8))
