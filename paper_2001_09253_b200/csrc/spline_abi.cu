@@ -627,6 +627,57 @@ inline int host_streams(HostStreams **out) {
   return SPLINE_OK;
 }
 
+// One long curve with many queries: the knots go up and the build runs first (every query
+// needs the whole y2), then the queries flow in chunks through the internal streams (each
+// chunk: H2D q, eval, D2H out/idx), overlapping the two PCIe directions.  Few, large chunks:
+// an eval call on a long curve re-packs its interval records.
+template <typename T>
+int build_eval_host_one_t(const T *x, const T *y, int64_t n, int bc, const T *yp1, const T *ypn, T *y2, const T *q,
+                          int64_t m, T *out, int32_t *idx, int flags, cudaStream_t st, HostStreams *hs) {
+  const size_t s = sizeof(T);
+  const int64_t K = std::max<int64_t>(2, std::min<int64_t>(8, (int64_t)(((size_t)m * (2 * s + 4)) / (256u << 20))));
+  const int64_t QC = (m + K - 1) / K;
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t bx = al(s * n), bq = al(s * QC), bi = al(4 * (size_t)QC), bs = al(s);
+  const size_t slot = 2 * bq + bi;
+  char *base = nullptr;
+  if (int rc = ws_alloc((void **)&base, 3 * bx + 2 * bs + kHostStreams * slot, st)) return rc;
+  T *dx = (T *)base, *dy = (T *)(base + bx), *dz = (T *)(base + 2 * bx);
+  T *ds1 = (T *)(base + 3 * bx), *ds2 = (T *)(base + 3 * bx + bs);
+  char *sb = base + 3 * bx + 2 * bs;
+  int rc = cuda_rc(cudaEventRecord(hs->start, st));
+  cudaStream_t s0 = hs->s[0];
+  if (!rc) rc = cuda_rc(cudaStreamWaitEvent(s0, hs->start, 0));
+  if (!rc) rc = cuda_rc(cudaMemcpyAsync(dx, x, s * n, cudaMemcpyHostToDevice, s0));
+  if (!rc) rc = cuda_rc(cudaMemcpyAsync(dy, y, s * n, cudaMemcpyHostToDevice, s0));
+  if (!rc && (bc & 1)) rc = cuda_rc(cudaMemcpyAsync(ds1, yp1, s, cudaMemcpyHostToDevice, s0));
+  if (!rc && (bc & 2)) rc = cuda_rc(cudaMemcpyAsync(ds2, ypn, s, cudaMemcpyHostToDevice, s0));
+  if (!rc) rc = build_t<T>(dx, dy, n, 1, bc, (bc & 1) ? ds1 : nullptr, (bc & 2) ? ds2 : nullptr, dz, s0);
+  if (!rc) rc = cuda_rc(cudaEventRecord(hs->done[0], s0));  // y2 ready
+  for (int k = 1; !rc && k < kHostStreams; ++k) rc = cuda_rc(cudaStreamWaitEvent(hs->s[k], hs->done[0], 0));
+  if (!rc && y2) rc = cuda_rc(cudaMemcpyAsync(y2, dz, s * n, cudaMemcpyDeviceToHost, s0));
+  const int fl = flags & (SPLINE_Q_SORTED | SPLINE_X_UNIFORM);
+  for (int64_t i = 0; !rc && i < K; ++i) {
+    const int k = (int)(i % kHostStreams);
+    cudaStream_t ss = hs->s[k];
+    const int64_t k0 = i * QC, mc = std::min<int64_t>(QC, m - k0);
+    if (mc <= 0) break;
+    char *b = sb + slot * k;
+    T *dq = (T *)b, *dout = (T *)(b + bq);
+    int32_t *didx = (int32_t *)(b + 2 * bq);
+    rc = cuda_rc(cudaMemcpyAsync(dq, q + k0, s * mc, cudaMemcpyHostToDevice, ss));
+    if (!rc) rc = eval_t<T>(dx, dy, dz, n, 1, dq, mc, dout, idx ? didx : nullptr, fl, ss);
+    if (!rc) rc = cuda_rc(cudaMemcpyAsync(out + k0, dout, s * mc, cudaMemcpyDeviceToHost, ss));
+    if (!rc && idx) rc = cuda_rc(cudaMemcpyAsync(idx + k0, didx, 4 * (size_t)mc, cudaMemcpyDeviceToHost, ss));
+  }
+  for (int k = 0; k < kHostStreams; ++k) {
+    cudaEventRecord(hs->done[k], hs->s[k]);
+    cudaStreamWaitEvent(st, hs->done[k], 0);
+  }
+  cudaFreeAsync(base, st);
+  return rc;
+}
+
 template <typename T>
 int build_eval_host_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
                       const T *q, int64_t m, T *out, int32_t *idx, int flags, cudaStream_t st) {
@@ -642,6 +693,8 @@ int build_eval_host_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, 
   C = std::min<int64_t>(C, (batch + kHostStreams - 1) / kHostStreams);  // and at least kHostStreams chunks
   C = std::max<int64_t>(1, std::min<int64_t>(C, batch));
   const int64_t nchunk = (batch + C - 1) / C;
+  if (nchunk == 1 && batch == 1 && (size_t)m * (2 * s + 4) > 8 * kHostChunkBytes)
+    return build_eval_host_one_t<T>(x, y, n, bc, yp1, ypn, y2, q, m, out, idx, flags, st, hs);
   const int nslot = (int)std::min<int64_t>(kHostStreams, nchunk);
   // slot layout (16-byte aligned pieces)
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };

@@ -334,3 +334,19 @@ def test_build_eval_host_equals_device(api, cid, kw, pinned):
     assert torch.equal(y2h.view(torch.int8), y2d.cpu().view(torch.int8))
     assert torch.equal(idh, idd.cpu())
     assert torch.equal(oh.view(torch.int8), od.cpu().view(torch.int8))
+
+
+@pytest.mark.slow
+def test_build_eval_host_one_long_curve(api):
+    """One curve with enough queries that spline_build_eval_host streams them in chunks after the
+    build (the one-curve pipeline): bitwise the device call."""
+    wl = workloads.generate(5, n=100003, m=14_000_000)
+    t = parity.to_dev
+    h = lambda a: torch.from_numpy(a).pin_memory()
+    api.status()
+    y2d, od, idd = api.build_eval(t(wl.x), t(wl.y), t(wl.q), wl.bc, None, None, wl.flags)
+    y2h, oh, idh = api.build_eval_host(h(wl.x), h(wl.y), h(wl.q), wl.bc, None, None, wl.flags)
+    assert api.status() == 0
+    assert torch.equal(y2h.view(torch.int8), y2d.cpu().view(torch.int8))
+    assert torch.equal(idh, idd.cpu())
+    assert torch.equal(oh.view(torch.int8), od.cpu().view(torch.int8))
