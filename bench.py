@@ -513,10 +513,11 @@ def main():
     # the library's choice inside spline_build_eval (spline_abi.cu build_eval_t): one fused kernel
     # when the problem is small (batch*m <= 2^19) and fusable, else the two kernels
     fused_step = fusable and B * m <= (1 << 19)
+    small_step = s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0  # k_eval_small<true>: solve + eval
     launches = 2 * K  # 1 build kernel + 1 eval kernel per step for configs 2-4
     if long_curve:
         launches = 5 * K  # tiled SPIKE: reduce + top + finish; eval: pack records + gather
-    if fused_step:
+    if fused_step or small_step:
         launches = K
     if wl.flags & workloads.FLAG_Q_SORTED:
         ekern = "k_eval_sorted"
@@ -555,7 +556,8 @@ def main():
         "build_ms": bms,
         "eval_ms": ems,
         "build_gbs": bbytes / (bms * 1e-3) / 1e9,
-        "step_path": "fused (k_fused_staged)" if fused_step else "split (build kernel(s), then eval kernel(s))",
+        "step_path": ("fused (k_eval_small<true>: K1r's solve + the small-curve eval)" if small_step else
+                      "fused (k_fused_staged)" if fused_step else "split (build kernel(s), then eval kernel(s))"),
         "roofline": {"kernel": ekern, "bound": "hbm",
                      "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": traffic_for(wkey, "eval"), "peak_source": peak_src,

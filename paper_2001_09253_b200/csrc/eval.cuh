@@ -657,13 +657,20 @@ struct alignas(16) SmallCurve {  // 208 B: 52 words, so the 4 curves of a warp a
   float pad[7];
 };
 
-__global__ void __launch_bounds__(kSmallWarps * 32, 6) k_eval_small(const float *__restrict__ x,
+// SOLVE (k_fused_small path of spline_build_eval): lane l also solves its curve -- K1r's
+// thomas_regs on the same registers, so y2 is bitwise K1r's -- stores y2 (when y2w is
+// non-null) and builds the records from registers: x, y are read once and y2 is never read back.
+template <bool SOLVE>
+__global__ void __launch_bounds__(kSmallWarps * 32, SOLVE ? 4 : 6) k_eval_small(const float *__restrict__ x,
                                                                  const float *__restrict__ y,
                                                                  const float *__restrict__ y2, int n, int64_t batch,
                                                                  const float *__restrict__ q, int m,
                                                                  float *__restrict__ out, int32_t *__restrict__ idx,
-                                                                 int vecn) {
-  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
+                                                                 int vecn, int bc = 0,
+                                                                 const float *__restrict__ yp1 = nullptr,
+                                                                 const float *__restrict__ ypn = nullptr,
+                                                                 float *__restrict__ y2w = nullptr) {
+  if constexpr (!SOLVE) pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
   constexpr int MV = kSmallM;  // at most m vectors per lane (32 curves x m queries / (32 lanes x 4))
   __shared__ SmallCurve tab[kSmallWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -685,10 +692,12 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 6) k_eval_small(const float 
         for (int h = 0; h < 2; ++h) {
           const float4 a = __ldg(reinterpret_cast<const float4 *>(x + c * 8) + h);
           const float4 b = __ldg(reinterpret_cast<const float4 *>(y + c * 8) + h);
-          const float4 d = __ldg(reinterpret_cast<const float4 *>(y2 + c * 8) + h);
           xv[4 * h] = a.x; xv[4 * h + 1] = a.y; xv[4 * h + 2] = a.z; xv[4 * h + 3] = a.w;
           yv[4 * h] = b.x; yv[4 * h + 1] = b.y; yv[4 * h + 2] = b.z; yv[4 * h + 3] = b.w;
-          zv[4 * h] = d.x; zv[4 * h + 1] = d.y; zv[4 * h + 2] = d.z; zv[4 * h + 3] = d.w;
+          if constexpr (!SOLVE) {
+            const float4 d = __ldg(reinterpret_cast<const float4 *>(y2 + c * 8) + h);
+            zv[4 * h] = d.x; zv[4 * h + 1] = d.y; zv[4 * h + 2] = d.z; zv[4 * h + 3] = d.w;
+          }
         }
       } else {
 #pragma unroll
@@ -696,7 +705,21 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 6) k_eval_small(const float 
           const int jj = min(j, n - 1);
           xv[j] = __ldg(x + c * n + jj);
           yv[j] = __ldg(y + c * n + jj);
-          zv[j] = __ldg(y2 + c * n + jj);
+          if constexpr (!SOLVE) zv[j] = __ldg(y2 + c * n + jj);
+        }
+      }
+      if constexpr (SOLVE) {  // K1r's sweep (build_thomas.cuh thomas_regs), then y2 out
+        const bool ok = thomas_regs<float, kSmallN>(xv, yv, n, bc, (bc & 1) ? yp1[c] : 0.f, (bc & 2) ? ypn[c] : 0.f, zv);
+        if (!ok) raise_status(kBadKnots);
+        if (y2w) {
+          if (vecn) {
+            reinterpret_cast<float4 *>(y2w + c * 8)[0] = make_float4(zv[0], zv[1], zv[2], zv[3]);
+            reinterpret_cast<float4 *>(y2w + c * 8)[1] = make_float4(zv[4], zv[5], zv[6], zv[7]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kSmallN; ++j)
+              if (j < n) y2w[c * n + j] = zv[j];
+          }
         }
       }
       SmallCurve &S = T[lane];

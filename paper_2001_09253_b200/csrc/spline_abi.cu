@@ -426,12 +426,14 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
       const int vecn = n == kSmallN && aligned16(x) && aligned16(y) && aligned16(y2);
       const int64_t ntiles = (batch + 31) / 32;
       int occ = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_small, kSmallWarps * 32, 0) != cudaSuccess ||
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_small<false>, kSmallWarps * 32, 0) !=
+              cudaSuccess ||
           occ < 1)
         occ = 1;
       const int64_t grid = std::min<int64_t>((ntiles + kSmallWarps - 1) / kSmallWarps, (int64_t)occ * num_sms());
-      return launch_pdl(k_eval_small, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, x, y, y2, (int)n, batch, q,
-                        (int)m, out, idx, vecn);
+      return launch_pdl(k_eval_small<false>, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, x, y, y2, (int)n,
+                        batch, q, (int)m, out, idx, vecn, 0, (const float *)nullptr, (const float *)nullptr,
+                        (float *)nullptr);
     }
   }
   {  // curves of up to 64 knots, unsorted queries: one warp per curve (k_eval_curvewarp)
@@ -573,6 +575,21 @@ template <typename T>
 int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
                  const T *q, int64_t m, T *out, int32_t *idx, int flags, cudaStream_t st) {
   if (m == 0) return y2 ? build_t<T>(x, y, n, batch, bc, yp1, ypn, y2, st) : SPLINE_OK;
+  if constexpr (sizeof(T) == 4) {  // very short fp32 curves, few queries: solve + eval in k_eval_small<true>
+    if (!(flags & (SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT)) && n <= kSmallN && m <= kSmallM && m % 4 == 0 &&
+        aligned16(q) && aligned16(out) && (!idx || aligned16(idx))) {
+      const int vecn = n == kSmallN && aligned16(x) && aligned16(y) && (!y2 || aligned16(y2));
+      const int64_t ntiles = (batch + 31) / 32;
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval_small<true>, kSmallWarps * 32, 0) !=
+              cudaSuccess ||
+          occ < 1)
+        occ = 1;
+      const int64_t grid = std::min<int64_t>((ntiles + kSmallWarps - 1) / kSmallWarps, (int64_t)occ * num_sms());
+      return launch_pdl(k_eval_small<true>, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, x, y,
+                        (const float *)nullptr, (int)n, batch, q, (int)m, out, idx, vecn, bc, yp1, ypn, y2);
+    }
+  }
   const bool want_fused =
       (flags & SPLINE_PATH_FUSED) || (!(flags & SPLINE_PATH_SPLIT) && batch * m <= (int64_t(1) << 19));
   flags &= (SPLINE_Q_SORTED | SPLINE_X_UNIFORM);

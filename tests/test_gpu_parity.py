@@ -350,3 +350,25 @@ def test_build_eval_host_one_long_curve(api):
     assert torch.equal(y2h.view(torch.int8), y2d.cpu().view(torch.int8))
     assert torch.equal(idh, idd.cpu())
     assert torch.equal(oh.view(torch.int8), od.cpu().view(torch.int8))
+
+
+@pytest.mark.parametrize("kw", [dict(batch=20000), dict(batch=1001, n=5, m=12), dict(batch=77, n=8, m=32)])
+@pytest.mark.parametrize("bc", [0, 3])
+def test_build_eval_default_equals_build_then_eval(api, kw, bc):
+    """spline_build_eval without a path hint (short fp32 curves: the solve+eval small kernel) gives
+    bitwise spline_build followed by spline_eval, and the oracle's answer."""
+    wl = workloads.generate(3, **kw)
+    t = parity.to_dev
+    B = wl.x.shape[0]
+    rng = np.random.default_rng(B)
+    s1 = t(rng.normal(size=B).astype(np.float32)) if bc & 1 else None
+    s2 = t(rng.normal(size=B).astype(np.float32)) if bc & 2 else None
+    x, y, q = t(wl.x), t(wl.y), t(wl.q)
+    api.status()
+    y2a, oa, ia = api.build_eval(x, y, q, bc, s1, s2, wl.flags)
+    y2b = api.build(x, y, bc, s1, s2)
+    ob, ib = api.evaluate(x, y, y2b, q, wl.flags)
+    assert api.status() == 0
+    assert torch.equal(y2a.view(torch.int8), y2b.view(torch.int8))
+    assert torch.equal(ia, ib)
+    assert torch.equal(oa.view(torch.int8), ob.view(torch.int8))
