@@ -390,7 +390,7 @@ def main():
         raise RuntimeError("data-error status raised on the benchmark inputs")
 
     K = args.steps
-    # the step: spline_build_eval (C ABI) -- one fused kernel for small problems (batch*m <= 2^19),
+    # the step: spline_build_eval (C ABI) -- one fused kernel for small problems (batch*m <= 2^17),
     # else build then eval back to back (the eval launch may overlap the build's drain:
     # programmatic dependent launch); CUDA events around it
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
@@ -511,8 +511,8 @@ def main():
     wkey = f"cfg{args.config}"
     long_curve = n > 256 * (16 if s == 8 else 32)
     # the library's choice inside spline_build_eval (spline_abi.cu build_eval_t): one fused kernel
-    # when the problem is small (batch*m <= 2^19) and fusable, else the two kernels
-    fused_step = fusable and B * m <= (1 << 19)
+    # when the problem is small (batch*m <= 2^17) and fusable, else the two kernels
+    fused_step = fusable and B * m <= (1 << 17)
     small_step = s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0  # k_eval_small<true>: solve + eval
     launches = 2 * K  # 1 build kernel + 1 eval kernel per step for configs 2-4
     if long_curve:

@@ -110,7 +110,7 @@ int spline_eval(const void *x, const void *y, const void *y2, int64_t n, int64_t
  * 3 <= n <= 128, n*sizeof(T) % 16 == 0, m % (16/sizeof(T)) == 0 and x, y, y2, q, out are
  * 16-byte aligned (idx 16-byte aligned for f32, 8-byte for f64); otherwise the two kernels run
  * back to back (with stream-ordered scratch for y2 when y2 is NULL).  Without a PATH hint the
- * library fuses only launch-latency-bound problems (batch*m <= 2^19): on B200 the larger
+ * library fuses only launch-latency-bound problems (batch*m <= 2^17): on B200 the larger
  * staged evaluations are bound by shared-memory bandwidth, which fusion does not relieve
  * (measured: DESIGN.md).  m == 0 builds only.
  * Errors: the union of spline_build's and spline_eval's.

@@ -30,6 +30,10 @@ using namespace fs;
 namespace {
 
 constexpr int kK1MaxN = 128;
+// spline_build_eval's automatic choice: the fused warp-specialised kernel only for
+// launch-latency-sized problems (measured: tools/cmp_paths.py; K1h + curvewarp win from ~2^18)
+constexpr int64_t kFuseMaxWork = int64_t(1) << 17;
+constexpr int kNoFusedStaged = 1 << 30;  // internal: automatic path, but not k_fused_staged
 
 template <typename T> constexpr int rmax() { return sizeof(T) == 8 ? 16 : 32; }
 
@@ -591,7 +595,8 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
     }
   }
   const bool want_fused =
-      (flags & SPLINE_PATH_FUSED) || (!(flags & SPLINE_PATH_SPLIT) && batch * m <= (int64_t(1) << 19));
+      (flags & SPLINE_PATH_FUSED) ||
+      (!(flags & (SPLINE_PATH_SPLIT | kNoFusedStaged)) && batch * m <= kFuseMaxWork);
   flags &= (SPLINE_Q_SORTED | SPLINE_X_UNIFORM);
   if (want_fused && fused_eligible<T>(x, y, n, q, m, out, idx, y2)) {
     if (flags & SPLINE_X_UNIFORM)
@@ -702,7 +707,7 @@ int build_eval_host_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, 
   if (int rc = host_streams(&hs)) return rc;
   // the whole problem's fused/split choice, kept for every chunk
   if (!(flags & (SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT)))
-    flags |= (batch * m <= (int64_t(1) << 19)) ? SPLINE_PATH_FUSED : SPLINE_PATH_SPLIT;
+    if (batch * m > kFuseMaxWork) flags |= kNoFusedStaged;  // chunks must not pick the small-problem kernel
   const size_t s = sizeof(T);
   const size_t per_curve = s * (3 * (size_t)n + 2 * (size_t)m + 2) + 4 * (size_t)m;  // device bytes per curve
   int64_t C = std::max<int64_t>(1, (int64_t)(kHostChunkBytes / per_curve));
