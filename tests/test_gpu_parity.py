@@ -372,3 +372,21 @@ def test_build_eval_default_equals_build_then_eval(api, kw, bc):
     assert torch.equal(y2a.view(torch.int8), y2b.view(torch.int8))
     assert torch.equal(ia, ib)
     assert torch.equal(oa.view(torch.int8), ob.view(torch.int8))
+
+
+def test_build_eval_host_edge_cases(api):
+    """Host entry: m = 0 builds only; no y2 / no idx outputs; a single curve with few queries."""
+    wl = workloads.generate(2, batch=50, m=8)
+    t = parity.to_dev
+    x, y, q = torch.from_numpy(wl.x), torch.from_numpy(wl.y), torch.from_numpy(wl.q)
+    s1, s2 = torch.from_numpy(wl.yp1), torch.from_numpy(wl.ypn)
+    y2d = api.build(t(wl.x), t(wl.y), wl.bc, t(wl.yp1), t(wl.ypn)).cpu()
+    e = q[:, :0].contiguous()
+    y2h, oh, ih = api.build_eval_host(x, y, e, wl.bc, s1, s2)
+    assert torch.equal(y2h.view(torch.int8), y2d.view(torch.int8)) and oh.shape == (50, 0)
+    _, od, _ = api.build_eval(t(wl.x), t(wl.y), t(wl.q), wl.bc, t(wl.yp1), t(wl.ypn), want_y2=False, want_idx=False)
+    z, oh, ih = api.build_eval_host(x, y, q, wl.bc, s1, s2, want_y2=False, want_idx=False)
+    assert z is None and ih is None and torch.equal(oh.view(torch.int8), od.cpu().view(torch.int8))
+    y2h, oh, ih = api.build_eval_host(x[0], y[0], q[0], wl.bc, s1[:1], s2[:1])
+    assert oh.shape == (8,) and ih.shape == (8,)
+    assert api.status() == 0
