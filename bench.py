@@ -514,10 +514,11 @@ def main():
     # when the problem is small (batch*m <= 2^17) and fusable, else the two kernels
     fused_step = fusable and B * m <= (1 << 17)
     small_step = s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0  # k_eval_small<true>: solve + eval
+    tiny_step = (n == 16 or (s == 4 and n in (32, 64))) and B <= 16 and m <= 8192 and m % (16 // s) == 0
     launches = 2 * K  # 1 build kernel + 1 eval kernel per step for configs 2-4
     if long_curve:
         launches = 5 * K  # tiled SPIKE: reduce + top + finish; eval: pack records + gather
-    if fused_step or small_step:
+    if fused_step or small_step or tiny_step:
         launches = K
     if wl.flags & workloads.FLAG_Q_SORTED:
         ekern = "k_eval_sorted"
@@ -557,6 +558,7 @@ def main():
         "eval_ms": ems,
         "build_gbs": bbytes / (bms * 1e-3) / 1e9,
         "step_path": ("fused (k_eval_small<true>: K1r's solve + the small-curve eval)" if small_step else
+                      "fused (k_build_eval_tiny: one CTA per curve, K1h's solve + eval)" if tiny_step else
                       "fused (k_fused_staged)" if fused_step else "split (build kernel(s), then eval kernel(s))"),
         "roofline": {"kernel": ekern, "bound": "hbm",
                      "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,

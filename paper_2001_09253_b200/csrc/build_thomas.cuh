@@ -448,17 +448,16 @@ __global__ void __launch_bounds__(256) k1_thomas_regs(const T *__restrict__ x, c
 // reverses the element order).  The arithmetic is babe_first/babe_row/babe_meet/babe_back, so
 // y2 is bitwise the shared-memory K1's (and the fused kernel's).
 constexpr int kK1hThreads = 128;
+// One lane pair's curve cv (lane parity: top / bottom) -- the body of K1h, also called by the
+// one-CTA build+eval kernel for tiny problems.  Every lane of the warp must call it.
 template <typename T, int N>
-__global__ void __launch_bounds__(kK1hThreads) k1_thomas_half(const T *__restrict__ x, const T *__restrict__ y,
-                                                              int64_t batch, int bc, const T *__restrict__ yp1,
-                                                              const T *__restrict__ ypn, T *__restrict__ y2) {
-  pdl_trigger();
+__device__ __forceinline__ void k1h_solve(const T *__restrict__ x, const T *__restrict__ y, int64_t batch, int bc,
+                                          const T *__restrict__ yp1, const T *__restrict__ ypn, T *__restrict__ y2,
+                                          int64_t cv, bool top) {
   constexpr int K = N / 2;
   constexpr int VW = 16 / sizeof(T);
   static_assert(K % VW == 0 && K >= 2 * VW, "each half is whole 16-byte vectors");
   using VT = typename Vec16<T>::V;
-  const int64_t cv = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 1;
-  const bool top = (threadIdx.x & 1) == 0;
   const bool act = cv < batch;
   const int64_t c = act ? cv : batch - 1;  // a ragged last warp shadows the last curve, stores nothing
   const int dir = top ? 1 : -1;
@@ -535,6 +534,15 @@ __global__ void __launch_bounds__(kK1hThreads) k1_thomas_half(const T *__restric
       *reinterpret_cast<VT *>(zh + (top ? g : K - g - VW)) = a;
     }
   }
+}
+
+template <typename T, int N>
+__global__ void __launch_bounds__(kK1hThreads) k1_thomas_half(const T *__restrict__ x, const T *__restrict__ y,
+                                                              int64_t batch, int bc, const T *__restrict__ yp1,
+                                                              const T *__restrict__ ypn, T *__restrict__ y2) {
+  pdl_trigger();
+  k1h_solve<T, N>(x, y, batch, bc, yp1, ypn, y2, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 1,
+                  (threadIdx.x & 1) == 0);
 }
 
 }  // namespace fs

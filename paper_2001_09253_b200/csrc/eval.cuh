@@ -22,6 +22,7 @@
 //  k_eval_global : the same without workspace (gathers x, y, y2; used if the workspace
 //                  cannot be allocated).
 #pragma once
+#include "build_thomas.cuh"
 #include "common.cuh"
 
 namespace fs {
@@ -634,6 +635,56 @@ __global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(const T *__
       if (ic) VecIO<T, VW>::store_idx(ic + (size_t)v * VW, jj);
     }
     __syncwarp();  // the table is rebuilt for the next curve
+  }
+  raise_status_warp(oor, kOutOfRange);
+}
+
+// ---- tiny problems (a few K1h-sized curves: BASELINE cfg1) -------------------------------
+// One CTA per curve does the whole call: warp 0's lanes 0/1 run K1h's two-ended register sweep
+// (k1h_solve: bitwise K1h's y2), the CTA builds the interval records and Eytzinger keys, and
+// every thread evaluates its queries with eval_packed -- one launch, no TMA pipeline, no
+// warp-specialised hand-off.  The queries' first vectors load at kernel entry.
+template <typename T, int N, int L2>
+__global__ void __launch_bounds__(256) k_build_eval_tiny(const T *__restrict__ x, const T *__restrict__ y,
+                                                         int64_t batch, int bc, const T *__restrict__ yp1,
+                                                         const T *__restrict__ ypn, T *__restrict__ y2,
+                                                         const T *__restrict__ q, int m, T *__restrict__ out,
+                                                         int32_t *__restrict__ idx) {
+  constexpr int VW = 16 / sizeof(T);
+  constexpr int P = 1 << L2;
+  using VT = typename Vec16<T>::V;
+  __shared__ CwTable<T> tb;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t c = blockIdx.x;
+  const T *qc = q + c * m;
+  const int nv = m / VW;
+  VT q0;
+  if (tid < nv) q0 = __ldcs(reinterpret_cast<const VT *>(qc) + tid);
+  if (tid < 32) k1h_solve<T, N>(x, y, batch, bc, yp1, ypn, y2, (lane < 2) ? c : batch, (lane & 1) == 0);
+  __syncthreads();  // y2 of the curve is in memory
+  const T *X = x + c * N, *Y = y + c * N, *Z = y2 + c * N;
+  if (tid < N) tb.xk[tid] = X[tid];
+  if (tid < N - 1) tb.c[tid] = make_cub<T>(X[tid], X[tid + 1], Y[tid], Y[tid + 1], Z[tid], Z[tid + 1], tb.e2[tid]);
+  if (tid > 0 && tid < P) {
+    const int r = eytz_rank(tid, L2) + 1;
+    tb.ey[tid] = (r <= N - 2) ? X[r] : (T)INFINITY;
+  }
+  __syncthreads();
+  const CurveHdr<T> hd{tb.xk[0], tb.xk[N - 1], T(0), T(0)};
+  const uint32_t ebase = smem_u32(tb.ey);
+  bool oor = false;
+  for (int v = tid; v < nv; v += 256) {
+    const VT a = (v == tid) ? q0 : __ldcs(reinterpret_cast<const VT *>(qc) + v);
+    const T *qa = reinterpret_cast<const T *>(&a);
+    T val[VW];
+    int jj[VW];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+      eval_packed<T, MODE_BISECT, L2>(tb.c, tb.e2, tb.xk, ebase, nullptr, hd, N, 0, qa[e], val[e], jj[e]);
+      oor |= jj[e] < 0;
+    }
+    VecIO<T, VW>::store(out + c * m + (size_t)v * VW, val);
+    if (idx) VecIO<T, VW>::store_idx(idx + c * m + (size_t)v * VW, jj);
   }
   raise_status_warp(oor, kOutOfRange);
 }

@@ -390,3 +390,27 @@ def test_build_eval_host_edge_cases(api):
     y2h, oh, ih = api.build_eval_host(x[0], y[0], q[0], wl.bc, s1[:1], s2[:1])
     assert oh.shape == (8,) and ih.shape == (8,)
     assert api.status() == 0
+
+
+@pytest.mark.parametrize("cid,kw", [(1, dict()), (1, dict(batch=3)), (2, dict(batch=5, m=1000)),
+                                    (2, dict(batch=16, n=32, m=64)), (2, dict(batch=1, n=16, m=8192))])
+def test_build_eval_tiny_equals_build_then_eval(api, cid, kw):
+    """spline_build_eval without a hint on a few K1h-sized curves (the one-CTA-per-curve kernel):
+    bitwise spline_build then spline_eval, including out-of-range and NaN queries."""
+    wl = workloads.generate(cid, **kw)
+    q = wl.q.copy()
+    q[:, 0], q[:, 1] = wl.x[:, 0] - 1, np.nan
+    t = parity.to_dev
+    s1 = t(wl.yp1) if wl.bc & 1 else None
+    s2 = t(wl.ypn) if wl.bc & 2 else None
+    x, y, qd = t(wl.x), t(wl.y), t(q)
+    api.status()
+    y2a, oa, ia = api.build_eval(x, y, qd, wl.bc, s1, s2, wl.flags)
+    y2b = api.build(x, y, wl.bc, s1, s2)
+    ob, ib = api.evaluate(x, y, y2b, qd, wl.flags)
+    assert api.status() == api.STATUS_Q_OUT_OF_RANGE
+    assert torch.equal(y2a.view(torch.int8), y2b.view(torch.int8))
+    assert torch.equal(ia, ib)
+    assert torch.equal(torch.nan_to_num(oa, 7.0).view(torch.int8), torch.nan_to_num(ob, 7.0).view(torch.int8))
+    out_ref, idx_ref, _ = oracle.evaluate(wl.x, wl.y, y2b.cpu().numpy(), q)
+    np.testing.assert_array_equal(ia.cpu().numpy(), idx_ref)
