@@ -517,7 +517,10 @@ def main():
     tiny_step = (n == 16 or (s == 4 and n in (32, 64))) and B <= 16 and m <= 8192 and m % (16 // s) == 0
     launches = 2 * K  # 1 build kernel + 1 eval kernel per step for configs 2-4
     if long_curve:
-        launches = 5 * K  # tiled SPIKE: reduce + top + finish; eval: pack records + gather
+        # tiled SPIKE: reduce + top (grouped for one curve of > 128 tiles: up, root, down) + finish;
+        # eval: pack records + gather
+        ntiles = -(-n // (256 * (16 if s == 8 else 32)))
+        launches = (7 if (B == 1 and ntiles > 128) else 5) * K
     if fused_step or small_step or tiny_step:
         launches = K
     if wl.flags & workloads.FLAG_Q_SORTED:
