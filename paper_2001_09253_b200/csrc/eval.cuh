@@ -14,9 +14,16 @@
 //                    MODE_TABLE   -- per-curve bucket table brackets each query
 //                    MODE_UNIFORM -- direct index (q-x_0)(n-1)/(x_{n-1}-x_0), corrected
 //                    MODE_BSEARCH -- bisection on the raw arrays (curves too big to pack)
+//  k_eval_warps  : the same stages with per-warp curve ownership (no CTA barrier in the loop).
+//  k_eval_curvewarp : n <= 64, many curves: one warp per curve, knots loaded directly (next
+//                  curve prefetched), records + Eytzinger keys in a per-warp table.
+//  k_eval_small  : fp32 n <= 8, m <= 32: a warp per 32 curves, per-lane record build; its
+//                  SOLVE form also runs K1r's sweep (spline_build_eval).
+//  k_build_eval_tiny : spline_build_eval on a few K1h-sized curves, one CTA per curve.
 //  k_eval_sorted : SPLINE_Q_SORTED.  A warp walks a contiguous run of queries with a
 //                  carried bracket (the paper's forward scan, made
-//                  warp-cooperative); knots are read through L1 (no staging), any n.
+//                  warp-cooperative); dense runs keep a window of interval records in
+//                  shared memory, sparse runs read knots through L1, any n.
 //  k_pack_records + k_eval_records : unsorted queries on long curves: interval records in
 //                  an HBM workspace, one gather per query at the interpolation guess.
 //  k_eval_global : the same without workspace (gathers x, y, y2; used if the workspace
