@@ -112,7 +112,9 @@ int spline_eval(const void *x, const void *y, const void *y2, int64_t n, int64_t
  * back to back (with stream-ordered scratch for y2 when y2 is NULL).  Without a PATH hint the
  * library fuses only launch-latency-bound problems (batch*m <= 2^17): on B200 the larger
  * staged evaluations are bound by shared-memory bandwidth, which fusion does not relieve
- * (measured: DESIGN.md).  m == 0 builds only.
+ * (measured: DESIGN.md).  Also without a hint: a few curves of n = 16 (or fp32 n = 32, 64)
+ * run in one CTA per curve, and fp32 curves of n <= 8 with m <= 32 queries (m % 4 == 0) in
+ * one solve+eval kernel -- the same results bitwise.  m == 0 builds only.
  * Errors: the union of spline_build's and spline_eval's.
  */
 int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1,
