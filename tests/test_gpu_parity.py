@@ -414,3 +414,26 @@ def test_build_eval_tiny_equals_build_then_eval(api, cid, kw):
     assert torch.equal(torch.nan_to_num(oa, 7.0).view(torch.int8), torch.nan_to_num(ob, 7.0).view(torch.int8))
     out_ref, idx_ref, _ = oracle.evaluate(wl.x, wl.y, y2b.cpu().numpy(), q)
     np.testing.assert_array_equal(ia.cpu().numpy(), idx_ref)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("B,n,m", [(1000, 40, 64), (700, 3, 8), (650, 64, 2), (900, 17, 130)])
+def test_curvewarp_shapes(api, dt, B, n, m):
+    """k_eval_curvewarp (n <= 64, >= 4 curves per SM) across n (Eytzinger depth 2..6), ragged
+    query counts per lane and both dtypes, with ties, ends, out-of-range and NaN queries."""
+    rng = np.random.default_rng(B + n + m)
+    x = np.cumsum(rng.exponential(1.0, (B, n)) + 0.01, axis=1).astype(dt)
+    y = rng.normal(size=(B, n)).astype(dt)
+    y2 = rng.normal(size=(B, n)).astype(dt)
+    q = rng.uniform(x[:, :1] - 0.5, x[:, -1:] + 0.5, (B, m)).astype(dt)
+    q[:, 0] = x[:, min(1, n - 1)]
+    if m > 1:
+        q[:, 1] = np.nan
+    out_ref, idx_ref, nbad = oracle.evaluate(x, y, y2, q)
+    api.status()
+    out, idx = api.evaluate(parity.to_dev(x), parity.to_dev(y), parity.to_dev(y2), parity.to_dev(q), 0)
+    bits = api.status()
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_ref)
+    e = parity.out_rel_err(out.cpu().numpy(), out_ref, y)
+    assert np.all(e <= parity.tol_for(dt))
+    assert (bits & api.STATUS_Q_OUT_OF_RANGE) == (api.STATUS_Q_OUT_OF_RANGE if nbad else 0)
