@@ -523,6 +523,8 @@ def main():
         launches = (7 if (B == 1 and ntiles > 128) else 5) * K
     if fused_step or small_step or tiny_step:
         launches = K
+    one_kernel = fused_step or small_step or tiny_step
+    step_bytes = ((2 * s + 4) * B * m + 3 * s * B * n) if one_kernel else (bbytes + ebytes)
     if wl.flags & workloads.FLAG_Q_SORTED:
         ekern = "k_eval_sorted"
     elif s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0:
@@ -560,6 +562,11 @@ def main():
         "build_ms": bms,
         "eval_ms": ems,
         "build_gbs": bbytes / (bms * 1e-3) / 1e9,
+        "step_roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak,
+                          "algorithmic_bytes": step_bytes, "achieved": step_bytes / (step_ms * 1e-3) / 1e9,
+                          "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak,
+                          "note": "the whole timed step (build + eval); one kernel reads x, y once and never "
+                                  "reads y2 back, the split path pays both kernels' bytes"},
         "step_path": ("fused (k_eval_small<true>: K1r's solve + the small-curve eval)" if small_step else
                       "fused (k_build_eval_tiny: one CTA per curve, K1h's solve + eval)" if tiny_step else
                       "fused (k_fused_staged)" if fused_step else "split (build kernel(s), then eval kernel(s))"),
