@@ -578,9 +578,14 @@ __global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(const T *__
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   CwTable<T> &tb = tabs[w];
   const uint32_t ebase = smem_u32(tb.ey);
-  // this lane's Eytzinger slots (lane, lane + 32 < P) and the knots they hold
-  const int r0 = (lane > 0 && lane < P) ? eytz_rank(lane, L2) + 1 : 0;
-  const int r1 = (lane + 32 < P) ? eytz_rank(lane + 32, L2) + 1 : 0;
+  // the Eytzinger slot of this lane's knots j = lane, lane+32 (the inverse of eytz_rank: knot
+  // j = in-order rank j of the complete tree), so the keys go to the table from registers
+  auto slot_of = [&](int j) {
+    const int sft = __ffs(j) - 1, d = L2 - 1 - sft;
+    return (1 << d) + (((j >> sft) - 1) >> 1);
+  };
+  const int s0 = (lane > 0 && lane < P) ? slot_of(lane) : 0;
+  const int s1 = (lane + 32 < P) ? slot_of(lane + 32) : 0;
   const int nv = m / VW;  // query vectors per curve
   const int64_t G = (int64_t)gridDim.x * kCwWarps;
   int64_t c = (int64_t)blockIdx.x * kCwWarps + w;
@@ -619,11 +624,10 @@ __global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(const T *__
       if (j < n) tb.xk[j] = kx[h];
       if (j < n - 1) tb.c[j] = make_cub<T>(kx[h], xb, ky[h], yb, kz[h], zb, tb.e2[j]);
     }
+    // Eytzinger keys x_1 .. x_{n-2}, +inf padded, straight from registers
+    if (lane > 0 && lane < P) tb.ey[s0] = (lane <= n - 2) ? kx[0] : (T)INFINITY;
+    if (lane + 32 < P) tb.ey[s1] = (lane + 32 <= n - 2) ? kx[1] : (T)INFINITY;
     load_knots(c + G);  // the next curve's knots, in flight during this curve's queries
-    __syncwarp();
-    // Eytzinger keys x_1 .. x_{n-2}, +inf padded
-    if (lane > 0 && lane < P) tb.ey[lane] = (r0 <= n - 2) ? tb.xk[r0] : (T)INFINITY;
-    if (lane + 32 < P) tb.ey[lane + 32] = (r1 <= n - 2) ? tb.xk[r1] : (T)INFINITY;
     __syncwarp();
     const CurveHdr<T> hd{tb.xk[0], tb.xk[n - 1], T(0), T(0)};
     T *oc = out + c * m;
