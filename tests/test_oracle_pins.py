@@ -258,6 +258,79 @@ def test_out_of_range_and_nan_queries():
     assert nbad == 3
 
 
+# ------------------------------------------------------------- batch-driver pins
+# oracle_build_batch / oracle_eval_batch (oracle.c) pick each curve's slopes and offsets; these
+# pins check every curve of a batch against its OWN exact solution, so a driver that reads curve
+# 0's slope (yp1[c] -> yp1[0]) or drops a per-curve offset (x + c*n -> x) fails.
+
+def _distinct_batch(rng, B, n):
+    xs, ys = [], []
+    for c in range(B):
+        x, y = _random_curve(rng, n, spread=0.5 + c)   # every curve its own range and spacing
+        xs.append(x + 3.0 * c)
+        ys.append(y * (1 + c))
+    return np.array(xs), np.array(ys)
+
+
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
+@pytest.mark.parametrize("nthreads", [1, 3])
+def test_batch_build_each_curve_exact(bc, nthreads):
+    """Every row of a batched build equals the exact rational solve of THAT curve with THAT
+    curve's clamped slopes (rows Eq. init_val)."""
+    rng = np.random.default_rng(40 + bc)
+    B, n = 5, 7
+    x, y = _distinct_batch(rng, B, n)
+    yp1 = rng.normal(size=B) * 3 + np.arange(B)       # distinct per curve
+    ypn = rng.normal(size=B) * 3 - np.arange(B)
+    y2, nbad = oracle.build_y2(x, y, bc, yp1, ypn, nthreads=nthreads)
+    assert nbad == 0
+    for c in range(B):
+        ex = refmath.exact_solve(x[c], y[c], bc, yp1[c], ypn[c])
+        scale = max(abs(float(v)) for v in ex)
+        err = max(abs(Fraction(float(a)) - b) for a, b in zip(y2[c], ex))
+        assert float(err) <= 1e-14 * scale, (bc, c)
+
+
+def test_batch_build_bad_curve_isolated():
+    """A bad curve in the middle of a batch NaN-fills only its own row."""
+    rng = np.random.default_rng(44)
+    x, y = _distinct_batch(rng, 4, 6)
+    x[2, 3] = x[2, 2]                                   # curve 2: repeated knot
+    y2, nbad = oracle.build_y2(x, y, 3, np.arange(4.0), -np.arange(4.0), nthreads=2)
+    assert nbad == 1
+    assert np.isnan(y2[2]).all()
+    for c in (0, 1, 3):
+        ex = refmath.exact_solve(x[c], y[c], 3, float(c), -float(c))
+        assert np.max(np.abs(y2[c] - np.array([float(v) for v in ex]))) <= 1e-13 * max(abs(float(v)) for v in ex)
+
+
+@pytest.mark.parametrize("nthreads", [1, 4])
+def test_batch_eval_each_curve_exact(nthreads):
+    """Every (curve, query) of a batched eval: idx = the brute-force scan over THAT curve's knots
+    (reading c1) and out = Eq. nr_formula in exact rationals on THAT curve.  The
+    curves occupy disjoint x ranges, so a query routed to another curve is out of its range."""
+    rng = np.random.default_rng(45)
+    B, n, m = 4, 6, 9
+    x, y = _distinct_batch(rng, B, n)
+    y2 = rng.normal(size=(B, n)) * np.arange(1, B + 1)[:, None]  # any y2: eval is defined for it
+    q = np.array([rng.uniform(x[c, 0], x[c, -1], m) for c in range(B)])
+    q[1, 0] = x[1, 2]                                   # a knot tie
+    q[2, 1] = x[2, -1]                                  # the last knot
+    q[3, 2] = x[0, 1]                                   # inside curve 0's range, outside curve 3's
+    out, idx, nbad = oracle.evaluate(x, y, y2, q, nthreads=nthreads)
+    assert nbad == 1
+    for c in range(B):
+        for k in range(m):
+            j = refmath.brute_locate(x[c], q[c, k])
+            assert idx[c, k] == j, (c, k)
+            if j < 0:
+                assert np.isnan(out[c, k])
+                continue
+            ex = refmath.exact_eval(q[c, k], x[c], y[c], [Fraction(float(v)) for v in y2[c]], j)
+            tol = 8 * np.finfo(float).eps * (np.max(np.abs(y[c])) + np.max(np.abs(y2[c])) * np.max(np.diff(x[c])) ** 2)
+            assert abs(float(Fraction(float(out[c, k])) - ex)) <= tol, (c, k)
+
+
 def test_batch_threads_identical():
     wl = workloads.generate(2, batch=64, m=32)
     a, _ = oracle.build_y2(wl.x, wl.y, wl.bc, wl.yp1, wl.ypn, nthreads=1)
