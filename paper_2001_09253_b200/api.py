@@ -42,20 +42,48 @@ def _as2d(t):
     return t.unsqueeze(0) if t is not None and t.dim() == 1 else t
 
 
+def _check_buf(t, shape, dtype, device, what, host=False):
+    """A caller-supplied buffer the C library reads or writes in full: exact shape, dtype,
+    placement (the curves' device, or a CPU tensor for the host entry) and contiguity."""
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{what} must be a torch tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{what} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if t.dtype != dtype:
+        raise ValueError(f"{what} must be {dtype}, got {t.dtype}")
+    if host:
+        if t.device.type != "cpu":
+            raise ValueError(f"{what} must be a CPU tensor (build_eval_host)")
+    elif t.device != device:
+        raise ValueError(f"{what} must be on {device}, got {t.device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+
+
+def _slopes(v, B, like, host=False):
+    """Per-curve clamped slope: a scalar is broadcast, a tensor must be (B,)."""
+    if v is None:
+        return None
+    if not isinstance(v, torch.Tensor):
+        return torch.full((B,), float(v), dtype=like.dtype, device="cpu" if host else like.device)
+    return v
+
+
 def build(x: torch.Tensor, y: torch.Tensor, bc: int = BC_NATURAL, yp1=None, ypn=None, out=None, stream=None):
     """Second derivatives y2 of the curves (x, y): (B, n) or (n,).  Returns y2."""
     squeeze = x.dim() == 1
     x, y = _as2d(x), _as2d(y)
     B, n = x.shape
-    if yp1 is not None and not isinstance(yp1, torch.Tensor):
-        yp1 = torch.full((B,), float(yp1), dtype=x.dtype, device=x.device)
-    if ypn is not None and not isinstance(ypn, torch.Tensor):
-        ypn = torch.full((B,), float(ypn), dtype=x.dtype, device=x.device)
-    _check_curves(x, y, yp1, ypn)
+    yp1, ypn = _slopes(yp1, B, x), _slopes(ypn, B, x)
+    _check_curves(x, y)
     if y.shape != x.shape:
         raise ValueError("x and y must have the same shape")
+    _check_buf(yp1, (B,), x.dtype, x.device, "yp1")
+    _check_buf(ypn, (B,), x.dtype, x.device, "ypn")
     y2 = torch.empty_like(x) if out is None else _as2d(out)
-    _check_curves(x, y2)
+    _check_buf(y2, x.shape, x.dtype, x.device, "y2 (out)")
     rc = _lib.load().spline_build(_p(x), _p(y), n, B, bc, _p(yp1), _p(ypn), _p(y2), _DT[x.dtype],
                                   ctypes.c_void_p(_stream(stream)))
     _lib.check(rc, "spline_build")
@@ -69,14 +97,14 @@ def evaluate(x, y, y2, q, flags: int = 0, out=None, idx=None, want_idx: bool = T
     B, n = x.shape
     m = q.shape[1]
     _check_curves(x, y, y2, q)
-    if q.shape[0] != B:
-        raise ValueError("q must be (B, m)")
+    if y.shape != x.shape or y2.shape != x.shape or q.dim() != 2 or q.shape[0] != B:
+        raise ValueError("x, y, y2 must be (B, n) and q (B, m)")
     o = torch.empty_like(q) if out is None else _as2d(out)
+    _check_buf(o, q.shape, q.dtype, q.device, "out")
     i = None
     if want_idx:
         i = torch.empty(q.shape, dtype=torch.int32, device=q.device) if idx is None else _as2d(idx)
-        if i.dtype != torch.int32 or not i.is_contiguous():
-            raise ValueError("idx must be contiguous int32")
+        _check_buf(i, q.shape, torch.int32, q.device, "idx")
     rc = _lib.load().spline_eval(_p(x), _p(y), _p(y2), n, B, _p(q), m, _p(o), _p(i), flags, _DT[x.dtype],
                                  ctypes.c_void_p(_stream(stream)))
     _lib.check(rc, "spline_eval")
@@ -93,23 +121,22 @@ def build_eval(x, y, q, bc: int = BC_NATURAL, yp1=None, ypn=None, flags: int = 0
     x, y, q = _as2d(x), _as2d(y), _as2d(q)
     B, n = x.shape
     m = q.shape[1]
-    if yp1 is not None and not isinstance(yp1, torch.Tensor):
-        yp1 = torch.full((B,), float(yp1), dtype=x.dtype, device=x.device)
-    if ypn is not None and not isinstance(ypn, torch.Tensor):
-        ypn = torch.full((B,), float(ypn), dtype=x.dtype, device=x.device)
-    _check_curves(x, y, q, yp1, ypn)
-    if y.shape != x.shape or q.shape[0] != B:
+    yp1, ypn = _slopes(yp1, B, x), _slopes(ypn, B, x)
+    _check_curves(x, y, q)
+    if y.shape != x.shape or q.dim() != 2 or q.shape[0] != B:
         raise ValueError("x, y must be (B, n) and q (B, m)")
+    _check_buf(yp1, (B,), x.dtype, x.device, "yp1")
+    _check_buf(ypn, (B,), x.dtype, x.device, "ypn")
     z = None
     if want_y2:
         z = torch.empty_like(x) if y2 is None else _as2d(y2)
-        _check_curves(x, z)
+        _check_buf(z, x.shape, x.dtype, x.device, "y2")
     o = torch.empty_like(q) if out is None else _as2d(out)
+    _check_buf(o, q.shape, q.dtype, q.device, "out")
     i = None
     if want_idx:
         i = torch.empty(q.shape, dtype=torch.int32, device=q.device) if idx is None else _as2d(idx)
-        if i.dtype != torch.int32 or not i.is_contiguous():
-            raise ValueError("idx must be contiguous int32")
+        _check_buf(i, q.shape, torch.int32, q.device, "idx")
     rc = _lib.load().spline_build_eval(_p(x), _p(y), n, B, bc, _p(yp1), _p(ypn), _p(z), _p(q), m, _p(o), _p(i),
                                        flags, _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
     _lib.check(rc, "spline_build_eval")
@@ -140,15 +167,15 @@ def build_eval_host(x, y, q, bc: int = BC_NATURAL, yp1=None, ypn=None, flags: in
         t = torch.empty(shape, dtype=dtype)
         return t.pin_memory() if pin else t
 
-    def slope(v):
-        if v is None or isinstance(v, torch.Tensor):
-            return v
-        return torch.full((B,), float(v), dtype=x.dtype)
-
-    yp1, ypn = slope(yp1), slope(ypn)
+    yp1, ypn = _slopes(yp1, B, x, host=True), _slopes(ypn, B, x, host=True)
+    _check_buf(yp1, (B,), x.dtype, None, "yp1", host=True)
+    _check_buf(ypn, (B,), x.dtype, None, "ypn", host=True)
     z = (host_like(x.shape, x.dtype) if y2 is None else _as2d(y2)) if want_y2 else None
     o = host_like(q.shape, q.dtype) if out is None else _as2d(out)
     i = (host_like(q.shape, torch.int32) if idx is None else _as2d(idx)) if want_idx else None
+    _check_buf(z, x.shape, x.dtype, None, "y2", host=True)
+    _check_buf(o, q.shape, q.dtype, None, "out", host=True)
+    _check_buf(i, q.shape, torch.int32, None, "idx", host=True)
     rc = _lib.load().spline_build_eval_host(_p(x), _p(y), n, B, bc, _p(yp1), _p(ypn), _p(z), _p(q), m, _p(o),
                                             _p(i), flags, _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
     _lib.check(rc, "spline_build_eval_host")
@@ -166,8 +193,14 @@ def evaluate_ablation(x, y, y2, q, form: str, out=None, idx=None, stream=None):
     B, n = x.shape
     m = q.shape[1]
     _check_curves(x, y, y2, q)
-    o = torch.empty_like(q) if out is None else out
-    i = torch.empty(q.shape, dtype=torch.int32, device=q.device) if idx is None else idx
+    if y.shape != x.shape or y2.shape != x.shape or q.shape[0] != B:
+        raise ValueError("x, y, y2 must be (B, n) and q (B, m)")
+    if form not in _lib.FORMS:
+        raise ValueError(f"form must be one of {sorted(_lib.FORMS)}")
+    o = torch.empty_like(q) if out is None else _as2d(out)
+    i = torch.empty(q.shape, dtype=torch.int32, device=q.device) if idx is None else _as2d(idx)
+    _check_buf(o, q.shape, q.dtype, q.device, "out")
+    _check_buf(i, q.shape, torch.int32, q.device, "idx")
     rc = _lib.load().spline_eval_ablation(_p(x), _p(y), _p(y2), n, B, _p(q), m, _p(o), _p(i), _lib.FORMS[form],
                                           _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
     _lib.check(rc, "spline_eval_ablation")
@@ -181,8 +214,13 @@ def gather_probe(x, y, y2, q, idx_in, mode: int, out=None, idx=None, stream=None
     B, n = x.shape
     m = q.shape[1]
     _check_curves(x, y, y2, q)
-    o = torch.empty_like(q) if out is None else out
-    i = torch.empty(q.shape, dtype=torch.int32, device=q.device) if idx is None else idx
+    if y.shape != x.shape or y2.shape != x.shape or q.shape[0] != B:
+        raise ValueError("x, y, y2 must be (B, n) and q (B, m)")
+    _check_buf(idx_in, q.shape, torch.int32, q.device, "idx_in")
+    o = torch.empty_like(q) if out is None else _as2d(out)
+    i = torch.empty(q.shape, dtype=torch.int32, device=q.device) if idx is None else _as2d(idx)
+    _check_buf(o, q.shape, q.dtype, q.device, "out")
+    _check_buf(i, q.shape, torch.int32, q.device, "idx")
     rc = _lib.load().spline_gather_probe(_p(x), _p(y), _p(y2), n, B, _p(q), m, _p(idx_in), _p(o), _p(i), mode,
                                          _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
     _lib.check(rc, "spline_gather_probe")
@@ -202,8 +240,25 @@ def spike_workspace(n: int, row_begin: int, row_end: int, dtype, device) -> torc
     return torch.empty(nbytes, dtype=torch.uint8, device=device)
 
 
+def _check_spike(x, y, row_begin, row_end, yp1, ypn, workspace):
+    _check_curves(x, y)
+    if x.dim() != 1 or y.shape != x.shape:
+        raise ValueError("the long-curve seam takes one curve: x, y of shape (n,)")
+    n = x.shape[0]
+    if not (0 <= row_begin < row_end <= n):
+        raise ValueError("need 0 <= row_begin < row_end <= n")
+    _check_buf(yp1, (1,), x.dtype, x.device, "yp1")
+    _check_buf(ypn, (1,), x.dtype, x.device, "ypn")
+    need = _lib.load().spline_spike_workspace_size(n, row_begin, row_end, _DT[x.dtype])
+    if not (isinstance(workspace, torch.Tensor) and workspace.device == x.device and workspace.is_contiguous()
+            and workspace.numel() * workspace.element_size() >= need):
+        raise ValueError(f"workspace must be a contiguous device buffer of >= {need} bytes")
+    return n
+
+
 def spike_reduce(x, y, row_begin: int, row_end: int, bc: int, yp1, ypn, record, workspace, stream=None):
-    n = x.shape[-1]
+    n = _check_spike(x, y, row_begin, row_end, yp1, ypn, workspace)
+    _check_buf(record, (6,), x.dtype, x.device, "record")
     rc = _lib.load().spline_spike_reduce(_p(x), _p(y), n, row_begin, row_end, bc, _p(yp1), _p(ypn), _p(record),
                                          _p(workspace), _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
     _lib.check(rc, "spline_spike_reduce")
@@ -211,7 +266,9 @@ def spike_reduce(x, y, row_begin: int, row_end: int, bc: int, yp1, ypn, record, 
 
 def spike_finish(x, y, row_begin: int, row_end: int, bc: int, yp1, ypn, all_records, nranks: int, rank: int,
                  y2_shard, workspace, stream=None):
-    n = x.shape[-1]
+    n = _check_spike(x, y, row_begin, row_end, yp1, ypn, workspace)
+    _check_buf(all_records, (6 * nranks,), x.dtype, x.device, "all_records")
+    _check_buf(y2_shard, (row_end - row_begin,), x.dtype, x.device, "y2_shard")
     rc = _lib.load().spline_spike_finish(_p(x), _p(y), n, row_begin, row_end, bc, _p(yp1), _p(ypn),
                                          _p(all_records), nranks, rank, _p(y2_shard), _p(workspace),
                                          _DT[x.dtype], ctypes.c_void_p(_stream(stream)))

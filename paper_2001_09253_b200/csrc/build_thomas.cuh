@@ -112,7 +112,7 @@ template <typename T> __device__ __forceinline__ T babe_meet(bool top, T hc, T g
 template <typename T> __device__ __forceinline__ T babe_back(T cb, T db, T yv) { return r_fma(-cb, yv, db); }
 
 template <typename T>
-__device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int bc, T sl, T *dummy, int tid) {
+__device__ __forceinline__ void babe_tile(unsigned *__restrict__ status, T *X, T *Y, int S, int n, int nc, int bc, T sl, T *dummy, int tid) {
   const int t = tid >> 1;  // curve within the tile (tid = thread index within the solving group)
   const bool top = (tid & 1) == 0;
   const bool act = t < nc;         // pairs are lane-adjacent, so shuffles stay in-warp
@@ -178,11 +178,11 @@ __device__ __forceinline__ void babe_tile(T *X, T *Y, int S, int n, int nc, int 
     const T nanv = qnan<T>();
     for (int r = top ? 0 : k + 1; r < (top ? k + 1 : n); ++r) Yc[r] = nanv;
   }
-  raise_status_warp(act && !ok && top, kBadKnots);
+  raise_status_warp(status, act && !ok && top, kBadKnots);
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict__ x, const T *__restrict__ y, int n,
+__global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int n,
                                                              int64_t batch, int bc, const T *__restrict__ yp1,
                                                              const T *__restrict__ ypn, T *__restrict__ y2, int S,
                                                              FastDiv divn) {
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict
   }
   __syncthreads();
 
-  babe_tile(X, Y, S, n, nc, bc, sl, dummy, threadIdx.x);
+  babe_tile(status, X, Y, S, n, nc, bc, sl, dummy, threadIdx.x);
   __syncthreads();
 
   T *y2b = y2 + c0 * n;
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_babe(const T *__restrict
 // stores of tile i.  Requires n*sizeof(T) % 16 == 0 and 16-byte aligned x, y (else
 // k1_thomas_babe).
 template <typename T>
-__global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(const T *__restrict__ x, const T *__restrict__ y, int n,
+__global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int n,
                                                              int64_t batch, int bc, const T *__restrict__ yp1,
                                                              const T *__restrict__ ypn, T *__restrict__ y2, int S,
                                                              int64_t ntiles, FastDiv divn) {
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_thomas_pipe(const T *__restrict
     }
     __syncthreads();
     if (threadIdx.x == 0) issue(it + G);  // raw stage consumed: next tile in flight
-    babe_tile(X, Y, S, n, nc, bc, sl, dummy, threadIdx.x);
+    babe_tile(status, X, Y, S, n, nc, bc, sl, dummy, threadIdx.x);
     __syncthreads();
     T *y2b = y2 + c0 * n;
     for (int e = threadIdx.x * VW; e < tot; e += blockDim.x * VW) {
@@ -382,7 +382,7 @@ __device__ __forceinline__ bool thomas_regs(const T (&xv)[NMAX], const T (&yv)[N
 
 // K1r: one thread per curve, n <= NMAX, all in registers.
 template <typename T, int NMAX>
-__global__ void __launch_bounds__(256) k1_thomas_regs(const T *__restrict__ x, const T *__restrict__ y, int n,
+__global__ void __launch_bounds__(256) k1_thomas_regs(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int n,
                                                       int64_t batch, int bc, const T *__restrict__ yp1,
                                                       const T *__restrict__ ypn, T *__restrict__ y2, int vec) {
   pdl_trigger();
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(256) k1_thomas_regs(const T *__restrict__ x, c
   }
   T z[NMAX];
   const bool ok = thomas_regs<T, NMAX>(xv, yv, n, bc, (bc & 1) ? yp1[c] : T(0), (bc & 2) ? ypn[c] : T(0), z);
-  raise_status_warp(!ok, kBadKnots);
+  raise_status_warp(status, !ok, kBadKnots);
   T *zc = y2 + c * n;
   if (vec) {
     using VT = typename Vec16<T>::V;
@@ -451,7 +451,7 @@ constexpr int kK1hThreads = 128;
 // One lane pair's curve cv (lane parity: top / bottom) -- the body of K1h, also called by the
 // one-CTA build+eval kernel for tiny problems.  Every lane of the warp must call it.
 template <typename T, int N>
-__device__ __forceinline__ void k1h_solve(const T *__restrict__ x, const T *__restrict__ y, int64_t batch, int bc,
+__device__ __forceinline__ void k1h_solve(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int64_t batch, int bc,
                                           const T *__restrict__ yp1, const T *__restrict__ ypn, T *__restrict__ y2,
                                           int64_t cv, bool top) {
   constexpr int K = N / 2;
@@ -522,7 +522,7 @@ __device__ __forceinline__ void k1h_solve(const T *__restrict__ x, const T *__re
 #pragma unroll
     for (int s = 0; s < K; ++s) dpr[s] = qnan<T>();
   }
-  raise_status_warp(act && !ok && top, kBadKnots);
+  raise_status_warp(status, act && !ok && top, kBadKnots);
   if (act) {
     T *zh = y2 + c * N + hoff;
 #pragma unroll
@@ -537,11 +537,11 @@ __device__ __forceinline__ void k1h_solve(const T *__restrict__ x, const T *__re
 }
 
 template <typename T, int N>
-__global__ void __launch_bounds__(kK1hThreads) k1_thomas_half(const T *__restrict__ x, const T *__restrict__ y,
+__global__ void __launch_bounds__(kK1hThreads) k1_thomas_half(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y,
                                                               int64_t batch, int bc, const T *__restrict__ yp1,
                                                               const T *__restrict__ ypn, T *__restrict__ y2) {
   pdl_trigger();
-  k1h_solve<T, N>(x, y, batch, bc, yp1, ypn, y2, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 1,
+  k1h_solve<T, N>(status, x, y, batch, bc, yp1, ypn, y2, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 1,
                   (threadIdx.x & 1) == 0);
 }
 

@@ -125,7 +125,7 @@ template <typename T, int R> __host__ __device__ constexpr size_t tile_smem_byte
 //  FINISH : reads the tile's outer (L, R) from tile_ext[(c*ntiles + t)*2]; writes y2 rows
 //           [P, Q] to y2 + c*(row_end-row_begin) + (P - row_begin).
 template <typename T, int R, int MODE>
-__global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, const T *__restrict__ y, int64_t n,
+__global__ void __launch_bounds__(kTileThreads) k_tile(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int64_t n,
                                                       int64_t row_begin, int64_t row_end, int bc,
                                                       const T *__restrict__ yp1, const T *__restrict__ ypn,
                                                       T *__restrict__ y2, T *__restrict__ tile_rec,
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
       const Rec<T> r = rec[0];
       T *o = tile_rec + (c * ntiles + tile) * 6;
       o[0] = r.Gp; o[1] = r.Vp; o[2] = r.Wp; o[3] = r.Gq; o[4] = r.Vq; o[5] = r.Wq;
-      if (bad) { atomicOr(badflag + c, 1); raise_status(kBadKnots); }
+      if (bad) { atomicOr(badflag + c, 1); raise_status(status, kBadKnots); }
     }
     return;
   }
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(const T *__restrict__ x, 
   T *y2o = (MODE == TILE_FULL) ? y2 + c * n + P : y2 + c * (row_end - row_begin) + (P - row_begin);
   const bool curve_bad = (MODE == TILE_FULL) ? bad : (badflag[c] != 0);
   if (curve_bad) {
-    if (MODE == TILE_FULL && threadIdx.x == 0) raise_status(kBadKnots);
+    if (MODE == TILE_FULL && threadIdx.x == 0) raise_status(status, kBadKnots);
     for (int e = threadIdx.x; e < nrows; e += NT) y2o[e] = qnan<T>();
     return;
   }

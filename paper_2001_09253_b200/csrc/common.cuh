@@ -5,20 +5,19 @@
 
 namespace fs {
 
-// Device-wide data-error word (see spline_status in include/spline.h).  The library is a
-// single translation unit (spline_abi.cu), so the definition lives here.
-__device__ unsigned int g_status = 0;
-
+// Data-error bits (see spline_status in include/spline.h).  Every kernel receives the
+// launching stream's status word (`status`, a device pointer chosen by the host per stream),
+// so bits raised on one stream never reach another stream's spline_status.
 constexpr unsigned kBadKnots = 1u;
 constexpr unsigned kOutOfRange = 2u;
 
-__device__ __forceinline__ void raise_status(unsigned bits) { atomicOr(&g_status, bits); }
+__device__ __forceinline__ void raise_status(unsigned *status, unsigned bits) { atomicOr(status, bits); }
 
 // Warp-aggregated status raise: one atomic per warp at most.
-__device__ __forceinline__ void raise_status_warp(bool pred, unsigned bits) {
+__device__ __forceinline__ void raise_status_warp(unsigned *status, bool pred, unsigned bits) {
   unsigned mask = __activemask();
   unsigned any = __ballot_sync(mask, pred);
-  if (any && (threadIdx.x & 31) == (__ffs(mask) - 1)) atomicOr(&g_status, bits);
+  if (any && (threadIdx.x & 31) == (__ffs(mask) - 1)) atomicOr(status, bits);
 }
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }

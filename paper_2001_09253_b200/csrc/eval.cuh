@@ -365,7 +365,7 @@ __device__ __forceinline__ bool eval_item_queries(const T *Qs, const T *__restri
 // queries (one curve per group: m % V == 0 when V > 1).
 template <typename T, int MODE, int V, bool BULK, int L2>
 __global__ void __launch_bounds__(kEvalThreads, 3)
-    k_eval_staged(const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ y2, int n, int64_t batch,
+    k_eval_staged(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ y2, int n, int64_t batch,
                   const T *__restrict__ q, int m, T *__restrict__ out, int32_t *__restrict__ idx, int cpb,
                   int nchunks, int qchunk, int qmax, int64_t nitems, FastDiv divn, FastDiv divm) {
   pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
     if (threadIdx.x == 0) issue(it + 2 * G, s);
     s ^= 1;
   }
-  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
+  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(status, kOutOfRange);
 }
 
 // Persistent staged eval with per-warp curve ownership (cpb a multiple of the warp count, 16-
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
 // by up to one item and the pack of one warp overlaps the evaluation of another.
 template <typename T, int MODE, int L2>
 __global__ void __launch_bounds__(kEvalThreads, 3)
-    k_eval_warps(const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ y2, int n, int64_t batch,
+    k_eval_warps(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, const T *__restrict__ y2, int n, int64_t batch,
                  const T *__restrict__ q, int m, T *__restrict__ out, int32_t *__restrict__ idx, int cpb,
                  int64_t nitems, FastDiv divn, FastDiv divm) {
   pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kEvalThreads, 3)
       issue(it + 2 * G, s);
     }
   }
-  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
+  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(status, kOutOfRange);
 }
 
 // ---- one warp per curve, no staging pass (n <= 64, unsorted queries: BASELINE cfg2) -----
@@ -566,7 +566,7 @@ template <typename T> struct CwTable {
 };
 
 template <typename T, int L2>
-__global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(const T *__restrict__ x, const T *__restrict__ y,
+__global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y,
                                                                      const T *__restrict__ y2, int n, int64_t batch,
                                                                      const T *__restrict__ q, int m,
                                                                      T *__restrict__ out, int32_t *__restrict__ idx) {
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(const T *__
     }
     __syncwarp();  // the table is rebuilt for the next curve
   }
-  raise_status_warp(oor, kOutOfRange);
+  raise_status_warp(status, oor, kOutOfRange);
 }
 
 // ---- tiny problems (a few K1h-sized curves: BASELINE cfg1) -------------------------------
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(const T *__
 // every thread evaluates its queries with eval_packed -- one launch, no TMA pipeline, no
 // warp-specialised hand-off.  The queries' first vectors load at kernel entry.
 template <typename T, int N, int L2>
-__global__ void __launch_bounds__(256) k_build_eval_tiny(const T *__restrict__ x, const T *__restrict__ y,
+__global__ void __launch_bounds__(256) k_build_eval_tiny(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y,
                                                          int64_t batch, int bc, const T *__restrict__ yp1,
                                                          const T *__restrict__ ypn, T *__restrict__ y2,
                                                          const T *__restrict__ q, int m, T *__restrict__ out,
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(256) k_build_eval_tiny(const T *__restrict__ x
   const int nv = m / VW;
   VT q0;
   if (tid < nv) q0 = __ldcs(reinterpret_cast<const VT *>(qc) + tid);
-  if (tid < 32) k1h_solve<T, N>(x, y, batch, bc, yp1, ypn, y2, (lane < 2) ? c : batch, (lane & 1) == 0);
+  if (tid < 32) k1h_solve<T, N>(status, x, y, batch, bc, yp1, ypn, y2, (lane < 2) ? c : batch, (lane & 1) == 0);
   __syncthreads();  // y2 of the curve is in memory
   const T *X = x + c * N, *Y = y + c * N, *Z = y2 + c * N;
   if (tid < N) tb.xk[tid] = X[tid];
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(256) k_build_eval_tiny(const T *__restrict__ x
     VecIO<T, VW>::store(out + c * m + (size_t)v * VW, val);
     if (idx) VecIO<T, VW>::store_idx(idx + c * m + (size_t)v * VW, jj);
   }
-  raise_status_warp(oor, kOutOfRange);
+  raise_status_warp(status, oor, kOutOfRange);
 }
 
 // ---- very short curves, few queries (fp32, n <= 8, m <= 32: BASELINE cfg3) -----------------
@@ -723,7 +723,7 @@ struct alignas(16) SmallCurve {  // 208 B: 52 words, so the 4 curves of a warp a
 // thomas_regs on the same registers, so y2 is bitwise K1r's -- stores y2 (when y2w is
 // non-null) and builds the records from registers: x, y are read once and y2 is never read back.
 template <bool SOLVE>
-__global__ void __launch_bounds__(kSmallWarps * 32, SOLVE ? 4 : 6) k_eval_small(const float *__restrict__ x,
+__global__ void __launch_bounds__(kSmallWarps * 32, SOLVE ? 4 : 6) k_eval_small(unsigned *__restrict__ status, const float *__restrict__ x,
                                                                  const float *__restrict__ y,
                                                                  const float *__restrict__ y2, int n, int64_t batch,
                                                                  const float *__restrict__ q, int m,
@@ -732,7 +732,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SOLVE ? 4 : 6) k_eval_small(
                                                                  const float *__restrict__ yp1 = nullptr,
                                                                  const float *__restrict__ ypn = nullptr,
                                                                  float *__restrict__ y2w = nullptr) {
-  if constexpr (!SOLVE) pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
+  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch; SOLVE too: its
+              // launch carries the attribute, and its outputs must not race the predecessor)
   constexpr int MV = kSmallM;  // at most m vectors per lane (32 curves x m queries / (32 lanes x 4))
   __shared__ SmallCurve tab[kSmallWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -772,7 +773,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SOLVE ? 4 : 6) k_eval_small(
       }
       if constexpr (SOLVE) {  // K1r's sweep (build_thomas.cuh thomas_regs), then y2 out
         const bool ok = thomas_regs<float, kSmallN>(xv, yv, n, bc, (bc & 1) ? yp1[c] : 0.f, (bc & 2) ? ypn[c] : 0.f, zv);
-        if (!ok) raise_status(kBadKnots);
+        if (!ok) raise_status(status, kBadKnots);
         if (y2w) {
           if (vecn) {
             reinterpret_cast<float4 *>(y2w + c * 8)[0] = make_float4(zv[0], zv[1], zv[2], zv[3]);
@@ -838,7 +839,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SOLVE ? 4 : 6) k_eval_small(
     }
     __syncwarp();  // the table is rebuilt for the next tile
   }
-  raise_status_warp(oor, kOutOfRange);
+  raise_status_warp(status, oor, kOutOfRange);
 }
 
 // ---- sorted query runs ------------------------------------------------------------------
@@ -888,7 +889,7 @@ template <typename T> struct SortWin {
 };
 
 template <typename T, int V, int FORM = FORM_RECORD, bool WIN = false>
-__global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x, const T *__restrict__ y,
+__global__ void __launch_bounds__(256, 4) k_eval_sorted(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y,
                                                        const T *__restrict__ y2, int n, const T *__restrict__ q,
                                                        int64_t m, T *__restrict__ out, int32_t *__restrict__ idx,
                                                        int64_t qrun, int64_t runs_per_curve, int64_t ntasks) {
@@ -1015,7 +1016,7 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(const T *__restrict__ x,
 #pragma unroll
     for (int i = 0; i < V; ++i) qa[i] = qn[i];
   }
-  raise_status_warp(oor, kOutOfRange);
+  raise_status_warp(status, oor, kOutOfRange);
 }
 
 // ---- long curves through interval records in HBM ---------------------------------------
@@ -1108,7 +1109,7 @@ __global__ void __launch_bounds__(256) k_pack_records(const T *__restrict__ x, c
 // one record; if x_g <= q < x_{g+1} fails (jitter, or a non-uniform grid) the neighbour on the
 // indicated side, then a bisection over the records' x_j (any grid: never a wrong idx).
 template <typename T>
-__global__ void __launch_bounds__(256) k_eval_records(const Ival<T> *__restrict__ R, const CurveHdr<T> *__restrict__ H,
+__global__ void __launch_bounds__(256) k_eval_records(unsigned *__restrict__ status, const Ival<T> *__restrict__ R, const CurveHdr<T> *__restrict__ H,
                                                       int n, int64_t batch, const T *__restrict__ q, int64_t m,
                                                       T *__restrict__ out, int32_t *__restrict__ idx) {
   constexpr int U = 4;
@@ -1167,7 +1168,7 @@ __global__ void __launch_bounds__(256) k_eval_records(const Ival<T> *__restrict_
       oor |= !in[u];
     }
   }
-  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
+  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(status, kOutOfRange);
 }
 
 // ---- diagnostics: the random-gather ceiling of the long-curve evaluation ---
@@ -1206,7 +1207,7 @@ __global__ void __launch_bounds__(256) k_probe_rec(const Ival<T> *__restrict__ R
 // (q - x_0)(n-1)/(x_{n-1} - x_0) is exact up to +-1 interval on near-uniform grids; any
 // other outcome falls back to galloping + bisection (correct for every grid).
 template <typename T>
-__global__ void __launch_bounds__(256) k_eval_global(const T *__restrict__ x, const T *__restrict__ y,
+__global__ void __launch_bounds__(256) k_eval_global(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y,
                                                      const T *__restrict__ y2, int n, int64_t batch,
                                                      const T *__restrict__ q, int64_t m, T *__restrict__ out,
                                                      int32_t *__restrict__ idx) {
@@ -1273,7 +1274,7 @@ __global__ void __launch_bounds__(256) k_eval_global(const T *__restrict__ x, co
       if (idx) st_stream(idx + k, (int32_t)j);
     }
   }
-  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
+  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(status, kOutOfRange);
 }
 
 template <typename T>

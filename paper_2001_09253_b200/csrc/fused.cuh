@@ -89,7 +89,7 @@ template <typename T> struct FusedLayout {
 
 // Solver warp, SOLVE_BABE: curves [0, nc) of the item in passes of 16 (2 lanes each).
 template <typename T>
-__device__ __forceinline__ void fused_solve_babe(const T *Xr, const T *Yr, T *Yt, T *scr, int S, int n, int nc,
+__device__ __forceinline__ void fused_solve_babe(unsigned *__restrict__ status, const T *Xr, const T *Yr, T *Yt, T *scr, int S, int n, int nc,
                                                  int64_t c0, int bc, const T *__restrict__ yp1,
                                                  const T *__restrict__ ypn, T *__restrict__ y2, FastDiv divn,
                                                  int lane, int sw, int nsw) {
@@ -114,7 +114,7 @@ __device__ __forceinline__ void fused_solve_babe(const T *Xr, const T *Yr, T *Yt
       }
     }
     __syncwarp();
-    babe_tile(Xs, Yp, S, n, np, bc, sl, dummy, lane);
+    babe_tile(status, Xs, Yp, S, n, np, bc, sl, dummy, lane);
     __syncwarp();
     if (y2) {
       T *yb = y2 + (c0 + p0) * n;
@@ -134,7 +134,7 @@ __device__ __forceinline__ void fused_solve_babe(const T *Xr, const T *Yr, T *Yt
 // Solver warp, SOLVE_REGS (n <= 8, n * sizeof(T) % 16 == 0): one lane per curve, the
 // paper's sweep in registers (thomas_regs).
 template <typename T>
-__device__ __forceinline__ void fused_solve_regs(const T *Xr, const T *Yr, T *Yt, int n, int nc, int64_t c0, int bc,
+__device__ __forceinline__ void fused_solve_regs(unsigned *__restrict__ status, const T *Xr, const T *Yr, T *Yt, int n, int nc, int64_t c0, int bc,
                                                  const T *__restrict__ yp1, const T *__restrict__ ypn,
                                                  T *__restrict__ y2, int lane, int sw, int nsw) {
   constexpr int VW = 16 / sizeof(T);
@@ -173,7 +173,7 @@ __device__ __forceinline__ void fused_solve_regs(const T *Xr, const T *Yr, T *Yt
         }
       }
     }
-    raise_status_warp(!ok, kBadKnots);
+    raise_status_warp(status, !ok, kBadKnots);
   }
 }
 
@@ -186,7 +186,7 @@ __device__ __forceinline__ void fused_solve_regs(const T *Xr, const T *Yr, T *Yt
 // the hand-offs are named barriers.
 template <typename T, int MODE, int L2, int SOLVE, bool WOWN>
 __global__ void __launch_bounds__(fused_threads(WOWN), WOWN ? 2 : 3)
-    k_fused_staged(const T *__restrict__ x, const T *__restrict__ y, int n, int64_t batch, int bc,
+    k_fused_staged(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int n, int64_t batch, int bc,
                    const T *__restrict__ yp1, const T *__restrict__ ypn, T *__restrict__ y2, const T *__restrict__ q,
                    int m, T *__restrict__ out, int32_t *__restrict__ idx, int cpb, int nchunks, int qchunk, int qmax,
                    int64_t nitems, FastDiv divn, FastDiv divm) {
@@ -295,10 +295,10 @@ __global__ void __launch_bounds__(fused_threads(WOWN), WOWN ? 2 : 3)
       const T *Yr = Xr + cn;
       T *y2o = (y2 && (cpb > 1 || it % nchunks == 0)) ? y2 : nullptr;  // chunk 0 writes y2
       if constexpr (SOLVE == SOLVE_BABE)
-        fused_solve_babe<T>(Xr, Yr, ytile(ks), reinterpret_cast<T *>(smem_raw + L.scratch + sw * L.scrstep), S2, n,
+        fused_solve_babe<T>(status, Xr, Yr, ytile(ks), reinterpret_cast<T *>(smem_raw + L.scratch + sw * L.scrstep), S2, n,
                             nc, c0, bc, yp1, ypn, y2o, divn, lane, 0, 1);
       else
-        fused_solve_regs<T>(Xr, Yr, ytile(ks), n, nc, c0, bc, yp1, ypn, y2o, lane, 0, 1);
+        fused_solve_regs<T>(status, Xr, Yr, ytile(ks), n, nc, c0, bc, yp1, ypn, y2o, lane, 0, 1);
       __syncwarp();
       if constexpr (WOWN) {
         if (lane == 0) mbar_arrive(tfull + ks);
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(fused_threads(WOWN), WOWN ? 2 : 3)
       if (threadIdx.x == 0) issue_queries(it + kQueryStages * G, qs);
     }
   }
-  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(kOutOfRange);
+  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(status, kOutOfRange);
 }
 
 }  // namespace fs

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <unordered_map>
 
 #include "../../include/spline.h"
 #include "build_thomas.cuh"
@@ -90,6 +91,46 @@ inline int ws_alloc(void **p, size_t bytes, cudaStream_t st) {
   }
   return cuda_rc(cudaMallocFromPoolAsync(p, bytes, pools[dev], st));
 }
+// Per-stream data-error words (spline_status).  Each device has a slab of kStatusSlots words;
+// a stream handle is given its own slot the first time it is seen (slot 0 is the shared
+// overflow slot once all are taken).  Every kernel receives its launching call's word, so bits
+// raised on one stream are read and cleared by spline_status on that stream only.
+constexpr int kStatusSlots = 4096;
+struct StatusSlab {
+  unsigned *words = nullptr;
+  std::unordered_map<uintptr_t, int> slot;
+  int next = 1;
+};
+inline unsigned *status_word(cudaStream_t st) {
+  static std::mutex mu;
+  static StatusSlab slabs[128];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 128) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  StatusSlab &s = slabs[dev];
+  if (!s.words) {
+    unsigned *w = nullptr;
+    if (cudaMalloc(&w, sizeof(unsigned) * kStatusSlots) != cudaSuccess) return nullptr;
+    if (cudaMemset(w, 0, sizeof(unsigned) * kStatusSlots) != cudaSuccess) return nullptr;
+    s.words = w;
+  }
+  const uintptr_t key = (uintptr_t)st;
+  auto it = s.slot.find(key);
+  int k = 0;
+  if (it != s.slot.end()) k = it->second;
+  else if (s.next < kStatusSlots) s.slot.emplace(key, k = s.next++);
+  return s.words + k;
+}
+// The word of the API call being enqueued on this host thread (set by StatusScope in every
+// entry point; the launch helpers below pass it to their kernels).
+thread_local unsigned *tl_status = nullptr;
+struct StatusScope {
+  unsigned *prev;
+  explicit StatusScope(cudaStream_t st) : prev(tl_status) { tl_status = status_word(st); }
+  ~StatusScope() { tl_status = prev; }
+  bool ok() const { return tl_status != nullptr; }
+};
+
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 inline int num_sms() {
   static int sms = 0;
@@ -111,7 +152,7 @@ int launch_tile_full(const T *x, const T *y, int64_t n, int64_t batch, int bc, c
   auto kern = k_tile<T, R, TILE_FULL>;
   const size_t sm = tile_smem_bytes<T, R>();
   if (int rc = set_smem(kern, sm)) return rc;
-  kern<<<(unsigned)batch, kTileThreads, sm, st>>>(x, y, n, 0, n, bc, yp1, ypn, y2, nullptr, nullptr, nullptr, 1);
+  kern<<<(unsigned)batch, kTileThreads, sm, st>>>(tl_status, x, y, n, 0, n, bc, yp1, ypn, y2, nullptr, nullptr, nullptr, 1);
   return launch_rc();
 }
 
@@ -185,7 +226,7 @@ int launch_tile_part(const T *x, const T *y, int64_t n, int64_t rb, int64_t re, 
   const size_t sm = tile_smem_bytes<T, R>();
   if (int rc = set_smem(kern, sm)) return rc;
   if (ntiles * batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
-  kern<<<(unsigned)(ntiles * batch), kTileThreads, sm, st>>>(x, y, n, rb, re, bc, yp1, ypn, y2, (T *)w.tile_rec,
+  kern<<<(unsigned)(ntiles * batch), kTileThreads, sm, st>>>(tl_status, x, y, n, rb, re, bc, yp1, ypn, y2, (T *)w.tile_rec,
                                                              (const T *)w.tile_ext, (int *)w.badflag, (int)ntiles);
   return launch_rc();
 }
@@ -221,7 +262,7 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
     constexpr int VW = 16 / sizeof(T);
     const int vec = (n % VW == 0) && aligned16(x) && aligned16(y) && aligned16(y2);
     const int64_t grid = (batch + 255) / 256;
-    k1_thomas_regs<T, kRegsNMax><<<(unsigned)grid, 256, 0, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, vec);
+    k1_thomas_regs<T, kRegsNMax><<<(unsigned)grid, 256, 0, st>>>(tl_status, x, y, (int)n, batch, bc, yp1, ypn, y2, vec);
     return launch_rc();
   }
   if (n <= kK1MaxN) {  // K1: two threads per curve, staged odd-stride tiles
@@ -231,13 +272,13 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
       const unsigned grid = (unsigned)((2 * batch + kK1hThreads - 1) / kK1hThreads);
       if constexpr (sizeof(T) == 4) {
         if (n == 64 || n == 32) {
-          if (n == 64) k1_thomas_half<T, 64><<<grid, kK1hThreads, 0, st>>>(x, y, batch, bc, yp1, ypn, y2);
-          else k1_thomas_half<T, 32><<<grid, kK1hThreads, 0, st>>>(x, y, batch, bc, yp1, ypn, y2);
+          if (n == 64) k1_thomas_half<T, 64><<<grid, kK1hThreads, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, y2);
+          else k1_thomas_half<T, 32><<<grid, kK1hThreads, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, y2);
           return launch_rc();
         }
       }
       if (n == 16) {
-        k1_thomas_half<T, 16><<<grid, kK1hThreads, 0, st>>>(x, y, batch, bc, yp1, ypn, y2);
+        k1_thomas_half<T, 16><<<grid, kK1hThreads, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, y2);
         return launch_rc();
       }
     }
@@ -256,7 +297,7 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 2 * cpb, sm) != cudaSuccess || occ < 1) occ = 1;
       const int64_t ntiles = (batch + cpb - 1) / cpb;
       const int64_t grid = std::min<int64_t>(ntiles, (int64_t)occ * num_sms());
-      kern<<<(unsigned)grid, 2 * cpb, sm, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, S, ntiles,
+      kern<<<(unsigned)grid, 2 * cpb, sm, st>>>(tl_status, x, y, (int)n, batch, bc, yp1, ypn, y2, S, ntiles,
                                                  FastDiv((uint32_t)n));
       return launch_rc();
     }
@@ -266,7 +307,7 @@ int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *y
     auto kern = k1_thomas_babe<T>;
     if (int rc = set_smem(kern, sm)) return rc;
     const int64_t grid = (batch + cpb - 1) / cpb;
-    kern<<<(unsigned)grid, 2 * cpb, sm, st>>>(x, y, (int)n, batch, bc, yp1, ypn, y2, S, FastDiv((uint32_t)n));
+    kern<<<(unsigned)grid, 2 * cpb, sm, st>>>(tl_status, x, y, (int)n, batch, bc, yp1, ypn, y2, S, FastDiv((uint32_t)n));
     return launch_rc();
   }
   if (n <= 256 * rmax<T>()) return build_mid<T>(x, y, n, batch, bc, yp1, ypn, y2, st);
@@ -300,7 +341,7 @@ int launch_staged_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, sm) != cudaSuccess || occ < 1) occ = 1;
   const int64_t grid = std::min<int64_t>(nitems, (int64_t)occ * num_sms());
-  return launch_pdl(kern, dim3((unsigned)grid), dim3(kEvalThreads), sm, st, x, y, y2, n, batch, q, (int)m, out, idx,
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kEvalThreads), sm, st, tl_status, x, y, y2, n, batch, q, (int)m, out, idx,
                     cpb, nchunks, qchunk, qmax, nitems, FastDiv((uint32_t)n), FastDiv((uint32_t)m));
 }
 
@@ -327,7 +368,7 @@ int launch_warps_k(const T *x, const T *y, const T *y2, int n, int64_t batch, co
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEvalThreads, sm) != cudaSuccess || occ < 1) occ = 1;
     const int64_t grid = std::min<int64_t>(nitems, (int64_t)occ * num_sms());
-    return launch_pdl(kern, dim3((unsigned)grid), dim3(kEvalThreads), sm, st, x, y, y2, n, batch, q, (int)m, out,
+    return launch_pdl(kern, dim3((unsigned)grid), dim3(kEvalThreads), sm, st, tl_status, x, y, y2, n, batch, q, (int)m, out,
                       idx, cpb, nitems, FastDiv((uint32_t)n), FastDiv((uint32_t)m));
   }
 }
@@ -388,9 +429,9 @@ int launch_sorted_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
   const int64_t ntasks = batch * rpc;
   const int64_t grid = (ntasks + 7) / 8;
   if (FORM == FORM_RECORD && m >= (int64_t)kSortWinDensity * (n - 1))  // dense: the record window pays
-    return launch_pdl(k_eval_sorted<T, V, FORM_RECORD, true>, dim3((unsigned)grid), dim3(256), 0, st, x, y, y2, n, q,
+    return launch_pdl(k_eval_sorted<T, V, FORM_RECORD, true>, dim3((unsigned)grid), dim3(256), 0, st, tl_status, x, y, y2, n, q,
                       m, out, idx, qrun, rpc, ntasks);
-  return launch_pdl(k_eval_sorted<T, V, FORM>, dim3((unsigned)grid), dim3(256), 0, st, x, y, y2, n, q, m, out, idx,
+  return launch_pdl(k_eval_sorted<T, V, FORM>, dim3((unsigned)grid), dim3(256), 0, st, tl_status, x, y, y2, n, q, m, out, idx,
                     qrun, rpc, ntasks);
 }
 
@@ -401,7 +442,7 @@ int launch_curvewarp_k(const T *x, const T *y, const T *y2, int n, int64_t batch
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCwWarps * 32, 0) != cudaSuccess || occ < 1) occ = 1;
   const int64_t grid = std::min<int64_t>((batch + kCwWarps - 1) / kCwWarps, (int64_t)occ * num_sms());
-  return launch_pdl(kern, dim3((unsigned)grid), dim3(kCwWarps * 32), 0, st, x, y, y2, n, batch, q, m, out, idx);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kCwWarps * 32), 0, st, tl_status, x, y, y2, n, batch, q, m, out, idx);
 }
 template <typename T>
 int launch_curvewarp(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int m, T *out,
@@ -435,7 +476,7 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
           occ < 1)
         occ = 1;
       const int64_t grid = std::min<int64_t>((ntiles + kSmallWarps - 1) / kSmallWarps, (int64_t)occ * num_sms());
-      return launch_pdl(k_eval_small<false>, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, x, y, y2, (int)n,
+      return launch_pdl(k_eval_small<false>, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, tl_status, x, y, y2, (int)n,
                         batch, q, (int)m, out, idx, vecn, 0, (const float *)nullptr, (const float *)nullptr,
                         (float *)nullptr);
     }
@@ -472,7 +513,7 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
     int rc = launch_pdl(k_pack_records<T>, dim3((unsigned)pg), dim3(256), 0, st, x, y, y2, (int)n, batch, R, H);
     if (!rc) {
       const int64_t grid = std::min<int64_t>((total + 1023) / 1024, (int64_t)num_sms() * 16);
-      k_eval_records<T><<<(unsigned)grid, 256, 0, st>>>(R, H, (int)n, batch, q, m, out, idx);
+      k_eval_records<T><<<(unsigned)grid, 256, 0, st>>>(tl_status, R, H, (int)n, batch, q, m, out, idx);
       rc = launch_rc();
     }
     cudaFreeAsync(ws, st);
@@ -480,7 +521,7 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
   }
   cudaGetLastError();  // clear the failed allocation
   const int64_t grid = std::min<int64_t>((total + 1023) / 1024, 148 * 16);
-  k_eval_global<T><<<(unsigned)grid, 256, 0, st>>>(x, y, y2, (int)n, batch, q, m, out, idx);
+  k_eval_global<T><<<(unsigned)grid, 256, 0, st>>>(tl_status, x, y, y2, (int)n, batch, q, m, out, idx);
   return launch_rc();
 }
 
@@ -515,7 +556,7 @@ int launch_fused_k(const T *x, const T *y, int n, int64_t batch, int bc, const T
     constexpr int NT = fused_threads(WOWN);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, sm) != cudaSuccess || occ < 1) occ = 1;
     const int64_t grid = std::min<int64_t>(nitems, (int64_t)occ * num_sms());
-    kern<<<(unsigned)grid, NT, sm, st>>>(x, y, n, batch, bc, yp1, ypn, y2, q, (int)m, out, idx, cpb, nchunks,
+    kern<<<(unsigned)grid, NT, sm, st>>>(tl_status, x, y, n, batch, bc, yp1, ypn, y2, q, (int)m, out, idx, cpb, nchunks,
                                                    qchunk, qmax, nitems, FastDiv((uint32_t)n), FastDiv((uint32_t)m));
     return launch_rc();
   }
@@ -590,7 +631,7 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
           occ < 1)
         occ = 1;
       const int64_t grid = std::min<int64_t>((ntiles + kSmallWarps - 1) / kSmallWarps, (int64_t)occ * num_sms());
-      return launch_pdl(k_eval_small<true>, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, x, y,
+      return launch_pdl(k_eval_small<true>, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, tl_status, x, y,
                         (const float *)nullptr, (int)n, batch, q, (int)m, out, idx, vecn, bc, yp1, ypn, y2);
     }
   }
@@ -605,10 +646,10 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
         if (int rc = ws_alloc((void **)&yy, sizeof(T) * (size_t)n * batch, st)) return rc;
       }
       const unsigned g = (unsigned)batch;
-      if (n == 16) k_build_eval_tiny<T, 16, 4><<<g, 256, 0, st>>>(x, y, batch, bc, yp1, ypn, yy, q, (int)m, out, idx);
+      if (n == 16) k_build_eval_tiny<T, 16, 4><<<g, 256, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, yy, q, (int)m, out, idx);
       if constexpr (sizeof(T) == 4) {
-        if (n == 32) k_build_eval_tiny<T, 32, 5><<<g, 256, 0, st>>>(x, y, batch, bc, yp1, ypn, yy, q, (int)m, out, idx);
-        if (n == 64) k_build_eval_tiny<T, 64, 6><<<g, 256, 0, st>>>(x, y, batch, bc, yp1, ypn, yy, q, (int)m, out, idx);
+        if (n == 32) k_build_eval_tiny<T, 32, 5><<<g, 256, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, yy, q, (int)m, out, idx);
+        if (n == 64) k_build_eval_tiny<T, 64, 6><<<g, 256, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, yy, q, (int)m, out, idx);
       }
       const int rc = launch_rc();
       if (!y2) cudaFreeAsync(yy, st);
@@ -647,8 +688,6 @@ constexpr size_t kHostChunkBytes = 32u << 20;  // target copy traffic per chunk
 
 struct HostStreams {
   cudaStream_t s[kHostStreams];
-  cudaEvent_t done[kHostStreams];
-  cudaEvent_t start;
 };
 inline int host_streams(HostStreams **out) {
   static std::mutex mu;
@@ -659,16 +698,34 @@ inline int host_streams(HostStreams **out) {
   std::lock_guard<std::mutex> lk(mu);
   if (!per_dev[dev]) {
     auto *h = new HostStreams;
-    for (int i = 0; i < kHostStreams; ++i) {
+    for (int i = 0; i < kHostStreams; ++i)
       if (int rc = cuda_rc(cudaStreamCreateWithFlags(&h->s[i], cudaStreamNonBlocking))) return rc;
-      if (int rc = cuda_rc(cudaEventCreateWithFlags(&h->done[i], cudaEventDisableTiming))) return rc;
-    }
-    if (int rc = cuda_rc(cudaEventCreateWithFlags(&h->start, cudaEventDisableTiming))) return rc;
     per_dev[dev] = h;
   }
   *out = per_dev[dev];
   return SPLINE_OK;
 }
+// The events of ONE host call (never shared between calls, so concurrent calls from several
+// threads cannot re-record each other's start/done points).  Destroyed at the end of the call:
+// CUDA releases an event still pending on the device once it completes.
+struct CallEvents {
+  cudaEvent_t start = nullptr, ready = nullptr, done[kHostStreams] = {};
+  int init() {
+    int rc = cuda_rc(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    for (int k = 0; !rc && k < kHostStreams; ++k) rc = cuda_rc(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+    return rc;
+  }
+  ~CallEvents() {
+    if (start) cudaEventDestroy(start);
+    if (ready) cudaEventDestroy(ready);
+    for (int k = 0; k < kHostStreams; ++k)
+      if (done[k]) cudaEventDestroy(done[k]);
+  }
+};
+// Device bytes one chunk slot may take (3 slots in flight): caps the curves per chunk for very
+// long curves / many queries, whatever the SM floor asks for.
+constexpr size_t kMaxSlotBytes = size_t(4) << 30;
 
 // One long curve with many queries: the knots go up and the build runs first (every query
 // needs the whole y2), then the queries flow in chunks through the internal streams (each
@@ -677,6 +734,8 @@ inline int host_streams(HostStreams **out) {
 template <typename T>
 int build_eval_host_one_t(const T *x, const T *y, int64_t n, int bc, const T *yp1, const T *ypn, T *y2, const T *q,
                           int64_t m, T *out, int32_t *idx, int flags, cudaStream_t st, HostStreams *hs) {
+  CallEvents ev;
+  if (int rc = ev.init()) return rc;
   const size_t s = sizeof(T);
   const int64_t K = std::max<int64_t>(2, std::min<int64_t>(8, (int64_t)(((size_t)m * (2 * s + 4)) / (256u << 20))));
   const int64_t QC = (m + K - 1) / K;
@@ -688,16 +747,16 @@ int build_eval_host_one_t(const T *x, const T *y, int64_t n, int bc, const T *yp
   T *dx = (T *)base, *dy = (T *)(base + bx), *dz = (T *)(base + 2 * bx);
   T *ds1 = (T *)(base + 3 * bx), *ds2 = (T *)(base + 3 * bx + bs);
   char *sb = base + 3 * bx + 2 * bs;
-  int rc = cuda_rc(cudaEventRecord(hs->start, st));
+  int rc = cuda_rc(cudaEventRecord(ev.start, st));
   cudaStream_t s0 = hs->s[0];
-  if (!rc) rc = cuda_rc(cudaStreamWaitEvent(s0, hs->start, 0));
+  if (!rc) rc = cuda_rc(cudaStreamWaitEvent(s0, ev.start, 0));
   if (!rc) rc = cuda_rc(cudaMemcpyAsync(dx, x, s * n, cudaMemcpyHostToDevice, s0));
   if (!rc) rc = cuda_rc(cudaMemcpyAsync(dy, y, s * n, cudaMemcpyHostToDevice, s0));
   if (!rc && (bc & 1)) rc = cuda_rc(cudaMemcpyAsync(ds1, yp1, s, cudaMemcpyHostToDevice, s0));
   if (!rc && (bc & 2)) rc = cuda_rc(cudaMemcpyAsync(ds2, ypn, s, cudaMemcpyHostToDevice, s0));
   if (!rc) rc = build_t<T>(dx, dy, n, 1, bc, (bc & 1) ? ds1 : nullptr, (bc & 2) ? ds2 : nullptr, dz, s0);
-  if (!rc) rc = cuda_rc(cudaEventRecord(hs->done[0], s0));  // y2 ready
-  for (int k = 1; !rc && k < kHostStreams; ++k) rc = cuda_rc(cudaStreamWaitEvent(hs->s[k], hs->done[0], 0));
+  if (!rc) rc = cuda_rc(cudaEventRecord(ev.ready, s0));  // y2 ready
+  for (int k = 1; !rc && k < kHostStreams; ++k) rc = cuda_rc(cudaStreamWaitEvent(hs->s[k], ev.ready, 0));
   if (!rc && y2) rc = cuda_rc(cudaMemcpyAsync(y2, dz, s * n, cudaMemcpyDeviceToHost, s0));
   const int fl = flags & (SPLINE_Q_SORTED | SPLINE_X_UNIFORM);
   for (int64_t i = 0; !rc && i < K; ++i) {
@@ -714,8 +773,8 @@ int build_eval_host_one_t(const T *x, const T *y, int64_t n, int bc, const T *yp
     if (!rc && idx) rc = cuda_rc(cudaMemcpyAsync(idx + k0, didx, 4 * (size_t)mc, cudaMemcpyDeviceToHost, ss));
   }
   for (int k = 0; k < kHostStreams; ++k) {
-    cudaEventRecord(hs->done[k], hs->s[k]);
-    cudaStreamWaitEvent(st, hs->done[k], 0);
+    cudaEventRecord(ev.done[k], hs->s[k]);
+    cudaStreamWaitEvent(st, ev.done[k], 0);
   }
   cudaFreeAsync(base, st);
   return rc;
@@ -733,6 +792,7 @@ int build_eval_host_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, 
   const size_t per_curve = s * (3 * (size_t)n + 2 * (size_t)m + 2) + 4 * (size_t)m;  // device bytes per curve
   int64_t C = std::max<int64_t>(1, (int64_t)(kHostChunkBytes / per_curve));
   C = std::max<int64_t>(C, 2 * (int64_t)num_sms());            // keep every chunk GPU-wide
+  C = std::min<int64_t>(C, std::max<int64_t>(1, (int64_t)(kMaxSlotBytes / per_curve)));  // within memory
   C = std::min<int64_t>(C, (batch + kHostStreams - 1) / kHostStreams);  // and at least kHostStreams chunks
   C = std::max<int64_t>(1, std::min<int64_t>(C, batch));
   const int64_t nchunk = (batch + C - 1) / C;
@@ -745,8 +805,13 @@ int build_eval_host_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, 
   const size_t slot = 3 * bx + 2 * bq + bi + 2 * bs;
   char *base = nullptr;
   if (int rc = ws_alloc((void **)&base, slot * nslot, st)) return rc;
-  int rc = cuda_rc(cudaEventRecord(hs->start, st));
-  for (int k = 0; !rc && k < nslot; ++k) rc = cuda_rc(cudaStreamWaitEvent(hs->s[k], hs->start, 0));
+  CallEvents ev;
+  if (int rc = ev.init()) {
+    cudaFreeAsync(base, st);
+    return rc;
+  }
+  int rc = cuda_rc(cudaEventRecord(ev.start, st));
+  for (int k = 0; !rc && k < nslot; ++k) rc = cuda_rc(cudaStreamWaitEvent(hs->s[k], ev.start, 0));
   for (int64_t i = 0; !rc && i < nchunk; ++i) {
     const int k = (int)(i % nslot);
     cudaStream_t ss = hs->s[k];
@@ -769,8 +834,8 @@ int build_eval_host_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, 
     if (!rc && m && idx) rc = cuda_rc(cudaMemcpyAsync(idx + c0 * m, didx, 4 * (size_t)nc * m, cudaMemcpyDeviceToHost, ss));
   }
   for (int k = 0; k < nslot; ++k) {
-    cudaEventRecord(hs->done[k], hs->s[k]);
-    cudaStreamWaitEvent(st, hs->done[k], 0);
+    cudaEventRecord(ev.done[k], hs->s[k]);
+    cudaStreamWaitEvent(st, ev.done[k], 0);
   }
   cudaFreeAsync(base, st);
   return rc;
@@ -885,6 +950,8 @@ int spline_build(const void *x, const void *y, int64_t n, int64_t batch, int bc,
   if (int rc = check_build(x, y, n, batch, bc, yp1, ypn, y2, dtype)) return rc;
   if (batch == 0) return SPLINE_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
   if (dtype == SPLINE_F32)
     return build_t<float>((const float *)x, (const float *)y, n, batch, bc, (const float *)yp1, (const float *)ypn,
                           (float *)y2, st);
@@ -900,6 +967,8 @@ int spline_eval(const void *x, const void *y, const void *y2, int64_t n, int64_t
   if (batch == 0 || m == 0) return SPLINE_OK;
   if (!x || !y || !y2 || !q || !out) return SPLINE_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
   if (dtype == SPLINE_F32)
     return eval_t<float>((const float *)x, (const float *)y, (const float *)y2, n, batch, (const float *)q, m,
                          (float *)out, idx, flags, st);
@@ -919,6 +988,8 @@ int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, in
   if (!x || !y || ((bc & 1) && !yp1) || ((bc & 2) && !ypn)) return SPLINE_EINVAL;
   if (m > 0 && (!q || !out)) return SPLINE_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
   if (dtype == SPLINE_F32)
     return build_eval_t<float>((const float *)x, (const float *)y, n, batch, bc, (const float *)yp1,
                                (const float *)ypn, (float *)y2, (const float *)q, m, (float *)out, idx, flags, st);
@@ -938,6 +1009,8 @@ int spline_build_eval_host(const void *x, const void *y, int64_t n, int64_t batc
   if (!x || !y || ((bc & 1) && !yp1) || ((bc & 2) && !ypn)) return SPLINE_EINVAL;
   if (m > 0 && (!q || !out)) return SPLINE_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
   if (dtype == SPLINE_F32)
     return build_eval_host_t<float>((const float *)x, (const float *)y, n, batch, bc, (const float *)yp1,
                                     (const float *)ypn, (float *)y2, (const float *)q, m, (float *)out, idx, flags, st);
@@ -954,6 +1027,8 @@ int spline_eval_ablation(const void *x, const void *y, const void *y2, int64_t n
   if (batch == 0 || m == 0) return SPLINE_OK;
   if (!x || !y || !y2 || !q || !out) return SPLINE_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
   if (dtype == SPLINE_F32)
     return ablation_t<float>((const float *)x, (const float *)y, (const float *)y2, n, batch, (const float *)q, m,
                              (float *)out, idx, form, st);
@@ -969,6 +1044,8 @@ int spline_gather_probe(const void *x, const void *y, const void *y2, int64_t n,
   if (batch == 0 || m == 0) return SPLINE_OK;
   if (!x || !y || !y2 || !q || !idx_in || !out || !idx) return SPLINE_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
   if (dtype == SPLINE_F32)
     return probe_t<float>((const float *)x, (const float *)y, (const float *)y2, n, batch, (const float *)q, m,
                           idx_in, (float *)out, idx, mode, st);
@@ -996,9 +1073,11 @@ int spline_eval_f64(const double *x, const double *y, const double *y2, int64_t 
 int spline_status(spline_stream_t stream, unsigned int *bits_out) {
   cudaStream_t st = (cudaStream_t)stream;
   unsigned int bits = 0;
-  const unsigned int zero = 0;
-  cudaError_t e = cudaMemcpyFromSymbolAsync(&bits, fs::g_status, sizeof(bits), 0, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(fs::g_status, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
+  unsigned *w = status_word(st);
+  if (!w) return SPLINE_ENOMEM;
+  // read, then clear, this stream's word -- both ordered on the stream after its prior work
+  cudaError_t e = cudaMemcpyAsync(&bits, w, sizeof(bits), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(w, 0, sizeof(unsigned), st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (bits_out) *bits_out = bits;
   return cuda_rc(e);
@@ -1019,6 +1098,8 @@ int spline_spike_reduce(const void *x, const void *y, int64_t n, int64_t row_beg
   if (int rc = check_spike(x, y, n, row_begin, row_end, bc, yp1, ypn, workspace, dtype)) return rc;
   if (!record) return SPLINE_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
   if (dtype == SPLINE_F32)
     return spike_reduce_t<float>((const float *)x, (const float *)y, n, row_begin, row_end, bc, (const float *)yp1,
                                  (const float *)ypn, (float *)record, workspace, st);
@@ -1033,6 +1114,8 @@ int spline_spike_finish(const void *x, const void *y, int64_t n, int64_t row_beg
   if (!all_records || !y2_shard || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
     return SPLINE_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
   if (dtype == SPLINE_F32)
     return spike_finish_t<float>((const float *)x, (const float *)y, n, row_begin, row_end, bc, (const float *)yp1,
                                  (const float *)ypn, (const float *)all_records, nranks, rank, (float *)y2_shard,
