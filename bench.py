@@ -4,9 +4,11 @@
 One step = the whole hot path over one batch: spline_build (validate, assemble rows,
 forward elimination, back-substitution) then spline_eval (locate + Eq. nr_formula),
 through the C ABI, on inputs resident in HBM.  Default workload: BASELINE.json
-configs[1] (65,536 curves x 64 knots, fp32, clamped, 256 unsorted queries per curve).
+configs[3], cfg4 (4,096 curves x 4,096 knots, fp64 -- the paper's binary64, P:1747-1748 --,
+clamped, 16 sorted queries per knot): the largest batched configuration on one GPU.  The other
+configurations via --config (cfg2 = configs[1], the fp32 many-curve case).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
 Multi-GPU (torchrun, one rank per GPU): weak scaling -- every rank builds and evaluates
 its own shard of curves (same shape, its own seed); no collective on the data path.
@@ -38,7 +40,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -60,11 +62,27 @@ def peaks():
 
 
 def traffic_for(workload_key: str, kernel: str):
+    """Per-launch DRAM traffic of the kernel from the current ncu capture (profiles/traffic.json,
+    written by tools/traffic_capture.py): dram__bytes_read.sum + the bytes the kernel WROTE --
+    the larger of dram__bytes_write.sum and the L2 write sectors from the SMs
+    (lts__t_sectors_srcunit_tex_op_write.sum x 32 B), because writes still dirty in L2 when the
+    kernel ends reach DRAM only later and dram__bytes_write.sum misses them."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
-        return None
+        return None, None
     d = json.load(open(p))
-    return d.get(workload_key, {}).get(kernel)
+    e = d.get(workload_key, {}).get(kernel)
+    if isinstance(e, dict):
+        return e.get("traffic"), e
+    return e, None
+
+
+def pstats(ms):
+    """Median with p16 / p84 (the paper's own summary of a timing distribution)
+    and the mean."""
+    a = np.asarray(ms, dtype=np.float64)
+    p16, p50, p84 = np.percentile(a, [16, 50, 84])
+    return {"median": float(p50), "p16": float(p16), "p84": float(p84), "mean": float(a.mean()), "n": int(a.size)}
 
 
 class ClockSampler:
@@ -142,7 +160,10 @@ def algorithmic_bytes(B, n, m, s):
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle as it stands, timed on the host cores (rank 0)."""
+    """--impl reference: the CPU oracle as it stands, timed on the host cores (rank 0 only).
+    Each step is one whole build + eval pass of the SAME workload as our arm when K + W such
+    passes fit the time budget (~3 min); otherwise of a bounded sample of it (curves; for the
+    one-curve cfg5, queries), chosen from one timed full pass and stated in `sample`."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -150,27 +171,46 @@ def run_reference(args):
     from paper_2001_09253_b200 import workloads
     spec = workloads.CONFIGS[args.config]
     cores = os.cpu_count() or 1
-    sample_curves = {1: 1, 2: 8192, 3: 65536, 4: 8, 5: 1}[args.config]
-    kw = dict(batch=sample_curves)
-    if args.config == 5:
-        kw.update(n=1 << 20, m=1 << 20)
-    wl = workloads.generate(args.config, **kw)
+    budget = 180.0
+    wl = workloads.generate(args.config)
+
+    def one_pass(w):
+        t0 = time.perf_counter()
+        y2, _ = oracle.build_y2(w.x, w.y, w.bc, w.yp1, w.ypn, nthreads=cores)
+        oracle.evaluate(w.x, w.y, y2, w.q, nthreads=cores)
+        return time.perf_counter() - t0
+
+    full = wl
+    if args.config == 5:  # a full pass is ~10-20 s of host work: probe with a query sample first
+        probe = workloads.Workload(wl.spec, wl.x, wl.y, wl.q[:, : 1 << 22], wl.yp1, wl.ypn, wl.bc, wl.flags)
+        per = one_pass(probe) * wl.m / probe.m
+    else:
+        per = one_pass(wl)
+    frac = min(1.0, budget / max(per * (args.steps + args.warmup), 1e-9))
+    if frac < 1.0:
+        if args.config == 5:
+            mm = max(1 << 16, int(wl.m * frac))
+            wl = workloads.Workload(wl.spec, wl.x, wl.y, wl.q[:, :mm], wl.yp1, wl.ypn, wl.bc, wl.flags)
+        else:
+            bb = max(1, int(wl.batch * frac))
+            sl = lambda a: None if a is None else a[:bb]
+            wl = workloads.Workload(wl.spec, wl.x[:bb], wl.y[:bb], wl.q[:bb], sl(wl.yp1), sl(wl.ypn), wl.bc, wl.flags)
     times = []
     for it in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        y2, _ = oracle.build_y2(wl.x, wl.y, wl.bc, wl.yp1, wl.ypn, nthreads=cores)
-        oracle.evaluate(wl.x, wl.y, y2, wl.q, nthreads=cores)
-        t1 = time.perf_counter()
+        t = one_pass(wl)
         if it >= args.warmup:
-            times.append(t1 - t0)
-    t = statistics.mean(times)
+            times.append(t)
+    st = pstats([t * 1e3 for t in times])
+    t = st["median"] * 1e-3
     qps = wl.batch * wl.m / t
-    sample = f"{wl.batch} curves x n={wl.n} x m={wl.m} of {spec.name} per step (build + eval)"
+    same = wl.batch == full.batch and wl.m == full.m
+    sample = (f"{'the full workload' if same else 'a sample'}: {wl.batch} curves x n={wl.n} x m={wl.m} of {spec.name} "
+              f"per step (build + eval, {cores} threads)")
     line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle; inputs widened)",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": st["median"], "step_ms_stats": st,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle; inputs widened)",
             "data": "synthetic (seeded, BASELINE.json config recipe)",
-            "config": {"workload": spec.name, "batch": wl.batch, "n": wl.n, "m": wl.m},
+            "config": {"workload": spec.name, "batch": wl.batch, "n": wl.n, "m": wl.m, "same_config": same},
             "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "knots_per_s": wl.batch * wl.n / t}
@@ -410,7 +450,9 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    step_ms = statistics.mean(ev[k][0].elapsed_time(ev[k][1]) for k in range(K))
+    step_list = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
+    step_st = pstats(step_list)
+    step_ms = step_st["median"]
     # per-kernel breakdown (for the rooflines): each kernel timed alone, same flush protocol
     bev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     for k in range(K):
@@ -445,8 +487,8 @@ def main():
             fev[k][1].record(stream)
         torch.cuda.synchronize()
         fused_ms = statistics.mean(a.elapsed_time(b) for a, b in fev)
-    t = torch.tensor([step_ms, statistics.mean(build_ms), statistics.mean(eval_ms), fused_ms], dtype=torch.float64,
-                     device=dev)
+    build_st, eval_st = pstats(build_ms), pstats(eval_ms)
+    t = torch.tensor([step_ms, build_st["median"], eval_st["median"], fused_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms, bms, ems, fused_ms = t.tolist()
@@ -511,6 +553,8 @@ def main():
 
     bbytes, ebytes = algorithmic_bytes(B, n, m, s)
     peak, peak_src = peaks()
+    etr, etr_d = traffic_for(f"cfg{args.config}", "eval")
+    btr, btr_d = traffic_for(f"cfg{args.config}", "build")
     ach = ebytes / (ems * 1e-3) / 1e9
     wkey = f"cfg{args.config}"
     long_curve = n > 256 * (16 if s == 8 else 32)
@@ -552,6 +596,7 @@ def main():
         "steps": K,
         "warmup": args.warmup,
         "ms_per_step": step_ms,
+        "step_ms_stats": step_st,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -565,6 +610,10 @@ def main():
         "frac_of_spec_8tbs_step": (bbytes + ebytes) / (step_ms * 1e-3) / 1e9 / SPEC_HBM_GBS,
         "build_ms": bms,
         "eval_ms": ems,
+        "build_ms_stats": build_st,
+        "eval_ms_stats": eval_st,
+        "timing": "CUDA events on the launching stream; value and ms_per_step use the median step "
+                  "(p16 / p84 / mean in step_ms_stats), max over ranks",
         "build_gbs": bbytes / (bms * 1e-3) / 1e9,
         "step_roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak,
                           "algorithmic_bytes": step_bytes, "achieved": step_bytes / (step_ms * 1e-3) / 1e9,
@@ -576,11 +625,11 @@ def main():
                       "fused (k_fused_staged)" if fused_step else "split (build kernel(s), then eval kernel(s))"),
         "roofline": {"kernel": ekern, "bound": "hbm",
                      "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "traffic": traffic_for(wkey, "eval"), "peak_source": peak_src,
+                     "traffic": etr, "traffic_detail": etr_d, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": ebytes,
                      "build": {"kernel": bkern, "achieved": bbytes / (bms * 1e-3) / 1e9,
                                "frac": bbytes / (bms * 1e-3) / 1e9 / peak,
-                               "algorithmic_bytes_per_launch": bbytes, "traffic": traffic_for(wkey, "build")}},
+                               "algorithmic_bytes_per_launch": bbytes, "traffic": btr, "traffic_detail": btr_d}},
         "fused": ({"kernel": "k_fused_staged", "ms_per_step": fused_ms, "value": world * B * m / (fused_ms * 1e-3),
                    "unit": "queries/s", "algorithmic_bytes": (2 * s + 4) * B * m + 3 * s * B * n,
                    "hbm_gbs": ((2 * s + 4) * B * m + 3 * s * B * n) / (fused_ms * 1e-3) / 1e9,
