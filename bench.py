@@ -487,11 +487,24 @@ def main():
             fev[k][1].record(stream)
         torch.cuda.synchronize()
         fused_ms = statistics.mean(a.elapsed_time(b) for a, b in fev)
+    # ---- the split path as one call (spline_build_eval with SPLINE_PATH_SPLIT), same protocol
+    sf = wl.flags | api.PATH_SPLIT
+    for _ in range(3):
+        api.build_eval(x, y, q, wl.bc, yp1, ypn, sf, y2=y2, out=out, idx=idx)
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for k in range(K):
+        flush.zero_()
+        sev[k][0].record(stream)
+        api.build_eval(x, y, q, wl.bc, yp1, ypn, sf, y2=y2, out=out, idx=idx)
+        sev[k][1].record(stream)
+    torch.cuda.synchronize()
+    split_ms = statistics.median(a.elapsed_time(b) for a, b in sev)
     build_st, eval_st = pstats(build_ms), pstats(eval_ms)
-    t = torch.tensor([step_ms, build_st["median"], eval_st["median"], fused_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([step_ms, build_st["median"], eval_st["median"], fused_ms, split_ms], dtype=torch.float64,
+                     device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    step_ms, bms, ems, fused_ms = t.tolist()
+    step_ms, bms, ems, fused_ms, split_ms = t.tolist()
 
     # ---- cfg5: the random-gather ceiling: the same gathers at known intervals
     gather = None
@@ -563,15 +576,17 @@ def main():
     fused_step = fusable and B * m <= (1 << 17)
     small_step = s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0  # k_eval_small<true>: solve + eval
     tiny_step = (n == 16 or (s == 4 and n in (32, 64))) and B <= 16 and m <= 8192 and m % (16 // s) == 0
+    # mid-length curves with sorted queries (cfg4): k_tile_eval solves and evaluates in one kernel
+    tile_step = bool(wl.flags & workloads.FLAG_Q_SORTED) and 128 < n <= 256 * (16 if s == 8 else 32)
     launches = 2 * K  # 1 build kernel + 1 eval kernel per step for configs 2-4
     if long_curve:
         # tiled SPIKE: reduce + top (grouped for one curve of > 128 tiles: up, root, down) + finish;
         # eval: pack records + gather
         ntiles = -(-n // (256 * (16 if s == 8 else 32)))
         launches = (7 if (B == 1 and ntiles > 128) else 5) * K
-    if fused_step or small_step or tiny_step:
+    if fused_step or small_step or tiny_step or tile_step:
         launches = K
-    one_kernel = fused_step or small_step or tiny_step
+    one_kernel = fused_step or small_step or tiny_step or tile_step
     step_bytes = ((2 * s + 4) * B * m + 3 * s * B * n) if one_kernel else (bbytes + ebytes)
     if wl.flags & workloads.FLAG_Q_SORTED:
         ekern = "k_eval_sorted"
@@ -588,6 +603,25 @@ def main():
     half = n == 16 or (s == 4 and n in (32, 64))  # K1h: half curves in registers
     bkern = ("k1_thomas_regs" if n <= 8 else "k1_thomas_half" if half else "k1_thomas_pipe" if n <= 128 else
              "k_tile<FULL>" if not long_curve else "k_tile<REDUCE> + k4_top + k_tile<FINISH>")
+    split_roof = {"kernel": ekern, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                  "frac": ach / peak, "traffic": etr, "traffic_detail": etr_d, "peak_source": peak_src,
+                  "algorithmic_bytes_per_launch": ebytes,
+                  "build": {"kernel": bkern, "achieved": bbytes / (bms * 1e-3) / 1e9,
+                            "frac": bbytes / (bms * 1e-3) / 1e9 / peak,
+                            "algorithmic_bytes_per_launch": bbytes, "traffic": btr, "traffic_detail": btr_d}}
+    if one_kernel:
+        # the step IS one kernel: it is the dominant kernel; its launch is bracketed by the step's events
+        skern = ("k_tile_eval" if tile_step else "k_eval_small<true>" if small_step else
+                 "k_build_eval_tiny" if tiny_step else "k_fused_staged")
+        str_, str_d = traffic_for(f"cfg{args.config}", "step")
+        sach = step_bytes / (step_ms * 1e-3) / 1e9
+        roof = {"kernel": skern, "bound": "hbm", "achieved": sach, "peak": peak, "unit": "GB/s", "frac": sach / peak,
+                "traffic": str_, "traffic_detail": str_d, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": step_bytes,
+                "note": "algorithmic bytes: (2s+4) B/query (q in; out, int32 idx out) + 3s B/knot (x, y in; y2 out)",
+                "split_path": split_roof}
+    else:
+        roof = split_roof
     line = {
         "metric": METRIC,
         "value": world * B * m / (step_ms * 1e-3),
@@ -610,6 +644,7 @@ def main():
         "frac_of_spec_8tbs_step": (bbytes + ebytes) / (step_ms * 1e-3) / 1e9 / SPEC_HBM_GBS,
         "build_ms": bms,
         "eval_ms": ems,
+        "split_step_ms": split_ms,
         "build_ms_stats": build_st,
         "eval_ms_stats": eval_st,
         "timing": "CUDA events on the launching stream; value and ms_per_step use the median step "
@@ -620,16 +655,11 @@ def main():
                           "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak,
                           "note": "the whole timed step (build + eval); one kernel reads x, y once and never "
                                   "reads y2 back, the split path pays both kernels' bytes"},
-        "step_path": ("fused (k_eval_small<true>: K1r's solve + the small-curve eval)" if small_step else
+        "step_path": ("fused (k_tile_eval: K2's solve, y2 kept on chip, sorted-run eval)" if tile_step else
+                      "fused (k_eval_small<true>: K1r's solve + the small-curve eval)" if small_step else
                       "fused (k_build_eval_tiny: one CTA per curve, K1h's solve + eval)" if tiny_step else
                       "fused (k_fused_staged)" if fused_step else "split (build kernel(s), then eval kernel(s))"),
-        "roofline": {"kernel": ekern, "bound": "hbm",
-                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "traffic": etr, "traffic_detail": etr_d, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": ebytes,
-                     "build": {"kernel": bkern, "achieved": bbytes / (bms * 1e-3) / 1e9,
-                               "frac": bbytes / (bms * 1e-3) / 1e9 / peak,
-                               "algorithmic_bytes_per_launch": bbytes, "traffic": btr, "traffic_detail": btr_d}},
+        "roofline": roof,
         "fused": ({"kernel": "k_fused_staged", "ms_per_step": fused_ms, "value": world * B * m / (fused_ms * 1e-3),
                    "unit": "queries/s", "algorithmic_bytes": (2 * s + 4) * B * m + 3 * s * B * n,
                    "hbm_gbs": ((2 * s + 4) * B * m + 3 * s * B * n) / (fused_ms * 1e-3) / 1e9,

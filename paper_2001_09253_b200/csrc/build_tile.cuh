@@ -124,14 +124,15 @@ template <typename T, int R> __host__ __device__ constexpr size_t tile_smem_byte
 //  REDUCE : writes the tile's block record to tile_rec[(c*ntiles + t)*6].
 //  FINISH : reads the tile's outer (L, R) from tile_ext[(c*ntiles + t)*2]; writes y2 rows
 //           [P, Q] to y2 + c*(row_end-row_begin) + (P - row_begin).
+// tile_solve is the body; on return (FULL / FINISH) the tile's y2 is ALSO in shared memory at
+// X[pad(i)] (pad(i) = i + i/R, all threads synchronised), which the fused build+eval kernel
+// evaluates from; y2 == nullptr skips the global store (FULL only).
 template <typename T, int R, int MODE>
-__global__ void __launch_bounds__(kTileThreads) k_tile(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int64_t n,
-                                                      int64_t row_begin, int64_t row_end, int bc,
-                                                      const T *__restrict__ yp1, const T *__restrict__ ypn,
-                                                      T *__restrict__ y2, T *__restrict__ tile_rec,
-                                                      const T *__restrict__ tile_ext, int *__restrict__ badflag,
-                                                      int ntiles) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+__device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const T *__restrict__ x,
+                                           const T *__restrict__ y, int64_t n, int64_t row_begin, int64_t row_end,
+                                           int bc, const T *__restrict__ yp1, const T *__restrict__ ypn,
+                                           T *__restrict__ y2, T *__restrict__ tile_rec, const T *__restrict__ tile_ext,
+                                           int *__restrict__ badflag, int ntiles, int64_t blk, unsigned char *smem_raw) {
   constexpr int NT = kTileThreads;
   constexpr int TR = NT * R;
   T *X = reinterpret_cast<T *>(smem_raw);
@@ -140,8 +141,8 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(unsigned *__restrict__ st
   T *mi = reinterpret_cast<T *>(rec + NT);
   T *ext = reinterpret_cast<T *>(rec);  // aliases rec: used only after tree_up
 
-  const int64_t c = blockIdx.x / ntiles;
-  const int tile = (int)(blockIdx.x - c * ntiles);
+  const int64_t c = blk / ntiles;
+  const int tile = (int)(blk - c * ntiles);
   const int64_t P = row_begin + (int64_t)tile * TR;
   const int nrows = (int)min64(TR, row_end - P);
   const int nleaf = (nrows + R - 1) / R;
@@ -272,11 +273,15 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(unsigned *__restrict__ st
     return;
   }
 
-  T *y2o = (MODE == TILE_FULL) ? y2 + c * n + P : y2 + c * (row_end - row_begin) + (P - row_begin);
+  T *y2o = !y2 ? nullptr : (MODE == TILE_FULL) ? y2 + c * n + P : y2 + c * (row_end - row_begin) + (P - row_begin);
   const bool curve_bad = (MODE == TILE_FULL) ? bad : (badflag[c] != 0);
   if (curve_bad) {
     if (MODE == TILE_FULL && threadIdx.x == 0) raise_status(status, kBadKnots);
-    for (int e = threadIdx.x; e < nrows; e += NT) y2o[e] = qnan<T>();
+    for (int e = threadIdx.x; e < nrows; e += NT) {
+      X[pad(e)] = qnan<T>();
+      if (y2o) y2o[e] = qnan<T>();
+    }
+    __syncthreads();
     return;
   }
   T Lr = T(0), Rr = T(0);
@@ -299,6 +304,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(unsigned *__restrict__ st
     }
   }
   __syncthreads();
+  if (!y2o) return;
   const bool vo = (((uintptr_t)y2o) & 15) == 0;
   const int novec = vo ? nrows / VW : 0;
   for (int v = threadIdx.x; v < novec; v += NT) {
@@ -308,6 +314,18 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(unsigned *__restrict__ st
     __stcs(reinterpret_cast<VT *>(y2o) + v, a);
   }
   for (int e = novec * VW + threadIdx.x; e < nrows; e += NT) y2o[e] = X[pad(e)];
+}
+
+template <typename T, int R, int MODE>
+__global__ void __launch_bounds__(kTileThreads) k_tile(unsigned *__restrict__ status, const T *__restrict__ x,
+                                                      const T *__restrict__ y, int64_t n, int64_t row_begin,
+                                                      int64_t row_end, int bc, const T *__restrict__ yp1,
+                                                      const T *__restrict__ ypn, T *__restrict__ y2,
+                                                      T *__restrict__ tile_rec, const T *__restrict__ tile_ext,
+                                                      int *__restrict__ badflag, int ntiles) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  tile_solve<T, R, MODE>(status, x, y, n, row_begin, row_end, bc, yp1, ypn, y2, tile_rec, tile_ext, badflag, ntiles,
+                         (int64_t)blockIdx.x, smem_raw);
 }
 
 // K4: merge the per-tile records of each curve (grid = batch, one CTA per curve) and,

@@ -259,11 +259,38 @@ template <typename T> struct Vec16;
 template <> struct Vec16<float> { using V = float4; using I = int4; static constexpr int N = 4; };
 template <> struct Vec16<double> { using V = double2; using I = int2; static constexpr int N = 2; };
 
+// 32-byte (256-bit) streaming accesses: one instruction per full sector (LDG.E.256 / STG.E.256)
+__device__ __forceinline__ void ld_cs_256(const double *p, double *v) {
+  asm volatile("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld_cs_256(const float *p, float *v) {
+  asm volatile("ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st_cs_256(double *p, const double *v) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void st_cs_256(float *p, const float *v) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void st_cs_256(int32_t *p, const int *v) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
 template <typename T, int V> struct VecIO {
-  // loads V consecutive elements (16-byte aligned when V > 1)
+  // loads V consecutive elements (16-byte aligned when V > 1; 32-byte aligned when V elements
+  // are 32 bytes)
   static __device__ __forceinline__ void load(const T *p, T *v) {
     if constexpr (V == 1) {
       v[0] = ld_stream(p);
+    } else if constexpr (V * sizeof(T) == 32) {
+      ld_cs_256(p, v);
     } else {
       using VT = typename Vec16<T>::V;
       const VT t = __ldcs(reinterpret_cast<const VT *>(p));
@@ -286,6 +313,8 @@ template <typename T, int V> struct VecIO {
   static __device__ __forceinline__ void store(T *p, const T *v) {
     if constexpr (V == 1) {
       st_stream(p, v[0]);
+    } else if constexpr (V * sizeof(T) == 32) {
+      st_cs_256(p, v);
     } else {
       using VT = typename Vec16<T>::V;
       VT t;
@@ -298,6 +327,8 @@ template <typename T, int V> struct VecIO {
   static __device__ __forceinline__ void store_idx(int32_t *p, const int *j) {
     if constexpr (V == 1) {
       st_stream(p, j[0]);
+    } else if constexpr (V == 8) {
+      st_cs_256(p, j);
     } else if constexpr (V == 4) {
       __stcs(reinterpret_cast<int4 *>(p), make_int4(j[0], j[1], j[2], j[3]));
     } else {

@@ -882,49 +882,69 @@ template <typename T> __device__ __forceinline__ int warp_locate(const T *X, int
 // interval per lane, at the carried bracket and reused while the carry stays in its first half.
 constexpr int kSortWin = 32;
 constexpr int kSortWinDensity = 8;  // queries per interval from which the window pays
+// One window record: the interval's left knot and its cubic (Cub + e2), 16-byte aligned so that
+// a lookup is 2 (fp32) or 3 (fp64) vector loads.
+template <typename T> struct alignas(16) WRec {
+  T x0, ih, y0, dy, e1, e2;
+};
+template <typename T> __device__ __forceinline__ WRec<T> ld_wrec(const WRec<T> *p) {
+  using VT = typename Vec16<T>::V;
+  constexpr int NV = (int)(sizeof(WRec<T>) / 16);
+  WRec<T> r;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) reinterpret_cast<VT *>(&r)[i] = reinterpret_cast<const VT *>(p)[i];
+  return r;
+}
 template <typename T> struct SortWin {
-  Cub<T> c[kSortWin];
-  T e2[kSortWin];
+  WRec<T> r[kSortWin];
   T x[kSortWin + 1];  // x[i] = x_{wb+i} (+inf past x_{n-2}); x[kSortWin] = x_{wb+kSortWin} or +inf
 };
 
-template <typename T, int V, int FORM = FORM_RECORD, bool WIN = false>
-__global__ void __launch_bounds__(256, 4) k_eval_sorted(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y,
-                                                       const T *__restrict__ y2, int n, const T *__restrict__ q,
-                                                       int64_t m, T *__restrict__ out, int32_t *__restrict__ idx,
-                                                       int64_t qrun, int64_t runs_per_curve, int64_t ntasks) {
-  static_assert(!WIN || FORM == FORM_RECORD, "the record window serves the product form");
-  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
-  const int lane = threadIdx.x & 31;
-  const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (task >= ntasks) return;  // whole warp; no block-level synchronisation below
-  const int64_t c = task / runs_per_curve;
-  const int64_t k0 = (task - c * runs_per_curve) * qrun;
-  const int64_t k1 = min64(m, k0 + qrun);
-  const T *X = x + c * n, *Y = y + c * n, *Z = y2 + c * n;
-  const T *qb = q + c * m;
-  T *ob = out + c * m;
-  int32_t *ib = idx ? idx + c * m : nullptr;
-  const T x0 = __ldg(X), xn = __ldg(X + n - 1);
+// Where a sorted run reads the second derivatives from: global memory (spline_eval) or the
+// shared-memory y2 a fused build just produced (k_tile_eval: padded rows, pad(j) = j + j/R).
+template <typename T> struct ZGlobal {
+  const T *Z;
+  __device__ __forceinline__ T operator()(int j) const { return __ldg(Z + j); }
+  __device__ __forceinline__ const T *prefetch_ptr() const { return Z; }
+};
+template <typename T, int R> struct ZShared {
+  const T *Zs;
+  __device__ __forceinline__ T operator()(int j) const { return Zs[j + j / R]; }
+  __device__ __forceinline__ const T *prefetch_ptr() const { return nullptr; }
+};
 
+// One warp's run of queries [k0, k1) of one curve (X, Y in global memory, Z through ZA).
+// Shared by k_eval_sorted and the fused long-curve kernel, so both give the same bits.
+template <typename T, int V, int FORM, bool WIN, int PF, typename ZA>
+__device__ __forceinline__ bool sorted_run(const T *__restrict__ X, const T *__restrict__ Y, const ZA &Z, int n,
+                                           const T *__restrict__ qb, T *__restrict__ ob, int32_t *__restrict__ ib,
+                                           int64_t k0, int64_t k1, SortWin<T> &sw, int lane) {
+  const T x0 = __ldg(X), xn = __ldg(X + n - 1);
   // initial bracket from the run's first query (clamped into range)
   T qf = __ldg(qb + k0);
   qf = (qf >= x0 && qf <= xn) ? qf : x0;
   int jc = warp_locate(X, n, qf, lane);
   bool oor = false;
-  __shared__ SortWin<T> wins[8];  // one per warp of the 256-thread CTA
-  SortWin<T> &sw = wins[threadIdx.x >> 5];
   int wb = -(1 << 30);            // window base: none yet
 
-  T qa[V], qn[V];
-  int64_t kb = k0 + (int64_t)lane * V;
-  if (kb < k1) VecIO<T, V>::load(qb + kb, qa);
+  // the queries of the next PF warp steps are in flight (a register ring, rotated each step):
+  // the run is bound by the bytes in flight per warp, not by its arithmetic
+  T qr[PF + 1][V];
+#pragma unroll
+  for (int d = 0; d < PF; ++d) {
+    const int64_t kd = k0 + (int64_t)(d * 32 + lane) * V;
+    if (kd < k1) VecIO<T, V>::load(qb + kd, qr[d]);
+  }
   for (int64_t base = k0; base < k1; base += 32 * V) {
     const int64_t k = base + (int64_t)lane * V;
-    const int64_t kn = k + 32 * V;
-    if (kn < k1) VecIO<T, V>::load(qb + kn, qn);  // next step in flight
+    const int64_t kn = k + (int64_t)PF * 32 * V;
+    if (kn < k1) VecIO<T, V>::load(qb + kn, qr[PF]);  // PF steps ahead
+    T qa[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) qa[i] = qr[0][i];
     if constexpr (!WIN) {
-      if (lane < 3) prefetch_l1((lane == 0 ? X : lane == 1 ? Y : Z) + min(jc + 32, n - 1));
+      const T *zp = Z.prefetch_ptr();
+      if (lane < 2 || (lane == 2 && zp)) prefetch_l1((lane == 0 ? X : lane == 1 ? Y : zp) + min(jc + 32, n - 1));
     } else {
       if (jc < wb || jc - wb > kSortWin / 2) {  // warp-uniform: rebuild the window at the carry
         __syncwarp();
@@ -933,8 +953,8 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(unsigned *__restrict__ s
         if (jw <= n - 2) {
           const T xa = __ldg(X + jw), xb = __ldg(X + jw + 1);
           T e2;
-          sw.c[lane] = make_cub<T>(xa, xb, __ldg(Y + jw), __ldg(Y + jw + 1), __ldg(Z + jw), __ldg(Z + jw + 1), e2);
-          sw.e2[lane] = e2;
+          const Cub<T> cb = make_cub<T>(xa, xb, __ldg(Y + jw), __ldg(Y + jw + 1), Z(jw), Z(jw + 1), e2);
+          sw.r[lane] = WRec<T>{xa, cb.ih, cb.y0, cb.dy, cb.e1, e2};
           sw.x[lane] = xa;
           if (lane == kSortWin - 1) sw.x[kSortWin] = xb;
         } else {
@@ -978,7 +998,8 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(unsigned *__restrict__ s
               }
             }
             lp = l;
-            const T v = cub_eval<T>(sw.c[l], sw.e2[l], sw.x[l], qc);
+            const WRec<T> wr = ld_wrec(&sw.r[l]);
+            const T v = cub_eval<T>(Cub<T>{wr.ih, wr.y0, wr.dy, wr.e1}, wr.e2, wr.x0, qc);
             j = wb + l;
             val[i] = in ? v : qnan<T>();
             jj[i] = in ? j : -1;
@@ -1002,7 +1023,7 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(unsigned *__restrict__ s
         const T xa = __ldg(X + j), xb = __ldg(X + j + 1);
         T v;
         if constexpr (FORM == FORM_NOOP) v = __ldg(Y + j);
-        else v = interp_form<T, FORM>(qc, xa, xb, __ldg(Y + j), __ldg(Y + j + 1), __ldg(Z + j), __ldg(Z + j + 1));
+        else v = interp_form<T, FORM>(qc, xa, xb, __ldg(Y + j), __ldg(Y + j + 1), Z(j), Z(j + 1));
         val[i] = in ? v : qnan<T>();
         jj[i] = in ? j : -1;
         oor |= !in;
@@ -1014,8 +1035,35 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(unsigned *__restrict__ s
     const int jm = __reduce_max_sync(0xffffffffu, jl);
     if (jm >= 0) jc = jm;
 #pragma unroll
-    for (int i = 0; i < V; ++i) qa[i] = qn[i];
+    for (int d = 0; d < PF; ++d)
+#pragma unroll
+      for (int i = 0; i < V; ++i) qr[d][i] = qr[d + 1][i];
   }
+  return oor;
+}
+
+#ifndef FS_SORTED_PF
+#define FS_SORTED_PF 1
+#endif
+constexpr int kSortedPF = FS_SORTED_PF;  // query prefetch depth of k_eval_sorted (warp steps)
+template <typename T, int V, int FORM = FORM_RECORD, bool WIN = false>
+__global__ void __launch_bounds__(256, 4) k_eval_sorted(unsigned *__restrict__ status, const T *__restrict__ x,
+                                                       const T *__restrict__ y, const T *__restrict__ y2, int n,
+                                                       const T *__restrict__ q, int64_t m, T *__restrict__ out,
+                                                       int32_t *__restrict__ idx, int64_t qrun,
+                                                       int64_t runs_per_curve, int64_t ntasks) {
+  static_assert(!WIN || FORM == FORM_RECORD, "the record window serves the product form");
+  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
+  const int lane = threadIdx.x & 31;
+  const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (task >= ntasks) return;  // whole warp; no block-level synchronisation below
+  const int64_t c = task / runs_per_curve;
+  const int64_t k0 = (task - c * runs_per_curve) * qrun;
+  const int64_t k1 = min64(m, k0 + qrun);
+  __shared__ SortWin<T> wins[8];  // one per warp of the 256-thread CTA
+  const bool oor = sorted_run<T, V, FORM, WIN, kSortedPF>(x + c * n, y + c * n, ZGlobal<T>{y2 + c * n}, n, q + c * m,
+                                               out + c * m, idx ? idx + c * m : nullptr, k0, k1,
+                                               wins[threadIdx.x >> 5], lane);
   raise_status_warp(status, oor, kOutOfRange);
 }
 

@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "eval.cuh"
 #include "fused.cuh"
+#include "fused_tile.cuh"
 
 using namespace fs;
 
@@ -418,6 +419,13 @@ int launch_staged(const T *x, const T *y, const T *y2, int n, int64_t batch, con
   return launch_staged_k<T, MODE, 1, false>(x, y, y2, n, batch, q, m, out, idx, cpb, nchunks, qchunk, nitems, st);
 }
 
+// Sorted runs with 4 queries per lane: q, out aligned to 4 elements (32 B fp64, 16 B fp32), idx to
+// 16 B, m a multiple of 4.
+template <typename T> bool sorted_v4_ok(const T *q, int64_t m, const T *out, const int32_t *idx) {
+  constexpr uintptr_t A = 4 * sizeof(T) - 1;
+  return m % 4 == 0 && (((uintptr_t)q | (uintptr_t)out) & A) == 0 && (!idx || ((uintptr_t)idx & 15) == 0);
+}
+
 template <typename T, int V, int FORM = FORM_RECORD>
 int launch_sorted_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
                     int32_t *idx, cudaStream_t st) {
@@ -461,6 +469,8 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
            int32_t *idx, int flags, cudaStream_t st) {
   if (flags & SPLINE_Q_SORTED) {
     constexpr int VW = 16 / sizeof(T);
+    // 4 queries per lane and step (fp64: one 256-bit access each for q and out)
+    if (sorted_v4_ok(q, m, out, idx)) return launch_sorted_k<T, 4>(x, y, y2, (int)n, batch, q, m, out, idx, st);
     const bool vec = (m % VW == 0) && aligned16(q) && aligned16(out) && (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0));
     if (vec) return launch_sorted_k<T, VW>(x, y, y2, (int)n, batch, q, m, out, idx, st);
     return launch_sorted_k<T, 1>(x, y, y2, (int)n, batch, q, m, out, idx, st);
@@ -616,6 +626,60 @@ int launch_fused(const T *x, const T *y, int n, int64_t batch, int bc, const T *
                                                        nchunks, qchunk, nitems, st);
 }
 
+// ---- fused build + eval of mid-length curves with sorted queries (k_tile_eval) ---------------
+template <typename T, int R, int V, bool WIN>
+int launch_tile_eval_k(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+                       const T *q, int64_t m, T *out, int32_t *idx, cudaStream_t st) {
+  auto kern = k_tile_eval<T, R, V, WIN>;
+  const size_t sm = tile_eval_smem_bytes<T, R>();
+  if (int rc = set_smem(kern, sm)) return rc;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTileThreads, sm) != cudaSuccess || occ < 1) occ = 1;
+  // few curves: split each curve's queries over several CTAs (each solves the curve again, on
+  // chip) so that the grid still fills ~3 waves of the GPU
+  const int64_t slots = (int64_t)occ * num_sms();
+  int nchunks = 1;
+  while (batch * nchunks < 3 * slots && m / (2 * nchunks) >= (int64_t)kTileEvalWarps * 32 * V * 8 && nchunks < 1024)
+    nchunks *= 2;
+  int64_t qchunk = (m + nchunks - 1) / nchunks;
+  qchunk = (qchunk + 32 * V - 1) / (32 * V) * (32 * V);
+  nchunks = (int)((m + qchunk - 1) / qchunk);
+  if (batch * nchunks >= (int64_t(1) << 31)) return SPLINE_EINVAL;
+  kern<<<(unsigned)(batch * nchunks), kTileThreads, sm, st>>>(tl_status, x, y, (int)n, bc, yp1, ypn, y2, q, m, out, idx,
+                                                              nchunks, qchunk);
+  return launch_rc();
+}
+template <typename T, int R>
+int launch_tile_eval_r(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+                       const T *q, int64_t m, T *out, int32_t *idx, cudaStream_t st) {
+  constexpr int VW = 16 / sizeof(T);
+  const bool vec = (m % VW == 0) && aligned16(q) && aligned16(out) && (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0));
+  const bool win = m >= (int64_t)kSortWinDensity * (n - 1);  // dense runs: the record window pays (as eval_t)
+  if (sorted_v4_ok(q, m, out, idx)) {
+    if (win) return launch_tile_eval_k<T, R, 4, true>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+    return launch_tile_eval_k<T, R, 4, false>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  }
+  if (vec) {
+    if (win) return launch_tile_eval_k<T, R, VW, true>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+    return launch_tile_eval_k<T, R, VW, false>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  }
+  if (win) return launch_tile_eval_k<T, R, 1, true>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  return launch_tile_eval_k<T, R, 1, false>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+}
+template <typename T>
+int launch_tile_eval(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+                     const T *q, int64_t m, T *out, int32_t *idx, cudaStream_t st) {
+  if (n <= 256 * 1) return launch_tile_eval_r<T, 1>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  if (n <= 256 * 2) return launch_tile_eval_r<T, 2>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  if (n <= 256 * 4) return launch_tile_eval_r<T, 4>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  if (n <= 256 * 8) return launch_tile_eval_r<T, 8>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  if (n <= 256 * 16) return launch_tile_eval_r<T, 16>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  if constexpr (rmax<T>() >= 32) {
+    if (n <= 256 * 32) return launch_tile_eval_r<T, 32>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  }
+  return SPLINE_EINVAL;
+}
+
 template <typename T>
 int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
                  const T *q, int64_t m, T *out, int32_t *idx, int flags, cudaStream_t st) {
@@ -656,6 +720,10 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
       return rc;
     }
   }
+  // mid-length curves (K2's range) with sorted queries: solve and evaluate in one kernel
+  if ((flags & SPLINE_Q_SORTED) && !(flags & SPLINE_PATH_SPLIT) && n > kK1MaxN &&
+      n <= 256 * rmax<T>())
+    return launch_tile_eval<T>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
   const bool want_fused =
       (flags & SPLINE_PATH_FUSED) ||
       (!(flags & (SPLINE_PATH_SPLIT | kNoFusedStaged)) && batch * m <= kFuseMaxWork);

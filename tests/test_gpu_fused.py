@@ -155,3 +155,55 @@ def test_fused_build_only_and_empty(api):
     assert out.shape == (10, 0)
     assert torch.equal(y2.view(torch.int8), api.build(x, y, wl.bc, yp1, ypn).view(torch.int8))
     assert api.status() == 0
+
+
+# ---- k_tile_eval: mid-length curves with sorted queries solved and evaluated in one kernel ----
+
+@pytest.mark.parametrize("kw", [dict(batch=6, n=4096, m=16384), dict(batch=5, n=1000, m=3001),
+                                dict(batch=3, n=129, m=2048), dict(batch=2, n=3000, m=100),
+                                dict(batch=2, n=4096, m=65536), dict(batch=40, n=257, m=9000)])
+def test_tile_eval_cfg4_f64(api, kw):
+    """cfg4-shaped (fp64, clamped, sorted): one launch per call (k_tile_eval) -- dense runs (record
+    window), sparse runs, odd m (scalar query I/O), one leaf row per thread (n <= 256), several
+    query chunks per curve (few curves), against the oracle and bitwise the split path."""
+    check_fused(api, workloads.generate(4, **kw))
+
+
+@pytest.mark.parametrize("bc", [0, 3])
+@pytest.mark.parametrize("dt,n,m", [(np.float32, 8000, 40000), (np.float32, 700, 6000), (np.float64, 2500, 777)])
+def test_tile_eval_dtypes_sorted(api, bc, dt, n, m):
+    rng = np.random.default_rng(7 * n + bc)
+    B = 7
+    x = np.cumsum(rng.exponential(1.0, (B, n)) + 0.05, axis=1).astype(dt)
+    y = np.cumsum(rng.normal(size=(B, n)), axis=1).astype(dt)
+    q = np.sort(rng.uniform(x[:, :1], x[:, -1:], (B, m)).astype(dt), axis=1)
+    q[:, 0] = x[:, 0]
+    q[:, -1] = x[:, -1]
+    q[:, m // 2] = x[:, n // 2]          # an exact interior knot (tie) inside the sorted run
+    q = np.sort(q, axis=1)
+    yp1 = rng.normal(size=B).astype(dt)
+    ypn = rng.normal(size=B).astype(dt)
+    spec = workloads.ConfigSpec(0, "t", B, n, m, "f32" if dt == np.float32 else "f64", bc, 1, 0)
+    check_fused(api, workloads.Workload(spec, x, y, q, yp1, ypn, bc, workloads.FLAG_Q_SORTED))
+
+
+def test_tile_eval_wrong_sorted_hint_and_bad_data(api):
+    """The sorted hint is only a hint: unsorted queries, out-of-range / NaN queries and a curve
+    with bad knots give the oracle's answer (and the split path's bits) in the fused kernel."""
+    wl = workloads.generate(4, batch=4, n=2048, m=8192)
+    rng = np.random.default_rng(3)
+    wl.q[1] = rng.permutation(wl.q[1])          # unsorted despite the flag
+    wl.q[2, 100] = wl.x[2, 0] - 1.0             # below the range
+    wl.q[2, 101] = np.nan
+    wl.q[3, 5000] = wl.x[3, -1] + 1.0           # above the range
+    check_fused(api, wl)
+    wl.x[0, 1000] = wl.x[0, 999]                # curve 0: a repeated knot -> NaN y2 and out
+    x, y, q, yp1, ypn = _dev(wl)
+    api.status()
+    y2, out, idx = api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags)
+    assert api.status() & api.STATUS_BAD_KNOTS
+    assert torch.isnan(y2[0]).all() and torch.isfinite(y2[1:]).all()
+    y2s = api.build(x, y, wl.bc, yp1, ypn)
+    outs, idxs = api.evaluate(x, y, y2s, q, wl.flags)
+    api.status()
+    assert torch.equal(idx, idxs) and torch.equal(out.view(torch.int8), outs.view(torch.int8))
