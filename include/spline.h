@@ -50,9 +50,10 @@ extern "C" {
 #endif
 
 typedef struct CUstream_st *spline_stream_t; /* identical to cudaStream_t */
+typedef struct ncclComm *spline_nccl_comm_t; /* identical to ncclComm_t (nccl.h) */
 
 enum { SPLINE_F32 = 0, SPLINE_F64 = 1 };
-enum { SPLINE_OK = 0, SPLINE_EINVAL = -1, SPLINE_ECUDA = -2, SPLINE_ENOMEM = -3 };
+enum { SPLINE_OK = 0, SPLINE_EINVAL = -1, SPLINE_ECUDA = -2, SPLINE_ENOMEM = -3, SPLINE_ENCCL = -4 };
 /* Boundary condition: a bitmask, the two ends are independent (the paper tests
  * its natural-end sentinel separately per end).  The 0.99e30
  * sentinel itself is never interpreted by the library. */
@@ -66,7 +67,10 @@ enum {
  * comparisons against the same locate rule).  SPLINE_PATH_* (spline_build_eval only) pick
  * the fused single kernel or the two kernels instead of the library's choice; both give
  * bitwise the same y2, out and idx. */
-enum { SPLINE_Q_SORTED = 1, SPLINE_X_UNIFORM = 2, SPLINE_PATH_FUSED = 4, SPLINE_PATH_SPLIT = 8 };
+/* SPLINE_NO_BUCKET (spline_eval only): on one curve too long for L2 with many unsorted queries, do
+ * not bucket the queries by curve chunk (eval_bucket.cuh); use the one-gather-per-query record
+ * path instead (measurement and A/B; same results bitwise). */
+enum { SPLINE_Q_SORTED = 1, SPLINE_X_UNIFORM = 2, SPLINE_PATH_FUSED = 4, SPLINE_PATH_SPLIT = 8, SPLINE_NO_BUCKET = 16 };
 /* Asynchronous data-error bits (spline_status). */
 enum { SPLINE_STATUS_BAD_KNOTS = 1, SPLINE_STATUS_Q_OUT_OF_RANGE = 2 };
 
@@ -206,6 +210,31 @@ int spline_spike_reduce(const void *x, const void *y, int64_t n, int64_t row_beg
 int spline_spike_finish(const void *x, const void *y, int64_t n, int64_t row_begin, int64_t row_end, int bc,
                         const void *yp1, const void *ypn, const void *all_records, int nranks, int rank,
                         void *y2_shard, void *workspace, int dtype, spline_stream_t stream);
+
+/*
+ * spline_build_dist -- the second derivatives of ONE long curve whose rows are partitioned over
+ * the G ranks of an NCCL communicator (the partitioned solve the paper points to
+ * for parallel hardware).  Rank r = ncclCommUserRank(comm) owns rows
+ * [r*n/G, (r+1)*n/G) (integer division) and writes their y2 to y2_shard[0 .. (r+1)*n/G - r*n/G).
+ *   x, y     [n] the WHOLE curve on this rank's device (replicated input);
+ *   bc       as spline_build; yp1 / ypn point to ONE value each (device), required iff clamped.
+ *   comm     an initialised NCCL communicator whose ranks each call this function (collective);
+ *            its device is the current device.
+ * Steps, all enqueued on `stream`: the rank's rows reduced to one 6-scalar block record
+ * (spline_spike_reduce), ncclAllGather of the G records (48 B per rank in fp64 -- the only
+ * exchange), the G-record reduced system solved redundantly and the rank's rows finished
+ * (spline_spike_finish).  Bitwise the two-phase seam's result.
+ * Errors: SPLINE_EINVAL (bad arguments, NULL comm, more ranks than rows, G > 1024);
+ * SPLINE_ENCCL (NCCL not loadable -- it is resolved at run time: the process's libnccl.so.2, or
+ * the path in the SPLINE_NCCL_LIB environment variable -- or an NCCL call failed); data errors
+ * as spline_build (BAD_KNOTS for this rank's rows; the whole curve's bad flag is per shard).
+ */
+int spline_build_dist(const void *x, const void *y, int64_t n, int bc, const void *yp1, const void *ypn,
+                      void *y2_shard, spline_nccl_comm_t comm, int dtype, spline_stream_t stream);
+int spline_build_dist_f32(const float *x, const float *y, int64_t n, int bc, const float *yp1, const float *ypn,
+                          float *y2_shard, spline_nccl_comm_t comm, spline_stream_t stream);
+int spline_build_dist_f64(const double *x, const double *y, int64_t n, int bc, const double *yp1, const double *ypn,
+                          double *y2_shard, spline_nccl_comm_t comm, spline_stream_t stream);
 
 /* Library version string (static storage). */
 const char *spline_version(void);

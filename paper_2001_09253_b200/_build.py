@@ -11,7 +11,7 @@ LIB = os.path.join(CSRC, "libfastspline.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-              "-Xcompiler", "-fPIC", "-shared", "-I" + INCLUDE]
+              "-Xcompiler", "-fPIC", "-shared", "-I" + INCLUDE, "-ldl"]
 
 
 def sources():

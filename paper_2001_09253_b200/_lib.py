@@ -11,14 +11,14 @@ import os
 from . import _build
 
 SPLINE_F32, SPLINE_F64 = 0, 1
-SPLINE_OK, SPLINE_EINVAL, SPLINE_ECUDA, SPLINE_ENOMEM = 0, -1, -2, -3
+SPLINE_OK, SPLINE_EINVAL, SPLINE_ECUDA, SPLINE_ENOMEM, SPLINE_ENCCL = 0, -1, -2, -3, -4
 BC_NATURAL, BC_CLAMP_START, BC_CLAMP_END, BC_CLAMPED = 0, 1, 2, 3
-Q_SORTED, X_UNIFORM, PATH_FUSED, PATH_SPLIT = 1, 2, 4, 8
+Q_SORTED, X_UNIFORM, PATH_FUSED, PATH_SPLIT, NO_BUCKET = 1, 2, 4, 8, 16
 STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE = 1, 2
 FORMS = {"record": 0, "splint_div": 1, "splint_mul": 2, "newint_orig": 3, "newint_noinv": 4, "noop": 5}
 
 _ERR = {SPLINE_EINVAL: "SPLINE_EINVAL (invalid argument)", SPLINE_ECUDA: "SPLINE_ECUDA (CUDA error)",
-        SPLINE_ENOMEM: "SPLINE_ENOMEM (out of device memory)"}
+        SPLINE_ENOMEM: "SPLINE_ENOMEM (out of device memory)", SPLINE_ENCCL: "SPLINE_ENCCL (NCCL unavailable or failed)"}
 
 # name -> (restype, argtypes)
 _vp, _i64, _i32, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
@@ -38,6 +38,9 @@ SIGNATURES = {
     "spline_spike_reduce": (_i32, [_vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp]),
     "spline_spike_finish": (_i32, [_vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _i32,
                                    _vp]),
+    "spline_build_dist": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "spline_build_dist_f32": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "spline_build_dist_f64": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "spline_version": (ctypes.c_char_p, []),
 }
 

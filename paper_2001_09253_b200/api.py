@@ -11,8 +11,8 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import (BC_CLAMP_END, BC_CLAMP_START, BC_CLAMPED, BC_NATURAL, PATH_FUSED, PATH_SPLIT,  # noqa: F401
-                   Q_SORTED, STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE, X_UNIFORM)
+from ._lib import (BC_CLAMP_END, BC_CLAMP_START, BC_CLAMPED, BC_NATURAL, NO_BUCKET, PATH_FUSED,  # noqa: F401
+                   PATH_SPLIT, Q_SORTED, STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE, X_UNIFORM)
 
 _DT = {torch.float32: _lib.SPLINE_F32, torch.float64: _lib.SPLINE_F64}
 
@@ -273,6 +273,61 @@ def spike_finish(x, y, row_begin: int, row_end: int, bc: int, yp1, ypn, all_reco
                                          _p(all_records), nranks, rank, _p(y2_shard), _p(workspace),
                                          _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
     _lib.check(rc, "spline_spike_finish")
+
+
+def build_dist(x, y, comm: int, bc: int = BC_NATURAL, yp1=None, ypn=None, y2_shard=None, stream=None):
+    """spline_build_dist: this rank's rows of ONE long curve (x, y: the whole curve, (n,)) over an
+    NCCL communicator given as its raw ncclComm_t handle (an int).  Rank r of G owns rows
+    [r n / G, (r+1) n / G); returns (y2_shard, (row_begin, row_end)).  Collective: every rank calls."""
+    _check_curves(x, y)
+    if x.dim() != 1 or y.shape != x.shape:
+        raise ValueError("build_dist takes one curve: x, y of shape (n,)")
+    if not comm:
+        raise ValueError("comm must be an initialised ncclComm_t handle")
+    n = x.shape[0]
+    yp1, ypn = _slopes(yp1, 1, x), _slopes(ypn, 1, x)
+    _check_buf(yp1, (1,), x.dtype, x.device, "yp1")
+    _check_buf(ypn, (1,), x.dtype, x.device, "ypn")
+    nccl = _nccl_lib()
+    G, r = ctypes.c_int(0), ctypes.c_int(0)
+    if nccl.ncclCommCount(ctypes.c_void_p(comm), ctypes.byref(G)) or nccl.ncclCommUserRank(ctypes.c_void_p(comm),
+                                                                                            ctypes.byref(r)):
+        raise RuntimeError("ncclCommCount / ncclCommUserRank failed")
+    rb, re = n * r.value // G.value, n * (r.value + 1) // G.value
+    out = torch.empty(re - rb, dtype=x.dtype, device=x.device) if y2_shard is None else y2_shard
+    _check_buf(out, (re - rb,), x.dtype, x.device, "y2_shard")
+    rc = _lib.load().spline_build_dist(_p(x), _p(y), n, bc, _p(yp1), _p(ypn), _p(out), ctypes.c_void_p(comm),
+                                       _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_build_dist")
+    return out, (rb, re)
+
+
+_NCCL = None
+
+
+def _nccl_lib():
+    """The NCCL the process already uses (torch's), for communicator queries in the binding."""
+    global _NCCL
+    if _NCCL is None:
+        import glob
+        import os
+        cands = []
+        try:
+            import nvidia.nccl
+            for d in list(getattr(nvidia.nccl, "__path__", [])):  # a namespace package
+                cands += glob.glob(os.path.join(d, "lib", "libnccl.so*"))
+        except ImportError:
+            pass
+        cands.append("libnccl.so.2")
+        for c in cands:
+            try:
+                _NCCL = ctypes.CDLL(c)
+                break
+            except OSError:
+                continue
+        if _NCCL is None:
+            raise RuntimeError("libnccl.so.2 not found")
+    return _NCCL
 
 
 def version() -> str:

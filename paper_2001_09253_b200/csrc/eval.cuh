@@ -884,8 +884,10 @@ constexpr int kSortWin = 32;
 constexpr int kSortWinDensity = 8;  // queries per interval from which the window pays
 // One window record: the interval's left knot and its cubic (Cub + e2), 16-byte aligned so that
 // a lookup is 2 (fp32) or 3 (fp64) vector loads.
+// fp64: 48 B -- a stride of 12 banks, so the 8 lanes of a quarter-warp phase reading 8 different
+// records hit disjoint banks (a 64 B record measured 22% slower on cfg4: 4-way conflicts).
 template <typename T> struct alignas(16) WRec {
-  T x0, ih, y0, dy, e1, e2;
+  T x0, ih, y0, dy, e1, e2;  // the interval's left knot, then its cubic (Cub + e2)
 };
 template <typename T> __device__ __forceinline__ WRec<T> ld_wrec(const WRec<T> *p) {
   using VT = typename Vec16<T>::V;
@@ -1042,12 +1044,143 @@ __device__ __forceinline__ bool sorted_run(const T *__restrict__ X, const T *__r
   return oor;
 }
 
+// The dense-run form (FORM_RECORD with the window): every lane takes V consecutive queries per
+// warp step; its first query is located by a branch-free 5-level search over the window's knots,
+// the following ones by two branch-free advance steps from the previous slot (sorted: rarely more
+// than one interval apart), and every hit is VERIFIED against the record's own [x0, x1] -- a
+// miss (below / beyond the window, or a wrong sorted hint) takes the general path, so idx is the
+// locate rule's on any input.  The window (32 records) is rebuilt at the carry when the carry
+// leaves it or the step's last query passes its end.  Bitwise the other forms' out (make_cub +
+// cub_eval on the same interval).
+template <typename T, int FORM, typename ZA>
+__device__ __forceinline__ T general_query(const T *__restrict__ X, const T *__restrict__ Y, const ZA &Z, int n, T qc,
+                                           int &j) {
+  if (__ldg(X + j) > qc) {
+    j = bisect(X, n, qc);  // below the carry: unsorted input despite the hint
+  } else {
+    int steps = 0;
+    while (j < n - 2 && __ldg(X + j + 1) <= qc) {
+      ++j;
+      if (++steps == 8) {  // sparse queries: gallop the rest of the way
+        j = gallop_up(X, n, j, qc);
+        break;
+      }
+    }
+  }
+  const T xa = __ldg(X + j), xb = __ldg(X + j + 1);
+  if constexpr (FORM == FORM_NOOP) return __ldg(Y + j);
+  else return interp_form<T, FORM>(qc, xa, xb, __ldg(Y + j), __ldg(Y + j + 1), Z(j), Z(j + 1));
+}
+
+template <typename T, int V, int PF, typename ZA>
+__device__ __forceinline__ bool sorted_run_win(const T *__restrict__ X, const T *__restrict__ Y, const ZA &Z, int n,
+                                               const T *__restrict__ qb, T *__restrict__ ob, int32_t *__restrict__ ib,
+                                               int64_t k0, int64_t k1, SortWin<T> &sw, int lane) {
+  const T x0 = __ldg(X), xn = __ldg(X + n - 1);
+  T qf = __ldg(qb + k0);
+  qf = (qf >= x0 && qf <= xn) ? qf : x0;
+  int jc = warp_locate(X, n, qf, lane);
+  bool oor = false;
+  int wb = -(1 << 30);
+  T xwhi = -inf_of<T>();  // x_{wb+32} (or +inf past the curve): the window's end, in a register
+  T qr[PF + 1][V];
+#pragma unroll
+  for (int d = 0; d <= PF; ++d)
+#pragma unroll
+    for (int i = 0; i < V; ++i) qr[d][i] = x0;  // lanes past the run's end keep a harmless value
+#pragma unroll
+  for (int d = 0; d < PF; ++d) {
+    const int64_t kd = k0 + (int64_t)(d * 32 + lane) * V;
+    if (kd < k1) VecIO<T, V>::load(qb + kd, qr[d]);
+  }
+  for (int64_t base = k0; base < k1; base += 32 * V) {
+    const int64_t k = base + (int64_t)lane * V;
+    const int64_t kn = k + (int64_t)PF * 32 * V;
+    if (kn < k1) VecIO<T, V>::load(qb + kn, qr[PF]);  // PF steps ahead
+    // warp-uniform rebuild: the carry left the window, or the step's last query passes its end
+    // (the last lane's query is only a hint: a miss is caught by the verification below)
+    const T ql = __shfl_sync(0xffffffffu, qr[0][V - 1], 31);
+    if (jc < wb || jc >= wb + kSortWin || !(ql < xwhi)) {
+      __syncwarp();
+      wb = jc;
+      const int jw = wb + lane;
+      if (jw <= n - 2) {
+        const T xa = __ldg(X + jw), xb = __ldg(X + jw + 1);
+        T e2;
+        const Cub<T> cb = make_cub<T>(xa, xb, __ldg(Y + jw), __ldg(Y + jw + 1), Z(jw), Z(jw + 1), e2);
+        sw.r[lane] = WRec<T>{xa, cb.ih, cb.y0, cb.dy, cb.e1, e2};
+        sw.x[lane] = xa;
+        if (lane == kSortWin - 1) sw.x[kSortWin] = xb;
+      } else {
+        sw.x[lane] = inf_of<T>();
+        if (lane == kSortWin - 1) sw.x[kSortWin] = inf_of<T>();
+      }
+      __syncwarp();
+      xwhi = sw.x[kSortWin];
+    }
+    int jl = -1;
+    if (k < k1) {
+      T val[V];
+      int jj[V];
+      int l = 0, j = jc;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const T qq = qr[0][i];
+        const bool in = (qq >= x0) && (qq <= xn);
+        const T qc = in ? qq : x0;
+        if (i == 0) {  // largest slot l <= 31 with x_{wb+l} <= qc (x_{wb} <= qc assumed; verified below)
+          l = 0;
+#pragma unroll
+          for (int d = kSortWin / 2; d >= 1; d >>= 1) l = (sw.x[l + d] <= qc) ? l + d : l;
+        } else {       // sorted: the previous query's slot, at most two intervals back
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            const int p = min(l + 1, kSortWin - 1);
+            l = (sw.x[p] <= qc) ? p : l;
+          }
+        }
+        const WRec<T> r = ld_wrec(&sw.r[l]);
+        const T rx1 = sw.x[l + 1];
+        T v;
+        if (qc >= r.x0 && (qc < rx1 || wb + l == n - 2)) {
+          j = wb + l;
+          v = cub_eval<T>(Cub<T>{r.ih, r.y0, r.dy, r.e1}, r.e2, r.x0, qc);
+        } else {  // outside the window or a wrong hint: the general path from the last interval
+          v = general_query<T, FORM_RECORD>(X, Y, Z, n, qc, j);
+        }
+        val[i] = in ? v : qnan<T>();
+        jj[i] = in ? j : -1;
+        oor |= !in;
+        if (in) jl = j;
+      }
+      VecIO<T, V>::store(ob + k, val);
+      if (ib) VecIO<T, V>::store_idx(ib + k, jj);
+    }
+    const int jm = __reduce_max_sync(0xffffffffu, jl);
+    if (jm >= 0) jc = jm;
+#pragma unroll
+    for (int d = 0; d < PF; ++d)
+#pragma unroll
+      for (int i = 0; i < V; ++i) qr[d][i] = qr[d + 1][i];
+  }
+  return oor;
+}
+
 #ifndef FS_SORTED_PF
 #define FS_SORTED_PF 1
 #endif
 constexpr int kSortedPF = FS_SORTED_PF;  // query prefetch depth of k_eval_sorted (warp steps)
+#ifndef FS_SORTED_SEARCH
+#define FS_SORTED_SEARCH 0
+#endif
+// 1: sorted_run_win (branch-free search + advance + verify); 0: the window lift of sorted_run
+// (measured faster on cfg4: 1113 vs 1266 us -- DESIGN.md)
+constexpr bool kSortedSearchForm = FS_SORTED_SEARCH != 0;
+#ifndef FS_SORTED_MINB
+#define FS_SORTED_MINB 4
+#endif
 template <typename T, int V, int FORM = FORM_RECORD, bool WIN = false>
-__global__ void __launch_bounds__(256, 4) k_eval_sorted(unsigned *__restrict__ status, const T *__restrict__ x,
+__global__ void __launch_bounds__(256, FS_SORTED_MINB) k_eval_sorted(unsigned *__restrict__ status, const T *__restrict__ x,
                                                        const T *__restrict__ y, const T *__restrict__ y2, int n,
                                                        const T *__restrict__ q, int64_t m, T *__restrict__ out,
                                                        int32_t *__restrict__ idx, int64_t qrun,
@@ -1061,9 +1194,14 @@ __global__ void __launch_bounds__(256, 4) k_eval_sorted(unsigned *__restrict__ s
   const int64_t k0 = (task - c * runs_per_curve) * qrun;
   const int64_t k1 = min64(m, k0 + qrun);
   __shared__ SortWin<T> wins[8];  // one per warp of the 256-thread CTA
-  const bool oor = sorted_run<T, V, FORM, WIN, kSortedPF>(x + c * n, y + c * n, ZGlobal<T>{y2 + c * n}, n, q + c * m,
-                                               out + c * m, idx ? idx + c * m : nullptr, k0, k1,
-                                               wins[threadIdx.x >> 5], lane);
+  bool oor;
+  if constexpr (WIN && kSortedSearchForm)
+    oor = sorted_run_win<T, V, kSortedPF>(x + c * n, y + c * n, ZGlobal<T>{y2 + c * n}, n, q + c * m, out + c * m,
+                                          idx ? idx + c * m : nullptr, k0, k1, wins[threadIdx.x >> 5], lane);
+  else
+    oor = sorted_run<T, V, FORM, WIN, kSortedPF>(x + c * n, y + c * n, ZGlobal<T>{y2 + c * n}, n, q + c * m,
+                                                   out + c * m, idx ? idx + c * m : nullptr, k0, k1,
+                                                   wins[threadIdx.x >> 5], lane);
   raise_status_warp(status, oor, kOutOfRange);
 }
 

@@ -21,7 +21,7 @@ namespace fs {
 
 constexpr int kTileEvalWarps = kTileThreads / 32;
 #ifndef FS_TILE_EVAL_PF
-#define FS_TILE_EVAL_PF 4
+#define FS_TILE_EVAL_PF 1
 #endif
 constexpr int kTileEvalPF = FS_TILE_EVAL_PF;  // query prefetch depth (warp steps) of the eval phase
 
@@ -49,9 +49,15 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   per = (per + 32 * V - 1) / (32 * V) * (32 * V);
   const int64_t k0 = q0 + w * per, k1 = min64(q1, k0 + per);
   bool oor = false;
-  if (k0 < k1)
-    oor = sorted_run<T, V, FORM_RECORD, WIN, kTileEvalPF>(x + c * n, y + c * n, ZShared<T, R>{Zs}, n, q + c * m, out + c * m,
-                                             idx ? idx + c * m : nullptr, k0, k1, wins[w], lane);
+  if (k0 < k1) {
+    if constexpr (WIN && kSortedSearchForm)
+      oor = sorted_run_win<T, V, kTileEvalPF>(x + c * n, y + c * n, ZShared<T, R>{Zs}, n, q + c * m, out + c * m,
+                                              idx ? idx + c * m : nullptr, k0, k1, wins[w], lane);
+    else
+      oor = sorted_run<T, V, FORM_RECORD, WIN, kTileEvalPF>(x + c * n, y + c * n, ZShared<T, R>{Zs}, n, q + c * m,
+                                                              out + c * m, idx ? idx + c * m : nullptr, k0, k1,
+                                                              wins[w], lane);
+  }
   raise_status_warp(status, oor, kOutOfRange);
 }
 

@@ -11,6 +11,7 @@
 //                                                          knots + bucket table; SORTED; UNIFORM; BSEARCH)
 //   larger                        k_eval_global          interpolation guess + gallop in HBM
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -24,6 +25,7 @@
 #include "build_tile.cuh"
 #include "common.cuh"
 #include "eval.cuh"
+#include "eval_bucket.cuh"
 #include "fused.cuh"
 #include "fused_tile.cuh"
 
@@ -36,6 +38,7 @@ constexpr int kK1MaxN = 128;
 // launch-latency-sized problems (measured: tools/cmp_paths.py; K1h + curvewarp win from ~2^18)
 constexpr int64_t kFuseMaxWork = int64_t(1) << 17;
 constexpr int kNoFusedStaged = 1 << 30;  // internal: automatic path, but not k_fused_staged
+constexpr int kEvalNoBucket = SPLINE_NO_BUCKET;  // spline_eval: the record-gather path for long curves
 
 template <typename T> constexpr int rmax() { return sizeof(T) == 8 ? 16 : 32; }
 
@@ -464,6 +467,61 @@ int launch_curvewarp(const T *x, const T *y, const T *y2, int n, int64_t batch, 
   }
 }
 
+// ---- one long curve, many unsorted queries: queries bucketed by L2-sized chunks (eval_bucket.cuh)
+constexpr size_t kBkChunkBytes = size_t(24) << 20;  // x, y, y2 of one chunk: 2-3 chunks live in the 126 MB L2
+template <typename T> bool bucket_eligible(int64_t n, int64_t batch, int64_t m) {
+  // the curve must dwarf L2 (else the record gathers hit L2 anyway) and carry many queries
+  return batch == 1 && 3 * sizeof(T) * (size_t)n > 4 * kBkChunkBytes && m >= (int64_t)1 << 20 && m >= n / 4;
+}
+template <typename T>
+int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, int64_t m, T *out, int32_t *idx,
+                  cudaStream_t st) {
+  int64_t K = (int64_t)(kBkChunkBytes / sizeof(Knot<T>));
+  K = std::max<int64_t>(K, (n - 1 + kBkMaxBuckets - 1) / kBkMaxBuckets);
+  const int nb = (int)((n - 1 + K - 1) / K);
+  const int64_t ntiles = (m + kBkTile - 1) / kBkTile;
+  const int64_t L = (int64_t)(nb + 1) * ntiles;  // (bucket, tile) runs, bucket-major
+  const int64_t nblk = (L + kScanBlock - 1) / kScanBlock;
+  const int64_t neval = (m + kBkEvalPer - 1) / kBkEvalPer;
+  if (ntiles >= (int64_t(1) << 31) || L >= (int64_t(1) << 31) || neval >= (int64_t(1) << 31) ||
+      m >= (int64_t(1) << 32))
+    return SPLINE_EINVAL;
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t bk = al(sizeof(Knot<T>) * (size_t)n), bq = al(sizeof(T) * (size_t)m), bd = al(4 * (size_t)m);
+  const size_t bp = al(2 * (size_t)m), bi = idx ? al(4 * (size_t)m) : 0;
+  const size_t bc = al(4 * (size_t)L), bs = al(4 * (size_t)nblk);
+  char *ws = nullptr;
+  if (int rc = ws_alloc((void **)&ws, bk + 2 * bq + bd + bp + bi + bc + bs, st)) return rc;
+  char *p = ws;
+  auto take = [&](size_t b) { char *r = p; p += b; return r; };
+  Knot<T> *kn = (Knot<T> *)take(bk);
+  T *qs = (T *)take(bq);
+  T *os = (T *)take(bq);
+  uint32_t *dest = (uint32_t *)take(bd);
+  uint16_t *perm = (uint16_t *)take(bp);
+  int32_t *is = idx ? (int32_t *)take(bi) : nullptr;
+  int *cnt = (int *)take(bc);
+  int *bsum = (int *)take(bs);
+  int rc = set_smem(k_bucket_scatter<T>, bucket_scatter_smem<T>());
+  if (!rc) rc = set_smem(k_bucket_gather<T>, bucket_gather_smem<T>());
+  if (!rc)
+    rc = launch_pdl(k_bucket_count<T>, dim3((unsigned)ntiles), dim3(kBkScThreads), 0, st, x, (int)n, K, nb, q, m, cnt);
+  if (!rc) {
+    const int64_t pg = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+    k_pack_knots<T><<<(unsigned)pg, 256, 0, st>>>(x, y, y2, n, kn);
+    k_scan_blocks<<<(unsigned)nblk, 1024, 0, st>>>(cnt, L, bsum);
+    k_scan_top<<<1, 1024, 0, st>>>(bsum, (int)nblk);
+    k_bucket_scatter<T><<<(unsigned)ntiles, kBkScThreads, bucket_scatter_smem<T>(), st>>>(x, (int)n, K, nb, q, m, cnt,
+                                                                                           bsum, qs, dest, perm);
+    k_bucket_eval<T><<<(unsigned)neval, kBkThreads, 0, st>>>(tl_status, kn, (int)n, K, nb, m, cnt, bsum, qs, dest, os,
+                                                             is);
+    k_bucket_gather<T><<<(unsigned)ntiles, kBkScThreads, bucket_gather_smem<T>(), st>>>(os, is, perm, m, out, idx);
+    rc = launch_rc();
+  }
+  cudaFreeAsync(ws, st);
+  return rc;
+}
+
 template <typename T>
 int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const T *q, int64_t m, T *out,
            int32_t *idx, int flags, cudaStream_t st) {
@@ -512,6 +570,8 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
     if (stage_total<T>(1, nn, MODE_BSEARCH, kQMax) <= kSmemCap)
       return launch_staged<T, MODE_BSEARCH>(x, y, y2, nn, batch, q, m, out, idx, st);
   }
+  if (bucket_eligible<T>(n, batch, m) && !(flags & kEvalNoBucket))
+    return eval_bucketed<T>(x, y, y2, n, q, m, out, idx, st);
   const int64_t total = batch * m;
   // interval records in a pooled workspace: one gather round trip per query
   const size_t rec_bytes = sizeof(Ival<T>) * (size_t)n * batch, hdr_bytes = sizeof(CurveHdr<T>) * (size_t)batch;
@@ -1011,6 +1071,68 @@ int check_spike(const void *x, const void *y, int64_t n, int64_t rb, int64_t re,
 }
 }  // namespace
 
+// ---- the multi-GPU long-curve build over an NCCL communicator (spline_build_dist) ------------
+// NCCL is resolved at run time (dlopen: the process's already-loaded libnccl.so.2, else the one
+// SPLINE_NCCL_LIB names, else the loader's), so the library needs no link-time NCCL and a
+// missing NCCL is an error code (SPLINE_ENCCL), not a load failure.
+namespace {
+typedef int (*nccl_count_fn)(void *, int *);
+typedef int (*nccl_rank_fn)(void *, int *);
+typedef int (*nccl_allgather_fn)(const void *, void *, size_t, int, void *, cudaStream_t);
+struct NcclApi {
+  nccl_count_fn count = nullptr;
+  nccl_rank_fn rank = nullptr;
+  nccl_allgather_fn allgather = nullptr;
+  bool ok = false;
+};
+const NcclApi &nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *h = nullptr;
+    const char *env = getenv("SPLINE_NCCL_LIB");
+    if (env && *env) {
+      h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+    } else {
+      h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+      if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    }
+    if (!h) return;
+    api.count = (nccl_count_fn)dlsym(h, "ncclCommCount");
+    api.rank = (nccl_rank_fn)dlsym(h, "ncclCommUserRank");
+    api.allgather = (nccl_allgather_fn)dlsym(h, "ncclAllGather");
+    api.ok = api.count && api.rank && api.allgather;
+  });
+  return api;
+}
+constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8;  // ncclDataType_t (nccl.h)
+
+template <typename T>
+int build_dist_t(const T *x, const T *y, int64_t n, int bc, const T *yp1, const T *ypn, T *y2_shard, void *comm,
+                 cudaStream_t st) {
+  const NcclApi &nc = nccl_api();
+  if (!nc.ok) return SPLINE_ENCCL;
+  int G = 0, r = 0;
+  if (nc.count(comm, &G) != 0 || nc.rank(comm, &r) != 0 || G < 1 || r < 0 || r >= G) return SPLINE_ENCCL;
+  if (G > kMaxRanks) return SPLINE_EINVAL;
+  const int64_t rb = n * r / G, re = n * (r + 1) / G;  // this rank's rows (dist.shard_rows)
+  if (re <= rb) return SPLINE_EINVAL;                  // more ranks than rows
+  constexpr int R = rmax<T>();
+  const int64_t ntiles = (re - rb + 256 * R - 1) / (256 * R);
+  const size_t wsb = (spike_ws_layout<T>(ntiles, 1, nullptr, nullptr) + 255) & ~(size_t)255;
+  const size_t recb = (sizeof(T) * 6 * (size_t)(G + 1) + 255) & ~(size_t)255;
+  char *base = nullptr;
+  if (int rc = ws_alloc((void **)&base, wsb + recb, st)) return rc;
+  T *rec = (T *)(base + wsb), *all = rec + 6;
+  int rc = spike_reduce_t<T>(x, y, n, rb, re, bc, yp1, ypn, rec, base, st);
+  // the exchange step of the partitioned solve: every rank's 6-scalar block record to every rank
+  if (!rc && nc.allgather(rec, all, 6, sizeof(T) == 8 ? kNcclFloat64 : kNcclFloat32, comm, st) != 0) rc = SPLINE_ENCCL;
+  if (!rc) rc = spike_finish_t<T>(x, y, n, rb, re, bc, yp1, ypn, all, G, r, y2_shard, base, st);
+  cudaFreeAsync(base, st);
+  return rc;
+}
+}  // namespace
+
 extern "C" {
 
 int spline_build(const void *x, const void *y, int64_t n, int64_t batch, int bc, const void *yp1, const void *ypn,
@@ -1031,7 +1153,7 @@ int spline_eval(const void *x, const void *y, const void *y2, int64_t n, int64_t
                 void *out, int32_t *idx, int flags, int dtype, spline_stream_t stream) {
   if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
   if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || m < 0 || m >= (int64_t(1) << 31)) return SPLINE_EINVAL;
-  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM)) return SPLINE_EINVAL;
+  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM | SPLINE_NO_BUCKET)) return SPLINE_EINVAL;
   if (batch == 0 || m == 0) return SPLINE_OK;
   if (!x || !y || !y2 || !q || !out) return SPLINE_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1193,6 +1315,30 @@ int spline_spike_finish(const void *x, const void *y, int64_t n, int64_t row_beg
                                 (double *)y2_shard, workspace, st);
 }
 
-const char *spline_version(void) { return "fastspline-b200 0.1 (sm_100a)"; }
+int spline_build_dist(const void *x, const void *y, int64_t n, int bc, const void *yp1, const void *ypn,
+                      void *y2_shard, spline_nccl_comm_t comm, int dtype, spline_stream_t stream) {
+  if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
+  if (n < 3 || n >= (int64_t(1) << 31) || bc < 0 || bc > 3) return SPLINE_EINVAL;
+  if (!x || !y || !y2_shard || !comm || ((bc & 1) && !yp1) || ((bc & 2) && !ypn)) return SPLINE_EINVAL;
+  if (!nccl_api().ok) return SPLINE_ENCCL;
+  cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
+  if (dtype == SPLINE_F32)
+    return build_dist_t<float>((const float *)x, (const float *)y, n, bc, (const float *)yp1, (const float *)ypn,
+                               (float *)y2_shard, (void *)comm, st);
+  return build_dist_t<double>((const double *)x, (const double *)y, n, bc, (const double *)yp1, (const double *)ypn,
+                              (double *)y2_shard, (void *)comm, st);
+}
+int spline_build_dist_f32(const float *x, const float *y, int64_t n, int bc, const float *yp1, const float *ypn,
+                          float *y2_shard, spline_nccl_comm_t comm, spline_stream_t stream) {
+  return spline_build_dist(x, y, n, bc, yp1, ypn, y2_shard, comm, SPLINE_F32, stream);
+}
+int spline_build_dist_f64(const double *x, const double *y, int64_t n, int bc, const double *yp1, const double *ypn,
+                          double *y2_shard, spline_nccl_comm_t comm, spline_stream_t stream) {
+  return spline_build_dist(x, y, n, bc, yp1, ypn, y2_shard, comm, SPLINE_F64, stream);
+}
+
+const char *spline_version(void) { return "fastspline-b200 0.2 (sm_100a)"; }
 
 }  // extern "C"

@@ -21,7 +21,8 @@ def declared_functions():
 def test_header_declares_the_north_star_entry_points():
     names = declared_functions()
     for required in ["spline_build", "spline_eval", "spline_build_f32", "spline_build_f64", "spline_eval_f32",
-                     "spline_eval_f64", "spline_status", "spline_spike_reduce", "spline_spike_finish"]:
+                     "spline_eval_f64", "spline_status", "spline_spike_reduce", "spline_spike_finish",
+                     "spline_build_dist", "spline_build_dist_f32", "spline_build_dist_f64"]:
         assert required in names
 
 
@@ -62,7 +63,7 @@ def test_einval_eval():
     assert lib.spline_eval(p, p, p, 2, 1, p, 4, p, None, 0, F32, None) == _lib.SPLINE_EINVAL   # n < 3
     assert lib.spline_eval(p, p, p, 8, 1, p, -1, p, None, 0, F32, None) == _lib.SPLINE_EINVAL  # m < 0
     assert lib.spline_eval(p, p, p, 8, 1, p, 4, p, None, 8, F32, None) == _lib.SPLINE_EINVAL   # unknown flag
-    assert lib.spline_eval(p, p, p, 8, 1, p, 4, p, None, 16, F32, None) == _lib.SPLINE_EINVAL  # unknown flag
+    assert lib.spline_eval(p, p, p, 8, 1, p, 4, p, None, 32, F32, None) == _lib.SPLINE_EINVAL  # unknown flag
     assert lib.spline_eval(p, None, p, 8, 1, p, 4, p, None, 0, F32, None) == _lib.SPLINE_EINVAL  # NULL y
     assert lib.spline_eval(None, None, None, 8, 1, None, 0, None, None, 0, F32, None) == _lib.SPLINE_OK  # m == 0
     assert lib.spline_eval(None, None, None, 8, 0, None, 9, None, None, 0, F32, None) == _lib.SPLINE_OK  # B == 0
@@ -121,3 +122,28 @@ def test_einval_gather_probe():
     assert lib.spline_gather_probe(p, p, p, 2, 1, p, 4, p, p, p, 0, F64, None) == E    # n < 3
     assert lib.spline_gather_probe(p, p, p, 8, 1, p, 4, None, p, p, 0, F64, None) == E  # NULL idx_in
     assert lib.spline_gather_probe(None, None, None, 8, 0, None, 4, None, None, None, 0, F64, None) == _lib.SPLINE_OK
+
+
+def test_einval_build_dist():
+    lib = _lib.load()
+    p = ctypes.c_void_p(16)
+    F64, E = _lib.SPLINE_F64, _lib.SPLINE_EINVAL
+    assert lib.spline_build_dist(p, p, 100, 0, None, None, p, None, F64, None) == E   # NULL communicator
+    assert lib.spline_build_dist(p, p, 2, 0, None, None, p, p, F64, None) == E        # n < 3
+    assert lib.spline_build_dist(p, p, 100, 1, None, None, p, p, F64, None) == E      # clamped, no yp1
+    assert lib.spline_build_dist(p, p, 100, 0, None, None, p, p, 9, None) == E        # bad dtype
+    assert lib.spline_build_dist(None, p, 100, 0, None, None, p, p, F64, None) == E   # NULL x
+
+
+def test_build_dist_enccl_without_nccl():
+    """NCCL is resolved at run time: with none loadable the distributed build returns SPLINE_ENCCL
+    (before any CUDA or NCCL call), instead of failing to load the library."""
+    import subprocess
+    import sys
+    code = ("import ctypes; from paper_2001_09253_b200 import _lib; p = ctypes.c_void_p(16); "
+            "print(_lib.load().spline_build_dist(p, p, 100, 0, None, None, p, p, _lib.SPLINE_F64, None))")
+    env = dict(os.environ, SPLINE_NCCL_LIB="/nonexistent/libnccl.so.2")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert int(out.stdout.strip().splitlines()[-1]) == _lib.SPLINE_ENCCL

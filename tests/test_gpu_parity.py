@@ -437,3 +437,39 @@ def test_curvewarp_shapes(api, dt, B, n, m):
     e = parity.out_rel_err(out.cpu().numpy(), out_ref, y)
     assert np.all(e <= parity.tol_for(dt))
     assert (bits & api.STATUS_Q_OUT_OF_RANGE) == (api.STATUS_Q_OUT_OF_RANGE if nbad else 0)
+
+
+# ------------------------------------------- one long curve: queries bucketed by L2-sized chunks
+
+@pytest.mark.parametrize("n,m", [((1 << 23) + 77, 1 << 22), (1 << 24, (1 << 21) + 13)])
+def test_long_curve_bucketed_eval(api, n, m):
+    """Curves far larger than L2 with many unsorted queries take the bucketed eval
+    (k_bucket_scatter -> k_bucket_eval -> k_bucket_gather): the oracle's idx bit for bit and out
+    within tolerance, including knot ties at chunk boundaries, both ends, out of range and NaN --
+    and bitwise the record-gather path (SPLINE_NO_BUCKET)."""
+    wl = workloads.generate(5, n=n, m=m)
+    K = (24 << 20) // 32                                   # chunk width of the fp64 path (24 MB of 32 B knots)
+    ties = [wl.x[0, k] for k in range(0, n - 1, K)] + [wl.x[0, K - 1], wl.x[0, K + 1], wl.x[0, 2 * K - 1]]
+    wl.q[0, :len(ties)] = ties                             # queries ON chunk-boundary knots
+    wl.q[0, 100] = wl.x[0, -1]
+    wl.q[0, 101] = wl.x[0, 0]
+    wl.q[0, 102] = -0.5
+    wl.q[0, 103] = 2.0
+    wl.q[0, 104] = np.nan
+    wl.q[0, 105] = np.nextafter(wl.x[0, -1], 2.0)
+    api.status()
+    x, y, y2 = parity.gpu_build(api, wl)
+    y2_ref = parity.oracle_build(wl)
+    assert parity.y2_rel_err(y2.cpu().numpy(), y2_ref).max() <= 1e-12
+    q = parity.to_dev(wl.q)
+    out_ref, idx_ref, nbad = oracle.evaluate(wl.x, wl.y, y2_ref, wl.q, nthreads=16)
+    assert nbad == 4
+    out, idx = api.evaluate(x, y, parity.to_dev(y2_ref), q, 0)
+    assert api.status() == api.STATUS_Q_OUT_OF_RANGE
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_ref)
+    assert parity.out_rel_err(out.cpu().numpy(), out_ref, wl.y).max() <= 1e-12
+    out_r, idx_r = api.evaluate(x, y, parity.to_dev(y2_ref), q, api.NO_BUCKET)
+    api.status()
+    assert torch.equal(idx, idx_r) and torch.equal(out.view(torch.int8), out_r.view(torch.int8))
+    _, none = api.evaluate(x, y, parity.to_dev(y2_ref), q, 0, want_idx=False)  # no idx output
+    assert none is None
