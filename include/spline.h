@@ -70,7 +70,15 @@ enum {
 /* SPLINE_NO_BUCKET (spline_eval only): on one curve too long for L2 with many unsorted queries, do
  * not bucket the queries by curve chunk (eval_bucket.cuh); use the one-gather-per-query record
  * path instead (measurement and A/B; same results bitwise). */
-enum { SPLINE_Q_SORTED = 1, SPLINE_X_UNIFORM = 2, SPLINE_PATH_FUSED = 4, SPLINE_PATH_SPLIT = 8, SPLINE_NO_BUCKET = 16 };
+/* SPLINE_X_SHARED (shared-knot mode): every curve of the batch has the SAME knots; x is then ONE
+ * row [n] (not [batch][n]).  Given in `bc` of spline_build and in `flags` of spline_eval /
+ * spline_build_eval / spline_build_eval_host.  The paper evaluates on one grid right after the
+ * build; BASELINE cfg3's grid is one uniform grid.  Native (knots read once per
+ * curve tile, not per curve) in the short-curve kernels (n <= 8: K1r, and k_eval_small for fp32
+ * with m <= 32); other shapes broadcast the row into stream-ordered scratch first.  Results are
+ * bitwise those of the same call with the row repeated per curve. */
+enum { SPLINE_Q_SORTED = 1, SPLINE_X_UNIFORM = 2, SPLINE_PATH_FUSED = 4, SPLINE_PATH_SPLIT = 8, SPLINE_NO_BUCKET = 16,
+       SPLINE_X_SHARED = 32 };
 /* Asynchronous data-error bits (spline_status). */
 enum { SPLINE_STATUS_BAD_KNOTS = 1, SPLINE_STATUS_Q_OUT_OF_RANGE = 2 };
 

@@ -13,7 +13,7 @@ from . import _build
 SPLINE_F32, SPLINE_F64 = 0, 1
 SPLINE_OK, SPLINE_EINVAL, SPLINE_ECUDA, SPLINE_ENOMEM, SPLINE_ENCCL = 0, -1, -2, -3, -4
 BC_NATURAL, BC_CLAMP_START, BC_CLAMP_END, BC_CLAMPED = 0, 1, 2, 3
-Q_SORTED, X_UNIFORM, PATH_FUSED, PATH_SPLIT, NO_BUCKET = 1, 2, 4, 8, 16
+Q_SORTED, X_UNIFORM, PATH_FUSED, PATH_SPLIT, NO_BUCKET, X_SHARED = 1, 2, 4, 8, 16, 32
 STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE = 1, 2
 FORMS = {"record": 0, "splint_div": 1, "splint_mul": 2, "newint_orig": 3, "newint_noinv": 4, "noop": 5}
 

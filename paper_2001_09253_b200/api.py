@@ -12,7 +12,7 @@ import torch
 
 from . import _lib
 from ._lib import (BC_CLAMP_END, BC_CLAMP_START, BC_CLAMPED, BC_NATURAL, NO_BUCKET, PATH_FUSED,  # noqa: F401
-                   PATH_SPLIT, Q_SORTED, STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE, X_UNIFORM)
+                   PATH_SPLIT, Q_SORTED, STATUS_BAD_KNOTS, STATUS_Q_OUT_OF_RANGE, X_SHARED, X_UNIFORM)
 
 _DT = {torch.float32: _lib.SPLINE_F32, torch.float64: _lib.SPLINE_F64}
 
@@ -62,6 +62,21 @@ def _check_buf(t, shape, dtype, device, what, host=False):
         raise ValueError(f"{what} must be contiguous")
 
 
+def _curves(x, y):
+    """The knots and values of a call: (x2d, y2d, shared, squeeze).  x (n,) with y (B, n) is the
+    shared-knot mode (SPLINE_X_SHARED: one knot vector for the whole batch); x, y both (n,) is
+    one curve; both (B, n) a batch."""
+    if isinstance(x, torch.Tensor) and isinstance(y, torch.Tensor) and x.dim() == 1 and y.dim() == 2:
+        if x.shape[0] != y.shape[1]:
+            raise ValueError("shared knots: x must be (n,) for y (B, n)")
+        return x.unsqueeze(0), y, True, False
+    squeeze = x.dim() == 1
+    x, y = _as2d(x), _as2d(y)
+    if y.shape != x.shape:
+        raise ValueError("x and y must have the same shape (or x (n,) shared by y (B, n))")
+    return x, y, False, squeeze
+
+
 def _slopes(v, B, like, host=False):
     """Per-curve clamped slope: a scalar is broadcast, a tensor must be (B,)."""
     if v is None:
@@ -72,33 +87,34 @@ def _slopes(v, B, like, host=False):
 
 
 def build(x: torch.Tensor, y: torch.Tensor, bc: int = BC_NATURAL, yp1=None, ypn=None, out=None, stream=None):
-    """Second derivatives y2 of the curves (x, y): (B, n) or (n,).  Returns y2."""
-    squeeze = x.dim() == 1
-    x, y = _as2d(x), _as2d(y)
-    B, n = x.shape
+    """Second derivatives y2 of the curves (x, y): (B, n) or (n,), or x (n,) shared by y (B, n).
+    Returns y2 (y's shape)."""
+    x, y, shared, squeeze = _curves(x, y)
+    B, n = y.shape
     yp1, ypn = _slopes(yp1, B, x), _slopes(ypn, B, x)
     _check_curves(x, y)
-    if y.shape != x.shape:
-        raise ValueError("x and y must have the same shape")
     _check_buf(yp1, (B,), x.dtype, x.device, "yp1")
     _check_buf(ypn, (B,), x.dtype, x.device, "ypn")
-    y2 = torch.empty_like(x) if out is None else _as2d(out)
-    _check_buf(y2, x.shape, x.dtype, x.device, "y2 (out)")
-    rc = _lib.load().spline_build(_p(x), _p(y), n, B, bc, _p(yp1), _p(ypn), _p(y2), _DT[x.dtype],
-                                  ctypes.c_void_p(_stream(stream)))
+    y2 = torch.empty_like(y) if out is None else _as2d(out)
+    _check_buf(y2, y.shape, x.dtype, x.device, "y2 (out)")
+    rc = _lib.load().spline_build(_p(x), _p(y), n, B, bc | (X_SHARED if shared else 0), _p(yp1), _p(ypn), _p(y2),
+                                  _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
     _lib.check(rc, "spline_build")
     return y2[0] if squeeze else y2
 
 
 def evaluate(x, y, y2, q, flags: int = 0, out=None, idx=None, want_idx: bool = True, stream=None):
-    """Locate + evaluate queries q (B, m) on curves (B, n).  Returns (out, idx or None)."""
-    squeeze = x.dim() == 1
-    x, y, y2, q = _as2d(x), _as2d(y), _as2d(y2), _as2d(q)
-    B, n = x.shape
+    """Locate + evaluate queries q (B, m) on curves (B, n) (x may be (n,) shared by the batch).
+    Returns (out, idx or None)."""
+    x, y, shared, squeeze = _curves(x, y)
+    y2, q = _as2d(y2), _as2d(q)
+    B, n = y.shape
     m = q.shape[1]
     _check_curves(x, y, y2, q)
-    if y.shape != x.shape or y2.shape != x.shape or q.dim() != 2 or q.shape[0] != B:
+    if y2.shape != y.shape or q.dim() != 2 or q.shape[0] != B:
         raise ValueError("x, y, y2 must be (B, n) and q (B, m)")
+    if shared:
+        flags |= X_SHARED
     o = torch.empty_like(q) if out is None else _as2d(out)
     _check_buf(o, q.shape, q.dtype, q.device, "out")
     i = None
@@ -117,20 +133,22 @@ def build_eval(x, y, q, bc: int = BC_NATURAL, yp1=None, ypn=None, flags: int = 0
                y2=None, out=None, idx=None, want_idx: bool = True, stream=None):
     """Build + evaluate in one call (spline_build_eval; one fused kernel for n <= 128).
     Returns (y2 or None, out, idx or None); bitwise equal to build() then evaluate()."""
-    squeeze = x.dim() == 1
-    x, y, q = _as2d(x), _as2d(y), _as2d(q)
-    B, n = x.shape
+    x, y, shared, squeeze = _curves(x, y)
+    q = _as2d(q)
+    B, n = y.shape
     m = q.shape[1]
     yp1, ypn = _slopes(yp1, B, x), _slopes(ypn, B, x)
     _check_curves(x, y, q)
-    if y.shape != x.shape or q.dim() != 2 or q.shape[0] != B:
+    if q.dim() != 2 or q.shape[0] != B:
         raise ValueError("x, y must be (B, n) and q (B, m)")
+    if shared:
+        flags |= X_SHARED
     _check_buf(yp1, (B,), x.dtype, x.device, "yp1")
     _check_buf(ypn, (B,), x.dtype, x.device, "ypn")
     z = None
     if want_y2:
-        z = torch.empty_like(x) if y2 is None else _as2d(y2)
-        _check_buf(z, x.shape, x.dtype, x.device, "y2")
+        z = torch.empty_like(y) if y2 is None else _as2d(y2)
+        _check_buf(z, y.shape, x.dtype, x.device, "y2")
     o = torch.empty_like(q) if out is None else _as2d(out)
     _check_buf(o, q.shape, q.dtype, q.device, "out")
     i = None
@@ -153,12 +171,14 @@ def build_eval_host(x, y, q, bc: int = BC_NATURAL, yp1=None, ypn=None, flags: in
     for t in (x, y, q):
         if not isinstance(t, torch.Tensor) or t.device.type != "cpu" or not t.is_contiguous():
             raise ValueError("build_eval_host takes contiguous CPU tensors (pinned for overlap)")
-    squeeze = x.dim() == 1
-    x, y, q = _as2d(x), _as2d(y), _as2d(q)
-    B, n = x.shape
+    x, y, shared, squeeze = _curves(x, y)
+    q = _as2d(q)
+    B, n = y.shape
     m = q.shape[1]
-    if y.shape != x.shape or q.shape[0] != B or y.dtype != x.dtype or q.dtype != x.dtype:
+    if q.shape[0] != B or y.dtype != x.dtype or q.dtype != x.dtype:
         raise ValueError("x, y must be (B, n) and q (B, m), one dtype")
+    if shared:
+        flags |= X_SHARED
     if x.dtype not in _DT:
         raise ValueError("dtype must be float32 or float64")
     pin = x.is_pinned()
@@ -170,10 +190,10 @@ def build_eval_host(x, y, q, bc: int = BC_NATURAL, yp1=None, ypn=None, flags: in
     yp1, ypn = _slopes(yp1, B, x, host=True), _slopes(ypn, B, x, host=True)
     _check_buf(yp1, (B,), x.dtype, None, "yp1", host=True)
     _check_buf(ypn, (B,), x.dtype, None, "ypn", host=True)
-    z = (host_like(x.shape, x.dtype) if y2 is None else _as2d(y2)) if want_y2 else None
+    z = (host_like(y.shape, x.dtype) if y2 is None else _as2d(y2)) if want_y2 else None
     o = host_like(q.shape, q.dtype) if out is None else _as2d(out)
     i = (host_like(q.shape, torch.int32) if idx is None else _as2d(idx)) if want_idx else None
-    _check_buf(z, x.shape, x.dtype, None, "y2", host=True)
+    _check_buf(z, y.shape, x.dtype, None, "y2", host=True)
     _check_buf(o, q.shape, q.dtype, None, "out", host=True)
     _check_buf(i, q.shape, torch.int32, None, "idx", host=True)
     rc = _lib.load().spline_build_eval_host(_p(x), _p(y), n, B, bc, _p(yp1), _p(ypn), _p(z), _p(q), m, _p(o),

@@ -384,12 +384,13 @@ __device__ __forceinline__ bool thomas_regs(const T (&xv)[NMAX], const T (&yv)[N
 template <typename T, int NMAX>
 __global__ void __launch_bounds__(256) k1_thomas_regs(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int n,
                                                       int64_t batch, int bc, const T *__restrict__ yp1,
-                                                      const T *__restrict__ ypn, T *__restrict__ y2, int vec) {
+                                                      const T *__restrict__ ypn, T *__restrict__ y2, int vec,
+                                                      int64_t xs) {
   pdl_trigger();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= batch) return;
   T xv[NMAX], yv[NMAX];
-  const T *xc = x + c * n, *yc = y + c * n;
+  const T *xc = x + c * xs, *yc = y + c * n;  // xs = n, or 0: one knot vector shared by the batch
   constexpr int VW = 16 / sizeof(T);
   if (vec) {  // n % VW == 0 and 16-byte aligned rows
     using VT = typename Vec16<T>::V;

@@ -180,6 +180,15 @@ __device__ __forceinline__ T nr_interp(T q, T x0, T x1, T y0, T y1, T z0, T z1) 
   return cub_eval<T>(c, e2, x0, q);
 }
 
+// Shared-knot mode (SPLINE_X_SHARED) for kernels that read a knot row per curve: the one
+// knot vector broadcast into a [batch][n] scratch (row r = x).  out[i] = x[i mod n].
+template <typename T>
+__global__ void __launch_bounds__(256) k_broadcast_rows(const T *__restrict__ x, int64_t n, int64_t total,
+                                                        T *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __ldg(x + i % n);
+}
+
 }  // namespace fs
 
 namespace fs {

@@ -731,7 +731,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SOLVE ? 4 : 6) k_eval_small(
                                                                  int vecn, int bc = 0,
                                                                  const float *__restrict__ yp1 = nullptr,
                                                                  const float *__restrict__ ypn = nullptr,
-                                                                 float *__restrict__ y2w = nullptr) {
+                                                                 float *__restrict__ y2w = nullptr,
+                                                                 int64_t xs = -1) {
   pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch; SOLVE too: its
               // launch carries the attribute, and its outputs must not race the predecessor)
   constexpr int MV = kSmallM;  // at most m vectors per lane (32 curves x m queries / (32 lanes x 4))
@@ -746,14 +747,15 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SOLVE ? 4 : 6) k_eval_small(
     const int nq = nc * m;          // the tile's queries, contiguous from q + c0 m
     const int nv = nq >> 2;         // 16-byte vectors
     const float *qt = q + c0 * m;
-    // records of curve c0 + lane
+    // records of curve c0 + lane (xs: the knot row stride -- n, or 0 when the batch shares x)
     if (lane < nc) {
       const int64_t c = c0 + lane;
+      const float *xr = x + c * (xs < 0 ? (int64_t)n : xs);
       float xv[kSmallN], yv[kSmallN], zv[kSmallN];
       if (vecn) {  // n == 8 with 16-byte aligned rows
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const float4 a = __ldg(reinterpret_cast<const float4 *>(x + c * 8) + h);
+          const float4 a = __ldg(reinterpret_cast<const float4 *>(xr) + h);
           const float4 b = __ldg(reinterpret_cast<const float4 *>(y + c * 8) + h);
           xv[4 * h] = a.x; xv[4 * h + 1] = a.y; xv[4 * h + 2] = a.z; xv[4 * h + 3] = a.w;
           yv[4 * h] = b.x; yv[4 * h + 1] = b.y; yv[4 * h + 2] = b.z; yv[4 * h + 3] = b.w;
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SOLVE ? 4 : 6) k_eval_small(
 #pragma unroll
         for (int j = 0; j < kSmallN; ++j) {
           const int jj = min(j, n - 1);
-          xv[j] = __ldg(x + c * n + jj);
+          xv[j] = __ldg(xr + jj);
           yv[j] = __ldg(y + c * n + jj);
           if constexpr (!SOLVE) zv[j] = __ldg(y2 + c * n + jj);
         }

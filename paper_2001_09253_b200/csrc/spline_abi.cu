@@ -148,6 +148,17 @@ inline int num_sms() {
 
 
 
+// Shared-knot mode (SPLINE_X_SHARED): kernels without a native knot-row stride get the knot
+// vector broadcast into stream-ordered scratch ([batch][n]) first; results are bitwise the
+// per-curve-x call's (the kernels see the same values).
+template <typename T> int broadcast_x(const T *x, int64_t n, int64_t batch, cudaStream_t st, T **out) {
+  if (int rc = ws_alloc((void **)out, sizeof(T) * (size_t)n * batch, st)) return rc;
+  const int64_t total = n * batch;
+  const int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+  k_broadcast_rows<T><<<(unsigned)grid, 256, 0, st>>>(x, n, total, *out);
+  return launch_rc();
+}
+
 // ------------------------------------------------------------------------ build
 
 template <typename T, int R>
@@ -261,13 +272,21 @@ int build_long(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T
 
 template <typename T>
 int build_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
-            cudaStream_t st) {
+            cudaStream_t st, bool xshared = false) {
   if (n <= kRegsNMax) {  // K1r: registers only (the fused kernel's SOLVE_REGS takes the same n)
     constexpr int VW = 16 / sizeof(T);
     const int vec = (n % VW == 0) && aligned16(x) && aligned16(y) && aligned16(y2);
     const int64_t grid = (batch + 255) / 256;
-    k1_thomas_regs<T, kRegsNMax><<<(unsigned)grid, 256, 0, st>>>(tl_status, x, y, (int)n, batch, bc, yp1, ypn, y2, vec);
+    k1_thomas_regs<T, kRegsNMax><<<(unsigned)grid, 256, 0, st>>>(tl_status, x, y, (int)n, batch, bc, yp1, ypn, y2, vec,
+                                                                 xshared ? (int64_t)0 : n);
     return launch_rc();
+  }
+  if (xshared && batch > 1) {  // no native knot-row stride: broadcast the knot vector first
+    T *xb = nullptr;
+    int rc = broadcast_x<T>(x, n, batch, st, &xb);
+    if (!rc) rc = build_t<T>(xb, y, n, batch, bc, yp1, ypn, y2, st, false);
+    if (xb) cudaFreeAsync(xb, st);
+    return rc;
   }
   if (n <= kK1MaxN) {  // K1: two threads per curve, staged odd-stride tiles
     // K1h: the same sweep with each half curve in registers (16-byte-aligned rows)
@@ -467,6 +486,12 @@ int launch_curvewarp(const T *x, const T *y, const T *y2, int n, int64_t batch, 
   }
 }
 
+// k_eval_small's shapes: fp32, n <= 8, m <= 32 with m % 4 == 0, 16-byte aligned q, out, idx
+template <typename T> bool small_eval_ok(int64_t n, const T *q, int64_t m, const T *out, const int32_t *idx) {
+  return sizeof(T) == 4 && n <= kSmallN && m > 0 && m <= kSmallM && m % 4 == 0 && aligned16(q) && aligned16(out) &&
+         (!idx || aligned16(idx));
+}
+
 // ---- one long curve, many unsorted queries: queries bucketed by L2-sized chunks (eval_bucket.cuh)
 constexpr size_t kBkChunkBytes = size_t(24) << 20;  // x, y, y2 of one chunk: 2-3 chunks live in the 126 MB L2
 template <typename T> bool bucket_eligible(int64_t n, int64_t batch, int64_t m) {
@@ -525,6 +550,15 @@ int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, in
 template <typename T>
 int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const T *q, int64_t m, T *out,
            int32_t *idx, int flags, cudaStream_t st) {
+  const bool xshared = (flags & SPLINE_X_SHARED) && batch > 1;
+  flags &= ~SPLINE_X_SHARED;
+  if (xshared && !small_eval_ok<T>(n, q, m, out, idx)) {  // no native knot-row stride: broadcast x
+    T *xb = nullptr;
+    int rc = broadcast_x<T>(x, n, batch, st, &xb);
+    if (!rc) rc = eval_t<T>(xb, y, y2, n, batch, q, m, out, idx, flags, st);
+    if (xb) cudaFreeAsync(xb, st);
+    return rc;
+  }
   if (flags & SPLINE_Q_SORTED) {
     constexpr int VW = 16 / sizeof(T);
     // 4 queries per lane and step (fp64: one 256-bit access each for q and out)
@@ -534,8 +568,7 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
     return launch_sorted_k<T, 1>(x, y, y2, (int)n, batch, q, m, out, idx, st);
   }
   if constexpr (sizeof(T) == 4) {  // very short curves with few queries (cfg3): k_eval_small
-    if (n <= kSmallN && m <= kSmallM && m % 4 == 0 && m > 0 && aligned16(q) && aligned16(out) &&
-        (!idx || aligned16(idx))) {
+    if (small_eval_ok<T>(n, q, m, out, idx)) {
       const int vecn = n == kSmallN && aligned16(x) && aligned16(y) && aligned16(y2);
       const int64_t ntiles = (batch + 31) / 32;
       int occ = 0;
@@ -546,7 +579,7 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
       const int64_t grid = std::min<int64_t>((ntiles + kSmallWarps - 1) / kSmallWarps, (int64_t)occ * num_sms());
       return launch_pdl(k_eval_small<false>, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, tl_status, x, y, y2, (int)n,
                         batch, q, (int)m, out, idx, vecn, 0, (const float *)nullptr, (const float *)nullptr,
-                        (float *)nullptr);
+                        (float *)nullptr, xshared ? (int64_t)0 : n);
     }
   }
   {  // curves of up to 64 knots, unsorted queries: one warp per curve (k_eval_curvewarp)
@@ -743,10 +776,11 @@ int launch_tile_eval(const T *x, const T *y, int64_t n, int64_t batch, int bc, c
 template <typename T>
 int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
                  const T *q, int64_t m, T *out, int32_t *idx, int flags, cudaStream_t st) {
-  if (m == 0) return y2 ? build_t<T>(x, y, n, batch, bc, yp1, ypn, y2, st) : SPLINE_OK;
+  const bool xshared = (flags & SPLINE_X_SHARED) && batch > 1;
+  flags &= ~SPLINE_X_SHARED;
+  if (m == 0) return y2 ? build_t<T>(x, y, n, batch, bc, yp1, ypn, y2, st, xshared) : SPLINE_OK;
   if constexpr (sizeof(T) == 4) {  // very short fp32 curves, few queries: solve + eval in k_eval_small<true>
-    if (!(flags & (SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT)) && n <= kSmallN && m <= kSmallM && m % 4 == 0 &&
-        aligned16(q) && aligned16(out) && (!idx || aligned16(idx))) {
+    if (!(flags & (SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT)) && small_eval_ok<T>(n, q, m, out, idx)) {
       const int vecn = n == kSmallN && aligned16(x) && aligned16(y) && (!y2 || aligned16(y2));
       const int64_t ntiles = (batch + 31) / 32;
       int occ = 0;
@@ -756,8 +790,16 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
         occ = 1;
       const int64_t grid = std::min<int64_t>((ntiles + kSmallWarps - 1) / kSmallWarps, (int64_t)occ * num_sms());
       return launch_pdl(k_eval_small<true>, dim3((unsigned)grid), dim3(kSmallWarps * 32), 0, st, tl_status, x, y,
-                        (const float *)nullptr, (int)n, batch, q, (int)m, out, idx, vecn, bc, yp1, ypn, y2);
+                        (const float *)nullptr, (int)n, batch, q, (int)m, out, idx, vecn, bc, yp1, ypn, y2,
+                        xshared ? (int64_t)0 : n);
     }
+  }
+  if (xshared) {  // the other kernels read a knot row per curve: broadcast the knot vector first
+    T *xb = nullptr;
+    int rc = broadcast_x<T>(x, n, batch, st, &xb);
+    if (!rc) rc = build_eval_t<T>(xb, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, flags, st);
+    if (xb) cudaFreeAsync(xb, st);
+    return rc;
   }
   {  // a few K1h-sized curves with few queries: one CTA per curve does the whole call
     constexpr int VW = 16 / sizeof(T);
@@ -916,8 +958,10 @@ int build_eval_host_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, 
   // the whole problem's fused/split choice, kept for every chunk
   if (!(flags & (SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT)))
     if (batch * m > kFuseMaxWork) flags |= kNoFusedStaged;  // chunks must not pick the small-problem kernel
+  if (batch == 1) flags &= ~SPLINE_X_SHARED;
+  const bool xsh = (flags & SPLINE_X_SHARED) != 0;  // one knot vector: every chunk copies only it
   const size_t s = sizeof(T);
-  const size_t per_curve = s * (3 * (size_t)n + 2 * (size_t)m + 2) + 4 * (size_t)m;  // device bytes per curve
+  const size_t per_curve = s * ((xsh ? 2 : 3) * (size_t)n + 2 * (size_t)m + 2) + 4 * (size_t)m;  // device B/curve
   int64_t C = std::max<int64_t>(1, (int64_t)(kHostChunkBytes / per_curve));
   C = std::max<int64_t>(C, 2 * (int64_t)num_sms());            // keep every chunk GPU-wide
   C = std::min<int64_t>(C, std::max<int64_t>(1, (int64_t)(kMaxSlotBytes / per_curve)));  // within memory
@@ -949,7 +993,7 @@ int build_eval_host_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, 
     int32_t *didx = (int32_t *)(b + 3 * bx + 2 * bq);
     T *ds1 = (T *)(b + 3 * bx + 2 * bq + bi), *ds2 = (T *)(b + 3 * bx + 2 * bq + bi + bs);
     const size_t kn = s * nc * n, km = s * nc * m;
-    rc = cuda_rc(cudaMemcpyAsync(dx, x + c0 * n, kn, cudaMemcpyHostToDevice, ss));
+    rc = cuda_rc(cudaMemcpyAsync(dx, xsh ? x : x + c0 * n, xsh ? s * n : kn, cudaMemcpyHostToDevice, ss));
     if (!rc) rc = cuda_rc(cudaMemcpyAsync(dy, y + c0 * n, kn, cudaMemcpyHostToDevice, ss));
     if (!rc && m) rc = cuda_rc(cudaMemcpyAsync(dq, q + c0 * m, km, cudaMemcpyHostToDevice, ss));
     if (!rc && (bc & 1)) rc = cuda_rc(cudaMemcpyAsync(ds1, yp1 + c0, s * nc, cudaMemcpyHostToDevice, ss));
@@ -1021,6 +1065,7 @@ int check_build(const void *x, const void *y, int64_t n, int64_t batch, int bc, 
                 const void *y2, int dtype) {
   if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
   if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
+  bc &= ~SPLINE_X_SHARED;
   if (bc < 0 || bc > 3) return SPLINE_EINVAL;
   if (batch == 0) return SPLINE_OK;
   if (!x || !y || !y2) return SPLINE_EINVAL;
@@ -1142,18 +1187,20 @@ int spline_build(const void *x, const void *y, int64_t n, int64_t batch, int bc,
   cudaStream_t st = (cudaStream_t)stream;
   StatusScope scope(st);
   if (!scope.ok()) return SPLINE_ENOMEM;
+  const bool xsh = (bc & SPLINE_X_SHARED) != 0;
+  bc &= ~SPLINE_X_SHARED;
   if (dtype == SPLINE_F32)
     return build_t<float>((const float *)x, (const float *)y, n, batch, bc, (const float *)yp1, (const float *)ypn,
-                          (float *)y2, st);
+                          (float *)y2, st, xsh);
   return build_t<double>((const double *)x, (const double *)y, n, batch, bc, (const double *)yp1,
-                         (const double *)ypn, (double *)y2, st);
+                         (const double *)ypn, (double *)y2, st, xsh);
 }
 
 int spline_eval(const void *x, const void *y, const void *y2, int64_t n, int64_t batch, const void *q, int64_t m,
                 void *out, int32_t *idx, int flags, int dtype, spline_stream_t stream) {
   if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
   if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || m < 0 || m >= (int64_t(1) << 31)) return SPLINE_EINVAL;
-  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM | SPLINE_NO_BUCKET)) return SPLINE_EINVAL;
+  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM | SPLINE_NO_BUCKET | SPLINE_X_SHARED)) return SPLINE_EINVAL;
   if (batch == 0 || m == 0) return SPLINE_OK;
   if (!x || !y || !y2 || !q || !out) return SPLINE_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1172,7 +1219,8 @@ int spline_build_eval(const void *x, const void *y, int64_t n, int64_t batch, in
   if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
   if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
   if (m < 0 || m >= (int64_t(1) << 31) || bc < 0 || bc > 3) return SPLINE_EINVAL;
-  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM | SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT)) return SPLINE_EINVAL;
+  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM | SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT | SPLINE_X_SHARED))
+    return SPLINE_EINVAL;
   if ((flags & SPLINE_PATH_FUSED) && (flags & SPLINE_PATH_SPLIT)) return SPLINE_EINVAL;
   if (batch == 0) return SPLINE_OK;
   if (!x || !y || ((bc & 1) && !yp1) || ((bc & 2) && !ypn)) return SPLINE_EINVAL;
@@ -1193,7 +1241,8 @@ int spline_build_eval_host(const void *x, const void *y, int64_t n, int64_t batc
   if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
   if (n < 3 || n >= (int64_t(1) << 31) || batch < 0 || batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
   if (m < 0 || m >= (int64_t(1) << 31) || bc < 0 || bc > 3) return SPLINE_EINVAL;
-  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM | SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT)) return SPLINE_EINVAL;
+  if (flags & ~(SPLINE_Q_SORTED | SPLINE_X_UNIFORM | SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT | SPLINE_X_SHARED))
+    return SPLINE_EINVAL;
   if ((flags & SPLINE_PATH_FUSED) && (flags & SPLINE_PATH_SPLIT)) return SPLINE_EINVAL;
   if (batch == 0) return SPLINE_OK;
   if (!x || !y || ((bc & 1) && !yp1) || ((bc & 2) && !ypn)) return SPLINE_EINVAL;

@@ -63,7 +63,7 @@ def test_einval_eval():
     assert lib.spline_eval(p, p, p, 2, 1, p, 4, p, None, 0, F32, None) == _lib.SPLINE_EINVAL   # n < 3
     assert lib.spline_eval(p, p, p, 8, 1, p, -1, p, None, 0, F32, None) == _lib.SPLINE_EINVAL  # m < 0
     assert lib.spline_eval(p, p, p, 8, 1, p, 4, p, None, 8, F32, None) == _lib.SPLINE_EINVAL   # unknown flag
-    assert lib.spline_eval(p, p, p, 8, 1, p, 4, p, None, 32, F32, None) == _lib.SPLINE_EINVAL  # unknown flag
+    assert lib.spline_eval(p, p, p, 8, 1, p, 4, p, None, 64, F32, None) == _lib.SPLINE_EINVAL  # unknown flag
     assert lib.spline_eval(p, None, p, 8, 1, p, 4, p, None, 0, F32, None) == _lib.SPLINE_EINVAL  # NULL y
     assert lib.spline_eval(None, None, None, 8, 1, None, 0, None, None, 0, F32, None) == _lib.SPLINE_OK  # m == 0
     assert lib.spline_eval(None, None, None, 8, 0, None, 9, None, None, 0, F32, None) == _lib.SPLINE_OK  # B == 0
