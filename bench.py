@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--x-shared", action="store_true",
+                    help="shared-knot mode (SPLINE_X_SHARED): one knot vector for the batch (configs whose recipe "
+                         "has one grid: cfg3)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--ablation", action="store_true",
                     help="SURVEY §8(f) rows 2-3: the paper's control-point sweep (n = 4 .. 2^20) with its "
@@ -151,11 +154,13 @@ def long_curve_cfg(n, s):
     return n > 256 * (16 if s == 8 else 32)
 
 
-def algorithmic_bytes(B, n, m, s):
+def algorithmic_bytes(B, n, m, s, xshared=False):
     """SURVEY.md §8(d): build 3 s B/knot (read x, y; write y2) + 2 s per clamped curve;
-    eval (2 s + 4) B/query (read q; write out, int32 idx) + 3 n s per curve (x, y, y2)."""
-    build = 3 * s * B * n
-    evalb = (2 * s + 4) * B * m + 3 * n * s * B
+    eval (2 s + 4) B/query (read q; write out, int32 idx) + 3 n s per curve (x, y, y2).
+    Shared-knot mode: x is read once for the batch (n s), not per curve."""
+    xb = s * n if xshared else s * B * n
+    build = 2 * s * B * n + xb
+    evalb = (2 * s + 4) * B * m + 2 * n * s * B + xb
     return build, evalb
 
 
@@ -221,6 +226,9 @@ def cpu_baseline(args, wl_full):
     import oracle
     cores = os.cpu_count() or 1
     wl = wl_full
+    if wl.x.ndim == 1:  # shared knots: the oracle takes one row per curve
+        from paper_2001_09253_b200 import workloads
+        wl = workloads.Workload(wl.spec, np.tile(wl.x, (wl.batch, 1)), wl.y, wl.q, wl.yp1, wl.ypn, wl.bc, wl.flags)
     if args.config in (4, 5):  # bound the sample to ~10-30 s of CPU work
         from paper_2001_09253_b200 import workloads
         wl = workloads.generate(args.config, batch=64 if args.config == 4 else None,
@@ -402,9 +410,13 @@ def main():
     def dev_t(a):
         return torch.from_numpy(a).to(dev) if a is not None else None
 
+    if args.x_shared:
+        if not np.all(wl.x == wl.x[0]):
+            raise SystemExit("--x-shared: this configuration's curves do not share one grid")
+        wl.x = np.ascontiguousarray(wl.x[0])  # (n,): one knot vector for the batch
     x, y, q = dev_t(wl.x), dev_t(wl.y), dev_t(wl.q)
     yp1, ypn = dev_t(wl.yp1), dev_t(wl.ypn)
-    y2 = torch.empty_like(x)
+    y2 = torch.empty_like(y)
     out = torch.empty_like(q)
     idx = torch.empty(q.shape, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -470,7 +482,8 @@ def main():
 
     # ---- the fused single-kernel path (spline_build_eval, SPLINE_PATH_FUSED), same protocol
     fused_ms = 0.0
-    fusable = n <= 128 and (n * s) % 16 == 0 and m % (16 // s) == 0
+    tile_fusable = bool(wl.flags & workloads.FLAG_Q_SORTED) and 128 < n <= 256 * (16 if s == 8 else 32)
+    fusable = (n <= 128 and (n * s) % 16 == 0 and m % (16 // s) == 0) or tile_fusable
     if fusable:
         ff = wl.flags | api.PATH_FUSED
 
@@ -530,7 +543,7 @@ def main():
     if not args.no_e2e:
         h_in = [torch.from_numpy(a).pin_memory() for a in (wl.x, wl.y, wl.q)]
         h_sl = [torch.from_numpy(a).pin_memory() if a is not None else None for a in (wl.yp1, wl.ypn)]
-        h_y2 = torch.empty(x.shape, dtype=x.dtype).pin_memory()
+        h_y2 = torch.empty(y.shape, dtype=x.dtype).pin_memory()
         h_out = torch.empty(q.shape, dtype=q.dtype).pin_memory()
         h_idx = torch.empty(q.shape, dtype=torch.int32).pin_memory()
 
@@ -553,7 +566,7 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         h2d = sum(a.nbytes for a in (wl.x, wl.y, wl.q)) + sum(a.nbytes for a in (wl.yp1, wl.ypn) if a is not None)
-        d2h = x.numel() * s + q.numel() * s + q.numel() * 4
+        d2h = y.numel() * s + q.numel() * s + q.numel() * 4
         e2e = {"value": world * B * m / (te.item() * 1e-3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": te.item(), "pinned": True,
                "path": "api.build_eval_host (C ABI spline_build_eval_host): pinned host in/out, the batch in chunks "
@@ -564,7 +577,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    bbytes, ebytes = algorithmic_bytes(B, n, m, s)
+    bbytes, ebytes = algorithmic_bytes(B, n, m, s, args.x_shared)
     peak, peak_src = peaks()
     etr, etr_d = traffic_for(f"cfg{args.config}", "eval")
     btr, btr_d = traffic_for(f"cfg{args.config}", "build")
@@ -573,11 +586,11 @@ def main():
     long_curve = n > 256 * (16 if s == 8 else 32)
     # the library's choice inside spline_build_eval (spline_abi.cu build_eval_t): one fused kernel
     # when the problem is small (batch*m <= 2^17) and fusable, else the two kernels
-    fused_step = fusable and B * m <= (1 << 17)
+    fused_step = fusable and not tile_fusable and B * m <= (1 << 17)
     small_step = s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0  # k_eval_small<true>: solve + eval
     tiny_step = (n == 16 or (s == 4 and n in (32, 64))) and B <= 16 and m <= 8192 and m % (16 // s) == 0
     # mid-length curves with sorted queries (cfg4): k_tile_eval solves and evaluates in one kernel
-    tile_step = bool(wl.flags & workloads.FLAG_Q_SORTED) and 128 < n <= 256 * (16 if s == 8 else 32)
+    tile_step = False  # k_tile_eval runs on SPLINE_PATH_FUSED only (measured slower than split on cfg4)
     launches = 2 * K  # 1 build kernel + 1 eval kernel per step for configs 2-4
     if long_curve:
         # tiled SPIKE: reduce + top (grouped for one curve of > 128 tiles: up, root, down) + finish;
@@ -587,7 +600,8 @@ def main():
     if fused_step or small_step or tiny_step or tile_step:
         launches = K
     one_kernel = fused_step or small_step or tiny_step or tile_step
-    step_bytes = ((2 * s + 4) * B * m + 3 * s * B * n) if one_kernel else (bbytes + ebytes)
+    xread = s * n if args.x_shared else s * B * n
+    step_bytes = ((2 * s + 4) * B * m + 2 * s * B * n + xread) if one_kernel else (bbytes + ebytes)
     if wl.flags & workloads.FLAG_Q_SORTED:
         ekern = "k_eval_sorted"
     elif s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0:
@@ -636,7 +650,8 @@ def main():
         "vs_baseline": None,
         "dtype": spec.dtype,
         "data": "synthetic (seeded PCG64, BASELINE.json config recipe; DESIGN.md input recipe)",
-        "config": {"workload": spec.name, "batch_per_gpu": B, "n": n, "m": m, "bc": wl.bc, "flags": wl.flags,
+        "config": {"workload": spec.name + (" [shared knots: SPLINE_X_SHARED]" if args.x_shared else ""),
+                   "batch_per_gpu": B, "n": n, "m": m, "bc": wl.bc, "flags": wl.flags, "x_shared": args.x_shared,
                    "l2": "flushed (256 MiB write) between steps, outside the timed events",
                    "parallelism": f"dp{world} (curve shards, no data-path collective)"},
         "knots_per_s": world * B * n / (step_ms * 1e-3),
@@ -660,7 +675,7 @@ def main():
                       "fused (k_build_eval_tiny: one CTA per curve, K1h's solve + eval)" if tiny_step else
                       "fused (k_fused_staged)" if fused_step else "split (build kernel(s), then eval kernel(s))"),
         "roofline": roof,
-        "fused": ({"kernel": "k_fused_staged", "ms_per_step": fused_ms, "value": world * B * m / (fused_ms * 1e-3),
+        "fused": ({"kernel": "k_tile_eval" if tile_fusable else "k_fused_staged", "ms_per_step": fused_ms, "value": world * B * m / (fused_ms * 1e-3),
                    "unit": "queries/s", "algorithmic_bytes": (2 * s + 4) * B * m + 3 * s * B * n,
                    "hbm_gbs": ((2 * s + 4) * B * m + 3 * s * B * n) / (fused_ms * 1e-3) / 1e9,
                    "note": "spline_build_eval with SPLINE_PATH_FUSED (one launch; x, y read once, y2 written once)"}

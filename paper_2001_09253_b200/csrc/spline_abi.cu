@@ -822,9 +822,10 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
       return rc;
     }
   }
-  // mid-length curves (K2's range) with sorted queries: solve and evaluate in one kernel
-  if ((flags & SPLINE_Q_SORTED) && !(flags & SPLINE_PATH_SPLIT) && n > kK1MaxN &&
-      n <= 256 * rmax<T>())
+  // mid-length curves (K2's range) with sorted queries: solve and evaluate in one kernel -- on
+  // request only: measured on cfg4 the split path is faster (1.29 vs 1.69 ms: the evaluation is
+  // issue-bound and needs the 32 warps/SM that the solve's 94 KB tile leaves it no room for)
+  if ((flags & SPLINE_Q_SORTED) && (flags & SPLINE_PATH_FUSED) && n > kK1MaxN && n <= 256 * rmax<T>())
     return launch_tile_eval<T>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
   const bool want_fused =
       (flags & SPLINE_PATH_FUSED) ||

@@ -64,11 +64,11 @@ class Workload:
 
     @property
     def batch(self) -> int:
-        return self.x.shape[0]
+        return self.y.shape[0]
 
     @property
     def n(self) -> int:
-        return self.x.shape[1]
+        return self.y.shape[1]
 
     @property
     def m(self) -> int:
