@@ -42,7 +42,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="batched configs on N GPUs: strong = rank r owns curves [rB/N, (r+1)B/N) of the config "
+                         "(SURVEY §8(e)); weak = every rank its own full-size batch (seeded per rank)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cfg5-mode", default="recompute", choices=["recompute", "gather"],
+                    help="cfg5 on N GPUs (SURVEY §8(e)): recompute = tile records all-gathered, every rank "
+                         "finishes the whole curve; gather = the rank-record seam, then an all-gather of y2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--x-shared", action="store_true",
                     help="shared-knot mode (SPLINE_X_SHARED): one knot vector for the batch (configs whose recipe "
@@ -272,9 +278,14 @@ def run_long_curve_dist(args, world, rank, local, dev):
     idx = torch.empty(q.shape, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
+    wsf = api.spike_workspace(n, 0, n, x.dtype, dev) if args.cfg5_mode == "recompute" else None
+
     def step():
-        y2s, _ = sdist.build_long_curve(x, y, wl.bc, workspace=ws)
-        y2 = sdist.gather_curve(y2s, n)
+        if args.cfg5_mode == "recompute":  # §8(e)(ii): no y2 on the wire, every rank finishes all tiles
+            y2 = sdist.build_long_curve_recompute(x, y, wl.bc, workspace=wsf)
+        else:                              # §8(e)(i): rank records, then the y2 shards all-gathered
+            y2s, _ = sdist.build_long_curve(x, y, wl.bc, workspace=ws)
+            y2 = sdist.gather_curve(y2s, n)
         api.evaluate(x[None], y[None], y2[None], q, 0, out=out, idx=idx)
 
     for _ in range(max(args.warmup, 3)):
@@ -301,9 +312,12 @@ def run_long_curve_dist(args, world, rank, local, dev):
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded PCG64, BASELINE.json cfg5 recipe; per-rank query shards)",
-                "config": {"workload": spec.name, "n": n, "m_total": M,
-                           "parallelism": f"rows sharded over {world} GPUs (SPIKE, NCCL record all_gather), "
-                                          "y2 all_gather, queries sharded",
+                "config": {"workload": spec.name, "n": n, "m_total": M, "cfg5_mode": args.cfg5_mode,
+                           "parallelism": (f"whole tiles sharded over {world} GPUs, tile records all-gathered (NCCL), "
+                                           "every rank finishes the whole curve, queries sharded"
+                                           if args.cfg5_mode == "recompute" else
+                                           f"rows sharded over {world} GPUs (SPIKE, NCCL record all_gather), "
+                                           "y2 all_gather, queries sharded"),
                            "l2": "inputs (1.5 GiB curve, 2 GiB queries) exceed L2"},
                 "knots_per_s": n / (ms * 1e-3),
                 "hbm_gbs_step_per_gpu": (build_bytes / world + eval_bytes / world) / (ms * 1e-3) / 1e9,
@@ -401,8 +415,19 @@ def main():
         dist.destroy_process_group()
         return
 
+    from paper_2001_09253_b200 import dist as sdist
     spec = workloads.CONFIGS[args.config]
-    wl = workloads.generate(args.config, shard=rank)
+    # strong scaling (default): the config's batch split over the ranks -- the same inputs as at
+    # N = 1; a batch smaller than the rank count (cfg1) runs as replicas (weak)
+    scaling = args.scaling if spec.batch >= world else "weak"
+    if scaling == "strong" and world > 1:
+        full = workloads.generate(args.config)
+        b0, b1 = sdist.shard_batch(full.batch, world, rank)
+        wl = workloads.slice_batch(full, b0, b1)
+        del full
+    else:
+        wl = workloads.generate(args.config, shard=rank)
+    total_q = spec.batch * spec.m if (scaling == "strong" and world > 1) else world * wl.batch * wl.m
     B, n, m = wl.batch, wl.n, wl.m
     s = 4 if spec.dtype == "f32" else 8
     stream = torch.cuda.current_stream()
@@ -567,11 +592,17 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         h2d = sum(a.nbytes for a in (wl.x, wl.y, wl.q)) + sum(a.nbytes for a in (wl.yp1, wl.ypn) if a is not None)
         d2h = y.numel() * s + q.numel() * s + q.numel() * 4
-        e2e = {"value": world * B * m / (te.item() * 1e-3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+        e2e = {"value": total_q / (te.item() * 1e-3), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": te.item(), "pinned": True,
                "path": "api.build_eval_host (C ABI spline_build_eval_host): pinned host in/out, the batch in chunks "
                        "whose H2D copies, kernels and D2H copies overlap on internal streams"}
 
+    # the final statistics reduction (NCCL when N > 1): data-error bits, out-of-range and NaN counts
+    # over all ranks' outputs, and the slowest rank's step time
+    api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags, y2=y2, out=out, idx=idx)
+    bits = api.status()
+    stats = sdist.reduce_stats({"status_bits": float(bits), "n_idx_out_of_range": float((idx < 0).sum().item()),
+                                "n_out_nan": float(torch.isnan(out).sum().item()), "step_ms": step_ms})
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -638,7 +669,7 @@ def main():
         roof = split_roof
     line = {
         "metric": METRIC,
-        "value": world * B * m / (step_ms * 1e-3),
+        "value": total_q / (step_ms * 1e-3),
         "unit": "queries/s",
         "n_gpus": world,
         "steps": K,
@@ -646,15 +677,19 @@ def main():
         "ms_per_step": step_ms,
         "step_ms_stats": step_st,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": spec.dtype,
         "data": "synthetic (seeded PCG64, BASELINE.json config recipe; DESIGN.md input recipe)",
         "config": {"workload": spec.name + (" [shared knots: SPLINE_X_SHARED]" if args.x_shared else ""),
                    "batch_per_gpu": B, "n": n, "m": m, "bc": wl.bc, "flags": wl.flags, "x_shared": args.x_shared,
                    "l2": "flushed (256 MiB write) between steps, outside the timed events",
-                   "parallelism": f"dp{world} (curve shards, no data-path collective)"},
-        "knots_per_s": world * B * n / (step_ms * 1e-3),
+                   "parallelism": (f"dp{world}: rank r owns curves [rB/{world}, (r+1)B/{world}) of the config, "
+                                   "no data-path collective" if scaling == "strong" and world > 1 else
+                                   f"dp{world}: {'replicas' if spec.batch < world else 'a full batch per rank'}, "
+                                   "no data-path collective")},
+        "stats": stats,
+        "knots_per_s": (total_q // m) * n / (step_ms * 1e-3),
         "hbm_gbs_step": (bbytes + ebytes) / (step_ms * 1e-3) / 1e9,
         "frac_of_spec_8tbs_step": (bbytes + ebytes) / (step_ms * 1e-3) / 1e9 / SPEC_HBM_GBS,
         "build_ms": bms,
@@ -675,7 +710,7 @@ def main():
                       "fused (k_build_eval_tiny: one CTA per curve, K1h's solve + eval)" if tiny_step else
                       "fused (k_fused_staged)" if fused_step else "split (build kernel(s), then eval kernel(s))"),
         "roofline": roof,
-        "fused": ({"kernel": "k_tile_eval" if tile_fusable else "k_fused_staged", "ms_per_step": fused_ms, "value": world * B * m / (fused_ms * 1e-3),
+        "fused": ({"kernel": "k_tile_eval" if tile_fusable else "k_fused_staged", "ms_per_step": fused_ms, "value": total_q / (fused_ms * 1e-3),
                    "unit": "queries/s", "algorithmic_bytes": (2 * s + 4) * B * m + 3 * s * B * n,
                    "hbm_gbs": ((2 * s + 4) * B * m + 3 * s * B * n) / (fused_ms * 1e-3) / 1e9,
                    "note": "spline_build_eval with SPLINE_PATH_FUSED (one launch; x, y read once, y2 written once)"}

@@ -220,6 +220,28 @@ int spline_spike_finish(const void *x, const void *y, int64_t n, int64_t row_beg
                         void *y2_shard, void *workspace, int dtype, spline_stream_t stream);
 
 /*
+ * Recompute instead of communicate -- the multi-GPU long-curve build that
+ * leaves the FULL y2 on every rank without moving y2 between GPUs.  The curve's rows are cut in
+ * tiles of spline_spike_tile_rows(dtype) rows from row 0 (the last tile ragged); rank r owns a
+ * contiguous range of whole tiles.
+ * spline_spike_tile_records: the block record (6 values, as above) of every tile of rows
+ *   [row_begin, row_end) (row_begin a multiple of the tile rows; row_end a multiple or n), in
+ *   tile order, to tile_records [ceil((row_end - row_begin) / tile_rows)][6].  The caller
+ *   all-gathers them into the curve's full [ntiles][6] table.
+ * spline_spike_finish_tiles: from that full table, the reduced solve and the finish of EVERY
+ *   tile: writes y2[0 .. n).  workspace: spline_spike_workspace_size(n, 0, n, dtype) bytes.
+ * A tile with bad knots has a NaN record: y2 is then NaN on every rank (BAD_KNOTS is raised by the
+ * rank that owns the tile).
+ */
+int64_t spline_spike_tile_rows(int dtype);
+int spline_spike_tile_records(const void *x, const void *y, int64_t n, int64_t row_begin, int64_t row_end, int bc,
+                              const void *yp1, const void *ypn, void *tile_records, void *workspace, int dtype,
+                              spline_stream_t stream);
+int spline_spike_finish_tiles(const void *x, const void *y, int64_t n, int bc, const void *yp1, const void *ypn,
+                              const void *all_tile_records, void *y2, void *workspace, int dtype,
+                              spline_stream_t stream);
+
+/*
  * spline_build_dist -- the second derivatives of ONE long curve whose rows are partitioned over
  * the G ranks of an NCCL communicator (the partitioned solve the paper points to
  * for parallel hardware).  Rank r = ncclCommUserRank(comm) owns rows

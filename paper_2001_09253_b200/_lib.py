@@ -38,6 +38,9 @@ SIGNATURES = {
     "spline_spike_reduce": (_i32, [_vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp]),
     "spline_spike_finish": (_i32, [_vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _i32,
                                    _vp]),
+    "spline_spike_tile_rows": (_i64, [_i32]),
+    "spline_spike_tile_records": (_i32, [_vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "spline_spike_finish_tiles": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
     "spline_build_dist": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp]),
     "spline_build_dist_f32": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "spline_build_dist_f64": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),

@@ -295,6 +295,30 @@ def spike_finish(x, y, row_begin: int, row_end: int, bc: int, yp1, ypn, all_reco
     _lib.check(rc, "spline_spike_finish")
 
 
+def spike_tile_rows(dtype) -> int:
+    return int(_lib.load().spline_spike_tile_rows(_DT[dtype]))
+
+
+def spike_tile_records(x, y, row_begin: int, row_end: int, bc: int, yp1, ypn, tile_records, workspace, stream=None):
+    n = _check_spike(x, y, row_begin, row_end, yp1, ypn, workspace)
+    ts = spike_tile_rows(x.dtype)
+    _check_buf(tile_records, (-(-(row_end - row_begin) // ts), 6), x.dtype, x.device, "tile_records")
+    rc = _lib.load().spline_spike_tile_records(_p(x), _p(y), n, row_begin, row_end, bc, _p(yp1), _p(ypn),
+                                               _p(tile_records), _p(workspace), _DT[x.dtype],
+                                               ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_spike_tile_records")
+
+
+def spike_finish_tiles(x, y, bc: int, yp1, ypn, all_tile_records, y2, workspace, stream=None):
+    n = _check_spike(x, y, 0, x.shape[-1], yp1, ypn, workspace)
+    ts = spike_tile_rows(x.dtype)
+    _check_buf(all_tile_records, (-(-n // ts), 6), x.dtype, x.device, "all_tile_records")
+    _check_buf(y2, (n,), x.dtype, x.device, "y2")
+    rc = _lib.load().spline_spike_finish_tiles(_p(x), _p(y), n, bc, _p(yp1), _p(ypn), _p(all_tile_records), _p(y2),
+                                               _p(workspace), _DT[x.dtype], ctypes.c_void_p(_stream(stream)))
+    _lib.check(rc, "spline_spike_finish_tiles")
+
+
 def build_dist(x, y, comm: int, bc: int = BC_NATURAL, yp1=None, ypn=None, y2_shard=None, stream=None):
     """spline_build_dist: this rank's rows of ONE long curve (x, y: the whole curve, (n,)) over an
     NCCL communicator given as its raw ncclComm_t handle (an int).  Rank r of G owns rows

@@ -268,7 +268,11 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
       const Rec<T> r = rec[0];
       T *o = tile_rec + (c * ntiles + tile) * 6;
       o[0] = r.Gp; o[1] = r.Vp; o[2] = r.Wp; o[3] = r.Gq; o[4] = r.Vq; o[5] = r.Wq;
-      if (bad) { atomicOr(badflag + c, 1); raise_status(status, kBadKnots); }
+      if (bad) {  // a NaN record: every merge and every finish that uses it is NaN (the whole curve)
+        for (int k = 0; k < 6; ++k) o[k] = qnan<T>();
+        atomicOr(badflag + c, 1);
+        raise_status(status, kBadKnots);
+      }
     }
     return;
   }

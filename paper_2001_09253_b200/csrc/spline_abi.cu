@@ -1107,6 +1107,39 @@ int spike_finish_t(const T *x, const T *y, int64_t n, int64_t rb, int64_t re, in
   return rc;
 }
 
+// Recompute instead of communicate: the tile records of rows [rb, rb + k TS)
+// (K3 only; every rank its own tiles), then -- given ALL tile records of the curve -- the reduced
+// solve (K4) and the finish (K5) of the whole curve on every rank: the full y2 without moving it.
+template <typename T>
+int spike_tile_records_t(const T *x, const T *y, int64_t n, int64_t rb, int64_t re, int bc, const T *yp1,
+                         const T *ypn, T *recs, void *workspace, cudaStream_t st) {
+  constexpr int R = rmax<T>();
+  const int64_t ntiles = (re - rb + 256 * R - 1) / (256 * R);
+  SpikeWs w;
+  spike_ws_layout<T>(ntiles, 1, &w, (char *)workspace);
+  w.tile_rec = recs;
+  int rc = cuda_rc(cudaMemsetAsync(w.badflag, 0, sizeof(int), st));
+  if (!rc) rc = launch_tile_part<T, TILE_REDUCE>(x, y, n, rb, re, 1, bc, yp1, ypn, nullptr, w, st);
+  return rc;
+}
+template <typename T>
+int spike_finish_tiles_t(const T *x, const T *y, int64_t n, int bc, const T *yp1, const T *ypn, const T *all_recs,
+                         T *y2, void *workspace, cudaStream_t st) {
+  constexpr int R = rmax<T>();
+  const int64_t ntiles = (n + 256 * R - 1) / (256 * R);
+  SpikeWs w;
+  spike_ws_layout<T>(ntiles, 1, &w, (char *)workspace);
+  int rc = cuda_rc(cudaMemsetAsync(w.badflag, 0, sizeof(int), st));
+  if (!rc) {
+    if (ntiles > 2 * kGroupTiles && (ntiles + kGroupTiles - 1) / kGroupTiles <= kMaxRanks)
+      rc = launch_top_grouped<T>(all_recs, (int)ntiles, w, st);
+    else
+      rc = launch_top<T>(all_recs, (int)ntiles, 1, 0, nullptr, (T *)w.tile_ext, nullptr, (T *)w.foldq, st);
+  }
+  if (!rc) rc = launch_tile_part<T, TILE_FINISH>(x, y, n, 0, n, 1, bc, yp1, ypn, y2, w, st);
+  return rc;
+}
+
 int check_spike(const void *x, const void *y, int64_t n, int64_t rb, int64_t re, int bc, const void *yp1,
                 const void *ypn, const void *ws, int dtype) {
   if (dtype != SPLINE_F32 && dtype != SPLINE_F64) return SPLINE_EINVAL;
@@ -1363,6 +1396,39 @@ int spline_spike_finish(const void *x, const void *y, int64_t n, int64_t row_beg
   return spike_finish_t<double>((const double *)x, (const double *)y, n, row_begin, row_end, bc,
                                 (const double *)yp1, (const double *)ypn, (const double *)all_records, nranks, rank,
                                 (double *)y2_shard, workspace, st);
+}
+
+int64_t spline_spike_tile_rows(int dtype) { return 256 * (dtype == SPLINE_F64 ? rmax<double>() : rmax<float>()); }
+
+int spline_spike_tile_records(const void *x, const void *y, int64_t n, int64_t row_begin, int64_t row_end, int bc,
+                              const void *yp1, const void *ypn, void *tile_records, void *workspace, int dtype,
+                              spline_stream_t stream) {
+  if (int rc = check_spike(x, y, n, row_begin, row_end, bc, yp1, ypn, workspace, dtype)) return rc;
+  if (!tile_records || row_begin % spline_spike_tile_rows(dtype) != 0) return SPLINE_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
+  if (dtype == SPLINE_F32)
+    return spike_tile_records_t<float>((const float *)x, (const float *)y, n, row_begin, row_end, bc,
+                                       (const float *)yp1, (const float *)ypn, (float *)tile_records, workspace, st);
+  return spike_tile_records_t<double>((const double *)x, (const double *)y, n, row_begin, row_end, bc,
+                                      (const double *)yp1, (const double *)ypn, (double *)tile_records, workspace, st);
+}
+
+int spline_spike_finish_tiles(const void *x, const void *y, int64_t n, int bc, const void *yp1, const void *ypn,
+                              const void *all_tile_records, void *y2, void *workspace, int dtype,
+                              spline_stream_t stream) {
+  if (int rc = check_spike(x, y, n, 0, n, bc, yp1, ypn, workspace, dtype)) return rc;
+  if (!all_tile_records || !y2) return SPLINE_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  StatusScope scope(st);
+  if (!scope.ok()) return SPLINE_ENOMEM;
+  if (dtype == SPLINE_F32)
+    return spike_finish_tiles_t<float>((const float *)x, (const float *)y, n, bc, (const float *)yp1,
+                                       (const float *)ypn, (const float *)all_tile_records, (float *)y2, workspace, st);
+  return spike_finish_tiles_t<double>((const double *)x, (const double *)y, n, bc, (const double *)yp1,
+                                      (const double *)ypn, (const double *)all_tile_records, (double *)y2, workspace,
+                                      st);
 }
 
 int spline_build_dist(const void *x, const void *y, int64_t n, int bc, const void *yp1, const void *ypn,

@@ -52,6 +52,15 @@ class CudaOps:
     def evaluate(self, x, y, y2, q, flags):
         return self.api.evaluate(x, y, y2, q, flags)
 
+    def tile_rows(self, dtype):
+        return self.api.spike_tile_rows(dtype)
+
+    def tile_records(self, x, y, rb, re, bc, yp1, ypn, recs, ws):
+        self.api.spike_tile_records(x, y, rb, re, bc, yp1, ypn, recs, ws)
+
+    def finish_tiles(self, x, y, bc, yp1, ypn, all_recs, y2, ws):
+        self.api.spike_finish_tiles(x, y, bc, yp1, ypn, all_recs, y2, ws)
+
 
 def _slope(v, like):
     if v is None:
@@ -85,6 +94,45 @@ def build_long_curve(x: torch.Tensor, y: torch.Tensor, bc: int = 0, yp1=None, yp
     y2_shard = torch.empty(re - rb, dtype=x.dtype, device=x.device)
     ops.finish(x, y, rb, re, bc, s0, s1, all_records, world, rank, y2_shard, ws)
     return y2_shard, (rb, re)
+
+
+def shard_tiles(n: int, tile_rows: int, world: int, rank: int) -> tuple[int, int, int, int]:
+    """Whole tiles [t0, t1) of rank `rank` and their rows [rb, re) (the recompute build)."""
+    ntiles = -(-n // tile_rows)
+    t0, t1 = shard_batch(ntiles, world, rank)
+    return t0, t1, t0 * tile_rows, min(t1 * tile_rows, n)
+
+
+def build_long_curve_recompute(x: torch.Tensor, y: torch.Tensor, bc: int = 0, yp1=None, ypn=None, group=None,
+                               ops=None, workspace=None):
+    """Recompute instead of communicate: the FULL y2 (n,) on every rank.
+    Each rank reduces its own whole tiles to tile records (K3); the records of all tiles are
+    all-gathered (48 B per tile in fp64 -- 0.75 MB for cfg5's 16,384 tiles, instead of the 512 MB
+    y2); every rank then solves the reduced system and finishes every tile itself (K4 + K5)."""
+    ops = ops or CudaOps()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n = x.shape[-1]
+    ts = ops.tile_rows(x.dtype)
+    ntiles = -(-n // ts)
+    t0, t1, rb, re = shard_tiles(n, ts, world, rank)
+    s0, s1 = _slope(yp1, x), _slope(ypn, x)
+    ws = workspace if workspace is not None else ops.workspace(n, 0, n, x.dtype, x.device)
+    per = -(-ntiles // world)  # equal slabs for all_gather_into_tensor (the last ones padded)
+    slab = torch.zeros(per, 6, dtype=x.dtype, device=x.device)
+    if t1 > t0:
+        ops.tile_records(x, y, rb, re, bc, s0, s1, slab[: t1 - t0], ws)
+    if world > 1:
+        allr = torch.empty(per * world, 6, dtype=x.dtype, device=x.device)
+        dist.all_gather_into_tensor(allr, slab, group=group)
+        parts = [allr[r * per: r * per + (shard_batch(ntiles, world, r)[1] - shard_batch(ntiles, world, r)[0])]
+                 for r in range(world)]
+        recs = torch.cat(parts).contiguous()
+    else:
+        recs = slab[:ntiles].contiguous()
+    y2 = torch.empty(n, dtype=x.dtype, device=x.device)
+    ops.finish_tiles(x, y, bc, s0, s1, recs, y2, ws)
+    return y2
 
 
 def gather_curve(y2_shard: torch.Tensor, n: int, group=None) -> torch.Tensor:

@@ -79,6 +79,14 @@ class Workload:
         return np.float32 if self.spec.dtype == "f32" else np.float64
 
 
+def slice_batch(wl: "Workload", b0: int, b1: int) -> "Workload":
+    """Curves [b0, b1) of a workload (strong scaling: rank r owns [r B / G, (r+1) B / G) of the
+    config's batch), as contiguous copies."""
+    sl = lambda a: None if a is None else np.ascontiguousarray(a[b0:b1])
+    x = wl.x if wl.x.ndim == 1 else sl(wl.x)  # shared knots stay one row
+    return Workload(wl.spec, x, sl(wl.y), sl(wl.q), sl(wl.yp1), sl(wl.ypn), wl.bc, wl.flags)
+
+
 def _rng(seed: int, shard: int) -> np.random.Generator:
     return np.random.default_rng(seed if shard == 0 else [seed, shard])
 

@@ -56,3 +56,23 @@ class SeamRefOps:
         b[0] -= a * L
         b[-1] -= c * Rv
         y2_shard.copy_(torch.tensor(np.linalg.solve(T, b), dtype=y2_shard.dtype))
+
+    # ---- recompute instead of communicate: tiles of TILE rows act as the "ranks" of the seam
+    TILE = 1000
+
+    def tile_rows(self, dtype):
+        return self.TILE
+
+    def tile_records(self, x, y, rb, re, bc, yp1, ypn, recs, ws):
+        for k, t0 in enumerate(range(rb, re, self.TILE)):
+            self.reduce(x, y, t0, min(t0 + self.TILE, re), bc, yp1, ypn, recs[k], ws)
+
+    def finish_tiles(self, x, y, bc, yp1, ypn, all_recs, y2, ws):
+        n = y2.shape[0]
+        nt = all_recs.shape[0]
+        flat = all_recs.reshape(-1).cpu()
+        for t in range(nt):
+            rb, re = t * self.TILE, min((t + 1) * self.TILE, n)
+            out = torch.empty(re - rb, dtype=y2.dtype)
+            self.finish(x, y, rb, re, bc, yp1, ypn, flat, nt, t, out, ws)
+            y2[rb:re] = out

@@ -473,3 +473,32 @@ def test_long_curve_bucketed_eval(api, n, m):
     assert torch.equal(idx, idx_r) and torch.equal(out.view(torch.int8), out_r.view(torch.int8))
     _, none = api.evaluate(x, y, parity.to_dev(y2_ref), q, 0, want_idx=False)  # no idx output
     assert none is None
+    api.status()
+
+
+@pytest.mark.parametrize("world,n,bc", [(2, 300001, 0), (8, (1 << 20) + 5, 3), (3, 4096 * 7, 1)])
+def test_recompute_build_emulated_ranks(api, world, n, bc):
+    """§8(e)(ii) recompute-instead-of-gather, G ranks emulated on one GPU: each rank's tile records
+    (whole tiles), concatenated, then the full finish -> bitwise spline_build's y2 (the same tiles,
+    the same merges) and the oracle's within tolerance."""
+    from paper_2001_09253_b200 import dist as sdist
+    api.status()
+    wl = workloads.generate(5, n=n, m=16)
+    x, y = parity.to_dev(wl.x[0]), parity.to_dev(wl.y[0])
+    s0 = torch.full((1,), 0.3, dtype=x.dtype, device=x.device)
+    s1 = torch.full((1,), -0.2, dtype=x.dtype, device=x.device)
+    ts = api.spike_tile_rows(x.dtype)
+    ntiles = -(-n // ts)
+    ws = api.spike_workspace(n, 0, n, x.dtype, x.device)
+    recs = torch.empty(ntiles, 6, dtype=x.dtype, device=x.device)
+    for r in range(world):
+        t0, t1, rb, re = sdist.shard_tiles(n, ts, world, r)
+        if t1 > t0:
+            api.spike_tile_records(x, y, rb, re, bc, s0, s1, recs[t0:t1], ws)
+    y2 = torch.empty(n, dtype=x.dtype, device=x.device)
+    api.spike_finish_tiles(x, y, bc, s0, s1, recs, y2, ws)
+    ref_gpu = api.build(x[None], y[None], bc, 0.3, -0.2)[0]
+    assert api.status() == 0
+    assert torch.equal(y2.view(torch.int8), ref_gpu.view(torch.int8))
+    ref, _ = oracle.build_y2(wl.x[0], wl.y[0], bc, [0.3], [-0.2])
+    assert parity.y2_rel_err(y2.cpu().numpy()[None], ref[None]).max() <= 1e-12
