@@ -82,7 +82,7 @@ def traffic_for(workload_key: str, kernel: str):
     d = json.load(open(p))
     e = d.get(workload_key, {}).get(kernel)
     if isinstance(e, dict):
-        return e.get("traffic"), e
+        return e.get("traffic"), {k: v for k, v in e.items() if k != "traffic"} | {"source": d.get("_source")}
     return e, None
 
 
@@ -610,8 +610,9 @@ def main():
 
     bbytes, ebytes = algorithmic_bytes(B, n, m, s, args.x_shared)
     peak, peak_src = peaks()
-    etr, etr_d = traffic_for(f"cfg{args.config}", "eval")
-    btr, btr_d = traffic_for(f"cfg{args.config}", "build")
+    tkey = f"cfg{args.config}" + ("_xshared" if args.x_shared else "")
+    etr, etr_d = traffic_for(tkey, "eval")
+    btr, btr_d = traffic_for(tkey, "build")
     ach = ebytes / (ems * 1e-3) / 1e9
     wkey = f"cfg{args.config}"
     long_curve = n > 256 * (16 if s == 8 else 32)
@@ -658,7 +659,7 @@ def main():
         # the step IS one kernel: it is the dominant kernel; its launch is bracketed by the step's events
         skern = ("k_tile_eval" if tile_step else "k_eval_small<true>" if small_step else
                  "k_build_eval_tiny" if tiny_step else "k_fused_staged")
-        str_, str_d = traffic_for(f"cfg{args.config}", "step")
+        str_, str_d = traffic_for(tkey, "step")
         sach = step_bytes / (step_ms * 1e-3) / 1e9
         roof = {"kernel": skern, "bound": "hbm", "achieved": sach, "peak": peak, "unit": "GB/s", "frac": sach / peak,
                 "traffic": str_, "traffic_detail": str_d, "peak_source": peak_src,

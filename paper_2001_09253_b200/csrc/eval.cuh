@@ -26,8 +26,6 @@
 //                  shared memory, sparse runs read knots through L1, any n.
 //  k_pack_records + k_eval_records : unsorted queries on long curves: interval records in
 //                  an HBM workspace, one gather per query at the interpolation guess.
-//  k_eval_global : the same without workspace (gathers x, y, y2; used if the workspace
-//                  cannot be allocated).
 #pragma once
 #include "build_thomas.cuh"
 #include "common.cuh"
@@ -1388,82 +1386,6 @@ __global__ void __launch_bounds__(256) k_probe_rec(const Ival<T> *__restrict__ R
                                                    const T *__restrict__ q, int64_t m,
                                                    const int32_t *__restrict__ idx_in, T *__restrict__ out,
                                                    int32_t *__restrict__ idx);
-
-// Long curves (not stageable): locate in HBM.  Each thread carries U independent queries
-// through the three dependent round trips (q -> x pair at the interpolation guess -> y, y2
-// pairs) so that U x (threads per SM) gathers are in flight.  The guess
-// (q - x_0)(n-1)/(x_{n-1} - x_0) is exact up to +-1 interval on near-uniform grids; any
-// other outcome falls back to galloping + bisection (correct for every grid).
-template <typename T>
-__global__ void __launch_bounds__(256) k_eval_global(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y,
-                                                     const T *__restrict__ y2, int n, int64_t batch,
-                                                     const T *__restrict__ q, int64_t m, T *__restrict__ out,
-                                                     int32_t *__restrict__ idx) {
-  constexpr int U = 4;
-  const int64_t total = batch * m;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  bool oor = false;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += U * stride) {
-    T qq[U], xa[U], xb[U];
-    int g[U];
-    int64_t off[U];
-    bool act[U], in[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t k = base + u * stride;
-      act[u] = k < total;
-      qq[u] = act[u] ? ld_stream(q + k) : T(0);
-      off[u] = act[u] ? ((batch == 1) ? 0 : (k / m) * n) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const T *X = x + off[u];
-      const T x0 = __ldg(X), xn = __ldg(X + n - 1);
-      in[u] = act[u] && (qq[u] >= x0 && qq[u] <= xn);
-      int gg = in[u] ? (int)((qq[u] - x0) * (T)(n - 1) / (xn - x0)) : 0;
-      g[u] = max(0, min(gg, n - 2));
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      xa[u] = __ldg(x + off[u] + g[u]);
-      xb[u] = __ldg(x + off[u] + g[u] + 1);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (in[u] && !(xa[u] <= qq[u] && (qq[u] < xb[u] || g[u] == n - 2))) {
-        const T *X = x + off[u];
-        g[u] = locate_from(X, n, g[u], qq[u]);
-        xa[u] = __ldg(X + g[u]);
-        xb[u] = __ldg(X + g[u] + 1);
-      }
-    }
-    T ya[U], yb[U], za[U], zb[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = in[u] ? g[u] : 0;
-      ya[u] = __ldg(y + off[u] + j);
-      yb[u] = __ldg(y + off[u] + j + 1);
-      za[u] = __ldg(y2 + off[u] + j);
-      zb[u] = __ldg(y2 + off[u] + j + 1);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!act[u]) continue;
-      const int64_t k = base + u * stride;
-      T val = qnan<T>();
-      int j = -1;
-      if (in[u]) {
-        j = g[u];
-        val = nr_interp(qq[u], xa[u], xb[u], ya[u], yb[u], za[u], zb[u]);
-      } else {
-        oor = true;
-      }
-      st_stream(out + k, val);
-      if (idx) st_stream(idx + k, (int32_t)j);
-    }
-  }
-  if (__syncthreads_or(oor) && threadIdx.x == 0) raise_status(status, kOutOfRange);
-}
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_probe_rec(const Ival<T> *__restrict__ R, int n, int64_t batch,

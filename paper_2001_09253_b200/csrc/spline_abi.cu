@@ -2,14 +2,21 @@
 //
 // Dispatch (build, by n and dtype):
 //   n <= 8                        K1r k1_thomas_regs     one thread per curve, registers
+//   n = 16 (f32: 32, 64)          K1h k1_thomas_half     two threads per curve, half curves in registers
 //   n <= 128                      K1 k1_thomas_pipe      two threads per curve, sweep from both ends
 //   n <= 256*RMAX (4096 f64,      K2 k_tile<FULL>        one CTA per curve: 256 leaves x R rows,
 //                  8192 f32)                              merge tree in shared memory
 //   longer                        K3 k_tile<REDUCE> -> K4 k4_top -> K5 k_tile<FINISH>   (tiled SPIKE)
-// Dispatch (eval, by the curve's staged footprint 3 n s):
-//   fits shared memory (2 stages) k_eval_staged<MODE>    curves staged in shared memory (TABLE: packed
-//                                                          knots + bucket table; SORTED; UNIFORM; BSEARCH)
-//   larger                        k_eval_global          interpolation guess + gallop in HBM
+// Dispatch (eval):
+//   SPLINE_Q_SORTED               k_eval_sorted          carried bracket + per-warp record window
+//   fp32 n <= 8, m <= 32          k_eval_small           a warp per 32 curves, records in registers
+//   n <= 64, many curves          k_eval_curvewarp       a warp per curve, Eytzinger keys
+//   fits shared memory            k_eval_warps / k_eval_staged   TMA-staged curves (BISECT, TABLE,
+//                                                          UNIFORM, BSEARCH)
+//   one curve >> L2, many queries k_bucket_*             queries bucketed by L2-sized chunks
+//   otherwise                     k_pack_records + k_eval_records   one record gather per query
+// spline_build_eval: k_build_eval_tiny | k_eval_small<true> | k_fused_staged | k_tile_eval (on
+// SPLINE_PATH_FUSED) | the two above back to back.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -622,10 +629,8 @@ int eval_t(const T *x, const T *y, const T *y2, int64_t n, int64_t batch, const 
     cudaFreeAsync(ws, st);
     return rc;
   }
-  cudaGetLastError();  // clear the failed allocation
-  const int64_t grid = std::min<int64_t>((total + 1023) / 1024, 148 * 16);
-  k_eval_global<T><<<(unsigned)grid, 256, 0, st>>>(tl_status, x, y, y2, (int)n, batch, q, m, out, idx);
-  return launch_rc();
+  cudaGetLastError();  // clear the failed allocation: the caller sees SPLINE_ENOMEM
+  return SPLINE_ENOMEM;
 }
 
 // ------------------------------------------------------------------ fused build + eval
