@@ -502,13 +502,20 @@ template <typename T> bool small_eval_ok(int64_t n, const T *q, int64_t m, const
 // ---- one long curve, many unsorted queries: queries bucketed by L2-sized chunks (eval_bucket.cuh)
 constexpr size_t kBkChunkBytes = size_t(24) << 20;  // x, y, y2 of one chunk: 2-3 chunks live in the 126 MB L2
 template <typename T> bool bucket_eligible(int64_t n, int64_t batch, int64_t m) {
-  // the curve must dwarf L2 (else the record gathers hit L2 anyway) and carry many queries
+  // the curve must dwarf L2 (else the record gathers hit L2 anyway) and carry many queries;
+  // FASTSPLINE_BUCKET_MIN_N (test tooling: sanitizer runs on small shapes) lowers the size bar
+  static const int64_t min_n = [] {
+    const char *e = getenv("FASTSPLINE_BUCKET_MIN_N");
+    return e && *e ? (int64_t)atoll(e) : (int64_t)-1;
+  }();
+  if (min_n >= 0) return batch == 1 && n >= min_n && m >= n / 4;
   return batch == 1 && 3 * sizeof(T) * (size_t)n > 4 * kBkChunkBytes && m >= (int64_t)1 << 20 && m >= n / 4;
 }
 template <typename T>
 int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, int64_t m, T *out, int32_t *idx,
                   cudaStream_t st) {
   int64_t K = (int64_t)(kBkChunkBytes / sizeof(Knot<T>));
+  K = std::min<int64_t>(K, std::max<int64_t>(1024, (n - 1) / 8));  // at least ~8 chunks on shorter curves
   K = std::max<int64_t>(K, (n - 1 + kBkMaxBuckets - 1) / kBkMaxBuckets);
   const int nb = (int)((n - 1 + K - 1) / K);
   const int64_t ntiles = (m + kBkTile - 1) / kBkTile;
