@@ -78,13 +78,20 @@ __device__ __forceinline__ float nr_rcp(float a) {
   const float e = __fmaf_rn(-a, r, 1.0f);
   return __fmaf_rn(r, e, r);
 }
+#ifndef FS_BUILD_RCP_RN
+#define FS_BUILD_RCP_RN 0
+#endif
 __device__ __forceinline__ double nr_rcp(double a) {
+#if FS_BUILD_RCP_RN
+  return __drcp_rn(a);  // correctly rounded (A/B: DESIGN.md)
+#else
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
   double e = __fma_rn(-a, r, 1.0);
   r = __fma_rn(r, e, r);
   e = __fma_rn(-a, r, 1.0);
   return __fma_rn(r, e, r);
+#endif
 }
 // The eval kernels' fp64 reciprocal: the correctly rounded __drcp_rn costs a slow-path
 // sequence per query in the sorted-run kernel; the Newton-refined seed is within ~1 ulp and is
