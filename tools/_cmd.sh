@@ -1,8 +1,6 @@
-T=gpurun_out/r02w; mkdir -p $T
+T=gpurun_out/r02x; mkdir -p $T
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fused.py tests/test_gpu_ablation.py tests/test_gpu_determinism.py -q -x --timeout 600 > $T/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $T/pytest.log
 L=paper_2001_09253_b200/csrc/libfastspline.so
 cp $L /tmp/live.so
-for v in A P; do cp paper_2001_09253_b200/csrc/libfastspline_$v.so $L
-  timeout 600 python tools/precision_report.py $T/precision_$v.json > $T/precision_$v.log 2>&1; echo "$v prec rc=$?"; tail -12 $T/precision_$v.log
-  for c in 1 4 5; do timeout 300 python tools/time_paths.py $c 10 2>&1 | grep -E " build | build\+eval" | sed "s/^/$v /"; done
-done
+for r in 1 2; do for v in A F; do cp paper_2001_09253_b200/csrc/libfastspline_$v.so $L; timeout 300 python tools/time_paths.py 4 20 2>&1 | grep -E " eval" | sed "s/^/$v r$r /"; done; done
 cp /tmp/live.so $L
