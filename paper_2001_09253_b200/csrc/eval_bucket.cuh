@@ -393,8 +393,12 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
   raise_status_warp(status, oor, kOutOfRange);
 }
 
+#ifndef FS_BK_GATHER_THREADS
+#define FS_BK_GATHER_THREADS 512
+#endif
+constexpr int kBkGaThreads = FS_BK_GATHER_THREADS;  // the gather's CTA (kBkTile / kBkGaThreads slots per thread)
 template <typename T>
-__global__ void __launch_bounds__(kBkScThreads, 2) k_bucket_gather(const T *__restrict__ os, const int32_t *__restrict__ is,
+__global__ void __launch_bounds__(kBkGaThreads, 2048 / kBkGaThreads) k_bucket_gather(const T *__restrict__ os, const int32_t *__restrict__ is,
                                                                    const uint16_t *__restrict__ perm, int64_t m,
                                                                    T *__restrict__ out, int32_t *__restrict__ idx) {
   extern __shared__ __align__(16) unsigned char bk_smem[];  // bucket_gather_smem<T>() bytes
@@ -404,8 +408,8 @@ __global__ void __launch_bounds__(kBkScThreads, 2) k_bucket_gather(const T *__re
   const int nq = (int)min64(kBkTile, m - q0);
   // the tile's results in slot order -> query order through perm, then coalesced stores
 #pragma unroll
-  for (int u = 0; u < kBkPerThread; ++u) {
-    const int s = u * kBkScThreads + threadIdx.x;
+  for (int u = 0; u < (kBkTile / kBkGaThreads); ++u) {
+    const int s = u * kBkGaThreads + threadIdx.x;
     if (s < nq) {
       const int i = perm[q0 + s];
       so[i] = ld_stream(os + q0 + s);
@@ -413,7 +417,7 @@ __global__ void __launch_bounds__(kBkScThreads, 2) k_bucket_gather(const T *__re
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nq; i += kBkScThreads) {
+  for (int i = threadIdx.x; i < nq; i += kBkGaThreads) {
     st_stream(out + q0 + i, so[i]);
     if (idx) st_stream(idx + q0 + i, si[i]);
   }

@@ -554,7 +554,7 @@ int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, in
                                                                                            bsum, qs, dest, perm);
     k_bucket_eval<T><<<(unsigned)neval, kBkThreads, 0, st>>>(tl_status, kn, (int)n, K, nb, m, cnt, bsum, qs, dest, os,
                                                              is);
-    k_bucket_gather<T><<<(unsigned)ntiles, kBkScThreads, bucket_gather_smem<T>(), st>>>(os, is, perm, m, out, idx);
+    k_bucket_gather<T><<<(unsigned)ntiles, kBkGaThreads, bucket_gather_smem<T>(), st>>>(os, is, perm, m, out, idx);
     rc = launch_rc();
   }
   cudaFreeAsync(ws, st);
