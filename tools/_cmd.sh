@@ -1,6 +1,3 @@
-T=gpurun_out/r02y; mkdir -p $T
-L=paper_2001_09253_b200/csrc/libfastspline.so
-cp $L /tmp/live.so
-timeout 300 python tools/time_paths.py 5 5 2>&1 | grep -E " eval" | sed "s/^/old /"
-for r in 1 2; do for v in A E G; do cp paper_2001_09253_b200/csrc/libfastspline_$v.so $L; timeout 300 python tools/time_paths.py 5 5 2>&1 | grep -E " eval" | sed "s/^/$v r$r /"; done; done
-cp /tmp/live.so $L
+T=gpurun_out/r02z; mkdir -p $T
+nproc > $T/nproc.txt; free -g >> $T/nproc.txt
+timeout 2400 python -m pytest tests -m gpu -q -x --timeout 1800 -s -p no:cacheprovider > $T/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $T/pytest.log; grep -E "full|every query" $T/pytest.log | head
