@@ -628,7 +628,10 @@ def main():
         # tiled SPIKE: reduce + top (grouped for one curve of > 128 tiles: up, root, down) + finish;
         # eval: pack records + gather
         ntiles = -(-n // (256 * (16 if s == 8 else 32)))
-        launches = (7 if (B == 1 and ntiles > 128) else 5) * K
+        bucketed = B == 1 and 3 * s * n > 4 * (24 << 20) and m >= (1 << 20) and m >= n // 4
+        # build: memset + K3 + K4 (3 grouped launches for one curve of > 128 tiles, else 1) + K5;
+        # eval: bucketed (count, pack, scan x2, scatter, eval, gather) or records (pack, gather)
+        launches = ((5 if (B == 1 and ntiles > 128) else 3) + (7 if bucketed else 2)) * K
     if fused_step or small_step or tiny_step or tile_step:
         launches = K
     one_kernel = fused_step or small_step or tiny_step or tile_step
@@ -640,6 +643,8 @@ def main():
         ekern = "k_eval_small"
     elif (n <= 64 and B >= 4 * 148 and m % (16 // s) == 0 and not (wl.flags & workloads.FLAG_X_UNIFORM)):
         ekern = "k_eval_curvewarp"
+    elif long_curve and B == 1 and 3 * s * n > 4 * (24 << 20) and m >= (1 << 20) and m >= n // 4:
+        ekern = "k_bucket_count + k_pack_knots + k_scan + k_bucket_scatter + k_bucket_eval + k_bucket_gather"
     elif long_curve or 3 * n * s > 200 * 1024:
         ekern = "k_pack_records + k_eval_records"
     elif n <= 512 and not (wl.flags & workloads.FLAG_X_UNIFORM) and B >= 8 and m < 2048:
