@@ -885,6 +885,10 @@ constexpr int kSortWin = 32;
 #define FS_SORTED_FAST 0  // measured: 1497 vs 1112 us on cfg4 (A/B)
 #endif
 constexpr bool kSortedFast = FS_SORTED_FAST != 0;  // the warp-uniform fast path of sorted_run (WIN)
+#ifndef FS_SORTED_L1PF
+#define FS_SORTED_L1PF 1
+#endif
+constexpr bool kSortedL1Prefetch = FS_SORTED_L1PF != 0;  // L1 prefetch of the next window's knots
 constexpr int kSortWinDensity = 8;  // queries per interval from which the window pays
 // One window record: the interval's left knot and its cubic (Cub + e2), 16-byte aligned so that
 // a lookup is 2 (fp32) or 3 (fp64) vector loads.
@@ -968,6 +972,17 @@ __device__ __forceinline__ bool sorted_run(const T *__restrict__ X, const T *__r
           if (lane == kSortWin - 1) sw.x[kSortWin] = inf_of<T>();
         }
         __syncwarp();
+        if constexpr (kSortedL1Prefetch) {
+          // the next rebuild starts in (wb + 16, wb + 32] and reads up to 32 intervals on: pull
+          // those knots into L1 now (3 lines of x, y, y2 each), so its loads hit L1 instead of
+          // waiting on L2 (ncu r02: the rebuild's x/y loads were 28% of the stall samples)
+          if (lane < 9) {
+            const int a = lane / 3, part = lane % 3;
+            const T *base = a == 0 ? X : a == 1 ? Y : Z.prefetch_ptr();
+            const int j = min(wb + kSortWin + part * (128 / (int)sizeof(T)), n - 1);
+            if (base) prefetch_l1(base + j);
+          }
+        }
       }
     }
     int jl = -1;

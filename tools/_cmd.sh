@@ -1,3 +1,5 @@
-T=gpurun_out/r02z; mkdir -p $T
-nproc > $T/nproc.txt; free -g >> $T/nproc.txt
-timeout 2400 python -m pytest tests -m gpu -q -x --timeout 1800 -s -p no:cacheprovider > $T/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $T/pytest.log; grep -E "full|every query" $T/pytest.log | head
+T=gpurun_out/r02aa; mkdir -p $T
+L=paper_2001_09253_b200/csrc/libfastspline.so
+cp $L /tmp/live.so
+for r in 1 2; do for v in A L; do cp paper_2001_09253_b200/csrc/libfastspline_$v.so $L; timeout 300 python tools/time_paths.py 4 20 2>&1 | grep -E " eval" | sed "s/^/$v r$r /"; done; done
+cp /tmp/live.so $L
