@@ -1268,6 +1268,177 @@ __global__ void __launch_bounds__(256, FS_SORTED_MINB) k_eval_sorted(unsigned *_
   raise_status_warp(status, oor, kOutOfRange);
 }
 
+// ---- dense sorted runs: each lane walks its own contiguous queries (k_eval_walk) -----------
+// A warp takes its run in supersteps of kWalkQ = 256 queries.  The superstep's queries are
+// loaded coalesced (256-bit accesses: 1 KB per warp instruction) and transposed through a padded
+// shared-memory stage so that lane l owns queries [8l, 8l+8) -- consecutive, hence (sorted) in the
+// same or the next interval.  Lane l locates its first query in the warp's window of 32 interval
+// records (built at the carry, as in sorted_run) by a 5-level branch-free search, keeps that
+// interval's record in REGISTERS and walks: each next query advances the slot by one when it
+// passes the record's right knot (predicated: no branch), and is verified against the record's
+// [x0, x1); a query that jumps further, falls outside the window or arrives out of order (a wrong
+// sorted hint) takes the general path.  Results go back through the stage and out with 256-bit
+// stores.  Per query: one shared-memory load, a compare, the 7-operation cubic and two stores --
+// against the window lift + record load of sorted_run.  Bitwise the other forms (make_cub +
+// cub_eval on the same interval).
+constexpr int kWalkQ = 256, kWalkPer = kWalkQ / 32, kWalkPad = kWalkPer + 1;
+#ifndef FS_WALK_REBUILD
+#define FS_WALK_REBUILD 4
+#endif
+constexpr int kWalkRebuild = FS_WALK_REBUILD;
+template <typename T> struct WalkStage {
+  T q[32 * kWalkPad];        // queries, then the results in place (row l = lane l's 8, padded)
+  int32_t j[32 * kWalkPad];  // interval indices
+};
+
+template <typename T, typename ZA>
+__device__ __forceinline__ bool walk_run(const T *__restrict__ X, const T *__restrict__ Y, const ZA &Z, int n,
+                                         const T *__restrict__ qb, T *__restrict__ ob, int32_t *__restrict__ ib,
+                                         int64_t k0, int64_t k1, SortWin<T> &sw, WalkStage<T> &st, int lane) {
+  constexpr int VE = 32 / sizeof(T);  // elements per 256-bit access
+  constexpr int NI = kWalkQ / (32 * VE);  // 256-bit loads per lane per superstep
+  const T x0 = __ldg(X), xn = __ldg(X + n - 1);
+  T qf = __ldg(qb + k0);
+  qf = (qf >= x0 && qf <= xn) ? qf : x0;
+  int jc = warp_locate(X, n, qf, lane);
+  bool oor = false;
+  int wb = -(1 << 30);
+  // this superstep's queries in registers (coalesced), the next superstep's in flight
+  T qn[NI][VE];
+#pragma unroll
+  for (int a = 0; a < NI; ++a) {
+    const int64_t k = k0 + (int64_t)(a * 32 + lane) * VE;
+    if (k < k1) ld_cs_256(qb + k, qn[a]);
+  }
+  for (int64_t base = k0; base < k1; base += kWalkQ) {
+    // stage: 256-bit group g = a*32 + lane holds queries [g VE, g VE + VE) -> row (g VE) / 8
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < NI; ++a) {
+      const int g = (a * 32 + lane) * VE;
+#pragma unroll
+      for (int e = 0; e < VE; ++e) st.q[(g + e) / kWalkPer * kWalkPad + (g + e) % kWalkPer] = qn[a][e];
+    }
+#pragma unroll
+    for (int a = 0; a < NI; ++a) {
+      const int64_t k = base + kWalkQ + (int64_t)(a * 32 + lane) * VE;
+      if (k < k1) ld_cs_256(qb + k, qn[a]);  // next superstep in flight
+    }
+    // the window at the carry (warp-uniform): a superstep spans ~kWalkQ / density intervals
+    // (16 on cfg4) beyond the carry, so the window moves on as soon as the carry is 4 past its base
+    if (jc < wb || jc - wb > kWalkRebuild) {
+      wb = jc;
+      const int jw = wb + lane;
+      if (jw <= n - 2) {
+        const T xa = __ldg(X + jw), xb = __ldg(X + jw + 1);
+        T e2;
+        const Cub<T> cb = make_cub<T>(xa, xb, __ldg(Y + jw), __ldg(Y + jw + 1), Z(jw), Z(jw + 1), e2);
+        sw.r[lane] = WRec<T>{xa, cb.ih, cb.y0, cb.dy, cb.e1, e2};
+        sw.x[lane] = xa;
+        if (lane == kSortWin - 1) sw.x[kSortWin] = xb;
+      } else {
+        sw.x[lane] = inf_of<T>();
+        if (lane == kSortWin - 1) sw.x[kSortWin] = inf_of<T>();
+      }
+      if constexpr (kSortedL1Prefetch) {
+        if (lane < 9) {
+          const int a = lane / 3, part = lane % 3;
+          const T *pb = a == 0 ? X : a == 1 ? Y : Z.prefetch_ptr();
+          if (pb) prefetch_l1(pb + min(wb + kSortWin + part * (128 / (int)sizeof(T)), n - 1));
+        }
+      }
+    }
+    __syncwarp();
+    // lane l: queries [8l, 8l+8) of the superstep
+    const int nq = (int)min64(kWalkPer, k1 - base - (int64_t)lane * kWalkPer);
+    T *rq = st.q + lane * kWalkPad;
+    int32_t *rj = st.j + lane * kWalkPad;
+    int jl = -1;
+    if (nq > 0) {
+      const T q0 = rq[0];
+      const T qs = (q0 >= x0 && q0 <= xn) ? q0 : x0;
+      int l = 0;
+#pragma unroll
+      for (int d = kSortWin / 2; d >= 1; d >>= 1) l = (sw.x[l + d] <= qs) ? l + d : l;
+      WRec<T> r = ld_wrec(&sw.r[l]);
+      T xr = sw.x[l + 1];
+      int j = wb + l;
+#pragma unroll
+      for (int i = 0; i < kWalkPer; ++i) {
+        if (i < nq) {
+          const T qq = rq[i];
+          const bool in = (qq >= x0) && (qq <= xn);
+          const T qc = in ? qq : x0;
+          if (qc >= xr && l < kSortWin - 1) {  // the next interval (predicated reload)
+            ++l;
+            r = ld_wrec(&sw.r[l]);
+            xr = sw.x[l + 1];
+          }
+          T v;
+          if (qc >= r.x0 && (qc < xr || wb + l == n - 2)) {
+            j = wb + l;
+            v = cub_eval<T>(Cub<T>{r.ih, r.y0, r.dy, r.e1}, r.e2, r.x0, qc);
+          } else {  // a longer jump, past the window, or out of order: the general path
+            j = max(0, min(j, n - 2));
+            v = general_query<T, FORM_RECORD>(X, Y, Z, n, qc, j);
+            if (j - wb >= 0 && j - wb < kSortWin) {  // resynchronise the walk at the found interval
+              l = j - wb;
+              r = ld_wrec(&sw.r[l]);
+              xr = sw.x[l + 1];
+            }
+          }
+          rq[i] = in ? v : qnan<T>();
+          rj[i] = in ? j : -1;
+          oor |= !in;
+          if (in) jl = j;
+        }
+      }
+    }
+    __syncwarp();
+    // results out: the same 256-bit groups the queries came in
+#pragma unroll
+    for (int a = 0; a < NI; ++a) {
+      const int g = (a * 32 + lane) * VE;
+      const int64_t k = base + g;
+      if (k < k1) {
+        T v[VE];
+        int jv[VE];
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+          v[e] = st.q[(g + e) / kWalkPer * kWalkPad + (g + e) % kWalkPer];
+          jv[e] = st.j[(g + e) / kWalkPer * kWalkPad + (g + e) % kWalkPer];
+        }
+        st_cs_256(ob + k, v);
+        if (ib) VecIO<int32_t, VE>::store_idx(ib + k, jv);
+      }
+    }
+    const int jm = __reduce_max_sync(0xffffffffu, jl);
+    if (jm >= 0) jc = jm;
+  }
+  return oor;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, FS_SORTED_MINB) k_eval_walk(unsigned *__restrict__ status, const T *__restrict__ x,
+                                                                   const T *__restrict__ y, const T *__restrict__ y2,
+                                                                   int n, const T *__restrict__ q, int64_t m,
+                                                                   T *__restrict__ out, int32_t *__restrict__ idx,
+                                                                   int64_t qrun, int64_t runs_per_curve,
+                                                                   int64_t ntasks) {
+  pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+  if (task >= ntasks) return;
+  const int64_t c = task / runs_per_curve;
+  const int64_t k0 = (task - c * runs_per_curve) * qrun;
+  const int64_t k1 = min64(m, k0 + qrun);
+  __shared__ SortWin<T> wins[8];
+  __shared__ WalkStage<T> stages[8];
+  const bool oor = walk_run<T>(x + c * n, y + c * n, ZGlobal<T>{y2 + c * n}, n, q + c * m, out + c * m,
+                               idx ? idx + c * m : nullptr, k0, k1, wins[w], stages[w], lane);
+  raise_status_warp(status, oor, kOutOfRange);
+}
+
 // ---- long curves through interval records in HBM ---------------------------------------
 // k_pack_records writes, per curve c, the interval records R[c n + j] (j < n-1; the full
 // common.cuh Ival, 32 B fp32 / 64 B fp64, one aligned DRAM burst) and a header

@@ -455,6 +455,9 @@ template <typename T> bool sorted_v4_ok(const T *q, int64_t m, const T *out, con
   return m % 4 == 0 && (((uintptr_t)q | (uintptr_t)out) & A) == 0 && (!idx || ((uintptr_t)idx & 15) == 0);
 }
 
+#ifndef FS_SORTED_WALK
+#define FS_SORTED_WALK 0  // A/B: 1.54 vs 1.10 ms on cfg4
+#endif
 template <typename T, int V, int FORM = FORM_RECORD>
 int launch_sorted_k(const T *x, const T *y, const T *y2, int n, int64_t batch, const T *q, int64_t m, T *out,
                     int32_t *idx, cudaStream_t st) {
@@ -462,6 +465,15 @@ int launch_sorted_k(const T *x, const T *y, const T *y2, int n, int64_t batch, c
   int64_t qrun = 8192;
   while (qrun > 256 && batch * ((m + qrun - 1) / qrun) < 148 * 32) qrun >>= 1;
   qrun = (qrun + 32 * V - 1) / (32 * V) * (32 * V);
+  // dense runs with 32-byte aligned q / out and m % 8 == 0: every lane walks its own queries
+  if (FS_SORTED_WALK && FORM == FORM_RECORD && m >= (int64_t)kSortWinDensity * (n - 1) && m % 8 == 0 &&
+      ((((uintptr_t)q) | ((uintptr_t)out)) & 31) == 0 && (!idx || (((uintptr_t)idx) & (sizeof(T) == 4 ? 31 : 15)) == 0)) {
+    const int64_t qw = (qrun + kWalkQ - 1) / kWalkQ * kWalkQ;
+    const int64_t rpcw = (m + qw - 1) / qw;
+    const int64_t ntw = batch * rpcw;
+    return launch_pdl(k_eval_walk<T>, dim3((unsigned)((ntw + 7) / 8)), dim3(256), 0, st, tl_status, x, y, y2, n, q, m,
+                      out, idx, qw, rpcw, ntw);
+  }
   const int64_t rpc = (m + qrun - 1) / qrun;
   const int64_t ntasks = batch * rpc;
   const int64_t grid = (ntasks + 7) / 8;
