@@ -1,4 +1,3 @@
-L=paper_2001_09253_b200/csrc/libfastspline.so
-cp $L /tmp/live.so
-for r in 1 2; do for v in A W0 W4 W8; do cp paper_2001_09253_b200/csrc/libfastspline_$v.so $L; timeout 300 python tools/time_paths.py 4 20 2>&1 | grep -E " eval" | sed "s/^/$v r$r /"; done; done
-cp /tmp/live.so $L
+T=gpurun_out/r02ae; mkdir -p $T
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/random_probe tools/probe/random_probe.cu && /tmp/random_probe > $T/random_probe.json 2>&1; echo "rc=$?"; cat $T/random_probe.json
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/stream_probe tools/probe/stream_probe.cu && /tmp/stream_probe > $T/stream_probe.txt 2>&1; cat $T/stream_probe.txt
