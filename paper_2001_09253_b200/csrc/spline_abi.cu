@@ -46,6 +46,10 @@ constexpr int kK1MaxN = 128;
 constexpr int64_t kFuseMaxWork = int64_t(1) << 17;
 constexpr int kNoFusedStaged = 1 << 30;  // internal: automatic path, but not k_fused_staged
 constexpr int kEvalNoBucket = SPLINE_NO_BUCKET;  // spline_eval: the record-gather path for long curves
+#ifndef FS_SPLIT_OVERLAP
+#define FS_SPLIT_OVERLAP 0  // A/B: 1358 vs 1283 us on cfg4 -- the concurrent build slows the evaluation more
+#endif
+constexpr bool kSplitOverlap = FS_SPLIT_OVERLAP != 0;  // build half B while half A is evaluated
 
 template <typename T> constexpr int rmax() { return sizeof(T) == 8 ? 16 : 32; }
 
@@ -743,6 +747,51 @@ int launch_fused(const T *x, const T *y, int n, int64_t batch, int bc, const T *
                                                        nchunks, qchunk, nitems, st);
 }
 
+// Internal streams and per-call events (the host path; the overlapped split path)
+constexpr int kHostStreams = 3;
+constexpr size_t kHostChunkBytes = 32u << 20;  // target copy traffic per chunk
+
+struct HostStreams {
+  cudaStream_t s[kHostStreams];
+};
+inline int host_streams(HostStreams **out) {
+  static std::mutex mu;
+  static HostStreams *per_dev[128] = {};
+  int dev = 0;
+  if (int rc = cuda_rc(cudaGetDevice(&dev))) return rc;
+  if (dev < 0 || dev >= 128) return SPLINE_ECUDA;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!per_dev[dev]) {
+    auto *h = new HostStreams;
+    for (int i = 0; i < kHostStreams; ++i)
+      if (int rc = cuda_rc(cudaStreamCreateWithFlags(&h->s[i], cudaStreamNonBlocking))) return rc;
+    per_dev[dev] = h;
+  }
+  *out = per_dev[dev];
+  return SPLINE_OK;
+}
+// The events of ONE host call (never shared between calls, so concurrent calls from several
+// threads cannot re-record each other's start/done points).  Destroyed at the end of the call:
+// CUDA releases an event still pending on the device once it completes.
+struct CallEvents {
+  cudaEvent_t start = nullptr, ready = nullptr, done[kHostStreams] = {};
+  int init() {
+    int rc = cuda_rc(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    for (int k = 0; !rc && k < kHostStreams; ++k) rc = cuda_rc(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+    return rc;
+  }
+  ~CallEvents() {
+    if (start) cudaEventDestroy(start);
+    if (ready) cudaEventDestroy(ready);
+    for (int k = 0; k < kHostStreams; ++k)
+      if (done[k]) cudaEventDestroy(done[k]);
+  }
+};
+// Device bytes one chunk slot may take (3 slots in flight): caps the curves per chunk for very
+// long curves / many queries, whatever the SM floor asks for.
+constexpr size_t kMaxSlotBytes = size_t(4) << 30;
+
 // ---- fused build + eval of mid-length curves with sorted queries (k_tile_eval) ---------------
 template <typename T, int R, int V, bool WIN>
 int launch_tile_eval_k(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
@@ -865,8 +914,31 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
   if (!yy) {
     if (int rc = ws_alloc((void **)&yy, sizeof(T) * (size_t)n * batch, st)) return rc;
   }
-  int rc = build_t<T>(x, y, n, batch, bc, yp1, ypn, yy, st);
-  if (!rc) rc = eval_t<T>(x, y, yy, n, batch, q, m, out, idx, flags, st);
+  int rc;
+  if (kSplitOverlap && n > kK1MaxN && n <= 256 * rmax<T>() && batch >= 8 * (int64_t)num_sms()) {
+    // many mid-length curves (cfg4): the partition build is latency-bound at 2 CTAs/SM, the
+    // evaluation issue-bound -- build the second half of the batch on an internal stream while
+    // the first half is evaluated:  st: build A -> eval A -> (wait B) -> eval B;  s2: build B
+    HostStreams *hs = nullptr;
+    CallEvents ev;
+    rc = host_streams(&hs);
+    if (!rc) rc = ev.init();
+    const int64_t h = batch / 2;
+    cudaStream_t s2 = hs ? hs->s[0] : st;
+    if (!rc) rc = build_t<T>(x, y, n, h, bc, yp1, ypn, yy, st);
+    if (!rc) rc = cuda_rc(cudaEventRecord(ev.start, st));
+    if (!rc) rc = cuda_rc(cudaStreamWaitEvent(s2, ev.start, 0));
+    if (!rc) rc = build_t<T>(x + h * n, y + h * n, n, batch - h, bc, (bc & 1) ? yp1 + h : yp1, (bc & 2) ? ypn + h : ypn,
+                             yy + h * n, s2);
+    if (!rc) rc = cuda_rc(cudaEventRecord(ev.done[0], s2));
+    if (!rc) rc = eval_t<T>(x, y, yy, n, h, q, m, out, idx, flags, st);
+    if (!rc) rc = cuda_rc(cudaStreamWaitEvent(st, ev.done[0], 0));
+    if (!rc) rc = eval_t<T>(x + h * n, y + h * n, yy + h * n, n, batch - h, q + h * m, m, out + h * m,
+                            idx ? idx + h * m : nullptr, flags, st);
+  } else {
+    rc = build_t<T>(x, y, n, batch, bc, yp1, ypn, yy, st);
+    if (!rc) rc = eval_t<T>(x, y, yy, n, batch, q, m, out, idx, flags, st);
+  }
   if (!y2) cudaFreeAsync(yy, st);
   return rc;
 }
@@ -878,50 +950,6 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
 // D2H overlap (PCIe is full duplex).  Device buffers come from the library pool; the call is
 // ordered after prior work on `stream`, and `stream` waits for all of it.  Pinned host memory
 // gives the overlap; pageable memory is correct but serialises the copies.
-constexpr int kHostStreams = 3;
-constexpr size_t kHostChunkBytes = 32u << 20;  // target copy traffic per chunk
-
-struct HostStreams {
-  cudaStream_t s[kHostStreams];
-};
-inline int host_streams(HostStreams **out) {
-  static std::mutex mu;
-  static HostStreams *per_dev[128] = {};
-  int dev = 0;
-  if (int rc = cuda_rc(cudaGetDevice(&dev))) return rc;
-  if (dev < 0 || dev >= 128) return SPLINE_ECUDA;
-  std::lock_guard<std::mutex> lk(mu);
-  if (!per_dev[dev]) {
-    auto *h = new HostStreams;
-    for (int i = 0; i < kHostStreams; ++i)
-      if (int rc = cuda_rc(cudaStreamCreateWithFlags(&h->s[i], cudaStreamNonBlocking))) return rc;
-    per_dev[dev] = h;
-  }
-  *out = per_dev[dev];
-  return SPLINE_OK;
-}
-// The events of ONE host call (never shared between calls, so concurrent calls from several
-// threads cannot re-record each other's start/done points).  Destroyed at the end of the call:
-// CUDA releases an event still pending on the device once it completes.
-struct CallEvents {
-  cudaEvent_t start = nullptr, ready = nullptr, done[kHostStreams] = {};
-  int init() {
-    int rc = cuda_rc(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-    if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    for (int k = 0; !rc && k < kHostStreams; ++k) rc = cuda_rc(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
-    return rc;
-  }
-  ~CallEvents() {
-    if (start) cudaEventDestroy(start);
-    if (ready) cudaEventDestroy(ready);
-    for (int k = 0; k < kHostStreams; ++k)
-      if (done[k]) cudaEventDestroy(done[k]);
-  }
-};
-// Device bytes one chunk slot may take (3 slots in flight): caps the curves per chunk for very
-// long curves / many queries, whatever the SM floor asks for.
-constexpr size_t kMaxSlotBytes = size_t(4) << 30;
-
 // One long curve with many queries: the knots go up and the build runs first (every query
 // needs the whole y2), then the queries flow in chunks through the internal streams (each
 // chunk: H2D q, eval, D2H out/idx), overlapping the two PCIe directions.  Few, large chunks:

@@ -48,6 +48,8 @@ paths = {
     "build+eval": (lambda: (api.build(x, y, wl.bc, yp1, ypn, out=y2),
                             api.evaluate(x, y, y2, q, wl.flags, out=out, idx=idx)),
                    (2 * s + 4) * B * m + 3 * s * B * n + 3 * s * B * n),
+    "step (auto)": (lambda: api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags, y2=y2, out=out, idx=idx),
+                    (2 * s + 4) * B * m + 3 * s * B * n + 3 * s * B * n),
     "fused(y2)": (lambda: api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags | api.PATH_FUSED, y2=y2, out=out, idx=idx),
                   (2 * s + 4) * B * m + 3 * s * B * n),
     "fused(no y2)": (lambda: api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags | api.PATH_FUSED, want_y2=False, out=out, idx=idx),
