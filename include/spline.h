@@ -19,7 +19,9 @@
  *     per (n, m) group).
  *   - Work is enqueued on `stream` (NULL = the legacy default stream) and the call
  *     returns without synchronising.  The library is re-entrant; the only shared
- *     mutable state is the device-wide data-error word read by spline_status().
+ *     mutable state is the per-stream data-error words read by spline_status() (one device
+ *     word per stream handle, allocated on a device's first call: make one call, e.g.
+ *     spline_status, before capturing a CUDA graph).
  *   - Temporary workspace (long-curve SPIKE records; y2 scratch of an unfused
  *     spline_build_eval called without y2) comes from a library-owned stream-ordered
  *     memory pool per device (cudaMallocFromPoolAsync on `stream`) that keeps its
@@ -32,7 +34,7 @@
  *     batch == 0 or m == 0 is a valid no-op.
  *   - CUDA launch/allocation failures return SPLINE_ECUDA / SPLINE_ENOMEM.
  *   - Data errors are asynchronous (cuSOLVER devInfo pattern) and OR'ed into the
- *     device-wide status word read (and cleared) by spline_status():
+ *     launching stream's status word, read (and cleared) by spline_status(stream):
  *       SPLINE_STATUS_BAD_KNOTS: a curve's knots are not strictly increasing or a
  *         value/slope is not finite; that curve's y2 is all NaN.
  *       SPLINE_STATUS_Q_OUT_OF_RANGE: a query is outside [x_0, x_{n-1}] or NaN
@@ -190,9 +192,9 @@ int spline_eval_f32(const float *x, const float *y, const float *y2, int64_t n, 
 int spline_eval_f64(const double *x, const double *y, const double *y2, int64_t n, int64_t batch,
                     const double *q, int64_t m, double *out, int32_t *idx, int flags, spline_stream_t stream);
 
-/* Synchronises `stream`, writes the OR of the data-error bits raised since the
- * last call into *bits_out (host pointer) and clears them.  Returns SPLINE_OK or
- * SPLINE_ECUDA. */
+/* Synchronises `stream`, writes the OR of the data-error bits raised ON THIS STREAM since the
+ * last call into *bits_out (host pointer) and clears them (other streams' words are untouched).
+ * Returns SPLINE_OK, SPLINE_ECUDA or SPLINE_ENOMEM (the word could not be allocated). */
 int spline_status(spline_stream_t stream, unsigned int *bits_out);
 
 /*
