@@ -170,6 +170,51 @@ template <typename T> int broadcast_x(const T *x, int64_t n, int64_t batch, cuda
   return launch_rc();
 }
 
+// Internal streams and per-call events (the host path; the overlapped split path)
+constexpr int kHostStreams = 3;
+constexpr size_t kHostChunkBytes = 32u << 20;  // target copy traffic per chunk
+
+struct HostStreams {
+  cudaStream_t s[kHostStreams];
+};
+inline int host_streams(HostStreams **out) {
+  static std::mutex mu;
+  static HostStreams *per_dev[128] = {};
+  int dev = 0;
+  if (int rc = cuda_rc(cudaGetDevice(&dev))) return rc;
+  if (dev < 0 || dev >= 128) return SPLINE_ECUDA;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!per_dev[dev]) {
+    auto *h = new HostStreams;
+    for (int i = 0; i < kHostStreams; ++i)
+      if (int rc = cuda_rc(cudaStreamCreateWithFlags(&h->s[i], cudaStreamNonBlocking))) return rc;
+    per_dev[dev] = h;
+  }
+  *out = per_dev[dev];
+  return SPLINE_OK;
+}
+// The events of ONE host call (never shared between calls, so concurrent calls from several
+// threads cannot re-record each other's start/done points).  Destroyed at the end of the call:
+// CUDA releases an event still pending on the device once it completes.
+struct CallEvents {
+  cudaEvent_t start = nullptr, ready = nullptr, done[kHostStreams] = {};
+  int init() {
+    int rc = cuda_rc(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    for (int k = 0; !rc && k < kHostStreams; ++k) rc = cuda_rc(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+    return rc;
+  }
+  ~CallEvents() {
+    if (start) cudaEventDestroy(start);
+    if (ready) cudaEventDestroy(ready);
+    for (int k = 0; k < kHostStreams; ++k)
+      if (done[k]) cudaEventDestroy(done[k]);
+  }
+};
+// Device bytes one chunk slot may take (3 slots in flight): caps the curves per chunk for very
+// long curves / many queries, whatever the SM floor asks for.
+constexpr size_t kMaxSlotBytes = size_t(4) << 30;
+
 // ------------------------------------------------------------------------ build
 
 template <typename T, int R>
@@ -559,15 +604,28 @@ int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, in
   int *bsum = (int *)take(bs);
   int rc = set_smem(k_bucket_scatter<T>, bucket_scatter_smem<T>());
   if (!rc) rc = set_smem(k_bucket_gather<T>, bucket_gather_smem<T>());
+  // the knot packing (bandwidth-bound) runs on an internal stream beside the counting and the
+  // scatter (shared-memory-atomic-bound); the evaluation waits for both
+  HostStreams *hs = nullptr;
+  CallEvents ev;
+  if (!rc) rc = host_streams(&hs);
+  if (!rc) rc = ev.init();
+  if (!rc) rc = cuda_rc(cudaEventRecord(ev.start, st));
+  if (!rc) rc = cuda_rc(cudaStreamWaitEvent(hs->s[0], ev.start, 0));
+  if (!rc) {
+    const int64_t pg = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+    k_pack_knots<T><<<(unsigned)pg, 256, 0, hs->s[0]>>>(x, y, y2, n, kn);
+    rc = launch_rc();
+  }
+  if (!rc) rc = cuda_rc(cudaEventRecord(ev.ready, hs->s[0]));
   if (!rc)
     rc = launch_pdl(k_bucket_count<T>, dim3((unsigned)ntiles), dim3(kBkScThreads), 0, st, x, (int)n, K, nb, q, m, cnt);
   if (!rc) {
-    const int64_t pg = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
-    k_pack_knots<T><<<(unsigned)pg, 256, 0, st>>>(x, y, y2, n, kn);
     k_scan_blocks<<<(unsigned)nblk, 1024, 0, st>>>(cnt, L, bsum);
     k_scan_top<<<1, 1024, 0, st>>>(bsum, (int)nblk);
     k_bucket_scatter<T><<<(unsigned)ntiles, kBkScThreads, bucket_scatter_smem<T>(), st>>>(x, (int)n, K, nb, q, m, cnt,
                                                                                            bsum, qs, dest, perm);
+    cudaStreamWaitEvent(st, ev.ready, 0);  // the packed knots
     k_bucket_eval<T><<<(unsigned)neval, kBkThreads, 0, st>>>(tl_status, kn, (int)n, K, nb, m, cnt, bsum, qs, dest, os,
                                                              is);
     k_bucket_gather<T><<<(unsigned)ntiles, kBkGaThreads, bucket_gather_smem<T>(), st>>>(os, is, perm, m, out, idx);
@@ -746,51 +804,6 @@ int launch_fused(const T *x, const T *y, int n, int64_t batch, int bc, const T *
   return launch_fused_k<T, MODE, 0, SOLVE_BABE, false>(x, y, n, batch, bc, yp1, ypn, y2, q, m, out, idx, cpb,
                                                        nchunks, qchunk, nitems, st);
 }
-
-// Internal streams and per-call events (the host path; the overlapped split path)
-constexpr int kHostStreams = 3;
-constexpr size_t kHostChunkBytes = 32u << 20;  // target copy traffic per chunk
-
-struct HostStreams {
-  cudaStream_t s[kHostStreams];
-};
-inline int host_streams(HostStreams **out) {
-  static std::mutex mu;
-  static HostStreams *per_dev[128] = {};
-  int dev = 0;
-  if (int rc = cuda_rc(cudaGetDevice(&dev))) return rc;
-  if (dev < 0 || dev >= 128) return SPLINE_ECUDA;
-  std::lock_guard<std::mutex> lk(mu);
-  if (!per_dev[dev]) {
-    auto *h = new HostStreams;
-    for (int i = 0; i < kHostStreams; ++i)
-      if (int rc = cuda_rc(cudaStreamCreateWithFlags(&h->s[i], cudaStreamNonBlocking))) return rc;
-    per_dev[dev] = h;
-  }
-  *out = per_dev[dev];
-  return SPLINE_OK;
-}
-// The events of ONE host call (never shared between calls, so concurrent calls from several
-// threads cannot re-record each other's start/done points).  Destroyed at the end of the call:
-// CUDA releases an event still pending on the device once it completes.
-struct CallEvents {
-  cudaEvent_t start = nullptr, ready = nullptr, done[kHostStreams] = {};
-  int init() {
-    int rc = cuda_rc(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-    if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    for (int k = 0; !rc && k < kHostStreams; ++k) rc = cuda_rc(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
-    return rc;
-  }
-  ~CallEvents() {
-    if (start) cudaEventDestroy(start);
-    if (ready) cudaEventDestroy(ready);
-    for (int k = 0; k < kHostStreams; ++k)
-      if (done[k]) cudaEventDestroy(done[k]);
-  }
-};
-// Device bytes one chunk slot may take (3 slots in flight): caps the curves per chunk for very
-// long curves / many queries, whatever the SM floor asks for.
-constexpr size_t kMaxSlotBytes = size_t(4) << 30;
 
 // ---- fused build + eval of mid-length curves with sorted queries (k_tile_eval) ---------------
 template <typename T, int R, int V, bool WIN>
