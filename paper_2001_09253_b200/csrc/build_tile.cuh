@@ -118,6 +118,80 @@ template <typename T, int R> __host__ __device__ constexpr size_t tile_smem_byte
   return sizeof(T) * (2 * (size_t)kTileThreads * (R + 1) + 6 * kTileThreads + 6 * kTileThreads);
 }
 
+// One leaf (thread l): rows [p, p + rows) of the tile (global P + p ...), the Thomas sweep with three
+// right-hand sides (d, a_p e_1, c_q e_q) storing c' in X and g' in Y (their pads) and
+// v' in registers, then the backward Horner pass -> the leaf's block record.
+// RAG = false: a full leaf (rows == R) -- the curve's first / last row can only be its row 0 /
+// R-1, so those two rows take the end-row coefficients by selects and no row carries a bounds
+// test; RAG = true: the ragged last leaf of a tile (the general code).  The same operations on
+// every row either way, so the same bits.
+template <typename T, int R, bool RAG>
+__device__ __forceinline__ Rec<T> leaf_sweep(T *X, T *Y, T (&v)[R], int p, int rows, int64_t P, int64_t n, int bc,
+                                             T s0, T s1, T xm1, T ym1, T xq1, T yq1, bool &ok) {
+  auto pad = [](int i) { return i + i / R; };
+  T xi = X[pad(p)], yi = Y[pad(p)];
+  T hprev = T(0), ddprev = T(0);
+  if (P + p > 0) {
+    hprev = xi - xm1;
+    ddprev = (yi - ym1) * nr_rcp(hprev);
+  }
+  T cprev = T(0), gprev = T(0), vprev = T(0);
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (!RAG || k < rows) {
+      const int i = p + k;
+      const int64_t gi = P + i;
+      T xn = T(0), yn = T(0), h = T(0), dd = T(0);
+      ok = ok && finite(xi) && finite(yi);
+      const bool has_next = (RAG || k == R - 1) ? (gi < n - 1) : true;  // rows before R-1 always have one
+      if (has_next) {
+        if (RAG ? (k < rows - 1) : (k < R - 1)) { xn = X[pad(i + 1)]; yn = Y[pad(i + 1)]; }
+        else { xn = xq1; yn = yq1; }
+        ok = ok && (xn > xi);
+        h = xn - xi;
+        dd = (yn - yi) * nr_rcp(h);
+      }
+      T a, b, cc, d;
+      const bool first = (RAG || k == 0) && gi == 0;           // only row 0 of a full leaf can be
+      const bool last = (RAG || k == R - 1) && gi == n - 1;    // only row R-1 of a full leaf can be
+      if (first) {
+        a = T(0);
+        if (bc & 1) { b = T(2) * h; cc = h; d = T(6) * (dd - s0); }
+        else { b = T(1); cc = T(0); d = T(0); }                       // y2_0 = 0
+      } else if (last) {
+        cc = T(0);
+        if (bc & 2) { a = hprev; b = T(2) * hprev; d = T(6) * (s1 - ddprev); }
+        else { a = T(0); b = T(1); d = T(0); }                                   // y2_{n-1} = 0
+      } else {  // Eq. init_val
+        a = hprev; b = T(2) * (hprev + h); cc = h; d = T(6) * (dd - ddprev);
+      }
+      const T inv = nr_rcp(k == 0 ? b : b - a * cprev);
+      const T cp = cc * inv;
+      const T gp = (k == 0 ? d : d - a * gprev) * inv;
+      const T vp = (k == 0 ? a : -(a * vprev)) * inv;
+      X[pad(i)] = cp;
+      Y[pad(i)] = gp;
+      v[k] = vp;
+      cprev = cp; gprev = gp; vprev = vp;
+      xi = xn; yi = yn; hprev = h; ddprev = dd;
+    }
+  }
+  Rec<T> r;
+  r.Gq = gprev; r.Vq = vprev; r.Wq = cprev;
+  T G = T(0), V = T(0), W = T(-1);  // y_{q+1} = R
+#pragma unroll
+  for (int k = R - 1; k >= 0; --k) {
+    if (!RAG || k < rows) {
+      const T ck = X[pad(p + k)], gk = Y[pad(p + k)];
+      G = gk - ck * G;
+      V = v[k] - ck * V;
+      W = -(ck * W);
+    }
+  }
+  r.Gp = G; r.Vp = V; r.Wp = W;
+  return r;
+}
+
 // One CTA solves rows [P, Q] of one curve: the linear block index is curve c times ntiles plus
 // tile t (a 1-D grid, so the batch is not capped at 65535), P = row_begin + t * 256R.
 //  FULL   : the tile is the whole curve (row_begin = 0, row_end = n <= 256R); writes y2.
@@ -201,63 +275,9 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
     const T s1 = (bc & 2) ? ypn[c] : T(0);
     if (bc & 1) ok = ok && finite(s0);
     if (bc & 2) ok = ok && finite(s1);
-    T xi = X[pad(p)], yi = Y[pad(p)];
-    T hprev = T(0), ddprev = T(0);
-    if (P + p > 0) {
-      hprev = xi - xm1;
-      ddprev = (yi - ym1) * nr_rcp(hprev);
-    }
-    T cprev = T(0), gprev = T(0), vprev = T(0);
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      if (k < rows) {
-        const int i = p + k;
-        const int64_t gi = P + i;
-        T xn = T(0), yn = T(0), h = T(0), dd = T(0);
-        ok = ok && finite(xi) && finite(yi);
-        if (gi < n - 1) {
-          if (k < rows - 1) { xn = X[pad(i + 1)]; yn = Y[pad(i + 1)]; }
-          else { xn = xq1; yn = yq1; }
-          ok = ok && (xn > xi);
-          h = xn - xi;
-          dd = (yn - yi) * nr_rcp(h);
-        }
-        T a, b, cc, d;
-        if (gi == 0) {
-          a = T(0);
-          if (bc & 1) { b = T(2) * h; cc = h; d = T(6) * (dd - s0); }
-          else { b = T(1); cc = T(0); d = T(0); }                       // y2_0 = 0
-        } else if (gi == n - 1) {
-          cc = T(0);
-          if (bc & 2) { a = hprev; b = T(2) * hprev; d = T(6) * (s1 - ddprev); }
-          else { a = T(0); b = T(1); d = T(0); }                                   // y2_{n-1} = 0
-        } else {  // Eq. init_val
-          a = hprev; b = T(2) * (hprev + h); cc = h; d = T(6) * (dd - ddprev);
-        }
-        const T inv = nr_rcp(k == 0 ? b : b - a * cprev);
-        const T cp = cc * inv;
-        const T gp = (k == 0 ? d : d - a * gprev) * inv;
-        const T vp = (k == 0 ? a : -(a * vprev)) * inv;
-        X[pad(i)] = cp;
-        Y[pad(i)] = gp;
-        v[k] = vp;
-        cprev = cp; gprev = gp; vprev = vp;
-        xi = xn; yi = yn; hprev = h; ddprev = dd;
-      }
-    }
-    Rec<T> r;
-    r.Gq = gprev; r.Vq = vprev; r.Wq = cprev;
-    T G = T(0), V = T(0), W = T(-1);  // y_{q+1} = R
-#pragma unroll
-    for (int k = R - 1; k >= 0; --k) {
-      if (k < rows) {
-        const T ck = X[pad(p + k)], gk = Y[pad(p + k)];
-        G = gk - ck * G;
-        V = v[k] - ck * V;
-        W = -(ck * W);
-      }
-    }
-    r.Gp = G; r.Vp = V; r.Wp = W;
+    // full leaves (all but a ragged last one) run without per-row bounds tests (leaf_sweep)
+    const Rec<T> r = rows == R ? leaf_sweep<T, R, false>(X, Y, v, p, rows, P, n, bc, s0, s1, xm1, ym1, xq1, yq1, ok)
+                               : leaf_sweep<T, R, true>(X, Y, v, p, rows, P, n, bc, s0, s1, xm1, ym1, xq1, yq1, ok);
     rec[l] = r;
   }
   const bool bad = __syncthreads_or(!ok);

@@ -1,4 +1,6 @@
-T=gpurun_out/r02ah; mkdir -p $T
-python tools/pcie_probe.py > $T/pcie.json 2>&1; cat $T/pcie.json
-for r in 1 2; do timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 5 > $T/b$r.log 2>&1; python -c "
-import json; d=json.loads(open('$T/b$r.log').read().strip().splitlines()[-1]); e=d['e2e']; print('e2e ms', e['ms_per_step'], 'Gq/s', e['value']/1e9, 'GB/s', (e['h2d_bytes_per_step']+e['d2h_bytes_per_step'])/e['ms_per_step']/1e6)"; done
+T=gpurun_out/r02aj; mkdir -p $T
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fused.py -q -x --timeout 600 > $T/pytest.log 2>&1; echo "pytest rc=$?"; tail -2 $T/pytest.log
+L=paper_2001_09253_b200/csrc/libfastspline.so
+cp $L /tmp/live.so
+for r in 1 2; do for v in O A; do cp paper_2001_09253_b200/csrc/libfastspline_$v.so $L; for c in 4 5; do timeout 300 python tools/time_paths.py $c 10 2>&1 | grep -E " build " | sed "s/^/$v r$r /"; done; done; done
+cp /tmp/live.so $L
