@@ -114,6 +114,56 @@ template <typename T> __device__ void tree_down(const T *mi, T *ext, int nleaf, 
 enum { TILE_FULL = 0, TILE_REDUCE = 1, TILE_FINISH = 2 };
 constexpr int kTileThreads = 256;
 
+// tree_up / tree_down for a full tile (kTileThreads leaves): the same merges in the same order,
+// with the level loop unrolled at compile time.
+__host__ __device__ constexpr int tile_levels() { return kTileThreads == 256 ? 8 : 0; }
+template <typename T> __device__ __forceinline__ void tree_up_full(Rec<T> *rec, T *mi) {
+  constexpr int NL = kTileThreads, LG = tile_levels();
+  const int t = threadIdx.x;
+  int off = 0;
+#pragma unroll
+  for (int lg = 0; lg < LG; ++lg) {
+    const int s = 1 << lg;
+    const int nn = NL >> (lg + 1);
+    if ((t & (2 * s - 1)) == 0) {
+      const Rec<T> A = rec[t], B = rec[t + s];
+      T *o = mi + 6 * (off + (t >> (lg + 1)));
+      o[0] = A.Gq; o[1] = A.Vq; o[2] = A.Wq; o[3] = B.Gp; o[4] = B.Vp; o[5] = B.Wp;
+      rec[t] = merge_rec(A, B);
+    }
+    off += nn;
+    if (4 * s <= 32) __syncwarp();
+    else __syncthreads();
+  }
+  __syncthreads();
+}
+template <typename T> __device__ __forceinline__ void tree_down_full(const T *mi, T *ext, T L, T R) {
+  constexpr int NL = kTileThreads, LG = tile_levels();
+  const int t = threadIdx.x;
+  if (t == 0) { ext[0] = L; ext[1] = R; }
+  __syncthreads();
+  int off = NL - 1;  // total merges
+#pragma unroll
+  for (int lg = LG - 1; lg >= 0; --lg) {
+    const int s = 1 << lg;
+    const int nn = NL >> (lg + 1);
+    off -= nn;
+    if ((t & (2 * s - 1)) == 0) {
+      const int j = t + s;
+      const T *o = mi + 6 * (off + (t >> (lg + 1)));
+      const T Li = ext[2 * t], Ri = ext[2 * t + 1];
+      T ym, ym1;
+      split_seam(o[0], o[1], o[2], o[3], o[4], o[5], Li, Ri, ym, ym1);
+      ext[2 * t + 1] = ym1;
+      ext[2 * j] = ym;
+      ext[2 * j + 1] = Ri;
+    }
+    if (2 * s <= 32) __syncwarp();
+    else __syncthreads();
+  }
+  __syncthreads();
+}
+
 template <typename T, int R> __host__ __device__ constexpr size_t tile_smem_bytes() {
   return sizeof(T) * (2 * (size_t)kTileThreads * (R + 1) + 6 * kTileThreads + 6 * kTileThreads);
 }
@@ -281,7 +331,8 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
     rec[l] = r;
   }
   const bool bad = __syncthreads_or(!ok);
-  tree_up(rec, mi, nleaf);
+  if (nleaf == NT) tree_up_full(rec, mi);
+  else tree_up(rec, mi, nleaf);
 
   if (MODE == TILE_REDUCE) {
     if (threadIdx.x == 0) {
@@ -313,17 +364,28 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
     Lr = tile_ext[(c * ntiles + tile) * 2];
     Rr = tile_ext[(c * ntiles + tile) * 2 + 1];
   }
-  tree_down(mi, ext, nleaf, Lr, Rr);
+  if (nleaf == NT) tree_down_full(mi, ext, Lr, Rr);
+  else tree_down(mi, ext, nleaf, Lr, Rr);
   if (l < nleaf) {
     const T L = ext[2 * l];
     T ynext = ext[2 * l + 1];
+    if (rows == R) {
 #pragma unroll
-    for (int k = R - 1; k >= 0; --k) {
-      if (k < rows) {
+      for (int k = R - 1; k >= 0; --k) {
         const int i = p + k;
         const T yv = Y[pad(i)] - v[k] * L - X[pad(i)] * ynext;  // y_i = g'_i - v'_i L - c'_i y_{i+1}
         X[pad(i)] = yv;
         ynext = yv;
+      }
+    } else {
+#pragma unroll
+      for (int k = R - 1; k >= 0; --k) {
+        if (k < rows) {
+          const int i = p + k;
+          const T yv = Y[pad(i)] - v[k] * L - X[pad(i)] * ynext;
+          X[pad(i)] = yv;
+          ynext = yv;
+        }
       }
     }
   }

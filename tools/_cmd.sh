@@ -1,4 +1,4 @@
-T=gpurun_out/r02aj; mkdir -p $T
+T=gpurun_out/r02ak; mkdir -p $T
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fused.py -q -x --timeout 600 > $T/pytest.log 2>&1; echo "pytest rc=$?"; tail -2 $T/pytest.log
 L=paper_2001_09253_b200/csrc/libfastspline.so
 cp $L /tmp/live.so
