@@ -113,6 +113,10 @@ template <typename T> __device__ void tree_down(const T *mi, T *ext, int nleaf, 
 
 enum { TILE_FULL = 0, TILE_REDUCE = 1, TILE_FINISH = 2 };
 constexpr int kTileThreads = 256;
+#ifndef FS_TILE_PREFETCH
+#define FS_TILE_PREFETCH 0  // A/B: cfg4 build 151 vs 148 us, cfg5 932 vs 945 us
+#endif
+constexpr int kTilePrefetchAhead = FS_TILE_PREFETCH;  // waves ahead whose x, y a tile prefetches to L2
 
 // tree_up / tree_down for a full tile (kTileThreads leaves): the same merges in the same order,
 // with the level loop unrolled at compile time.
@@ -408,8 +412,24 @@ __global__ void __launch_bounds__(kTileThreads) k_tile(unsigned *__restrict__ st
                                                       int64_t row_end, int bc, const T *__restrict__ yp1,
                                                       const T *__restrict__ ypn, T *__restrict__ y2,
                                                       T *__restrict__ tile_rec, const T *__restrict__ tile_ext,
-                                                      int *__restrict__ badflag, int ntiles) {
+                                                      int *__restrict__ badflag, int ntiles, int pf_blocks) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  if (pf_blocks > 0 && threadIdx.x == 0) {
+    // the tile this SM slot will most likely run a wave from now: its x, y into L2 now, so that
+    // tile's staging loads (the kernel's largest stall, ncu r02) are L2 hits
+    const int64_t nb = blockIdx.x + (int64_t)pf_blocks;  // pf_blocks: the CTAs resident at once
+    if (nb < (int64_t)gridDim.x) {
+      const int64_t c2 = nb / ntiles, t2 = nb - c2 * ntiles;
+      const int64_t P2 = row_begin + t2 * (int64_t)kTileThreads * R;
+      const int64_t r2 = min64((int64_t)kTileThreads * R, row_end - P2);
+      constexpr int64_t A = 16 / sizeof(T);
+      const int64_t e0 = (c2 * n + P2) & ~(A - 1), e1 = (c2 * n + P2 + r2) & ~(A - 1);
+      if (e1 > e0) {
+        prefetch_l2_bulk(x + e0, (uint32_t)((e1 - e0) * sizeof(T)));
+        prefetch_l2_bulk(y + e0, (uint32_t)((e1 - e0) * sizeof(T)));
+      }
+    }
+  }
   tile_solve<T, R, MODE>(status, x, y, n, row_begin, row_end, bc, yp1, ypn, y2, tile_rec, tile_ext, badflag, ntiles,
                          (int64_t)blockIdx.x, smem_raw);
 }

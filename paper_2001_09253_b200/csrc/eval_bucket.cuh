@@ -250,9 +250,6 @@ __global__ void __launch_bounds__(kBkScThreads, 2) k_bucket_scatter(const T *__r
   }
 }
 
-__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 // Knots interleaved for the evaluation: {x_j, y_j, y2_j, 0} (32 B fp64: one sector per knot), so an
 // interval is two 32-byte loads instead of six scattered 8-byte ones.

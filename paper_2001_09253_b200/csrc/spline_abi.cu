@@ -217,13 +217,22 @@ constexpr size_t kMaxSlotBytes = size_t(4) << 30;
 
 // ------------------------------------------------------------------------ build
 
+// k_tile's L2 prefetch distance: the CTAs resident at once (one wave ahead), 0 = off
+template <typename K> int tile_prefetch_blocks(K kern, size_t sm) {
+  if (kTilePrefetchAhead <= 0) return 0;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTileThreads, sm) != cudaSuccess || occ < 1) occ = 1;
+  return kTilePrefetchAhead * occ * num_sms();
+}
+
 template <typename T, int R>
 int launch_tile_full(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
                      cudaStream_t st) {
   auto kern = k_tile<T, R, TILE_FULL>;
   const size_t sm = tile_smem_bytes<T, R>();
   if (int rc = set_smem(kern, sm)) return rc;
-  kern<<<(unsigned)batch, kTileThreads, sm, st>>>(tl_status, x, y, n, 0, n, bc, yp1, ypn, y2, nullptr, nullptr, nullptr, 1);
+  kern<<<(unsigned)batch, kTileThreads, sm, st>>>(tl_status, x, y, n, 0, n, bc, yp1, ypn, y2, nullptr, nullptr, nullptr, 1,
+                                                  tile_prefetch_blocks(kern, sm));
   return launch_rc();
 }
 
@@ -298,7 +307,8 @@ int launch_tile_part(const T *x, const T *y, int64_t n, int64_t rb, int64_t re, 
   if (int rc = set_smem(kern, sm)) return rc;
   if (ntiles * batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
   kern<<<(unsigned)(ntiles * batch), kTileThreads, sm, st>>>(tl_status, x, y, n, rb, re, bc, yp1, ypn, y2, (T *)w.tile_rec,
-                                                             (const T *)w.tile_ext, (int *)w.badflag, (int)ntiles);
+                                                             (const T *)w.tile_ext, (int *)w.badflag, (int)ntiles,
+                                                             tile_prefetch_blocks(kern, sm));
   return launch_rc();
 }
 
