@@ -889,6 +889,10 @@ constexpr bool kSortedFast = FS_SORTED_FAST != 0;  // the warp-uniform fast path
 #define FS_SORTED_L1PF 1
 #endif
 constexpr bool kSortedL1Prefetch = FS_SORTED_L1PF != 0;  // L1 prefetch of the next window's knots
+#ifndef FS_SORTED_OUTLINE
+#define FS_SORTED_OUTLINE 0  // A/B: 1224 vs 1100 us on cfg4 (the call and its stack cost more than the registers saved)
+#endif
+constexpr bool kSortedOutlineGeneral = FS_SORTED_OUTLINE != 0;  // the window miss path out of line
 constexpr int kSortWinDensity = 8;  // queries per interval from which the window pays
 // One window record: the interval's left knot and its cubic (Cub + e2), 16-byte aligned so that
 // a lookup is 2 (fp32) or 3 (fp64) vector loads.
@@ -925,6 +929,27 @@ template <typename T, int R> struct ZShared {
 
 // One warp's run of queries [k0, k1) of one curve (X, Y in global memory, Z through ZA).
 // Shared by k_eval_sorted and the fused long-curve kernel, so both give the same bits.
+// The general path of a sorted run as an out-of-line call (rare: queries outside the window).
+template <typename T> struct GQ { T v; int j; };
+template <typename T, int FORM, typename ZA>
+__device__ __noinline__ GQ<T> general_query_ni(const T *__restrict__ X, const T *__restrict__ Y, ZA Z, int n, T qc,
+                                                int j) {
+  if (__ldg(X + j) > qc) {
+    j = bisect(X, n, qc);
+  } else {
+    int steps = 0;
+    while (j < n - 2 && __ldg(X + j + 1) <= qc) {
+      ++j;
+      if (++steps == 8) {
+        j = gallop_up(X, n, j, qc);
+        break;
+      }
+    }
+  }
+  const T xa = __ldg(X + j), xb = __ldg(X + j + 1);
+  return GQ<T>{interp_form<T, FORM>(qc, xa, xb, __ldg(Y + j), __ldg(Y + j + 1), Z(j), Z(j + 1)), j};
+}
+
 template <typename T, int V, int FORM, bool WIN, int PF, typename ZA>
 __device__ __forceinline__ bool sorted_run(const T *__restrict__ X, const T *__restrict__ Y, const ZA &Z, int n,
                                            const T *__restrict__ qb, T *__restrict__ ob, int32_t *__restrict__ ib,
@@ -1073,6 +1098,15 @@ __device__ __forceinline__ bool sorted_run(const T *__restrict__ X, const T *__r
             continue;
           }
         }  // outside the window: the general path, from this lane's previous interval
+        if constexpr (WIN && kSortedOutlineGeneral) {  // out of line: the hot window path keeps its registers
+          const GQ<T> g = general_query_ni<T, FORM_RECORD, ZA>(X, Y, Z, n, qc, j);
+          j = g.j;
+          val[i] = in ? g.v : qnan<T>();
+          jj[i] = in ? j : -1;
+          oor |= !in;
+          if (in) jl = j;
+          continue;
+        }
         if (__ldg(X + j) > qc) {
           j = bisect(X, n, qc);  // below the carry: unsorted input despite the hint
         } else {
