@@ -450,11 +450,12 @@ __global__ void __launch_bounds__(256) k1_thomas_regs(unsigned *__restrict__ sta
 // y2 is bitwise the shared-memory K1's (and the fused kernel's).
 constexpr int kK1hThreads = 128;
 // One lane pair's curve cv (lane parity: top / bottom) -- the body of K1h, also called by the
-// one-CTA build+eval kernel for tiny problems.  Every lane of the warp must call it.
+// fused build+eval kernels.  Every lane of the warp must call it.  y2 (nullable) receives the
+// curve's row in HBM; zs (nullable) is a 16-byte-aligned row in shared memory that receives it too.
 template <typename T, int N>
 __device__ __forceinline__ void k1h_solve(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int64_t batch, int bc,
                                           const T *__restrict__ yp1, const T *__restrict__ ypn, T *__restrict__ y2,
-                                          int64_t cv, bool top) {
+                                          int64_t cv, bool top, T *zs = nullptr) {
   constexpr int K = N / 2;
   constexpr int VW = 16 / sizeof(T);
   static_assert(K % VW == 0 && K >= 2 * VW, "each half is whole 16-byte vectors");
@@ -525,14 +526,15 @@ __device__ __forceinline__ void k1h_solve(unsigned *__restrict__ status, const T
   }
   raise_status_warp(status, act && !ok && top, kBadKnots);
   if (act) {
-    T *zh = y2 + c * N + hoff;
 #pragma unroll
     for (int g = 0; g < K; g += VW) {
       VT a;
       T *pa = reinterpret_cast<T *>(&a);
 #pragma unroll
       for (int e = 0; e < VW; ++e) pa[e] = top ? dpr[g + e] : dpr[g + VW - 1 - e];
-      *reinterpret_cast<VT *>(zh + (top ? g : K - g - VW)) = a;
+      const int o = hoff + (top ? g : K - g - VW);
+      if (y2) *reinterpret_cast<VT *>(y2 + c * N + o) = a;
+      if (zs) *reinterpret_cast<VT *>(zs + o) = a;
     }
   }
 }

@@ -563,27 +563,77 @@ template <typename T> struct CwTable {
   T ey[kCwMaxN];  // Eytzinger keys, slot 0 unused
 };
 
+// The Eytzinger slot of knot j (1 <= j < 2^L2): the node of in-order rank j-1 (the inverse of
+// eytz_rank), so each lane's keys go to the table straight from registers.
+template <int L2> __device__ __forceinline__ int cw_slot(int j) {
+  const int sft = __ffs(j) - 1, d = L2 - 1 - sft;
+  return (1 << d) + (((j >> sft) - 1) >> 1);
+}
+
+// One curve's table from its knots in registers (lane l holds knots l, l+32: kx, ky, kz): the
+// records of intervals l, l+32 (x_{j+1}, y_{j+1}, y2_{j+1} from the neighbour lane) and the
+// Eytzinger keys x_1 .. x_{n-2}, +inf padded (slots s0, s1 of cw_slot).  The caller syncs the warp.
+template <typename T, int L2>
+__device__ __forceinline__ void cw_build_table(CwTable<T> &tb, int s0, int s1, const T (&kx)[2], const T (&ky)[2],
+                                               const T (&kz)[2], int n, int lane) {
+  constexpr int P = 1 << L2;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j = lane + 32 * h;
+    const T xn1 = __shfl_down_sync(0xffffffffu, kx[h], 1), yn1 = __shfl_down_sync(0xffffffffu, ky[h], 1),
+            zn1 = __shfl_down_sync(0xffffffffu, kz[h], 1);
+    // lane 31's neighbour is lane 0 of the next half
+    const T xh = __shfl_sync(0xffffffffu, kx[1], 0), yh = __shfl_sync(0xffffffffu, ky[1], 0),
+            zh = __shfl_sync(0xffffffffu, kz[1], 0);
+    const T xb = (lane == 31) ? xh : xn1, yb = (lane == 31) ? yh : yn1, zb = (lane == 31) ? zh : zn1;
+    if (j < n) tb.xk[j] = kx[h];
+    if (j < n - 1) tb.c[j] = make_cub<T>(kx[h], xb, ky[h], yb, kz[h], zb, tb.e2[j]);
+  }
+  if (lane > 0 && lane < P) tb.ey[s0] = (lane <= n - 2) ? kx[0] : (T)INFINITY;
+  if (lane + 32 < P) tb.ey[s1] = (lane + 32 <= n - 2) ? kx[1] : (T)INFINITY;
+}
+
+// The curve's queries (nv 16-byte vectors at qc; the lane's first two already in qpf): lane l
+// takes vectors l, l+32, ...  Returns "some query was out of range".
+template <typename T, int L2>
+__device__ __forceinline__ bool cw_eval_queries(const CwTable<T> &tb, uint32_t ebase, int n, const T *__restrict__ qc,
+                                                int nv, T *__restrict__ oc, int32_t *__restrict__ ic,
+                                                const typename Vec16<T>::V (&qpf)[2], int lane) {
+  constexpr int VW = 16 / sizeof(T);
+  using VT = typename Vec16<T>::V;
+  const CurveHdr<T> hd{tb.xk[0], tb.xk[n - 1], T(0), T(0)};
+  bool oor = false;
+  for (int v = lane, i = 0; v < nv; v += 32, ++i) {
+    const VT a = (i == 0) ? qpf[0] : (i == 1) ? qpf[1] : __ldcs(reinterpret_cast<const VT *>(qc) + v);
+    const T *qa = reinterpret_cast<const T *>(&a);
+    T val[VW];
+    int jj[VW];
+#pragma unroll
+    for (int e = 0; e < VW; ++e) {
+      eval_packed<T, MODE_BISECT, L2>(tb.c, tb.e2, tb.xk, ebase, nullptr, hd, n, 0, qa[e], val[e], jj[e]);
+      oor |= jj[e] < 0;
+    }
+    VecIO<T, VW>::store(oc + (size_t)v * VW, val);
+    if (ic) VecIO<T, VW>::store_idx(ic + (size_t)v * VW, jj);
+  }
+  return oor;
+}
+
 template <typename T, int L2>
 __global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y,
                                                                      const T *__restrict__ y2, int n, int64_t batch,
                                                                      const T *__restrict__ q, int m,
                                                                      T *__restrict__ out, int32_t *__restrict__ idx) {
   pdl_wait();  // x, y, y2 may come from the preceding kernel (programmatic launch)
-  constexpr int VW = 16 / sizeof(T);
   constexpr int P = 1 << L2;  // <= 64
   using VT = typename Vec16<T>::V;
+  constexpr int VW = 16 / sizeof(T);
   __shared__ CwTable<T> tabs[kCwWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   CwTable<T> &tb = tabs[w];
   const uint32_t ebase = smem_u32(tb.ey);
-  // the Eytzinger slot of this lane's knots j = lane, lane+32 (the inverse of eytz_rank: knot
-  // j = in-order rank j of the complete tree), so the keys go to the table from registers
-  auto slot_of = [&](int j) {
-    const int sft = __ffs(j) - 1, d = L2 - 1 - sft;
-    return (1 << d) + (((j >> sft) - 1) >> 1);
-  };
-  const int s0 = (lane > 0 && lane < P) ? slot_of(lane) : 0;
-  const int s1 = (lane + 32 < P) ? slot_of(lane + 32) : 0;
+  const int s0 = (lane > 0 && lane < P) ? cw_slot<L2>(lane) : 0;
+  const int s1 = (lane + 32 < P) ? cw_slot<L2>(lane + 32) : 0;
   const int nv = m / VW;  // query vectors per curve
   const int64_t G = (int64_t)gridDim.x * kCwWarps;
   int64_t c = (int64_t)blockIdx.x * kCwWarps + w;
@@ -609,40 +659,10 @@ __global__ void __launch_bounds__(kCwWarps * 32, 4) k_eval_curvewarp(unsigned *_
 #pragma unroll
     for (int i = 0; i < 2; ++i)
       if (lane + 32 * i < nv) qpf[i] = __ldcs(reinterpret_cast<const VT *>(qc) + lane + 32 * i);
-    // records of intervals lane, lane+32 (x_{j+1}, y_{j+1}, y2_{j+1} from the neighbour lane)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int j = lane + 32 * h;
-      const T xn1 = __shfl_down_sync(0xffffffffu, kx[h], 1), yn1 = __shfl_down_sync(0xffffffffu, ky[h], 1),
-              zn1 = __shfl_down_sync(0xffffffffu, kz[h], 1);
-      // lane 31's neighbour is lane 0 of the next half
-      const T xh = __shfl_sync(0xffffffffu, kx[1], 0), yh = __shfl_sync(0xffffffffu, ky[1], 0),
-              zh = __shfl_sync(0xffffffffu, kz[1], 0);
-      const T xb = (lane == 31) ? xh : xn1, yb = (lane == 31) ? yh : yn1, zb = (lane == 31) ? zh : zn1;
-      if (j < n) tb.xk[j] = kx[h];
-      if (j < n - 1) tb.c[j] = make_cub<T>(kx[h], xb, ky[h], yb, kz[h], zb, tb.e2[j]);
-    }
-    // Eytzinger keys x_1 .. x_{n-2}, +inf padded, straight from registers
-    if (lane > 0 && lane < P) tb.ey[s0] = (lane <= n - 2) ? kx[0] : (T)INFINITY;
-    if (lane + 32 < P) tb.ey[s1] = (lane + 32 <= n - 2) ? kx[1] : (T)INFINITY;
+    cw_build_table<T, L2>(tb, s0, s1, kx, ky, kz, n, lane);
     load_knots(c + G);  // the next curve's knots, in flight during this curve's queries
     __syncwarp();
-    const CurveHdr<T> hd{tb.xk[0], tb.xk[n - 1], T(0), T(0)};
-    T *oc = out + c * m;
-    int32_t *ic = idx ? idx + c * m : nullptr;
-    for (int v = lane, i = 0; v < nv; v += 32, ++i) {
-      const VT a = (i == 0) ? qpf[0] : (i == 1) ? qpf[1] : __ldcs(reinterpret_cast<const VT *>(qc) + v);
-      const T *qa = reinterpret_cast<const T *>(&a);
-      T val[VW];
-      int jj[VW];
-#pragma unroll
-      for (int e = 0; e < VW; ++e) {
-        eval_packed<T, MODE_BISECT, L2>(tb.c, tb.e2, tb.xk, ebase, nullptr, hd, n, 0, qa[e], val[e], jj[e]);
-        oor |= jj[e] < 0;
-      }
-      VecIO<T, VW>::store(oc + (size_t)v * VW, val);
-      if (ic) VecIO<T, VW>::store_idx(ic + (size_t)v * VW, jj);
-    }
+    oor |= cw_eval_queries<T, L2>(tb, ebase, n, qc, nv, out + c * m, idx ? idx + c * m : nullptr, qpf, lane);
     __syncwarp();  // the table is rebuilt for the next curve
   }
   raise_status_warp(status, oor, kOutOfRange);
@@ -694,6 +714,87 @@ __global__ void __launch_bounds__(256) k_build_eval_tiny(unsigned *__restrict__ 
     }
     VecIO<T, VW>::store(out + c * m + (size_t)v * VW, val);
     if (idx) VecIO<T, VW>::store_idx(idx + c * m + (size_t)v * VW, jj);
+  }
+  raise_status_warp(status, oor, kOutOfRange);
+}
+
+// ---- many K1h-sized curves, unsorted queries: build + evaluate per warp (BASELINE cfg2) ------
+// spline_build_eval's fused path for n in {16, 32, 64}.  Each warp owns
+// a contiguous range of curves and walks it in groups of 16: the group is solved by K1h's
+// two-ended register sweep (k1h_solve, lane pair 2t/2t+1 on curve t: bitwise K1h's y2), which
+// leaves the y2 rows in the warp's shared-memory stage (and in HBM when the caller asked for y2);
+// then each curve of the group goes through k_eval_curvewarp's body (cw_build_table,
+// cw_eval_queries) with x, y re-read from L1/L2 (the solve just loaded them) and y2 from the
+// stage.  Against K1h + k_eval_curvewarp, HBM sees y2 written at most once and never read back,
+// and there is one launch.  The next group's x, y are prefetched to L2 during this group's queries.
+constexpr int kBwWarps = 8, kBwGroup = 16;
+template <typename T, int N> __host__ __device__ constexpr int bw_stride() { return N + 16 / (int)sizeof(T); }
+template <typename T, int N> struct BwStage {
+  CwTable<T> tb;
+  alignas(16) T z[kBwGroup * bw_stride<T, N>()];  // y2 rows of the group, padded: lane pairs hit distinct banks
+};
+#ifndef FS_BW_MINB
+#define FS_BW_MINB 2  // A/B on cfg2 (us, y2 written): 2 -> 74.2, 3 -> 79.9 (spills), 4 -> 88.1; split path 74.8
+#endif
+template <typename T, int N, int L2>
+__global__ void __launch_bounds__(kBwWarps * 32, FS_BW_MINB)
+    k_build_eval_warp(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int64_t batch,
+                      int bc, const T *__restrict__ yp1, const T *__restrict__ ypn, T *__restrict__ y2,
+                      const T *__restrict__ q, int m, T *__restrict__ out, int32_t *__restrict__ idx) {
+  constexpr int P = 1 << L2, S = bw_stride<T, N>();
+  constexpr int VW = 16 / sizeof(T);
+  using VT = typename Vec16<T>::V;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  BwStage<T, N> &st = reinterpret_cast<BwStage<T, N> *>(smem_raw)[w];
+  const uint32_t ebase = smem_u32(st.tb.ey);
+  const int s0 = (lane > 0 && lane < P) ? cw_slot<L2>(lane) : 0;
+  const int s1 = (lane + 32 < P) ? cw_slot<L2>(lane + 32) : 0;
+  const int nv = m / VW;
+  const int64_t GW = (int64_t)gridDim.x * kBwWarps, gw = (int64_t)blockIdx.x * kBwWarps + w;
+  const int64_t cb = batch * gw / GW, ce = batch * (gw + 1) / GW;  // this warp's curves
+  const int t = lane >> 1;
+  const bool top = (lane & 1) == 0;
+  bool oor = false;
+  for (int64_t g0 = cb; g0 < ce; g0 += kBwGroup) {
+    const int ng = (int)min64(kBwGroup, ce - g0);
+    if (g0 + kBwGroup < ce) {  // the next group's x, y rows to L2 (one 128-byte line per lane)
+      const int64_t nb = min64(kBwGroup, ce - g0 - kBwGroup) * N * (int64_t)sizeof(T);
+      const char *px = reinterpret_cast<const char *>(x + (g0 + kBwGroup) * N);
+      const char *py = reinterpret_cast<const char *>(y + (g0 + kBwGroup) * N);
+      for (int64_t o = (int64_t)lane * 128; o < nb; o += 32 * 128) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(px + o));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(py + o));
+      }
+    }
+    k1h_solve<T, N>(status, x, y, batch, bc, yp1, ypn, y2, t < ng ? g0 + t : batch, top, st.z + t * S);
+    __syncwarp();
+    T kx[2], ky[2], kz[2];
+    auto load_knots = [&](int k) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        if (j < N) {
+          kx[h] = __ldg(x + (g0 + k) * N + j);
+          ky[h] = __ldg(y + (g0 + k) * N + j);
+          kz[h] = st.z[k * S + j];
+        }
+      }
+    };
+    load_knots(0);
+    for (int k = 0; k < ng; ++k) {
+      const int64_t c = g0 + k;
+      const T *qc = q + c * m;
+      VT qpf[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        if (lane + 32 * i < nv) qpf[i] = __ldcs(reinterpret_cast<const VT *>(qc) + lane + 32 * i);
+      cw_build_table<T, L2>(st.tb, s0, s1, kx, ky, kz, N, lane);
+      if (k + 1 < ng) load_knots(k + 1);
+      __syncwarp();
+      oor |= cw_eval_queries<T, L2>(st.tb, ebase, N, qc, nv, out + c * m, idx ? idx + c * m : nullptr, qpf, lane);
+      __syncwarp();
+    }
   }
   raise_status_warp(status, oor, kOutOfRange);
 }

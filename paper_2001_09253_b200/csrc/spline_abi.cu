@@ -15,8 +15,9 @@
 //                                                          UNIFORM, BSEARCH)
 //   one curve >> L2, many queries k_bucket_*             queries bucketed by L2-sized chunks
 //   otherwise                     k_pack_records + k_eval_records   one record gather per query
-// spline_build_eval: k_build_eval_tiny | k_eval_small<true> | k_fused_staged | k_tile_eval (on
-// SPLINE_PATH_FUSED) | the two above back to back.
+// spline_build_eval: k_build_eval_tiny (few curves) | k_eval_small<true> | k_build_eval_warp
+// (many K1h-sized curves) | k_fused_staged | k_tile_eval (on SPLINE_PATH_FUSED) | the two above
+// back to back.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -44,6 +45,10 @@ constexpr int kK1MaxN = 128;
 // spline_build_eval's automatic choice: the fused warp-specialised kernel only for
 // launch-latency-sized problems (measured: tools/cmp_paths.py; K1h + curvewarp win from ~2^18)
 constexpr int64_t kFuseMaxWork = int64_t(1) << 17;
+#ifndef FS_BUILD_EVAL_WARP
+#define FS_BUILD_EVAL_WARP 1
+#endif
+constexpr bool kBuildEvalWarp = FS_BUILD_EVAL_WARP != 0;  // spline_build_eval: k_build_eval_warp for many K1h-sized curves
 constexpr int kNoFusedStaged = 1 << 30;  // internal: automatic path, but not k_fused_staged
 constexpr int kEvalNoBucket = SPLINE_NO_BUCKET;  // spline_eval: the record-gather path for long curves
 #ifndef FS_SPLIT_OVERLAP
@@ -869,6 +874,29 @@ int launch_tile_eval(const T *x, const T *y, int64_t n, int64_t batch, int bc, c
   return SPLINE_EINVAL;
 }
 
+template <typename T, int N, int L2>
+int launch_build_eval_warp_k(const T *x, const T *y, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
+                             const T *q, int m, T *out, int32_t *idx, cudaStream_t st) {
+  auto kern = k_build_eval_warp<T, N, L2>;
+  const size_t sm = kBwWarps * sizeof(BwStage<T, N>);
+  if (int rc = set_smem(kern, sm)) return rc;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBwWarps * 32, sm) != cudaSuccess || occ < 1) occ = 1;
+  const int64_t grid = std::min<int64_t>((batch + kBwWarps - 1) / kBwWarps, (int64_t)occ * num_sms());
+  kern<<<(unsigned)grid, kBwWarps * 32, sm, st>>>(tl_status, x, y, batch, bc, yp1, ypn, y2, q, m, out, idx);
+  return launch_rc();
+}
+template <typename T>
+int launch_build_eval_warp(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn,
+                           T *y2, const T *q, int m, T *out, int32_t *idx, cudaStream_t st) {
+  if (n == 16) return launch_build_eval_warp_k<T, 16, 4>(x, y, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  if constexpr (sizeof(T) == 4) {
+    if (n == 32) return launch_build_eval_warp_k<T, 32, 5>(x, y, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+    if (n == 64) return launch_build_eval_warp_k<T, 64, 6>(x, y, batch, bc, yp1, ypn, y2, q, m, out, idx, st);
+  }
+  return SPLINE_EINVAL;
+}
+
 template <typename T>
 int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const T *yp1, const T *ypn, T *y2,
                  const T *q, int64_t m, T *out, int32_t *idx, int flags, cudaStream_t st) {
@@ -917,6 +945,14 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
       if (!y2) cudaFreeAsync(yy, st);
       return rc;
     }
+  }
+  {  // many K1h-sized curves, unsorted (or sorted) queries: solve + evaluate per warp
+    constexpr int VW = 16 / sizeof(T);
+    const bool k1h_n = n == 16 || (sizeof(T) == 4 && (n == 32 || n == 64));
+    if (kBuildEvalWarp && !(flags & (SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT | SPLINE_X_UNIFORM)) && k1h_n &&
+        batch >= 4 * (int64_t)num_sms() && m > 0 && m <= INT32_MAX && m % VW == 0 && aligned16(x) && aligned16(y) &&
+        aligned16(q) && aligned16(out) && (!y2 || aligned16(y2)) && (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0)))
+      return launch_build_eval_warp<T>(x, y, n, batch, bc, yp1, ypn, y2, q, (int)m, out, idx, st);
   }
   // mid-length curves (K2's range) with sorted queries: solve and evaluate in one kernel -- on
   // request only: measured on cfg4 the split path is faster (1.29 vs 1.69 ms: the evaluation is

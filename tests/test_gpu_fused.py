@@ -207,3 +207,64 @@ def test_tile_eval_wrong_sorted_hint_and_bad_data(api):
     outs, idxs = api.evaluate(x, y, y2s, q, wl.flags)
     api.status()
     assert torch.equal(idx, idxs) and torch.equal(out.view(torch.int8), outs.view(torch.int8))
+
+
+# ---- k_build_eval_warp: many K1h-sized curves (cfg2), the automatic path ----------------------
+
+def check_auto(api, wl, nthreads=8):
+    """The automatic spline_build_eval path against the oracle and bitwise against the split
+    path (K1h + k_eval_curvewarp), with and without y2 / idx."""
+    tol = parity.tol_for(wl.np_dtype)
+    x, y, q, yp1, ypn = _dev(wl)
+    api.status()
+    y2, out, idx = api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags)
+    bits = api.status()
+    y2_ref = parity.oracle_build(wl, nthreads)
+    out_ref, idx_ref, nbad = oracle.evaluate(wl.x, wl.y, y2_ref, wl.q, nthreads=nthreads)
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_ref)
+    good = np.all(np.isfinite(y2_ref), axis=1)
+    e2 = parity.y2_rel_err(y2.cpu().numpy()[good], y2_ref[good], wl.x[good], wl.y[good])
+    eo = parity.out_rel_err(out.cpu().numpy()[good], out_ref[good], wl.y[good])
+    assert np.all(e2 <= tol) and np.all(eo <= tol), (e2.max(), eo.max())
+    assert bool(bits & api.STATUS_Q_OUT_OF_RANGE) == bool(nbad)
+    assert bool(bits & api.STATUS_BAD_KNOTS) == (not good.all())
+    y2s, outs, idxs = api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags | api.PATH_SPLIT)
+    api.status()
+    assert torch.equal(y2.view(torch.int8), y2s.view(torch.int8))
+    assert torch.equal(idx, idxs) and torch.equal(out.view(torch.int8), outs.view(torch.int8))
+    none, out2, none2 = api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags, want_y2=False, want_idx=False)
+    api.status()
+    assert none is None and none2 is None and torch.equal(out2.view(torch.int8), out.view(torch.int8))
+
+
+@pytest.mark.parametrize("kw", [dict(batch=4096), dict(batch=1000, m=4), dict(batch=2999, m=1000),
+                                dict(batch=700, n=32, m=64), dict(batch=650, n=16, m=12),
+                                dict(batch=20000, m=8)])
+def test_build_eval_warp_cfg2(api, kw):
+    """cfg2-shaped calls big enough for k_build_eval_warp: warp ranges that are not whole groups of
+    16 curves, fewer query vectors than lanes (m = 4), many per lane (m = 1000), n = 16/32/64."""
+    check_auto(api, workloads.generate(2, **kw))
+
+
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
+def test_build_eval_warp_f64_n16(api, bc):
+    rng = np.random.default_rng(50 + bc)
+    B, n, m = 1500, 16, 90
+    x = np.cumsum(rng.exponential(1.0, (B, n)) + 0.01, axis=1)
+    y = np.cumsum(rng.normal(size=(B, n)), axis=1)
+    q = rng.uniform(x[:, :1], x[:, -1:], (B, m))
+    q[:, :4] = x[:, [0, n - 1, 7, 1]]  # both ends and interior knots (ties)
+    spec = workloads.ConfigSpec(0, "t", B, n, m, "f64", bc, 0, 0)
+    check_auto(api, workloads.Workload(spec, x, y, q, rng.normal(size=B), rng.normal(size=B), bc, 0))
+
+
+def test_build_eval_warp_bad_data(api):
+    """Bad knots (NaN y2 and out for that curve only, BAD_KNOTS), out-of-range and NaN queries in
+    the middle of a warp's range, on the automatic path."""
+    wl = workloads.generate(2, batch=1200, m=256)
+    wl.x[17, 30] = wl.x[17, 29]
+    wl.y[600, 0] = np.inf
+    wl.q[5, 3] = wl.x[5, -1] + 1.0
+    wl.q[1100, 255] = np.nan
+    wl.q[18, 0] = wl.x[18, 0] - 1e-3
+    check_auto(api, wl)

@@ -50,6 +50,10 @@ paths = {
                    (2 * s + 4) * B * m + 3 * s * B * n + 3 * s * B * n),
     "step (auto)": (lambda: api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags, y2=y2, out=out, idx=idx),
                     (2 * s + 4) * B * m + 3 * s * B * n + 3 * s * B * n),
+    "step (no y2)": (lambda: api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags, want_y2=False, out=out, idx=idx),
+                     (2 * s + 4) * B * m + 3 * s * B * n + 3 * s * B * n),
+    "split": (lambda: api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags | api.PATH_SPLIT, y2=y2, out=out, idx=idx),
+              (2 * s + 4) * B * m + 3 * s * B * n + 3 * s * B * n),
     "fused(y2)": (lambda: api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags | api.PATH_FUSED, y2=y2, out=out, idx=idx),
                   (2 * s + 4) * B * m + 3 * s * B * n),
     "fused(no y2)": (lambda: api.build_eval(x, y, q, wl.bc, yp1, ypn, wl.flags | api.PATH_FUSED, want_y2=False, out=out, idx=idx),
