@@ -631,9 +631,12 @@ def main():
     long_curve = n > 256 * (16 if s == 8 else 32)
     # the library's choice inside spline_build_eval (spline_abi.cu build_eval_t): one fused kernel
     # when the problem is small (batch*m <= 2^17) and fusable, else the two kernels
-    fused_step = fusable and not tile_fusable and B * m <= (1 << 17)
     small_step = s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0  # k_eval_small<true>: solve + eval
     tiny_step = (n == 16 or (s == 4 and n in (32, 64))) and B <= 16 and m <= 8192 and m % (16 // s) == 0
+    # many K1h-sized curves (cfg2): k_build_eval_warp solves and evaluates per warp
+    warp_step = ((n == 16 or (s == 4 and n in (32, 64))) and B >= 4 * 148 and m > 0 and m % (16 // s) == 0
+                 and not (wl.flags & workloads.FLAG_X_UNIFORM) and not args.x_shared and not small_step)
+    fused_step = fusable and not tile_fusable and B * m <= (1 << 17) and not warp_step
     # mid-length curves with sorted queries (cfg4): k_tile_eval solves and evaluates in one kernel
     tile_step = False  # k_tile_eval runs on SPLINE_PATH_FUSED only (measured slower than split on cfg4)
     launches = 2 * K  # 1 build kernel + 1 eval kernel per step for configs 2-4
@@ -645,11 +648,15 @@ def main():
         # build: memset + K3 + K4 (3 grouped launches for one curve of > 128 tiles, else 1) + K5;
         # eval: bucketed (count, pack, scan x2, scatter, eval, gather) or records (pack, gather)
         launches = ((5 if (B == 1 and ntiles > 128) else 3) + (7 if bucketed else 2)) * K
-    if fused_step or small_step or tiny_step or tile_step:
+    if fused_step or small_step or tiny_step or tile_step or warp_step:
         launches = K
-    one_kernel = fused_step or small_step or tiny_step or tile_step
+    one_kernel = fused_step or small_step or tiny_step or tile_step or warp_step
     xread = s * n if args.x_shared else s * B * n
-    step_bytes = ((2 * s + 4) * B * m + 2 * s * B * n + xread) if one_kernel else (bbytes + ebytes)
+    # §8(d)'s per-unit figures x the units one step processes: build 3s B/knot + eval (2s+4) B/query
+    # + 3ns B/curve -- the same for one fused launch as for the two kernels; a fused kernel's own
+    # minimum (x, y read once, y2 written once, never read back) is reported beside it
+    step_bytes = bbytes + ebytes
+    fused_min_bytes = (2 * s + 4) * B * m + 2 * s * B * n + xread
     if wl.flags & workloads.FLAG_Q_SORTED:
         ekern = "k_eval_sorted"
     elif s == 4 and n <= 8 and 0 < m <= 32 and m % 4 == 0:
@@ -676,13 +683,18 @@ def main():
     if one_kernel:
         # the step IS one kernel: it is the dominant kernel; its launch is bracketed by the step's events
         skern = ("k_tile_eval" if tile_step else "k_eval_small<true>" if small_step else
-                 "k_build_eval_tiny" if tiny_step else "k_fused_staged")
+                 "k_build_eval_tiny" if tiny_step else "k_build_eval_warp" if warp_step else "k_fused_staged")
         str_, str_d = traffic_for(tkey, "step")
         sach = step_bytes / (step_ms * 1e-3) / 1e9
         roof = {"kernel": skern, "bound": "hbm", "achieved": sach, "peak": peak, "unit": "GB/s", "frac": sach / peak,
                 "traffic": str_, "traffic_detail": str_d, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": step_bytes,
-                "note": "algorithmic bytes: (2s+4) B/query (q in; out, int32 idx out) + 3s B/knot (x, y in; y2 out)",
+                "note": "algorithmic bytes (SURVEY.md §8(d) per unit): build 3s B/knot + eval (2s+4) B/query "
+                        "+ 3ns B/curve, for the build and eval units the one launch processes",
+                "fused_min_bytes": fused_min_bytes,
+                "fused_min_frac": fused_min_bytes / (step_ms * 1e-3) / 1e9 / peak,
+                "fused_min_note": "the fused kernel's own minimum traffic: x, y read once, y2 written once "
+                                  "and never read back, (2s+4) B/query",
                 "split_path": split_roof}
     else:
         roof = split_roof
@@ -723,11 +735,12 @@ def main():
         "step_roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak,
                           "algorithmic_bytes": step_bytes, "achieved": step_bytes / (step_ms * 1e-3) / 1e9,
                           "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak,
-                          "note": "the whole timed step (build + eval); one kernel reads x, y once and never "
-                                  "reads y2 back, the split path pays both kernels' bytes"},
+                          "note": "the whole timed step (build + eval), §8(d)'s per-unit bytes"},
         "step_path": ("fused (k_tile_eval: K2's solve, y2 kept on chip, sorted-run eval)" if tile_step else
                       "fused (k_eval_small<true>: K1r's solve + the small-curve eval)" if small_step else
                       "fused (k_build_eval_tiny: one CTA per curve, K1h's solve + eval)" if tiny_step else
+                      "fused (k_build_eval_warp: K1h's solve per group of 16 curves, y2 staged on chip, "
+                      "curvewarp eval)" if warp_step else
                       "fused (k_fused_staged)" if fused_step else "split (build kernel(s), then eval kernel(s))"),
         "roofline": roof,
         "fused": ({"kernel": "k_tile_eval" if tile_fusable else "k_fused_staged", "ms_per_step": fused_ms, "value": total_q / (fused_ms * 1e-3),

@@ -17,7 +17,7 @@
 // known.  One machinery serves three levels:
 //   leaf   : one thread, R consecutive rows -- a Thomas forward sweep with
 //            three right-hand sides (d, a_p e_1, c_q e_q) and a backward Horner pass;
-//   tile   : one CTA, 256 leaves -- merge tree in shared memory;
+//   tile   : one CTA, 256 leaves -- merge tree in registers (warp shuffles; tile_tree_up/down);
 //   curve  : tiles of one long curve (and ranks of a multi-GPU curve) -- k4_top.
 // The final per-row solve is the paper's back-substitution:
 // y_i = g'_i - v'_i L - c'_i y_{i+1}.
@@ -114,62 +114,141 @@ template <typename T> __device__ void tree_down(const T *mi, T *ext, int nleaf, 
 enum { TILE_FULL = 0, TILE_REDUCE = 1, TILE_FINISH = 2 };
 constexpr int kTileThreads = 256;
 #ifndef FS_TILE_PREFETCH
-#define FS_TILE_PREFETCH 0  // A/B: cfg4 build 151 vs 148 us, cfg5 932 vs 945 us
+#define FS_TILE_PREFETCH 1  // A/B at 3 CTAs/SM: cfg4 build 125.4 vs 133.1 us, cfg5 757 vs 840 us
 #endif
-constexpr int kTilePrefetchAhead = FS_TILE_PREFETCH;  // waves ahead whose x, y a tile prefetches to L2
+constexpr int kTilePrefetchAhead = FS_TILE_PREFETCH;
+#ifndef FS_TILE_STAGE_UNROLL
+#define FS_TILE_STAGE_UNROLL 4
+#endif
+constexpr int kTileStageUnroll = FS_TILE_STAGE_UNROLL;
+#ifndef FS_TILE_MINB
+#define FS_TILE_MINB 3  // 3 tiles of 4096 fp64 rows per SM (76 KB each): cfg4 build 133.1 vs 138.2 us at 2
+#endif  // staging loop unroll: vector loads per array in flight per thread  // waves ahead whose x, y a tile prefetches to L2
 
-// tree_up / tree_down for a full tile (kTileThreads leaves): the same merges in the same order,
-// with the level loop unrolled at compile time.
+// The tile's merge tree (tile_solve): the same merges, in the same order and on the same
+// operands, as tree_up / tree_down over the tile's nleaf <= 256 leaves, but with the records in
+// registers.  Levels 0-4 (blocks of up to 32 leaves) are inside a warp: the right child's record
+// comes by shuffle from lane t+s; levels 5-7 merge the 8 warp records in warp 0, lanes 0-7.  The
+// six seam values a merge hands to the top-down pass go to shared memory (TileTree::mi) except at
+// level 0, whose seams are the leaf records' own tips: lane t keeps its leaf's q-tip (even t) or
+// p-tip (odd t) in registers (k0).  Shared memory: 127 seams + 8 warp records -- 6.6 KB against
+// the 24 KB of a record and a seam per leaf, which lets three 4096-row fp64 tiles share an SM.
 __host__ __device__ constexpr int tile_levels() { return kTileThreads == 256 ? 8 : 0; }
-template <typename T> __device__ __forceinline__ void tree_up_full(Rec<T> *rec, T *mi) {
-  constexpr int NL = kTileThreads, LG = tile_levels();
-  const int t = threadIdx.x;
-  int off = 0;
-#pragma unroll
-  for (int lg = 0; lg < LG; ++lg) {
-    const int s = 1 << lg;
-    const int nn = NL >> (lg + 1);
-    if ((t & (2 * s - 1)) == 0) {
-      const Rec<T> A = rec[t], B = rec[t + s];
-      T *o = mi + 6 * (off + (t >> (lg + 1)));
-      o[0] = A.Gq; o[1] = A.Vq; o[2] = A.Wq; o[3] = B.Gp; o[4] = B.Vp; o[5] = B.Wp;
-      rec[t] = merge_rec(A, B);
-    }
-    off += nn;
-    if (4 * s <= 32) __syncwarp();
-    else __syncthreads();
-  }
-  __syncthreads();
+static_assert(kTileThreads == 256, "the tile tree is written for 8 warps of leaves");
+template <typename T> struct TileTree {
+  T mi[6 * (kTileThreads / 2 - 1)];  // seams of levels 1..7: level lg at mi_off(lg) + (t >> (lg + 1))
+  Rec<T> wrec[kTileThreads / 32];    // the warps' records (level 5's leaves)
+  T wext[2 * (kTileThreads / 32)];   // the warps' (L, R)
+};
+__device__ __forceinline__ int mi_off(int lg) { return kTileThreads / 2 - (kTileThreads >> lg); }  // lg >= 1
+
+template <typename T> __device__ __forceinline__ Rec<T> shfl_down_rec(const Rec<T> &r, int s) {
+  Rec<T> o;
+  o.Gp = __shfl_down_sync(0xffffffffu, r.Gp, s);
+  o.Vp = __shfl_down_sync(0xffffffffu, r.Vp, s);
+  o.Wp = __shfl_down_sync(0xffffffffu, r.Wp, s);
+  o.Gq = __shfl_down_sync(0xffffffffu, r.Gq, s);
+  o.Vq = __shfl_down_sync(0xffffffffu, r.Vq, s);
+  o.Wq = __shfl_down_sync(0xffffffffu, r.Wq, s);
+  return o;
 }
-template <typename T> __device__ __forceinline__ void tree_down_full(const T *mi, T *ext, T L, T R) {
-  constexpr int NL = kTileThreads, LG = tile_levels();
-  const int t = threadIdx.x;
-  if (t == 0) { ext[0] = L; ext[1] = R; }
-  __syncthreads();
-  int off = NL - 1;  // total merges
-#pragma unroll
-  for (int lg = LG - 1; lg >= 0; --lg) {
-    const int s = 1 << lg;
-    const int nn = NL >> (lg + 1);
-    off -= nn;
-    if ((t & (2 * s - 1)) == 0) {
-      const int j = t + s;
-      const T *o = mi + 6 * (off + (t >> (lg + 1)));
-      const T Li = ext[2 * t], Ri = ext[2 * t + 1];
-      T ym, ym1;
-      split_seam(o[0], o[1], o[2], o[3], o[4], o[5], Li, Ri, ym, ym1);
-      ext[2 * t + 1] = ym1;
-      ext[2 * j] = ym;
-      ext[2 * j + 1] = Ri;
-    }
-    if (2 * s <= 32) __syncwarp();
-    else __syncthreads();
-  }
-  __syncthreads();
+template <typename T> __device__ __forceinline__ void put_seam(T *o, const Rec<T> &A, const Rec<T> &B) {
+  o[0] = A.Gq; o[1] = A.Vq; o[2] = A.Wq; o[3] = B.Gp; o[4] = B.Vp; o[5] = B.Wp;
 }
 
+// Bottom-up.  r: this thread's leaf record (any value when t >= nleaf).  Returns the tile's
+// record in thread 0.  Every thread of the CTA must call it; ends with the warp-0 levels (no
+// trailing barrier: tile_tree_down starts with one).
+template <typename T> __device__ __forceinline__ Rec<T> tile_tree_up(Rec<T> r, int nleaf, TileTree<T> &tt, T (&k0)[3]) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const bool odd = lane & 1;
+  k0[0] = odd ? r.Gp : r.Gq;
+  k0[1] = odd ? r.Vp : r.Vq;
+  k0[2] = odd ? r.Wp : r.Wq;
+#pragma unroll
+  for (int lg = 0; lg < 5; ++lg) {
+    const int s = 1 << lg;
+    const Rec<T> B = shfl_down_rec(r, s);
+    if ((t & (2 * s - 1)) == 0 && t + s < nleaf) {
+      if (lg > 0) put_seam(tt.mi + 6 * (mi_off(lg) + (t >> (lg + 1))), r, B);
+      r = merge_rec(r, B);
+    }
+  }
+  if (lane == 0 && t < nleaf) tt.wrec[w] = r;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (nleaf + 31) >> 5;
+    r = tt.wrec[lane < nw ? lane : 0];
+#pragma unroll
+    for (int lg = 5; lg < tile_levels(); ++lg) {
+      const int s = 1 << (lg - 5);  // in warps
+      const Rec<T> B = shfl_down_rec(r, s);
+      if ((lane & (2 * s - 1)) == 0 && lane + s < nw) {
+        put_seam(tt.mi + 6 * (mi_off(lg) + ((32 * lane) >> (lg + 1))), r, B);
+        r = merge_rec(r, B);
+      }
+    }
+  }
+  return r;
+}
+
+// Top-down from the tile's outer (L, R): every leaf t < nleaf gets its own (L, R) in (Lo, Ro).
+// The split of a merge is done by its left child's thread, which keeps (L, y_{m+1}) and hands
+// (y_m, R) to the right child's thread.  Every thread of the CTA must call it.
+template <typename T>
+__device__ __forceinline__ void tile_tree_down(int nleaf, TileTree<T> &tt, const T (&k0)[3], T L, T R, T &Lo, T &Ro) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  __syncthreads();  // the seams of tile_tree_up are visible
+  if (w == 0) {
+    const int nw = (nleaf + 31) >> 5;
+    T Li = L, Ri = R;  // lane 0's; lanes 1..nw-1 receive theirs below
+#pragma unroll
+    for (int lg = tile_levels() - 1; lg >= 5; --lg) {
+      const int s = 1 << (lg - 5);
+      const bool act = (lane & (2 * s - 1)) == 0 && lane + s < nw;
+      T ym = T(0), ym1 = T(0);
+      if (act) {
+        const T *o = tt.mi + 6 * (mi_off(lg) + ((32 * lane) >> (lg + 1)));
+        split_seam(o[0], o[1], o[2], o[3], o[4], o[5], Li, Ri, ym, ym1);
+      }
+      const T rL = __shfl_up_sync(0xffffffffu, ym, s), rR = __shfl_up_sync(0xffffffffu, Ri, s);
+      if ((lane & (2 * s - 1)) == s && lane < nw) { Li = rL; Ri = rR; }
+      if (act) Ri = ym1;
+    }
+    if (lane < nw) { tt.wext[2 * lane] = Li; tt.wext[2 * lane + 1] = Ri; }
+  }
+  __syncthreads();
+  T Li = tt.wext[2 * w], Ri = tt.wext[2 * w + 1];  // lane 0's; the others receive theirs below
+  const T b0 = __shfl_down_sync(0xffffffffu, k0[0], 1), b1 = __shfl_down_sync(0xffffffffu, k0[1], 1),
+          b2 = __shfl_down_sync(0xffffffffu, k0[2], 1);  // level 0's right child: the odd lane's p-tip
+#pragma unroll
+  for (int lg = 4; lg >= 0; --lg) {
+    const int s = 1 << lg;
+    const bool act = (t & (2 * s - 1)) == 0 && t + s < nleaf;
+    T ym = T(0), ym1 = T(0);
+    if (act) {
+      if (lg > 0) {
+        const T *o = tt.mi + 6 * (mi_off(lg) + (t >> (lg + 1)));
+        split_seam(o[0], o[1], o[2], o[3], o[4], o[5], Li, Ri, ym, ym1);
+      } else {
+        split_seam(k0[0], k0[1], k0[2], b0, b1, b2, Li, Ri, ym, ym1);
+      }
+    }
+    const T rL = __shfl_up_sync(0xffffffffu, ym, s), rR = __shfl_up_sync(0xffffffffu, Ri, s);
+    if ((t & (2 * s - 1)) == s && t < nleaf) { Li = rL; Ri = rR; }
+    if (act) Ri = ym1;
+  }
+  Lo = Li;
+  Ro = Ri;
+}
+
+// X, Y: 256 leaves x R rows each, one pad element per leaf (pad(i) = i + i/R: a warp's 32 leaves
+// read their k-th rows from distinct banks); then the tree.
+template <typename T, int R> __host__ __device__ constexpr size_t tile_xy_bytes() {
+  return sizeof(T) * 2 * (size_t)kTileThreads * (R + 1);
+}
 template <typename T, int R> __host__ __device__ constexpr size_t tile_smem_bytes() {
-  return sizeof(T) * (2 * (size_t)kTileThreads * (R + 1) + 6 * kTileThreads + 6 * kTileThreads);
+  return tile_xy_bytes<T, R>() + sizeof(TileTree<T>);
 }
 
 // One leaf (thread l): rows [p, p + rows) of the tile (global P + p ...), the Thomas sweep with three
@@ -265,9 +344,7 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
   constexpr int TR = NT * R;
   T *X = reinterpret_cast<T *>(smem_raw);
   T *Y = X + NT * (R + 1);
-  Rec<T> *rec = reinterpret_cast<Rec<T> *>(Y + NT * (R + 1));
-  T *mi = reinterpret_cast<T *>(rec + NT);
-  T *ext = reinterpret_cast<T *>(rec);  // aliases rec: used only after tree_up
+  TileTree<T> &tt = *reinterpret_cast<TileTree<T> *>(smem_raw + tile_xy_bytes<T, R>());
 
   const int64_t c = blk / ntiles;
   const int tile = (int)(blk - c * ntiles);
@@ -284,7 +361,7 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
   using VT = typename Vec16<T>::V;
   const bool vec = ((((uintptr_t)(xc + P)) | ((uintptr_t)(yc + P))) & 15) == 0;
   const int nvec = vec ? nrows / VW : 0;
-#pragma unroll 4
+#pragma unroll kTileStageUnroll
   for (int v = threadIdx.x; v < nvec; v += NT) {
     const VT a = __ldcs(reinterpret_cast<const VT *>(xc + P) + v);
     const VT b = __ldcs(reinterpret_cast<const VT *>(yc + P) + v);
@@ -324,23 +401,22 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
   }
   __syncthreads();  // every neighbour value is in registers before the sweeps overwrite X/Y
 
+  Rec<T> r{T(0), T(0), T(0), T(0), T(0), T(0)};
   if (l < nleaf) {
     const T s0 = (bc & 1) ? yp1[c] : T(0);
     const T s1 = (bc & 2) ? ypn[c] : T(0);
     if (bc & 1) ok = ok && finite(s0);
     if (bc & 2) ok = ok && finite(s1);
     // full leaves (all but a ragged last one) run without per-row bounds tests (leaf_sweep)
-    const Rec<T> r = rows == R ? leaf_sweep<T, R, false>(X, Y, v, p, rows, P, n, bc, s0, s1, xm1, ym1, xq1, yq1, ok)
-                               : leaf_sweep<T, R, true>(X, Y, v, p, rows, P, n, bc, s0, s1, xm1, ym1, xq1, yq1, ok);
-    rec[l] = r;
+    r = rows == R ? leaf_sweep<T, R, false>(X, Y, v, p, rows, P, n, bc, s0, s1, xm1, ym1, xq1, yq1, ok)
+                  : leaf_sweep<T, R, true>(X, Y, v, p, rows, P, n, bc, s0, s1, xm1, ym1, xq1, yq1, ok);
   }
   const bool bad = __syncthreads_or(!ok);
-  if (nleaf == NT) tree_up_full(rec, mi);
-  else tree_up(rec, mi, nleaf);
+  T k0[3];
+  r = tile_tree_up(r, nleaf, tt, k0);
 
   if (MODE == TILE_REDUCE) {
     if (threadIdx.x == 0) {
-      const Rec<T> r = rec[0];
       T *o = tile_rec + (c * ntiles + tile) * 6;
       o[0] = r.Gp; o[1] = r.Vp; o[2] = r.Wp; o[3] = r.Gq; o[4] = r.Vq; o[5] = r.Wq;
       if (bad) {  // a NaN record: every merge and every finish that uses it is NaN (the whole curve)
@@ -368,11 +444,9 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
     Lr = tile_ext[(c * ntiles + tile) * 2];
     Rr = tile_ext[(c * ntiles + tile) * 2 + 1];
   }
-  if (nleaf == NT) tree_down_full(mi, ext, Lr, Rr);
-  else tree_down(mi, ext, nleaf, Lr, Rr);
+  T L, ynext;
+  tile_tree_down(nleaf, tt, k0, Lr, Rr, L, ynext);
   if (l < nleaf) {
-    const T L = ext[2 * l];
-    T ynext = ext[2 * l + 1];
     if (rows == R) {
 #pragma unroll
       for (int k = R - 1; k >= 0; --k) {
@@ -407,7 +481,7 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
 }
 
 template <typename T, int R, int MODE>
-__global__ void __launch_bounds__(kTileThreads) k_tile(unsigned *__restrict__ status, const T *__restrict__ x,
+__global__ void __launch_bounds__(kTileThreads, FS_TILE_MINB) k_tile(unsigned *__restrict__ status, const T *__restrict__ x,
                                                       const T *__restrict__ y, int64_t n, int64_t row_begin,
                                                       int64_t row_end, int bc, const T *__restrict__ yp1,
                                                       const T *__restrict__ ypn, T *__restrict__ y2,
