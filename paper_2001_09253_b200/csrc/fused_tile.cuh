@@ -25,12 +25,23 @@ constexpr int kTileEvalWarps = kTileThreads / 32;
 #endif
 constexpr int kTileEvalPF = FS_TILE_EVAL_PF;  // query prefetch depth (warp steps) of the eval phase
 
+// The warps' record windows reuse the solve's Y rows (the g' values, dead once tile_solve has
+// returned: it ends with a barrier after the back-substitution), so the fused kernel needs no
+// more shared memory than the solve.
+template <typename T, int R> __host__ __device__ constexpr size_t tile_eval_win_offset() {
+  return sizeof(T) * (size_t)kTileThreads * (R + 1);
+}
 template <typename T, int R> __host__ __device__ constexpr size_t tile_eval_smem_bytes() {
-  return ((tile_smem_bytes<T, R>() + 127) & ~(size_t)127) + kTileEvalWarps * sizeof(SortWin<T>);
+  return tile_smem_bytes<T, R>() > tile_eval_win_offset<T, R>() + kTileEvalWarps * sizeof(SortWin<T>)
+             ? tile_smem_bytes<T, R>()
+             : tile_eval_win_offset<T, R>() + kTileEvalWarps * sizeof(SortWin<T>);
 }
 
+#ifndef FS_TILE_EVAL_MINB
+#define FS_TILE_EVAL_MINB 3  // cfg4 PATH_FUSED: 1374 vs 1614 us at 2 (the split path: 1225-1233 us)
+#endif
 template <typename T, int R, int V, bool WIN>
-__global__ void __launch_bounds__(kTileThreads, 2)
+__global__ void __launch_bounds__(kTileThreads, FS_TILE_EVAL_MINB)
     k_tile_eval(unsigned *__restrict__ status, const T *__restrict__ x, const T *__restrict__ y, int n, int bc,
                 const T *__restrict__ yp1, const T *__restrict__ ypn, T *__restrict__ y2, const T *__restrict__ q,
                 int64_t m, T *__restrict__ out, int32_t *__restrict__ idx, int nchunks, int64_t qchunk) {
@@ -41,7 +52,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
   tile_solve<T, R, TILE_FULL>(status, x, y, n, 0, n, bc, yp1, ypn, chunk == 0 ? y2 : nullptr, nullptr, nullptr,
                               nullptr, 1, c, smem_raw);
   const T *Zs = reinterpret_cast<const T *>(smem_raw);  // y2, padded rows (tile_solve)
-  SortWin<T> *wins = reinterpret_cast<SortWin<T> *>(smem_raw + ((tile_smem_bytes<T, R>() + 127) & ~(size_t)127));
+  SortWin<T> *wins = reinterpret_cast<SortWin<T> *>(smem_raw + tile_eval_win_offset<T, R>());
   // the chunk's queries, one contiguous run per warp (whole 32V steps)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t q0 = chunk * qchunk, q1 = min64(m, q0 + qchunk);
