@@ -683,15 +683,17 @@ __global__ void __launch_bounds__(256) k_build_eval_tiny(unsigned *__restrict__ 
   constexpr int P = 1 << L2;
   using VT = typename Vec16<T>::V;
   __shared__ CwTable<T> tb;
+  __shared__ __align__(16) T zs[N];
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t c = blockIdx.x;
   const T *qc = q + c * m;
   const int nv = m / VW;
   VT q0;
   if (tid < nv) q0 = __ldcs(reinterpret_cast<const VT *>(qc) + tid);
-  if (tid < 32) k1h_solve<T, N>(status, x, y, batch, bc, yp1, ypn, y2, (lane < 2) ? c : batch, (lane & 1) == 0);
-  __syncthreads();  // y2 of the curve is in memory
-  const T *X = x + c * N, *Y = y + c * N, *Z = y2 + c * N;
+  // y2 to HBM (when asked) and to shared memory, which the table build reads
+  if (tid < 32) k1h_solve<T, N>(status, x, y, batch, bc, yp1, ypn, y2, (lane < 2) ? c : batch, (lane & 1) == 0, zs);
+  __syncthreads();  // y2 of the curve is in shared memory
+  const T *X = x + c * N, *Y = y + c * N, *Z = zs;
   if (tid < N) tb.xk[tid] = X[tid];
   if (tid < N - 1) tb.c[tid] = make_cub<T>(X[tid], X[tid + 1], Y[tid], Y[tid + 1], Z[tid], Z[tid + 1], tb.e2[tid]);
   if (tid > 0 && tid < P) {

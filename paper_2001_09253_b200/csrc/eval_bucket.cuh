@@ -35,6 +35,12 @@
 
 namespace fs {
 
+#ifndef FS_BK_CNT_MINB
+#define FS_BK_CNT_MINB 3  // A/B cfg5 eval: 9.18 ms at 3/3 vs 9.34 at 2/2 (count, scatter)
+#endif
+#ifndef FS_BK_SC_MINB
+#define FS_BK_SC_MINB 3
+#endif
 constexpr int kBkTile = 4096;         // queries per tile (tile-local slots fit u16)
 constexpr int kBkThreads = 256;
 constexpr int kBkScThreads = 512;     // count / scatter / gather: 8 queries per thread
@@ -69,7 +75,7 @@ __device__ __forceinline__ T load_bounds(T *xb, const T *__restrict__ x, int n, 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kBkScThreads, 2) k_bucket_count(const T *__restrict__ x, int n, int64_t K, int nb,
+__global__ void __launch_bounds__(kBkScThreads, FS_BK_CNT_MINB) k_bucket_count(const T *__restrict__ x, int n, int64_t K, int nb,
                                                                   const T *__restrict__ q, int64_t m,
                                                                   int *__restrict__ cnt) {
   pdl_wait();
@@ -174,7 +180,7 @@ template <typename T> constexpr size_t bucket_scatter_smem() {
 template <typename T> constexpr size_t bucket_gather_smem() { return (sizeof(T) + 4) * kBkTile; }
 
 template <typename T>
-__global__ void __launch_bounds__(kBkScThreads, 2) k_bucket_scatter(const T *__restrict__ x, int n, int64_t K, int nb,
+__global__ void __launch_bounds__(kBkScThreads, FS_BK_SC_MINB) k_bucket_scatter(const T *__restrict__ x, int n, int64_t K, int nb,
                                                                     const T *__restrict__ q, int64_t m,
                                                                     const int *__restrict__ goff,
                                                                     const int *__restrict__ bsum,

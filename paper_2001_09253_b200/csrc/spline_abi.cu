@@ -931,19 +931,13 @@ int build_eval_t(const T *x, const T *y, int64_t n, int64_t batch, int bc, const
     if (!(flags & (SPLINE_PATH_FUSED | SPLINE_PATH_SPLIT | kNoFusedStaged)) && k1h_n && batch <= 16 && m <= 8192 &&
         m % VW == 0 && aligned16(x) && aligned16(y) && aligned16(q) && aligned16(out) && (!y2 || aligned16(y2)) &&
         (!idx || (((uintptr_t)idx & (4 * VW - 1)) == 0))) {
-      T *yy = y2;
-      if (!yy) {
-        if (int rc = ws_alloc((void **)&yy, sizeof(T) * (size_t)n * batch, st)) return rc;
-      }
-      const unsigned g = (unsigned)batch;
-      if (n == 16) k_build_eval_tiny<T, 16, 4><<<g, 256, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, yy, q, (int)m, out, idx);
+      const unsigned g = (unsigned)batch;  // y2 == nullptr: the kernel keeps it on chip only
+      if (n == 16) k_build_eval_tiny<T, 16, 4><<<g, 256, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, y2, q, (int)m, out, idx);
       if constexpr (sizeof(T) == 4) {
-        if (n == 32) k_build_eval_tiny<T, 32, 5><<<g, 256, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, yy, q, (int)m, out, idx);
-        if (n == 64) k_build_eval_tiny<T, 64, 6><<<g, 256, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, yy, q, (int)m, out, idx);
+        if (n == 32) k_build_eval_tiny<T, 32, 5><<<g, 256, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, y2, q, (int)m, out, idx);
+        if (n == 64) k_build_eval_tiny<T, 64, 6><<<g, 256, 0, st>>>(tl_status, x, y, batch, bc, yp1, ypn, y2, q, (int)m, out, idx);
       }
-      const int rc = launch_rc();
-      if (!y2) cudaFreeAsync(yy, st);
-      return rc;
+      return launch_rc();
     }
   }
   {  // many K1h-sized curves, unsorted (or sorted) queries: solve + evaluate per warp
