@@ -46,8 +46,14 @@ constexpr int kBkThreads = 256;
 constexpr int kBkScThreads = 512;     // count / scatter / gather: 8 queries per thread
 constexpr int kBkPerThread = kBkTile / kBkScThreads;
 constexpr int kBkMaxBuckets = 512;    // in-range chunks per curve (+1 bucket: out of range / NaN)
-constexpr int kBkEvalIters = 4;       // rounds of the flat evaluation per block
-constexpr int kBkEvalPer = 1024 * kBkEvalIters;  // queries per block of the flat evaluation (4 per thread and round)
+#ifndef FS_BK_EVAL_ITERS
+#define FS_BK_EVAL_ITERS 8
+#endif
+constexpr int kBkEvalIters = FS_BK_EVAL_ITERS;  // rounds of the flat evaluation per block
+#ifndef FS_BK_EVAL_U
+#define FS_BK_EVAL_U 2  // A/B cfg5 eval (with kBkSpec): U2 x 8 rounds 8.38 ms, U4 x 4 11.08 (spills), U1 x 16 8.42, U2 x 4 8.62
+#endif
+constexpr int kBkEvalPer = kBkThreads * FS_BK_EVAL_U * kBkEvalIters;  // queries per block of the flat evaluation (U per thread and round)
 constexpr int kScanBlock = 4096;      // elements per block of the run-offset scan (4 per thread)
 
 // bucket of q: b in [0, nb) with x_{bK} <= q < x_{(b+1)K} (the last bucket ends at x_{n-1}
@@ -284,6 +290,10 @@ template <typename T> __device__ __forceinline__ Knot<T> ld_knot(const Knot<T> *
 }
 
 // The flat evaluation of the bucket-major queries; results to the tile slots named by dest.
+#ifndef FS_BK_SPEC
+#define FS_BK_SPEC 1  // A/B cfg5 eval: 8.38 vs 9.13 ms without (a miss of the guess costs no second round)
+#endif
+constexpr bool kBkSpec = FS_BK_SPEC != 0;  // the guess's likely neighbour knot loaded in the first round
 #ifndef FS_BK_EVAL_MINB
 #define FS_BK_EVAL_MINB 3
 #endif
@@ -340,19 +350,25 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
     uint32_t dd[U];
     int j[U];
     bool in[U];
-    Knot<T> ka[U], kb[U];
+    Knot<T> ka[U], kb[U], kc[U];
+    bool up[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const T v = qn[u];
       dd[u] = dn[u];
       in[u] = (v >= x0) && (v <= xn);
       qq[u] = in[u] ? v : x0;
-      j[u] = max(0, min((int)r_mul(r_sub(qq[u], x0), sc), n - 2));
+      const T f = r_mul(r_sub(qq[u], x0), sc);
+      j[u] = max(0, min((int)f, n - 2));
+      up[u] = f - (T)j[u] >= T(0.5);  // which neighbour a miss of the guess most likely needs
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       ka[u] = ld_knot(kn + j[u]);
       kb[u] = ld_knot(kn + j[u] + 1);
+      // the likely neighbour in the same round (kBkSpec): knot j-1 below the guess's middle,
+      // knot j+2 above it (clamped into the curve; only used when it is the right one)
+      if (kBkSpec) kc[u] = ld_knot(kn + (up[u] ? min(j[u] + 2, n - 1) : max(j[u] - 1, 0)));
     }
     if (it + 1 < kBkEvalIters) {
 #pragma unroll
@@ -364,6 +380,17 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      if (kBkSpec && !(ka[u].x <= qq[u] && (qq[u] < kb[u].x || j[u] == n - 2))) {
+        if (!up[u] && ka[u].x > qq[u] && j[u] > 0 && kc[u].x <= qq[u]) {  // one interval down
+          j[u] -= 1;
+          kb[u] = ka[u];
+          ka[u] = kc[u];
+        } else if (up[u] && !(ka[u].x > qq[u]) && j[u] + 2 <= n - 1 && qq[u] < kc[u].x) {  // one up
+          j[u] += 1;
+          ka[u] = kb[u];
+          kb[u] = kc[u];
+        }
+      }
       if (!(ka[u].x <= qq[u] && (qq[u] < kb[u].x || j[u] == n - 2))) {  // the guess missed
         if (ka[u].x > qq[u] && j[u] > 0 && __ldg(&kn[j[u] - 1].x) <= qq[u]) {
           j[u] -= 1;  // one interval down (the usual miss on a jittered grid)
