@@ -9,7 +9,7 @@ python tools/prof.py 5 1
 EOS
 bash $T/top.sh > $T/top_plain.log 2>&1 && \
 ncu --target-processes all --set full --clock-control none --import-source on \
-    -k regex:"k1_thomas_half|k_eval_curvewarp|k_tile<|k_eval_sorted|k_bucket_eval|k_bucket_scatter|k_bucket_gather" \
+    -k regex:"k1_thomas_half|k_eval_curvewarp|k_build_eval_warp|k_tile|k_eval_sorted|k_bucket_eval|k_bucket_scatter|k_bucket_gather" \
     -c 18 -o $T/top -f bash $T/top.sh > $T/ncu_top.log 2>&1; echo "ncu full rc=$?"; tail -2 $T/ncu_top.log
 # summaries travel back (gpurun_out is capped at 64 MiB): metrics per kernel + stall hot spots
 python tools/ncu_summary.py $T/top.ncu-rep --json $T/ncu_full_top.json > $T/ncu_full_top.txt 2>&1
