@@ -112,11 +112,35 @@ template <typename T> __device__ void tree_down(const T *mi, T *ext, int nleaf, 
 }
 
 enum { TILE_FULL = 0, TILE_REDUCE = 1, TILE_FINISH = 2 };
+// Diagnostic build only (-DFS_TILE_PHASES=1): thread 0 of every tile adds the SM cycles of each
+// phase of tile_solve to g_tile_phase[] (read by spline_debug_tile_phases).  Off in the product.
+#ifndef FS_TILE_PHASES
+#define FS_TILE_PHASES 0
+#endif
+#if FS_TILE_PHASES
+__device__ unsigned long long g_tile_phase[8];
+#define TILE_MARK(k)                                              \
+  do {                                                            \
+    if (threadIdx.x == 0) {                                       \
+      const long long t_ = clock64();                             \
+      atomicAdd(&g_tile_phase[k], (unsigned long long)(t_ - tp_)); \
+      tp_ = t_;                                                   \
+    }                                                             \
+  } while (0)
+#else
+#define TILE_MARK(k) \
+  do {               \
+  } while (0)
+#endif
 constexpr int kTileThreads = 256;
 #ifndef FS_TILE_PREFETCH
 #define FS_TILE_PREFETCH 1  // A/B at 3 CTAs/SM: cfg4 build 125.4 vs 133.1 us, cfg5 757 vs 840 us
 #endif
 constexpr int kTilePrefetchAhead = FS_TILE_PREFETCH;
+#ifndef FS_TILE_PF_LATE
+#define FS_TILE_PF_LATE 0  // A/B: cfg4 124.9 vs 125.0 us, cfg5 788 vs 755 us (prefetch at entry kept)
+#endif
+constexpr bool kTilePrefetchLate = FS_TILE_PF_LATE != 0;  // prefetch after the tile's own staging
 #ifndef FS_TILE_STAGE_UNROLL
 #define FS_TILE_STAGE_UNROLL 4
 #endif
@@ -125,14 +149,38 @@ constexpr int kTileStageUnroll = FS_TILE_STAGE_UNROLL;
 #define FS_TILE_MINB 3  // 3 tiles of 4096 fp64 rows per SM (76 KB each): cfg4 build 133.1 vs 138.2 us at 2
 #endif  // staging loop unroll: vector loads per array in flight per thread  // waves ahead whose x, y a tile prefetches to L2
 
-// The tile's merge tree (tile_solve): the same merges, in the same order and on the same
-// operands, as tree_up / tree_down over the tile's nleaf <= 256 leaves, but with the records in
-// registers.  Levels 0-4 (blocks of up to 32 leaves) are inside a warp: the right child's record
-// comes by shuffle from lane t+s; levels 5-7 merge the 8 warp records in warp 0, lanes 0-7.  The
-// six seam values a merge hands to the top-down pass go to shared memory (TileTree::mi) except at
-// level 0, whose seams are the leaf records' own tips: lane t keeps its leaf's q-tip (even t) or
-// p-tip (odd t) in registers (k0).  Shared memory: 127 seams + 8 warp records -- 6.6 KB against
-// the 24 KB of a record and a seam per leaf, which lets three 4096-row fp64 tiles share an SM.
+// Merge A, B like merge_rec, and also return the seam SOLVED for the outer unknowns:
+//   y_m = Gm - Vm L - Wm R,   y_{m+1} = Gm1 - Vm1 L - Wm1 R      (sm = {Gm, Vm, Wm, Gm1, Vm1, Wm1})
+// -- the intermediate values merge_rec computes anyway, so the top-down pass needs no
+// reciprocal: each seam row is two fused multiply-adds from the block's (L, R).
+template <typename T> __device__ __forceinline__ Rec<T> merge_rec_seam(const Rec<T> &A, const Rec<T> &B, T (&sm)[6]) {
+  const T iD = nr_rcp(T(1) - A.Wq * B.Vp);
+  const T Gm = (A.Gq - A.Wq * B.Gp) * iD, Vm = A.Vq * iD, Wm = -(A.Wq * B.Wp) * iD;    // y_m
+  const T Gm1 = (B.Gp - B.Vp * A.Gq) * iD, Vm1 = -(B.Vp * A.Vq) * iD, Wm1 = B.Wp * iD;  // y_{m+1}
+  sm[0] = Gm; sm[1] = Vm; sm[2] = Wm; sm[3] = Gm1; sm[4] = Vm1; sm[5] = Wm1;
+  Rec<T> o;
+  o.Gp = A.Gp - A.Wp * Gm1;
+  o.Vp = A.Vp - A.Wp * Vm1;
+  o.Wp = -(A.Wp * Wm1);
+  o.Gq = B.Gq - B.Vq * Gm;
+  o.Vq = -(B.Vq * Vm);
+  o.Wq = B.Wq - B.Vq * Wm;
+  return o;
+}
+// g - v L - w R
+template <typename T> __device__ __forceinline__ T seam_row(T g, T v, T w, T L, T R) {
+  return __fma_rn(-w, R, __fma_rn(-v, L, g));
+}
+
+// The tile's merge tree (tile_solve): the merges of tree_up over the tile's nleaf <= 256 leaves,
+// in the same order and on the same operands (so the tile record is bitwise tree_up's), with the
+// records in registers.  Levels 0-4 (blocks of up to 32 leaves) are inside a warp: the right
+// child's record comes by shuffle from lane t+s; levels 5-7 merge the 8 warp records in warp 0,
+// lanes 0-7.  Each merge's SOLVED seam (merge_rec_seam) goes to shared memory (TileTree::mi),
+// except at level 0, where lane t keeps the half its own leaf needs on the way down in registers
+// (k0: even t the y_{m+1} row -- its right neighbour --, odd t the y_m row -- its left one).
+// Shared memory: 127 seams + 8 warp records -- 6.6 KB against the 24 KB of a record and a seam
+// per leaf, which lets three 4096-row fp64 tiles share an SM.
 __host__ __device__ constexpr int tile_levels() { return kTileThreads == 256 ? 8 : 0; }
 static_assert(kTileThreads == 256, "the tile tree is written for 8 warps of leaves");
 template <typename T> struct TileTree {
@@ -152,8 +200,9 @@ template <typename T> __device__ __forceinline__ Rec<T> shfl_down_rec(const Rec<
   o.Wq = __shfl_down_sync(0xffffffffu, r.Wq, s);
   return o;
 }
-template <typename T> __device__ __forceinline__ void put_seam(T *o, const Rec<T> &A, const Rec<T> &B) {
-  o[0] = A.Gq; o[1] = A.Vq; o[2] = A.Wq; o[3] = B.Gp; o[4] = B.Vp; o[5] = B.Wp;
+template <typename T> __device__ __forceinline__ void put6(T *o, const T (&v)[6]) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i) o[i] = v[i];
 }
 
 // Bottom-up.  r: this thread's leaf record (any value when t >= nleaf).  Returns the tile's
@@ -161,17 +210,25 @@ template <typename T> __device__ __forceinline__ void put_seam(T *o, const Rec<T
 // trailing barrier: tile_tree_down starts with one).
 template <typename T> __device__ __forceinline__ Rec<T> tile_tree_up(Rec<T> r, int nleaf, TileTree<T> &tt, T (&k0)[3]) {
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const bool odd = lane & 1;
-  k0[0] = odd ? r.Gp : r.Gq;
-  k0[1] = odd ? r.Vp : r.Vq;
-  k0[2] = odd ? r.Wp : r.Wq;
+  T km[3] = {T(0), T(0), T(0)};
 #pragma unroll
   for (int lg = 0; lg < 5; ++lg) {
     const int s = 1 << lg;
     const Rec<T> B = shfl_down_rec(r, s);
     if ((t & (2 * s - 1)) == 0 && t + s < nleaf) {
-      if (lg > 0) put_seam(tt.mi + 6 * (mi_off(lg) + (t >> (lg + 1))), r, B);
-      r = merge_rec(r, B);
+      T sm[6];
+      r = merge_rec_seam(r, B, sm);
+      if (lg > 0) {
+        put6(tt.mi + 6 * (mi_off(lg) + (t >> (lg + 1))), sm);
+      } else {
+        km[0] = sm[0]; km[1] = sm[1]; km[2] = sm[2];  // y_m's row: the odd neighbour's
+        k0[0] = sm[3]; k0[1] = sm[4]; k0[2] = sm[5];  // y_{m+1}'s row: this lane's
+      }
+    }
+    if (lg == 0) {
+      const T a0 = __shfl_up_sync(0xffffffffu, km[0], 1), a1 = __shfl_up_sync(0xffffffffu, km[1], 1),
+              a2 = __shfl_up_sync(0xffffffffu, km[2], 1);
+      if (lane & 1) { k0[0] = a0; k0[1] = a1; k0[2] = a2; }
     }
   }
   if (lane == 0 && t < nleaf) tt.wrec[w] = r;
@@ -184,8 +241,9 @@ template <typename T> __device__ __forceinline__ Rec<T> tile_tree_up(Rec<T> r, i
       const int s = 1 << (lg - 5);  // in warps
       const Rec<T> B = shfl_down_rec(r, s);
       if ((lane & (2 * s - 1)) == 0 && lane + s < nw) {
-        put_seam(tt.mi + 6 * (mi_off(lg) + ((32 * lane) >> (lg + 1))), r, B);
-        r = merge_rec(r, B);
+        T sm[6];
+        r = merge_rec_seam(r, B, sm);
+        put6(tt.mi + 6 * (mi_off(lg) + ((32 * lane) >> (lg + 1))), sm);
       }
     }
   }
@@ -193,8 +251,10 @@ template <typename T> __device__ __forceinline__ Rec<T> tile_tree_up(Rec<T> r, i
 }
 
 // Top-down from the tile's outer (L, R): every leaf t < nleaf gets its own (L, R) in (Lo, Ro).
-// The split of a merge is done by its left child's thread, which keeps (L, y_{m+1}) and hands
-// (y_m, R) to the right child's thread.  Every thread of the CTA must call it.
+// A merged block's (L, R) sit with its left child's thread; the right child's thread gets them
+// by shuffle, and each child evaluates ITS half of the solved seam: the left child its new
+// R = y_{m+1}, the right child its new L = y_m (two FMAs each, no reciprocal).  Every thread of
+// the CTA must call it.
 template <typename T>
 __device__ __forceinline__ void tile_tree_down(int nleaf, TileTree<T> &tt, const T (&k0)[3], T L, T R, T &Lo, T &Ro) {
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -205,38 +265,31 @@ __device__ __forceinline__ void tile_tree_down(int nleaf, TileTree<T> &tt, const
 #pragma unroll
     for (int lg = tile_levels() - 1; lg >= 5; --lg) {
       const int s = 1 << (lg - 5);
-      const bool act = (lane & (2 * s - 1)) == 0 && lane + s < nw;
-      T ym = T(0), ym1 = T(0);
-      if (act) {
-        const T *o = tt.mi + 6 * (mi_off(lg) + ((32 * lane) >> (lg + 1)));
-        split_seam(o[0], o[1], o[2], o[3], o[4], o[5], Li, Ri, ym, ym1);
-      }
-      const T rL = __shfl_up_sync(0xffffffffu, ym, s), rR = __shfl_up_sync(0xffffffffu, Ri, s);
-      if ((lane & (2 * s - 1)) == s && lane < nw) { Li = rL; Ri = rR; }
-      if (act) Ri = ym1;
+      const T pL = __shfl_up_sync(0xffffffffu, Li, s), pR = __shfl_up_sync(0xffffffffu, Ri, s);
+      const bool left = (lane & (2 * s - 1)) == 0 && lane + s < nw;
+      const bool right = (lane & (2 * s - 1)) == s && lane < nw;
+      const T *o = tt.mi + 6 * (mi_off(lg) + ((32 * lane) >> (lg + 1)));
+      if (left) Ri = seam_row(o[3], o[4], o[5], Li, Ri);
+      if (right) { Li = seam_row(o[0], o[1], o[2], pL, pR); Ri = pR; }
     }
     if (lane < nw) { tt.wext[2 * lane] = Li; tt.wext[2 * lane + 1] = Ri; }
   }
   __syncthreads();
   T Li = tt.wext[2 * w], Ri = tt.wext[2 * w + 1];  // lane 0's; the others receive theirs below
-  const T b0 = __shfl_down_sync(0xffffffffu, k0[0], 1), b1 = __shfl_down_sync(0xffffffffu, k0[1], 1),
-          b2 = __shfl_down_sync(0xffffffffu, k0[2], 1);  // level 0's right child: the odd lane's p-tip
 #pragma unroll
   for (int lg = 4; lg >= 0; --lg) {
     const int s = 1 << lg;
-    const bool act = (t & (2 * s - 1)) == 0 && t + s < nleaf;
-    T ym = T(0), ym1 = T(0);
-    if (act) {
-      if (lg > 0) {
-        const T *o = tt.mi + 6 * (mi_off(lg) + (t >> (lg + 1)));
-        split_seam(o[0], o[1], o[2], o[3], o[4], o[5], Li, Ri, ym, ym1);
-      } else {
-        split_seam(k0[0], k0[1], k0[2], b0, b1, b2, Li, Ri, ym, ym1);
-      }
+    const T pL = __shfl_up_sync(0xffffffffu, Li, s), pR = __shfl_up_sync(0xffffffffu, Ri, s);
+    const bool left = (t & (2 * s - 1)) == 0 && t + s < nleaf;
+    const bool right = (t & (2 * s - 1)) == s && t < nleaf;
+    if (lg > 0) {
+      const T *o = tt.mi + 6 * (mi_off(lg) + (t >> (lg + 1)));
+      if (left) Ri = seam_row(o[3], o[4], o[5], Li, Ri);
+      if (right) { Li = seam_row(o[0], o[1], o[2], pL, pR); Ri = pR; }
+    } else {
+      if (left) Ri = seam_row(k0[0], k0[1], k0[2], Li, Ri);
+      if (right) { Li = seam_row(k0[0], k0[1], k0[2], pL, pR); Ri = pR; }
     }
-    const T rL = __shfl_up_sync(0xffffffffu, ym, s), rR = __shfl_up_sync(0xffffffffu, Ri, s);
-    if ((t & (2 * s - 1)) == s && t < nleaf) { Li = rL; Ri = rR; }
-    if (act) Ri = ym1;
   }
   Lo = Li;
   Ro = Ri;
@@ -325,6 +378,23 @@ __device__ __forceinline__ Rec<T> leaf_sweep(T *X, T *Y, T (&v)[R], int p, int r
   return r;
 }
 
+// The tile this SM slot will most likely run a wave from now (block nb): its x, y into L2, so
+// that tile's staging loads (the kernel's largest stall, ncu r02) are L2 hits.  One thread.
+template <typename T, int R>
+__device__ __forceinline__ void tile_prefetch_l2(const T *x, const T *y, int64_t n, int64_t row_begin, int64_t row_end,
+                                                 int ntiles, int64_t nb, int64_t nblocks) {
+  if (nb >= nblocks) return;
+  const int64_t c2 = nb / ntiles, t2 = nb - c2 * ntiles;
+  const int64_t P2 = row_begin + t2 * (int64_t)kTileThreads * R;
+  const int64_t r2 = min64((int64_t)kTileThreads * R, row_end - P2);
+  constexpr int64_t A = 16 / sizeof(T);
+  const int64_t e0 = (c2 * n + P2) & ~(A - 1), e1 = (c2 * n + P2 + r2) & ~(A - 1);
+  if (e1 > e0) {
+    prefetch_l2_bulk(x + e0, (uint32_t)((e1 - e0) * sizeof(T)));
+    prefetch_l2_bulk(y + e0, (uint32_t)((e1 - e0) * sizeof(T)));
+  }
+}
+
 // One CTA solves rows [P, Q] of one curve: the linear block index is curve c times ntiles plus
 // tile t (a 1-D grid, so the batch is not capped at 65535), P = row_begin + t * 256R.
 //  FULL   : the tile is the whole curve (row_begin = 0, row_end = n <= 256R); writes y2.
@@ -339,11 +409,15 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
                                            const T *__restrict__ y, int64_t n, int64_t row_begin, int64_t row_end,
                                            int bc, const T *__restrict__ yp1, const T *__restrict__ ypn,
                                            T *__restrict__ y2, T *__restrict__ tile_rec, const T *__restrict__ tile_ext,
-                                           int *__restrict__ badflag, int ntiles, int64_t blk, unsigned char *smem_raw) {
+                                           int *__restrict__ badflag, int ntiles, int64_t blk, unsigned char *smem_raw,
+                                           int pf_blocks = 0, int64_t nblocks = 0) {
   constexpr int NT = kTileThreads;
   constexpr int TR = NT * R;
   T *X = reinterpret_cast<T *>(smem_raw);
   T *Y = X + NT * (R + 1);
+#if FS_TILE_PHASES
+  long long tp_ = clock64();
+#endif
   TileTree<T> &tt = *reinterpret_cast<TileTree<T> *>(smem_raw + tile_xy_bytes<T, R>());
 
   const int64_t c = blk / ntiles;
@@ -377,6 +451,10 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
     Y[pad(e)] = ld_stream(yc + P + e);
   }
   __syncthreads();
+  TILE_MARK(0);
+  // (FS_TILE_PF_LATE) the next wave's tile is prefetched once this tile's own loads are done, so
+  // the two do not compete for DRAM at the start of a wave
+  if (pf_blocks > 0 && threadIdx.x == 0) tile_prefetch_l2<T, R>(x, y, n, row_begin, row_end, ntiles, blk + pf_blocks, nblocks);
 
   const int l = threadIdx.x;
   const int p = l * R;
@@ -400,6 +478,7 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
     }
   }
   __syncthreads();  // every neighbour value is in registers before the sweeps overwrite X/Y
+  TILE_MARK(1);
 
   Rec<T> r{T(0), T(0), T(0), T(0), T(0), T(0)};
   if (l < nleaf) {
@@ -412,8 +491,10 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
                   : leaf_sweep<T, R, true>(X, Y, v, p, rows, P, n, bc, s0, s1, xm1, ym1, xq1, yq1, ok);
   }
   const bool bad = __syncthreads_or(!ok);
+  TILE_MARK(2);
   T k0[3];
   r = tile_tree_up(r, nleaf, tt, k0);
+  TILE_MARK(3);
 
   if (MODE == TILE_REDUCE) {
     if (threadIdx.x == 0) {
@@ -446,6 +527,7 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
   }
   T L, ynext;
   tile_tree_down(nleaf, tt, k0, Lr, Rr, L, ynext);
+  TILE_MARK(4);
   if (l < nleaf) {
     if (rows == R) {
 #pragma unroll
@@ -468,6 +550,7 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
     }
   }
   __syncthreads();
+  TILE_MARK(5);
   if (!y2o) return;
   const bool vo = (((uintptr_t)y2o) & 15) == 0;
   const int novec = vo ? nrows / VW : 0;
@@ -478,6 +561,7 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
     __stcs(reinterpret_cast<VT *>(y2o) + v, a);
   }
   for (int e = novec * VW + threadIdx.x; e < nrows; e += NT) y2o[e] = X[pad(e)];
+  TILE_MARK(6);
 }
 
 template <typename T, int R, int MODE>
@@ -488,24 +572,10 @@ __global__ void __launch_bounds__(kTileThreads, FS_TILE_MINB) k_tile(unsigned *_
                                                       T *__restrict__ tile_rec, const T *__restrict__ tile_ext,
                                                       int *__restrict__ badflag, int ntiles, int pf_blocks) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  if (pf_blocks > 0 && threadIdx.x == 0) {
-    // the tile this SM slot will most likely run a wave from now: its x, y into L2 now, so that
-    // tile's staging loads (the kernel's largest stall, ncu r02) are L2 hits
-    const int64_t nb = blockIdx.x + (int64_t)pf_blocks;  // pf_blocks: the CTAs resident at once
-    if (nb < (int64_t)gridDim.x) {
-      const int64_t c2 = nb / ntiles, t2 = nb - c2 * ntiles;
-      const int64_t P2 = row_begin + t2 * (int64_t)kTileThreads * R;
-      const int64_t r2 = min64((int64_t)kTileThreads * R, row_end - P2);
-      constexpr int64_t A = 16 / sizeof(T);
-      const int64_t e0 = (c2 * n + P2) & ~(A - 1), e1 = (c2 * n + P2 + r2) & ~(A - 1);
-      if (e1 > e0) {
-        prefetch_l2_bulk(x + e0, (uint32_t)((e1 - e0) * sizeof(T)));
-        prefetch_l2_bulk(y + e0, (uint32_t)((e1 - e0) * sizeof(T)));
-      }
-    }
-  }
+  if (!kTilePrefetchLate && pf_blocks > 0 && threadIdx.x == 0)
+    tile_prefetch_l2<T, R>(x, y, n, row_begin, row_end, ntiles, (int64_t)blockIdx.x + pf_blocks, gridDim.x);
   tile_solve<T, R, MODE>(status, x, y, n, row_begin, row_end, bc, yp1, ypn, y2, tile_rec, tile_ext, badflag, ntiles,
-                         (int64_t)blockIdx.x, smem_raw);
+                         (int64_t)blockIdx.x, smem_raw, kTilePrefetchLate ? pf_blocks : 0, gridDim.x);
 }
 
 // K4: merge the per-tile records of each curve (grid = batch, one CTA per curve) and,

@@ -1562,4 +1562,14 @@ int spline_build_dist_f64(const double *x, const double *y, int64_t n, int bc, c
 
 const char *spline_version(void) { return "fastspline-b200 0.2 (sm_100a)"; }
 
+#if FS_TILE_PHASES
+// Diagnostic build only: the accumulated per-phase SM cycles of tile_solve (thread 0 of every
+// tile), copied to out[0..7] and reset.
+int spline_debug_tile_phases(unsigned long long *out) {
+  if (cudaMemcpyFromSymbol(out, g_tile_phase, sizeof(unsigned long long) * 8) != cudaSuccess) return SPLINE_ECUDA;
+  const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (cudaMemcpyToSymbol(g_tile_phase, z, sizeof(z)) != cudaSuccess) return SPLINE_ECUDA;
+  return SPLINE_OK;
+}
+#endif
 }  // extern "C"

@@ -60,7 +60,10 @@ paths = {
                      (2 * s + 4) * B * m + 2 * s * B * n),
 }
 assert api.status() == 0
+only = os.environ.get("ONLY")  # comma-separated path names
 for name, (fn, nbytes) in paths.items():
+    if only and name not in only.split(","):
+        continue
     ms = timeit(fn)
     print(f"cfg{cid} {name:14s} {ms * 1e3:9.1f} us  {nbytes / ms / 1e6:8.1f} GB/s  {B * m / ms / 1e6:9.2f} Gq/s")
 assert api.status() == 0
