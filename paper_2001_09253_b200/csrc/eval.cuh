@@ -1163,6 +1163,13 @@ __device__ __forceinline__ bool sorted_run(const T *__restrict__ X, const T *__r
       int jj[V];
       int j = jc;
       int lp = 0;  // this lane's previous window slot (FORM_RECORD)
+      // the window's bounds for this step (warp-uniform; read once, not per query)
+      const int l0 = WIN ? jc - wb : 0;
+      T wlo = T(0), whi = T(0);
+      if constexpr (WIN) {
+        wlo = sw.x[l0];
+        whi = sw.x[kSortWin];
+      }
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         const T qq = qa[i];
@@ -1171,34 +1178,44 @@ __device__ __forceinline__ bool sorted_run(const T *__restrict__ X, const T *__r
         if constexpr (WIN) {
           // in the window at or after the carry: branch-free lifting over the window's knots
           // (largest l < kSortWin with x_{wb+l} <= q; +inf past x_{n-2} keeps it <= n-2-wb)
-          const int l0 = jc - wb;
-          if (qc >= sw.x[l0] && qc < sw.x[kSortWin]) {
-            // a short lift from the carry (first query) or from this lane's previous query
-            // (sorted: at most a knot or two further), verified; a miss lifts the whole window
-            const int st = (i > 0 && qc >= sw.x[lp]) ? lp : l0;
-            int l = st;
-#pragma unroll
-            for (int d = (i == 0) ? 4 : 1; d >= 1; d >>= 1) {
-              const int p = min(l + d, kSortWin - 1);
-              l = (sw.x[p] <= qc) ? p : l;
-            }
-            if (sw.x[l + 1] <= qc && l < kSortWin - 1) {  // rare: a longer jump
+          if (qc >= wlo && qc < whi) {
+            int l;
+            if (i == 0) {
+              // the lane's first query: a full 5-level lift from the carry (the lanes' first
+              // queries spread over the whole window: a short lift would miss for the upper lanes)
               l = l0;
 #pragma unroll
               for (int d = kSortWin / 2; d >= 1; d >>= 1) {
                 const int p = min(l + d, kSortWin - 1);
                 l = (sw.x[p] <= qc) ? p : l;
               }
+            } else {
+              // the next query of the lane (sorted: the same or the next interval, as a rule):
+              // one step from the previous slot, verified; a longer jump lifts from there
+              l = lp;
+              {
+                const int p = min(l + 1, kSortWin - 1);
+                l = (sw.x[p] <= qc) ? p : l;
+              }
+              if (sw.x[l + 1] <= qc && l < kSortWin - 1) {  // clustered knots: a longer jump
+#pragma unroll
+                for (int d = kSortWin / 2; d >= 1; d >>= 1) {
+                  const int p = min(l + d, kSortWin - 1);
+                  l = (sw.x[p] <= qc) ? p : l;
+                }
+              }
             }
-            lp = l;
             const WRec<T> wr = ld_wrec(&sw.r[l]);
-            const T v = cub_eval<T>(Cub<T>{wr.ih, wr.y0, wr.dy, wr.e1}, wr.e2, wr.x0, qc);
-            j = wb + l;
-            val[i] = in ? v : qnan<T>();
-            jj[i] = in ? j : -1;
-            oor |= !in;
-            if (in) jl = j;
-            continue;
+            if (qc >= wr.x0) {  // always for i = 0; for i > 0 it guards a run that is not sorted
+              lp = l;
+              const T v = cub_eval<T>(Cub<T>{wr.ih, wr.y0, wr.dy, wr.e1}, wr.e2, wr.x0, qc);
+              j = wb + l;
+              val[i] = in ? v : qnan<T>();
+              jj[i] = in ? j : -1;
+              oor |= !in;
+              if (in) jl = j;
+              continue;
+            }
           }
         }  // outside the window: the general path, from this lane's previous interval
         if constexpr (WIN && kSortedOutlineGeneral) {  // out of line: the hot window path keeps its registers
