@@ -985,7 +985,7 @@ template <typename T> __device__ __forceinline__ int warp_locate(const T *X, int
 // interval per lane, at the carried bracket and reused while the carry stays in its first half.
 constexpr int kSortWin = 32;
 #ifndef FS_SORTED_FAST
-#define FS_SORTED_FAST 0  // measured: 1497 vs 1112 us on cfg4 (A/B)
+#define FS_SORTED_FAST 1  // round 1 (3-level first lift, a range pre-check): 1497 vs 1112 us on cfg4; now the default
 #endif
 constexpr bool kSortedFast = FS_SORTED_FAST != 0;  // the warp-uniform fast path of sorted_run (WIN)
 #ifndef FS_SORTED_L1PF
@@ -1115,47 +1115,52 @@ __device__ __forceinline__ bool sorted_run(const T *__restrict__ X, const T *__r
     }
     int jl = -1;
     if constexpr (WIN && kSortedFast) {
-      // warp-uniform fast path: every query of the step lies in the window (and in range) --
-      // branch-free lifts (3 levels from the carry for a lane's first query, 1 from its previous
-      // slot after that), every slot verified against the knots; any miss anywhere in the warp
-      // redoes the step on the general path below (the same arithmetic, so the same bits)
+      // warp-uniform fast path, no per-query branches: a lane's first query lifts 5 levels from
+      // the carry (any slot of the window), each next one 2 levels from the previous slot (a
+      // sorted run rarely passes more than 3 knots between two consecutive queries); every slot
+      // is VERIFIED against the window's knots (x_{wb+l} <= q < x_{wb+l+1}), which also rejects
+      // NaN, queries below the window and a run that is not sorted.  A query in a verified slot
+      // is in range unless the window reaches the curve's end (wtail: then q <= x_{n-1} is
+      // tested).  Any miss anywhere in the warp redoes the step on the general path below (the
+      // same make_cub / cub_eval arithmetic, so the same bits).
       const int l0 = jc - wb;
-      const T xlo = sw.x[l0], xhi = sw.x[kSortWin];
-      bool fit = true;
+      const bool wtail = !(sw.x[kSortWin] <= xn);
+      T val[V];
+      int jj[V];
+      bool ok = true, soor = false;
+      int l = l0, sjl = -1;
 #pragma unroll
-      for (int i = 0; i < V; ++i) fit &= (qa[i] >= xlo) && (qa[i] < xhi) && (qa[i] <= xn);
-      if (__all_sync(0xffffffffu, fit || k >= k1)) {
-        T val[V];
-        int jj[V];
-        bool ok = true;
-        int l = l0;
+      for (int i = 0; i < V; ++i) {
+        const T qc = qa[i];
 #pragma unroll
-        for (int i = 0; i < V; ++i) {
-          const T qc = qa[i];
-#pragma unroll
-          for (int d = (i == 0) ? 4 : 1; d >= 1; d >>= 1) {
-            const int p = min(l + d, kSortWin - 1);
-            l = (sw.x[p] <= qc) ? p : l;
-          }
-          const WRec<T> wr = ld_wrec(&sw.r[l]);
-          ok &= (qc >= wr.x0) && (qc < sw.x[l + 1]);
-          val[i] = cub_eval<T>(Cub<T>{wr.ih, wr.y0, wr.dy, wr.e1}, wr.e2, wr.x0, qc);
-          jj[i] = wb + l;
+        for (int d = (i == 0) ? kSortWin / 2 : 2; d >= 1; d >>= 1) {
+          const int p = min(l + d, kSortWin - 1);
+          l = (sw.x[p] <= qc) ? p : l;
         }
-        if (__all_sync(0xffffffffu, ok || k >= k1)) {
-          if (k < k1) {
-            VecIO<T, V>::store(ob + k, val);
-            if (ib) VecIO<T, V>::store_idx(ib + k, jj);
-            jl = jj[V - 1];
-          }
-          const int jm = __reduce_max_sync(0xffffffffu, jl);
-          if (jm >= 0) jc = jm;
-#pragma unroll
-          for (int d = 0; d < PF; ++d)
-#pragma unroll
-            for (int i = 0; i < V; ++i) qr[d][i] = qr[d + 1][i];
-          continue;
+        const WRec<T> wr = ld_wrec(&sw.r[l]);
+        const T xr = sw.x[l + 1];
+        ok &= (qc >= wr.x0) & (qc < xr);
+        const bool in = !wtail || qc <= xn;
+        const T v = cub_eval<T>(Cub<T>{wr.ih, wr.y0, wr.dy, wr.e1}, wr.e2, wr.x0, qc);
+        val[i] = in ? v : qnan<T>();
+        jj[i] = in ? wb + l : -1;
+        soor |= !in;
+        sjl = in ? wb + l : sjl;
+      }
+      if (__all_sync(0xffffffffu, ok || k >= k1)) {
+        if (k < k1) {
+          VecIO<T, V>::store(ob + k, val);
+          if (ib) VecIO<T, V>::store_idx(ib + k, jj);
+          jl = sjl;
+          oor |= soor;
         }
+        const int jm = __reduce_max_sync(0xffffffffu, jl);
+        if (jm >= 0) jc = jm;
+#pragma unroll
+        for (int d = 0; d < PF; ++d)
+#pragma unroll
+          for (int i = 0; i < V; ++i) qr[d][i] = qr[d + 1][i];
+        continue;
       }
     }
     if (k < k1) {
