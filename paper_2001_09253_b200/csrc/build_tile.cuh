@@ -137,6 +137,10 @@ constexpr int kTileThreads = 256;
 #define FS_TILE_PREFETCH 1  // A/B at 3 CTAs/SM: cfg4 build 125.4 vs 133.1 us, cfg5 757 vs 840 us
 #endif
 constexpr int kTilePrefetchAhead = FS_TILE_PREFETCH;
+#ifndef FS_TILE_WARP_STAGE
+#define FS_TILE_WARP_STAGE 1
+#endif
+constexpr bool kTileWarpStage = FS_TILE_WARP_STAGE != 0;  // full tiles staged and stored per warp (no CTA barrier)
 #ifndef FS_TILE_PF_LATE
 #define FS_TILE_PF_LATE 0  // A/B: cfg4 124.9 vs 125.0 us, cfg5 788 vs 755 us (prefetch at entry kept)
 #endif
@@ -208,7 +212,10 @@ template <typename T> __device__ __forceinline__ void put6(T *o, const T (&v)[6]
 // Bottom-up.  r: this thread's leaf record (any value when t >= nleaf).  Returns the tile's
 // record in thread 0.  Every thread of the CTA must call it; ends with the warp-0 levels (no
 // trailing barrier: tile_tree_down starts with one).
-template <typename T> __device__ __forceinline__ Rec<T> tile_tree_up(Rec<T> r, int nleaf, TileTree<T> &tt, T (&k0)[3]) {
+// notok: this thread's leaf saw bad knots; bad (out): any leaf of the tile did (the CTA barrier
+// between the warp levels and warp 0's levels carries the OR).
+template <typename T>
+__device__ __forceinline__ Rec<T> tile_tree_up(Rec<T> r, int nleaf, TileTree<T> &tt, T (&k0)[3], bool notok, bool &bad) {
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   T km[3] = {T(0), T(0), T(0)};
 #pragma unroll
@@ -232,7 +239,7 @@ template <typename T> __device__ __forceinline__ Rec<T> tile_tree_up(Rec<T> r, i
     }
   }
   if (lane == 0 && t < nleaf) tt.wrec[w] = r;
-  __syncthreads();
+  bad = __syncthreads_or(notok);
   if (w == 0) {
     const int nw = (nleaf + 31) >> 5;
     r = tt.wrec[lane < nw ? lane : 0];
@@ -402,7 +409,8 @@ __device__ __forceinline__ void tile_prefetch_l2(const T *x, const T *y, int64_t
 //  FINISH : reads the tile's outer (L, R) from tile_ext[(c*ntiles + t)*2]; writes y2 rows
 //           [P, Q] to y2 + c*(row_end-row_begin) + (P - row_begin).
 // tile_solve is the body; on return (FULL / FINISH) the tile's y2 is ALSO in shared memory at
-// X[pad(i)] (pad(i) = i + i/R, all threads synchronised), which the fused build+eval kernel
+// X[pad(i)] (pad(i) = i + i/R; a warp-staged tile may return per warp: the caller syncs before
+// reading other warps' rows), which the fused build+eval kernel
 // evaluates from; y2 == nullptr skips the global store (FULL only).
 template <typename T, int R, int MODE>
 __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const T *__restrict__ x,
@@ -430,27 +438,48 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
   auto pad = [](int i) { return i + i / R; };
 
   // coalesced staging with all of a thread's loads in flight before its first store;
-  // 16-byte vectors when the tile's rows are 16-byte aligned
+  // 16-byte vectors when the tile's rows are 16-byte aligned.  A full, aligned tile is staged
+  // PER WARP (kTileWarpStage): warp w loads the rows of its own 32 leaves and goes on to their
+  // sweeps after a __syncwarp -- no CTA barrier until the merge tree, so the warps of a tile
+  // overlap their loads with one another's arithmetic.
   constexpr int VW = 16 / sizeof(T);
   using VT = typename Vec16<T>::V;
   const bool vec = ((((uintptr_t)(xc + P)) | ((uintptr_t)(yc + P))) & 15) == 0;
-  const int nvec = vec ? nrows / VW : 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool wstage = kTileWarpStage && vec && nrows == TR;
+  if (wstage) {
+    constexpr int WR = 32 * R;  // rows of a warp's leaves
+    const int r0 = wid * WR;
 #pragma unroll kTileStageUnroll
-  for (int v = threadIdx.x; v < nvec; v += NT) {
-    const VT a = __ldcs(reinterpret_cast<const VT *>(xc + P) + v);
-    const VT b = __ldcs(reinterpret_cast<const VT *>(yc + P) + v);
+    for (int v = lane; v < WR / VW; v += 32) {
+      const VT a = __ldcs(reinterpret_cast<const VT *>(xc + P + r0) + v);
+      const VT b = __ldcs(reinterpret_cast<const VT *>(yc + P + r0) + v);
 #pragma unroll
-    for (int i = 0; i < VW; ++i) {
-      X[pad(v * VW + i)] = reinterpret_cast<const T *>(&a)[i];
-      Y[pad(v * VW + i)] = reinterpret_cast<const T *>(&b)[i];
+      for (int i = 0; i < VW; ++i) {
+        X[pad(r0 + v * VW + i)] = reinterpret_cast<const T *>(&a)[i];
+        Y[pad(r0 + v * VW + i)] = reinterpret_cast<const T *>(&b)[i];
+      }
     }
-  }
+    __syncwarp();
+  } else {
+    const int nvec = vec ? nrows / VW : 0;
+#pragma unroll kTileStageUnroll
+    for (int v = threadIdx.x; v < nvec; v += NT) {
+      const VT a = __ldcs(reinterpret_cast<const VT *>(xc + P) + v);
+      const VT b = __ldcs(reinterpret_cast<const VT *>(yc + P) + v);
+#pragma unroll
+      for (int i = 0; i < VW; ++i) {
+        X[pad(v * VW + i)] = reinterpret_cast<const T *>(&a)[i];
+        Y[pad(v * VW + i)] = reinterpret_cast<const T *>(&b)[i];
+      }
+    }
 #pragma unroll 8
-  for (int e = nvec * VW + threadIdx.x; e < nrows; e += NT) {
-    X[pad(e)] = ld_stream(xc + P + e);
-    Y[pad(e)] = ld_stream(yc + P + e);
+    for (int e = nvec * VW + threadIdx.x; e < nrows; e += NT) {
+      X[pad(e)] = ld_stream(xc + P + e);
+      Y[pad(e)] = ld_stream(yc + P + e);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   TILE_MARK(0);
   // (FS_TILE_PF_LATE) the next wave's tile is prefetched once this tile's own loads are done, so
   // the two do not compete for DRAM at the start of a wave
@@ -465,6 +494,9 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
   if (l < nleaf) {
     if (l == 0) {
       if (P > 0) { xm1 = xc[P - 1]; ym1 = yc[P - 1]; }
+    } else if (wstage && lane == 0) {  // the previous warp's last row: from global memory (L2)
+      xm1 = xc[P + p - 1];
+      ym1 = yc[P + p - 1];
     } else {
       xm1 = X[pad(p - 1)];
       ym1 = Y[pad(p - 1)];
@@ -472,12 +504,18 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
     const int q = p + rows - 1;
     if (l == nleaf - 1) {
       if (P + q + 1 < n) { xq1 = xc[P + q + 1]; yq1 = yc[P + q + 1]; }
+    } else if (wstage && lane == 31) {  // the next warp's first row
+      xq1 = xc[P + q + 1];
+      yq1 = yc[P + q + 1];
     } else {
       xq1 = X[pad(q + 1)];
       yq1 = Y[pad(q + 1)];
     }
   }
-  __syncthreads();  // every neighbour value is in registers before the sweeps overwrite X/Y
+  // every neighbour value is in registers before the sweeps overwrite X/Y (per warp: a warp's
+  // sweeps touch only its own rows when it staged them itself)
+  if (wstage) __syncwarp();
+  else __syncthreads();
   TILE_MARK(1);
 
   Rec<T> r{T(0), T(0), T(0), T(0), T(0), T(0)};
@@ -490,10 +528,10 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
     r = rows == R ? leaf_sweep<T, R, false>(X, Y, v, p, rows, P, n, bc, s0, s1, xm1, ym1, xq1, yq1, ok)
                   : leaf_sweep<T, R, true>(X, Y, v, p, rows, P, n, bc, s0, s1, xm1, ym1, xq1, yq1, ok);
   }
-  const bool bad = __syncthreads_or(!ok);
   TILE_MARK(2);
   T k0[3];
-  r = tile_tree_up(r, nleaf, tt, k0);
+  bool bad;
+  r = tile_tree_up(r, nleaf, tt, k0, !ok, bad);
   TILE_MARK(3);
 
   if (MODE == TILE_REDUCE) {
@@ -549,10 +587,24 @@ __device__ __forceinline__ void tile_solve(unsigned *__restrict__ status, const 
       }
     }
   }
+  const bool vo = y2o && (((uintptr_t)y2o) & 15) == 0;
+  if (wstage && vo) {  // each warp stores its own leaves' rows (no CTA barrier)
+    __syncwarp();
+    TILE_MARK(5);
+    constexpr int WR = 32 * R;
+    const int r0 = wid * WR;
+    for (int v = lane; v < WR / VW; v += 32) {
+      VT a;
+#pragma unroll
+      for (int i = 0; i < VW; ++i) reinterpret_cast<T *>(&a)[i] = X[pad(r0 + v * VW + i)];
+      __stcs(reinterpret_cast<VT *>(y2o + r0) + v, a);
+    }
+    TILE_MARK(6);
+    return;  // (the tile's y2 is in X; a caller that reads other warps' rows syncs first)
+  }
   __syncthreads();
   TILE_MARK(5);
   if (!y2o) return;
-  const bool vo = (((uintptr_t)y2o) & 15) == 0;
   const int novec = vo ? nrows / VW : 0;
   for (int v = threadIdx.x; v < novec; v += NT) {
     VT a;

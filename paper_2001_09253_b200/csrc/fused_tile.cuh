@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(kTileThreads, FS_TILE_EVAL_MINB)
   // the solve (chunk 0 writes y2 when asked; every chunk keeps its own copy on chip)
   tile_solve<T, R, TILE_FULL>(status, x, y, n, 0, n, bc, yp1, ypn, chunk == 0 ? y2 : nullptr, nullptr, nullptr,
                               nullptr, 1, c, smem_raw);
+  __syncthreads();  // every warp's rows of y2 are in shared memory (tile_solve may end per warp)
   const T *Zs = reinterpret_cast<const T *>(smem_raw);  // y2, padded rows (tile_solve)
   SortWin<T> *wins = reinterpret_cast<SortWin<T> *>(smem_raw + tile_eval_win_offset<T, R>());
   // the chunk's queries, one contiguous run per warp (whole 32V steps)
