@@ -141,6 +141,10 @@ constexpr int kTilePrefetchAhead = FS_TILE_PREFETCH;
 #define FS_TILE_WARP_STAGE 1
 #endif
 constexpr bool kTileWarpStage = FS_TILE_WARP_STAGE != 0;  // full tiles staged and stored per warp (no CTA barrier)
+#ifndef FS_TILE_FINISH_REVERSE
+#define FS_TILE_FINISH_REVERSE 1
+#endif
+constexpr bool kTileFinishReverse = FS_TILE_FINISH_REVERSE != 0;
 #ifndef FS_TILE_PF_LATE
 #define FS_TILE_PF_LATE 0  // A/B: cfg4 124.9 vs 125.0 us, cfg5 788 vs 755 us (prefetch at entry kept)
 #endif
@@ -624,10 +628,14 @@ __global__ void __launch_bounds__(kTileThreads, FS_TILE_MINB) k_tile(unsigned *_
                                                       T *__restrict__ tile_rec, const T *__restrict__ tile_ext,
                                                       int *__restrict__ badflag, int ntiles, int pf_blocks) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  if (!kTilePrefetchLate && pf_blocks > 0 && threadIdx.x == 0)
-    tile_prefetch_l2<T, R>(x, y, n, row_begin, row_end, ntiles, (int64_t)blockIdx.x + pf_blocks, gridDim.x);
+  // K5 (FINISH) walks the tiles last to first: K3 just read them first to last, so the L2 still
+  // holds the last tiles' x, y when K5 starts
+  const int64_t nbk = gridDim.x;
+  auto logical = [&](int64_t b) { return (MODE == TILE_FINISH && kTileFinishReverse) ? nbk - 1 - b : b; };
+  if (!kTilePrefetchLate && pf_blocks > 0 && threadIdx.x == 0 && (int64_t)blockIdx.x + pf_blocks < nbk)
+    tile_prefetch_l2<T, R>(x, y, n, row_begin, row_end, ntiles, logical((int64_t)blockIdx.x + pf_blocks), nbk);
   tile_solve<T, R, MODE>(status, x, y, n, row_begin, row_end, bc, yp1, ypn, y2, tile_rec, tile_ext, badflag, ntiles,
-                         (int64_t)blockIdx.x, smem_raw, kTilePrefetchLate ? pf_blocks : 0, gridDim.x);
+                         logical((int64_t)blockIdx.x), smem_raw, kTilePrefetchLate ? pf_blocks : 0, nbk);
 }
 
 // K4: merge the per-tile records of each curve (grid = batch, one CTA per curve) and,
