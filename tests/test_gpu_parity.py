@@ -289,16 +289,21 @@ def _sorted_case(rng, dt, B, n, m, kind):
         q[:, k + 4] = np.nan
     if kind != "unsorted":
         q = np.sort(q, axis=1)  # NaN sorts to the end
+    if kind == "nearly":  # sorted but for 1% of adjacent pairs swapped: a hint that is mostly right
+        sw = rng.choice(m - 1, m // 100, replace=False)
+        q[:, sw], q[:, sw + 1] = q[:, sw + 1].copy(), q[:, sw].copy()
     return x, y, y2, q
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
 @pytest.mark.parametrize("B,n,m,kind", [(3, 4096, 65536, "dense"), (2, 129, 8 * 1024 + 8, "nan"),
                                         (5, 3, 64, "dense"), (2, 2000, 40000, "clustered"), (3, 100, 3000, "dense"),
-                                        (2, 500, 8192, "unsorted"), (1, 257, 4100, "dense")])
+                                        (2, 500, 8192, "unsorted"), (1, 257, 4100, "dense"),
+                                        (3, 1000, 40000, "nearly")])
 def test_sorted_edge_cases(api, dt, B, n, m, kind):
     """SPLINE_Q_SORTED (k_eval_sorted): ties, both ends, out of range, NaN, ragged runs, dense
-    and clustered query densities and a wrong hint all match the oracle, idx bit-exact; out is
+    and clustered query densities, a wrong hint and a mostly-right one (adjacent pairs swapped:
+    the fast path's slot verification) all match the oracle, idx bit-exact; out is
     bitwise the unsorted path's (same make_cub / cub_eval arithmetic)."""
     rng = np.random.default_rng(n * 7 + m)
     x, y, y2, q = _sorted_case(rng, dt, B, n, m, kind)
