@@ -267,13 +267,34 @@ __global__ void __launch_bounds__(kBkScThreads, FS_BK_SC_MINB) k_bucket_scatter(
 // interval is two 32-byte loads instead of six scattered 8-byte ones.
 template <typename T> struct alignas(4 * sizeof(T)) Knot { T x, y, z, pad; };
 
+// The packing also measures how far the knots stray from the evaluation's interval guess
+// f(q) = (q - x_0) (n-1) / (x_{n-1} - x_0): dev = max_j |f(x_j) - j| (atomicMax on the bits of a
+// non-negative double into *dev, which the caller zeroes).  A query whose f lies farther than dev
+// from every integer is inside the guessed interval, so k_bucket_eval loads the guess's neighbour
+// knot only for the queries within dev of a cell boundary.
 template <typename T>
 __global__ void __launch_bounds__(256) k_pack_knots(const T *__restrict__ x, const T *__restrict__ y,
-                                                    const T *__restrict__ y2, int64_t n, Knot<T> *__restrict__ kn) {
+                                                    const T *__restrict__ y2, int64_t n, Knot<T> *__restrict__ kn,
+                                                    unsigned long long *__restrict__ dev) {
+  const double x0 = (double)__ldg(x), sc = (double)(n - 1) / ((double)__ldg(x + n - 1) - x0);
+  double dmax = 0.0;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     T v[4] = {ld_stream(x + j), ld_stream(y + j), ld_stream(y2 + j), T(0)};
     if constexpr (sizeof(T) == 8) st256(kn + j, reinterpret_cast<const double(&)[4]>(v));
     else *reinterpret_cast<float4 *>(kn + j) = make_float4(v[0], v[1], v[2], v[3]);
+    const double d = fabs(((double)v[0] - x0) * sc - (double)j);
+    dmax = (d > dmax || d != d) ? d : dmax;  // NaN knots: NaN (the eval then loads the neighbour always)
+  }
+  if (dev) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double t = __shfl_xor_sync(0xffffffffu, dmax, o);
+      dmax = (t > dmax || t != t) ? t : dmax;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      const double d = (dmax != dmax || dmax > 1.0) ? 1.0 : dmax;  // >= 0.5: every query is "near a boundary"
+      atomicMax(dev, (unsigned long long)__double_as_longlong(d));
+    }
   }
 }
 template <typename T> __device__ __forceinline__ Knot<T> ld_knot(const Knot<T> *p) {
@@ -302,7 +323,8 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
                                                             int n, int64_t K, int nb, int64_t m,
                                                             const int *__restrict__ goff, const int *__restrict__ bsum,
                                                             const T *__restrict__ qs, const uint32_t *__restrict__ dest,
-                                                            T *__restrict__ os, int32_t *__restrict__ is) {
+                                                            T *__restrict__ os, int32_t *__restrict__ is,
+                                                            const unsigned long long *__restrict__ dev) {
   constexpr int U = kBkEvalPer / kBkEvalIters / kBkThreads;  // independent queries per thread in flight
   const int64_t ntiles = (m + kBkTile - 1) / kBkTile;
   const int64_t p0 = (int64_t)blockIdx.x * kBkEvalPer;
@@ -332,6 +354,12 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
   }
   const T x0 = __ldg(&kn[0].x), xn = __ldg(&kn[n - 1].x);
   const T sc = (T)(n - 1) / (xn - x0);
+  // the band around the cell boundaries where the guess can miss (k_pack_knots' deviation, plus
+  // a margin for the rounding of f in either precision); outside it only the guess's two knots
+  // are loaded.  A miss outside the band (impossible up to that margin) still takes the general
+  // correction below, so the band only decides speed.
+  const double margin = 1e-3 + 8.0 * (double)n * (sizeof(T) == 8 ? 1.1102230246251565e-16 : 5.9604644775390625e-08);
+  const T band = dev ? (T)fmin(__longlong_as_double((long long)__ldg(dev)) + margin, 0.5) : T(0.5);
   bool oor = false;
   // the block's positions in kBkEvalIters rounds of U per thread; the next round's queries and
   // destinations are loaded before this round's knots are (two streams in flight)
@@ -351,7 +379,7 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
     int j[U];
     bool in[U];
     Knot<T> ka[U], kb[U], kc[U];
-    bool up[U];
+    bool up[U], risky[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const T v = qn[u];
@@ -360,15 +388,18 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
       qq[u] = in[u] ? v : x0;
       const T f = r_mul(r_sub(qq[u], x0), sc);
       j[u] = max(0, min((int)f, n - 2));
-      up[u] = f - (T)j[u] >= T(0.5);  // which neighbour a miss of the guess most likely needs
+      const T fr = f - (T)j[u];
+      up[u] = fr >= T(0.5);  // which neighbour a miss of the guess most likely needs
+      risky[u] = !(fr > band && fr < T(1) - band);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       ka[u] = ld_knot(kn + j[u]);
       kb[u] = ld_knot(kn + j[u] + 1);
-      // the likely neighbour in the same round (kBkSpec): knot j-1 below the guess's middle,
-      // knot j+2 above it (clamped into the curve; only used when it is the right one)
-      if (kBkSpec) kc[u] = ld_knot(kn + (up[u] ? min(j[u] + 2, n - 1) : max(j[u] - 1, 0)));
+      // the likely neighbour in the same round (kBkSpec), for the queries near a cell boundary:
+      // knot j-1 below the guess's middle, knot j+2 above it (clamped into the curve; only used
+      // when it is the right one)
+      if (kBkSpec && risky[u]) kc[u] = ld_knot(kn + (up[u] ? min(j[u] + 2, n - 1) : max(j[u] - 1, 0)));
     }
     if (it + 1 < kBkEvalIters) {
 #pragma unroll
@@ -380,7 +411,7 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (kBkSpec && !(ka[u].x <= qq[u] && (qq[u] < kb[u].x || j[u] == n - 2))) {
+      if (kBkSpec && risky[u] && !(ka[u].x <= qq[u] && (qq[u] < kb[u].x || j[u] == n - 2))) {
         if (!up[u] && ka[u].x > qq[u] && j[u] > 0 && kc[u].x <= qq[u]) {  // one interval down
           j[u] -= 1;
           kb[u] = ka[u];

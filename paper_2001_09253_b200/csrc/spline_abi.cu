@@ -51,6 +51,10 @@ constexpr int64_t kFuseMaxWork = int64_t(1) << 17;
 constexpr bool kBuildEvalWarp = FS_BUILD_EVAL_WARP != 0;  // spline_build_eval: k_build_eval_warp for many K1h-sized curves
 constexpr int kNoFusedStaged = 1 << 30;  // internal: automatic path, but not k_fused_staged
 constexpr int kEvalNoBucket = SPLINE_NO_BUCKET;  // spline_eval: the record-gather path for long curves
+#ifndef FS_BK_BAND
+#define FS_BK_BAND 1
+#endif
+constexpr bool kBkBand = FS_BK_BAND != 0;  // bucketed eval: the neighbour knot only near a cell boundary
 #ifndef FS_SPLIT_OVERLAP
 #define FS_SPLIT_OVERLAP 0  // A/B: 1358 vs 1283 us on cfg4 -- the concurrent build slows the evaluation more
 #endif
@@ -604,9 +608,9 @@ int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, in
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
   const size_t bk = al(sizeof(Knot<T>) * (size_t)n), bq = al(sizeof(T) * (size_t)m), bd = al(4 * (size_t)m);
   const size_t bp = al(2 * (size_t)m), bi = idx ? al(4 * (size_t)m) : 0;
-  const size_t bc = al(4 * (size_t)L), bs = al(4 * (size_t)nblk);
+  const size_t bc = al(4 * (size_t)L), bs = al(4 * (size_t)nblk), bv = al(sizeof(unsigned long long));
   char *ws = nullptr;
-  if (int rc = ws_alloc((void **)&ws, bk + 2 * bq + bd + bp + bi + bc + bs, st)) return rc;
+  if (int rc = ws_alloc((void **)&ws, bk + 2 * bq + bd + bp + bi + bc + bs + bv, st)) return rc;
   char *p = ws;
   auto take = [&](size_t b) { char *r = p; p += b; return r; };
   Knot<T> *kn = (Knot<T> *)take(bk);
@@ -617,6 +621,7 @@ int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, in
   int32_t *is = idx ? (int32_t *)take(bi) : nullptr;
   int *cnt = (int *)take(bc);
   int *bsum = (int *)take(bs);
+  unsigned long long *dev = (unsigned long long *)take(bv);  // the knots' deviation from the guess
   int rc = set_smem(k_bucket_scatter<T>, bucket_scatter_smem<T>());
   if (!rc) rc = set_smem(k_bucket_gather<T>, bucket_gather_smem<T>());
   // the knot packing (bandwidth-bound) runs on an internal stream beside the counting and the
@@ -629,7 +634,8 @@ int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, in
   if (!rc) rc = cuda_rc(cudaStreamWaitEvent(hs->s[0], ev.start, 0));
   if (!rc) {
     const int64_t pg = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
-    k_pack_knots<T><<<(unsigned)pg, 256, 0, hs->s[0]>>>(x, y, y2, n, kn);
+    rc = cuda_rc(cudaMemsetAsync(dev, 0, sizeof(unsigned long long), hs->s[0]));
+    if (!rc) k_pack_knots<T><<<(unsigned)pg, 256, 0, hs->s[0]>>>(x, y, y2, n, kn, kBkBand ? dev : nullptr);
     rc = launch_rc();
   }
   if (!rc) rc = cuda_rc(cudaEventRecord(ev.ready, hs->s[0]));
@@ -642,7 +648,7 @@ int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, in
                                                                                            bsum, qs, dest, perm);
     cudaStreamWaitEvent(st, ev.ready, 0);  // the packed knots
     k_bucket_eval<T><<<(unsigned)neval, kBkThreads, 0, st>>>(tl_status, kn, (int)n, K, nb, m, cnt, bsum, qs, dest, os,
-                                                             is);
+                                                             is, kBkBand ? dev : nullptr);
     k_bucket_gather<T><<<(unsigned)ntiles, kBkGaThreads, bucket_gather_smem<T>(), st>>>(os, is, perm, m, out, idx);
     rc = launch_rc();
   }
