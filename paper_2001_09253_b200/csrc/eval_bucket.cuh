@@ -57,26 +57,34 @@ constexpr int kBkEvalPer = kBkThreads * FS_BK_EVAL_U * kBkEvalIters;  // queries
 constexpr int kScanBlock = 4096;      // elements per block of the run-offset scan (4 per thread)
 
 // bucket of q: b in [0, nb) with x_{bK} <= q < x_{(b+1)K} (the last bucket ends at x_{n-1}
-// inclusive); nb for q outside [x_0, x_{n-1}] or NaN.  xb[0..nb-1] = x_{bK}, xb[nb] = x_{n-1}.
-// From the guess g = (q - x_0) sb (exact up to a step on near-uniform grids), corrected by
-// comparisons with the boundaries -- two steps each way, then a bisection: exact on any grid.
-template <typename T> __device__ __forceinline__ int bucket_of_q(const T *xb, int nb, T q, T sb) {
-  if (!(q >= xb[0] && q <= xb[nb])) return nb;
-  const int g = max(0, min((int)((q - xb[0]) * sb), nb - 1));
-  if (xb[g] <= q && (q < xb[g + 1] || g == nb - 1)) return g;  // the guess holds (near-uniform grids)
-  int lo = 0, hi = nb;  // xb[lo] <= q, and hi == nb or xb[hi] > q
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (xb[mid] <= q) lo = mid;
-    else hi = mid;
+// inclusive); nb for q outside [x_0, x_{n-1}] or NaN.  xb[0..nb-1] = x_{bK}, xb[nb] = x_{n-1};
+// xp[b] = {xb[b], xb[b+1]} (one vector load for the guess's test); lo = x_0, hi = x_{n-1} in
+// registers.  From the guess g = (q - x_0) sb (exact up to a step on near-uniform grids),
+// verified against the boundaries, else a bisection: exact on any grid.
+template <typename T> struct alignas(2 * sizeof(T)) BkPair { T a, b; };
+template <typename T>
+__device__ __forceinline__ int bucket_of_q(const T *xb, const BkPair<T> *xp, int nb, T q, T lo, T hi, T sb) {
+  if (!(q >= lo && q <= hi)) return nb;
+  const int g = max(0, min((int)((q - lo) * sb), nb - 1));
+  const BkPair<T> pr = xp[g];
+  if (pr.a <= q && (q < pr.b || g == nb - 1)) return g;  // the guess holds (near-uniform grids)
+  int l = 0, h = nb;  // xb[l] <= q, and h == nb or xb[h] > q
+  while (h - l > 1) {
+    const int mid = (l + h) >> 1;
+    if (xb[mid] <= q) l = mid;
+    else h = mid;
   }
-  return lo;
+  return l;
 }
 
-// The chunk boundaries and the bucket guess scale, in shared memory.
+// The chunk boundaries (and their pairs) in shared memory; returns the bucket guess scale.
 template <typename T>
-__device__ __forceinline__ T load_bounds(T *xb, const T *__restrict__ x, int n, int64_t K, int nb) {
-  for (int b = threadIdx.x; b <= nb; b += blockDim.x) xb[b] = (b < nb) ? __ldg(x + (int64_t)b * K) : __ldg(x + n - 1);
+__device__ __forceinline__ T load_bounds(T *xb, BkPair<T> *xp, const T *__restrict__ x, int n, int64_t K, int nb) {
+  for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+    const T v = (b < nb) ? __ldg(x + (int64_t)b * K) : __ldg(x + n - 1);
+    xb[b] = v;
+    if (b < nb) xp[b] = BkPair<T>{v, (b + 1 < nb) ? __ldg(x + (int64_t)(b + 1) * K) : __ldg(x + n - 1)};
+  }
   return (T)(n - 1) / ((__ldg(x + n - 1) - __ldg(x)) * (T)K);  // buckets per unit of x (a guess)
 }
 
@@ -86,12 +94,14 @@ __global__ void __launch_bounds__(kBkScThreads, FS_BK_CNT_MINB) k_bucket_count(c
                                                                   int *__restrict__ cnt) {
   pdl_wait();
   __shared__ T xb[kBkMaxBuckets + 1];
+  __shared__ BkPair<T> xp[kBkMaxBuckets];
   __shared__ int c[kBkMaxBuckets + 1];
   const int64_t ntiles = (m + kBkTile - 1) / kBkTile;
   const int64_t tile = blockIdx.x;
   const int64_t q0 = tile * kBkTile;
   const int nq = (int)min64(kBkTile, m - q0);
-  const T sb = load_bounds(xb, x, n, K, nb);
+  const T sb = load_bounds(xb, xp, x, n, K, nb);
+  const T lo = __ldg(x), hi = __ldg(x + n - 1);
   for (int b = threadIdx.x; b <= nb; b += kBkScThreads) c[b] = 0;
   T qv[kBkPerThread];
 #pragma unroll
@@ -102,7 +112,7 @@ __global__ void __launch_bounds__(kBkScThreads, FS_BK_CNT_MINB) k_bucket_count(c
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < kBkPerThread; ++u)
-    if (u * kBkScThreads + (int)threadIdx.x < nq) atomicAdd(&c[bucket_of_q(xb, nb, qv[u], sb)], 1);
+    if (u * kBkScThreads + (int)threadIdx.x < nq) atomicAdd(&c[bucket_of_q(xb, xp, nb, qv[u], lo, hi, sb)], 1);
   __syncthreads();
   for (int b = threadIdx.x; b <= nb; b += kBkScThreads) cnt[(int64_t)b * ntiles + tile] = c[b];
 }
@@ -181,7 +191,8 @@ __global__ void __launch_bounds__(1024) k_scan_top(int *__restrict__ bsum, int n
 }
 
 template <typename T> constexpr size_t bucket_scatter_smem() {
-  return sizeof(T) * (kBkTile + kBkMaxBuckets + 1) + sizeof(int) * (2 * kBkMaxBuckets + 3) + 2 * 2 * kBkTile;
+  return sizeof(T) * (kBkTile + kBkMaxBuckets + 1) + sizeof(BkPair<T>) * kBkMaxBuckets +
+         sizeof(int) * (2 * kBkMaxBuckets + 3) + 2 * 2 * kBkTile;
 }
 template <typename T> constexpr size_t bucket_gather_smem() { return (sizeof(T) + 4) * kBkTile; }
 
@@ -194,7 +205,8 @@ __global__ void __launch_bounds__(kBkScThreads, FS_BK_SC_MINB) k_bucket_scatter(
                                                                     uint16_t *__restrict__ perm) {
   extern __shared__ __align__(16) unsigned char bk_smem[];  // bucket_scatter_smem<T>() bytes
   T *sq = reinterpret_cast<T *>(bk_smem);                          // [kBkTile]
-  T *xb = sq + kBkTile;                                            // [kBkMaxBuckets + 1]
+  BkPair<T> *xp = reinterpret_cast<BkPair<T> *>(sq + kBkTile);  // [kBkMaxBuckets] (16/8-byte aligned)
+  T *xb = reinterpret_cast<T *>(xp + kBkMaxBuckets);               // [kBkMaxBuckets + 1]
   int *c = reinterpret_cast<int *>(xb + kBkMaxBuckets + 1);        // counts, then the run starts
   int *gb = c + kBkMaxBuckets + 2;                                 // global base of each run
   uint16_t *sp = reinterpret_cast<uint16_t *>(gb + kBkMaxBuckets + 1);
@@ -204,7 +216,8 @@ __global__ void __launch_bounds__(kBkScThreads, FS_BK_SC_MINB) k_bucket_scatter(
   const int64_t tile = blockIdx.x;
   const int64_t q0 = tile * kBkTile;
   const int nq = (int)min64(kBkTile, m - q0);
-  const T sb = load_bounds(xb, x, n, K, nb);
+  const T sb = load_bounds(xb, xp, x, n, K, nb);
+  const T lo = __ldg(x), hi = __ldg(x + n - 1);
   for (int b = tid; b <= nb + 1; b += kBkScThreads) c[b] = 0;
   for (int b = tid; b <= nb; b += kBkScThreads) {
     const int64_t e = (int64_t)b * ntiles + tile;
@@ -221,7 +234,7 @@ __global__ void __launch_bounds__(kBkScThreads, FS_BK_SC_MINB) k_bucket_scatter(
 #pragma unroll
   for (int u = 0; u < kBkPerThread; ++u) {
     if (u * kBkScThreads + tid < nq) {
-      bk[u] = bucket_of_q(xb, nb, qv[u], sb);
+      bk[u] = bucket_of_q(xb, xp, nb, qv[u], lo, hi, sb);
       rk[u] = atomicAdd(&c[bk[u]], 1);  // rank inside the run (any order: results go back by perm)
     }
   }
