@@ -43,7 +43,7 @@ namespace {
 
 constexpr int kK1MaxN = 128;
 // spline_build_eval's automatic choice: the fused warp-specialised kernel only for
-// launch-latency-sized problems (measured: tools/cmp_paths.py; K1h + curvewarp win from ~2^18)
+// launch-latency-sized problems (measured with spline_build_eval on scaled configs, round 1: K1h + curvewarp win from ~2^18)
 constexpr int64_t kFuseMaxWork = int64_t(1) << 17;
 #ifndef FS_BUILD_EVAL_WARP
 #define FS_BUILD_EVAL_WARP 1
