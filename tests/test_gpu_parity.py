@@ -486,6 +486,36 @@ def test_long_curve_bucketed_eval(api, n, m):
     api.status()
 
 
+@pytest.mark.parametrize("grid", ["jitter40", "exp"])
+def test_long_curve_bucketed_eval_nonuniform(api, grid):
+    """The bucketed eval on long curves whose knots stray far from the interval guess: a grid
+    jittered by +-40% of a cell (the packing's deviation band covers ~80% of the queries) and
+    exponential gaps (the guess misses by thousands of intervals: the general correction) -- idx
+    bit for bit against the oracle, out within tolerance, bitwise the record-gather path."""
+    rng = np.random.default_rng(11 if grid == "exp" else 12)
+    n, m = (1 << 23) + 5, (1 << 21) + 3
+    if grid == "exp":
+        x = np.cumsum(rng.exponential(1.0, n))
+    else:
+        x = np.arange(n, dtype=np.float64) + rng.uniform(-0.4, 0.4, n)
+    x = (x - x[0]) / (x[-1] - x[0])
+    y = np.cumsum(rng.normal(0.0, 1.0 / np.sqrt(n), n))
+    y2 = rng.normal(0.0, 1.0, n)
+    q = rng.uniform(-0.01, 1.01, m)
+    q[:4] = x[0], x[-1], x[n // 2], np.nan
+    x, y, y2, q = x[None], y[None], y2[None], q[None]
+    out_ref, idx_ref, nbad = oracle.evaluate(x, y, y2, q, nthreads=16)
+    t = parity.to_dev
+    api.status()
+    out, idx = api.evaluate(t(x), t(y), t(y2), t(q), 0)
+    assert api.status() == api.STATUS_Q_OUT_OF_RANGE and nbad > 0
+    np.testing.assert_array_equal(idx.cpu().numpy(), idx_ref)
+    assert parity.out_rel_err(out.cpu().numpy(), out_ref, y).max() <= 1e-12
+    out_r, idx_r = api.evaluate(t(x), t(y), t(y2), t(q), api.NO_BUCKET)
+    api.status()
+    assert torch.equal(idx, idx_r) and torch.equal(out.view(torch.int8), out_r.view(torch.int8))
+
+
 @pytest.mark.parametrize("world,n,bc", [(2, 300001, 0), (8, (1 << 20) + 5, 3), (3, 4096 * 7, 1)])
 def test_recompute_build_emulated_ranks(api, world, n, bc):
     """§8(e)(ii) recompute-instead-of-gather, G ranks emulated on one GPU: each rank's tile records
