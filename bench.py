@@ -404,9 +404,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test tooling only (tests/test_gpu_bench.py): FS_BENCH_BACKEND=gloo with FS_BENCH_ONE_GPU=1 runs
+    # the N-rank orchestration with every rank on device 0 -- a functional check of the multi-rank
+    # path on a one-GPU box, never a measurement (ranks sharing a GPU time each other)
+    backend = os.environ.get("FS_BENCH_BACKEND", "nccl")
+    if os.environ.get("FS_BENCH_ONE_GPU"):
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 

@@ -45,3 +45,29 @@ def test_bench_reference_arm():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+@pytest.mark.parametrize("cfg", ["2", "5"])
+def test_bench_two_ranks_functional(cfg):
+    """The N > 1 orchestration of bench.py (torchrun, 2 ranks) as a FUNCTIONAL check on a one-GPU
+    box: both ranks on device 0 over gloo (FS_BENCH_BACKEND / FS_BENCH_ONE_GPU, test tooling);
+    rank 0 alone prints one line, n_gpus = 2, the batched configs strong-scaled.  Not a
+    measurement (the ranks share the GPU)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, FS_BENCH_BACKEND="gloo", FS_BENCH_ONE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--config", cfg, "--steps", "3", "--warmup", "3", "--no-e2e"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, (r.stdout[-1500:], r.stderr[-3000:])
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] in ("strong", "weak")
+    if cfg == "2":
+        assert d["scaling"] == "strong"
