@@ -15,17 +15,18 @@
 //                       of every (bucket, tile) run (block-level scan + a scan of block sums).
 //   A2 k_bucket_scatter the same buckets again, a tile-local counting sort in shared memory,
 //                       each run written to its global position (qs: queries bucket-major) and
-//                       each query's tile slot (perm, u16, tile-local order) plus the tile's run
-//                       table (global base, tile-local start per bucket).
+//                       the query of each tile slot (perm, u16, tile-local order).
 //   B  k_bucket_eval    ONE flat pass over qs in bucket-major order (blocks dispatched in
 //                       order, so the GPU works on ~one chunk at a time): interpolation guess,
 //                       galloping correction (the locate rule's answer on any grid), Eq.
 //                       nr_formula in the factored form (bitwise the other eval kernels');
-//                       results in place of qs.  Each block prefetches
-//                       (cp.async.bulk.prefetch.L2) its share of the NEXT chunk's knots.
-//   C  k_bucket_gather  per tile: its runs read back (contiguous runs) into shared memory in
-//                       tile-slot order, scattered to query order through perm, written
-//                       coalesced.
+//                       results in the same bucket-major order (coalesced).  Each block
+//                       prefetches (cp.async.bulk.prefetch.L2) its share of the NEXT chunk's knots.
+//   C  k_bucket_gather  per tile: its runs found from the scanned counts (run (b, t) spans
+//                       [start(b ntiles + t), start(b ntiles + t + 1)); its tile-local slots
+//                       start at the sum of the tile's earlier runs), read back (contiguous
+//                       runs), scattered to query order through perm in shared memory, written
+//                       coalesced.  No per-query destination array.
 //
 // Algorithmic bytes are those of any eval ((2s+4) B/query + 3 s B/knot); this path moves the
 // q-sized arrays a few more times, but every access is a stream, a contiguous run or an L2 hit
@@ -194,14 +195,16 @@ template <typename T> constexpr size_t bucket_scatter_smem() {
   return sizeof(T) * (kBkTile + kBkMaxBuckets + 1) + sizeof(BkPair<T>) * kBkMaxBuckets +
          sizeof(int) * (2 * kBkMaxBuckets + 3) + 2 * 2 * kBkTile;
 }
-template <typename T> constexpr size_t bucket_gather_smem() { return (sizeof(T) + 4) * kBkTile; }
+template <typename T> constexpr size_t bucket_gather_smem() {
+  return (sizeof(T) + 4) * kBkTile + (sizeof(int64_t) + sizeof(int)) * (kBkMaxBuckets + 1);
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kBkScThreads, FS_BK_SC_MINB) k_bucket_scatter(const T *__restrict__ x, int n, int64_t K, int nb,
                                                                     const T *__restrict__ q, int64_t m,
                                                                     const int *__restrict__ goff,
                                                                     const int *__restrict__ bsum,
-                                                                    T *__restrict__ qs, uint32_t *__restrict__ dest,
+                                                                    T *__restrict__ qs,
                                                                     uint16_t *__restrict__ perm) {
   extern __shared__ __align__(16) unsigned char bk_smem[];  // bucket_scatter_smem<T>() bytes
   T *sq = reinterpret_cast<T *>(bk_smem);                          // [kBkTile]
@@ -270,8 +273,7 @@ __global__ void __launch_bounds__(kBkScThreads, FS_BK_SC_MINB) k_bucket_scatter(
     const int b = sbk[s];
     const int64_t p = gb[b] + (s - c[b]);  // consecutive slots of a run: consecutive addresses
     st_stream(qs + p, sq[s]);
-    dest[p] = (uint32_t)(q0 + s);          // where the result goes: the tile's slot s
-    perm[q0 + s] = sp[s];
+    perm[q0 + s] = sp[s];                  // the query of the tile's slot s
   }
 }
 
@@ -323,7 +325,8 @@ template <typename T> __device__ __forceinline__ Knot<T> ld_knot(const Knot<T> *
   return k;
 }
 
-// The flat evaluation of the bucket-major queries; results to the tile slots named by dest.
+// The flat evaluation of the bucket-major queries; results in the same bucket-major order
+// (coalesced; k_bucket_gather finds each tile's runs from the scan of the run counts).
 #ifndef FS_BK_SPEC
 #define FS_BK_SPEC 1  // A/B cfg5 eval: 8.38 vs 9.13 ms without (a miss of the guess costs no second round)
 #endif
@@ -335,7 +338,7 @@ template <typename T>
 __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(unsigned *__restrict__ status, const Knot<T> *__restrict__ kn,
                                                             int n, int64_t K, int nb, int64_t m,
                                                             const int *__restrict__ goff, const int *__restrict__ bsum,
-                                                            const T *__restrict__ qs, const uint32_t *__restrict__ dest,
+                                                            const T *__restrict__ qs,
                                                             T *__restrict__ os, int32_t *__restrict__ is,
                                                             const unsigned long long *__restrict__ dev) {
   constexpr int U = kBkEvalPer / kBkEvalIters / kBkThreads;  // independent queries per thread in flight
@@ -375,20 +378,18 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
   const T band = dev ? (T)fmin(__longlong_as_double((long long)__ldg(dev)) + margin, 0.5) : T(0.5);
   bool oor = false;
   // the block's positions in kBkEvalIters rounds of U per thread; the next round's queries and
-  // destinations are loaded before this round's knots are (two streams in flight)
+  // the next round's queries are loaded before this round's knots are (two streams in flight)
   T qn[U];
-  uint32_t dn[U];
+
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int64_t p = p0 + u * kBkThreads + threadIdx.x;
     qn[u] = (p < m) ? ld_stream(qs + p) : x0;
-    dn[u] = (p < m) ? __ldcs(dest + p) : 0u;
   }
   for (int it = 0; it < kBkEvalIters; ++it) {
     const int64_t pb = p0 + (int64_t)it * kBkThreads * U;
     if (pb >= m) break;
     T qq[U];
-    uint32_t dd[U];
     int j[U];
     bool in[U];
     Knot<T> ka[U], kb[U], kc[U];
@@ -396,7 +397,6 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const T v = qn[u];
-      dd[u] = dn[u];
       in[u] = (v >= x0) && (v <= xn);
       qq[u] = in[u] ? v : x0;
       const T f = r_mul(r_sub(qq[u], x0), sc);
@@ -419,8 +419,7 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
       for (int u = 0; u < U; ++u) {
         const int64_t p = pb + (int64_t)kBkThreads * U + u * kBkThreads + threadIdx.x;
         qn[u] = (p < m) ? ld_stream(qs + p) : x0;
-        dn[u] = (p < m) ? __ldcs(dest + p) : 0u;
-      }
+          }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -458,8 +457,8 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
       const int64_t p = pb + u * kBkThreads + threadIdx.x;
       if (p < m) {
         const T v = nr_interp(qq[u], ka[u].x, kb[u].x, ka[u].y, kb[u].y, ka[u].z, kb[u].z);
-        st_stream(os + dd[u], in[u] ? v : qnan<T>());
-        if (is) st_stream(is + dd[u], in[u] ? j[u] : -1);
+        st_stream(os + p, in[u] ? v : qnan<T>());
+        if (is) st_stream(is + p, in[u] ? j[u] : -1);
         oor |= !in[u];
       }
     }
@@ -470,28 +469,68 @@ __global__ void __launch_bounds__(kBkThreads, FS_BK_EVAL_MINB) k_bucket_eval(uns
 #ifndef FS_BK_GATHER_THREADS
 #define FS_BK_GATHER_THREADS 512
 #endif
-constexpr int kBkGaThreads = FS_BK_GATHER_THREADS;  // the gather's CTA (kBkTile / kBkGaThreads slots per thread)
+constexpr int kBkGaThreads = FS_BK_GATHER_THREADS;  // the gather's CTA
+// Tile t's results sit in nb + 1 runs of the bucket-major arrays: run (b, t) starts at the
+// scanned offset of cnt entry e = b ntiles + t and ends where entry e + 1 starts (the scan is
+// exclusive and bucket-major, so runs of one bucket follow each other tile by tile); inside
+// the tile, bucket b's slots start at the sum of the tile's earlier runs -- the tile-local
+// counting sort of k_bucket_scatter.  The gather copies the runs back through perm (slot ->
+// query) into shared memory and writes the tile's results in query order, coalesced.
 template <typename T>
 __global__ void __launch_bounds__(kBkGaThreads, 2048 / kBkGaThreads) k_bucket_gather(const T *__restrict__ os, const int32_t *__restrict__ is,
                                                                    const uint16_t *__restrict__ perm, int64_t m,
-                                                                   T *__restrict__ out, int32_t *__restrict__ idx) {
+                                                                   const int *__restrict__ goff, const int *__restrict__ bsum,
+                                                                   int nb, T *__restrict__ out, int32_t *__restrict__ idx) {
   extern __shared__ __align__(16) unsigned char bk_smem[];  // bucket_gather_smem<T>() bytes
   T *so = reinterpret_cast<T *>(bk_smem);                          // [kBkTile]
   int32_t *si = reinterpret_cast<int32_t *>(so + kBkTile);         // [kBkTile]
-  const int64_t q0 = (int64_t)blockIdx.x * kBkTile;
+  int64_t *gs = reinterpret_cast<int64_t *>(si + kBkTile);        // [kBkMaxBuckets + 1] global run starts
+  int *ls = reinterpret_cast<int *>(gs + kBkMaxBuckets + 1);       // [kBkMaxBuckets + 1] tile-local run starts
+  const int64_t ntiles = (m + kBkTile - 1) / kBkTile;
+  const int64_t tile = blockIdx.x;
+  const int64_t q0 = tile * kBkTile;
   const int nq = (int)min64(kBkTile, m - q0);
-  // the tile's results in slot order -> query order through perm, then coalesced stores
+  const int64_t L = (int64_t)(nb + 1) * ntiles;
+  auto start = [&](int64_t e) -> int64_t { return e >= L ? m : (int64_t)goff[e] + bsum[e / kScanBlock]; };
+  const int tid = threadIdx.x;
+  for (int b = tid; b <= nb; b += kBkGaThreads) {
+    const int64_t e = (int64_t)b * ntiles + tile;
+    const int64_t g = start(e);
+    gs[b] = g;
+    ls[b] = (int)(start(e + 1) - g);  // the run's length (its end: the next entry's start)
+  }
+  __syncthreads();
+  if (tid < 32) {  // tile-local starts: exclusive scan of the run lengths (one warp)
+    int carry = 0;
+    for (int b0 = 0; b0 <= nb; b0 += 32) {
+      const int b = b0 + tid;
+      const int v = (b <= nb) ? ls[b] : 0;
+      int sc = v;
 #pragma unroll
-  for (int u = 0; u < (kBkTile / kBkGaThreads); ++u) {
-    const int s = u * kBkGaThreads + threadIdx.x;
-    if (s < nq) {
-      const int i = perm[q0 + s];
-      so[i] = ld_stream(os + q0 + s);
-      if (idx) si[i] = __ldcs(is + q0 + s);
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t2 = __shfl_up_sync(0xffffffffu, sc, o);
+        if (tid >= o) sc += t2;
+      }
+      if (b <= nb) ls[b] = carry + sc - v;
+      carry += __shfl_sync(0xffffffffu, sc, 31);
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nq; i += kBkGaThreads) {
+  // each warp copies whole runs (buckets w, w + 16, ...): coalesced reads of the run, the
+  // results land at their queries' places in shared memory
+  const int lane = tid & 31, w = tid >> 5;
+  for (int b = w; b <= nb; b += kBkGaThreads / 32) {
+    const int64_t g = gs[b];
+    const int s0 = ls[b];  // (bucket b's slots in the tile: [s0, s0 + run length))
+    const int ln = (b < nb ? ls[b + 1] : nq) - s0;
+    for (int r = lane; r < ln; r += 32) {
+      const int i = perm[q0 + s0 + r];
+      so[i] = ld_stream(os + g + r);
+      if (idx) si[i] = __ldcs(is + g + r);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nq; i += kBkGaThreads) {
     st_stream(out + q0 + i, so[i]);
     if (idx) st_stream(idx + q0 + i, si[i]);
   }

@@ -606,17 +606,16 @@ int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, in
       m >= (int64_t(1) << 32))
     return SPLINE_EINVAL;
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  const size_t bk = al(sizeof(Knot<T>) * (size_t)n), bq = al(sizeof(T) * (size_t)m), bd = al(4 * (size_t)m);
+  const size_t bk = al(sizeof(Knot<T>) * (size_t)n), bq = al(sizeof(T) * (size_t)m);
   const size_t bp = al(2 * (size_t)m), bi = idx ? al(4 * (size_t)m) : 0;
   const size_t bc = al(4 * (size_t)L), bs = al(4 * (size_t)nblk), bv = al(sizeof(unsigned long long));
   char *ws = nullptr;
-  if (int rc = ws_alloc((void **)&ws, bk + 2 * bq + bd + bp + bi + bc + bs + bv, st)) return rc;
+  if (int rc = ws_alloc((void **)&ws, bk + 2 * bq + bp + bi + bc + bs + bv, st)) return rc;
   char *p = ws;
   auto take = [&](size_t b) { char *r = p; p += b; return r; };
   Knot<T> *kn = (Knot<T> *)take(bk);
   T *qs = (T *)take(bq);
   T *os = (T *)take(bq);
-  uint32_t *dest = (uint32_t *)take(bd);
   uint16_t *perm = (uint16_t *)take(bp);
   int32_t *is = idx ? (int32_t *)take(bi) : nullptr;
   int *cnt = (int *)take(bc);
@@ -645,11 +644,12 @@ int eval_bucketed(const T *x, const T *y, const T *y2, int64_t n, const T *q, in
     k_scan_blocks<<<(unsigned)nblk, 1024, 0, st>>>(cnt, L, bsum);
     k_scan_top<<<1, 1024, 0, st>>>(bsum, (int)nblk);
     k_bucket_scatter<T><<<(unsigned)ntiles, kBkScThreads, bucket_scatter_smem<T>(), st>>>(x, (int)n, K, nb, q, m, cnt,
-                                                                                           bsum, qs, dest, perm);
+                                                                                           bsum, qs, perm);
     cudaStreamWaitEvent(st, ev.ready, 0);  // the packed knots
-    k_bucket_eval<T><<<(unsigned)neval, kBkThreads, 0, st>>>(tl_status, kn, (int)n, K, nb, m, cnt, bsum, qs, dest, os,
+    k_bucket_eval<T><<<(unsigned)neval, kBkThreads, 0, st>>>(tl_status, kn, (int)n, K, nb, m, cnt, bsum, qs, os,
                                                              is, kBkBand ? dev : nullptr);
-    k_bucket_gather<T><<<(unsigned)ntiles, kBkGaThreads, bucket_gather_smem<T>(), st>>>(os, is, perm, m, out, idx);
+    k_bucket_gather<T><<<(unsigned)ntiles, kBkGaThreads, bucket_gather_smem<T>(), st>>>(os, is, perm, m, cnt, bsum, nb,
+                                                                                         out, idx);
     rc = launch_rc();
   }
   cudaFreeAsync(ws, st);
