@@ -628,6 +628,7 @@ __global__ void __launch_bounds__(kTileThreads, FS_TILE_MINB) k_tile(unsigned *_
                                                       T *__restrict__ tile_rec, const T *__restrict__ tile_ext,
                                                       int *__restrict__ badflag, int ntiles, int pf_blocks) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  pdl_wait();  // (programmatic launch after K4: its (L, R) per tile; x, y from any earlier kernel)
   // K5 (FINISH) walks the tiles last to first: K3 just read them first to last, so the L2 still
   // holds the last tiles' x, y when K5 starts
   const int64_t nbk = gridDim.x;
@@ -657,6 +658,8 @@ __global__ void __launch_bounds__(kTopThreads) k4_top(const T *__restrict__ recs
                                                       T *__restrict__ root_out, T *__restrict__ foldq,
                                                       int64_t ntot) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  pdl_trigger();  // the next kernel (K4's next phase, K5) may be launched now; it waits for this one
+  pdl_wait();     // the records of the previous kernel (programmatic launch)
   Rec<T> *rec = reinterpret_cast<Rec<T> *>(smem_raw);
   T *mi = reinterpret_cast<T *>(rec + kTopThreads);
   T *ext = reinterpret_cast<T *>(rec);

@@ -51,6 +51,10 @@ constexpr int64_t kFuseMaxWork = int64_t(1) << 17;
 constexpr bool kBuildEvalWarp = FS_BUILD_EVAL_WARP != 0;  // spline_build_eval: k_build_eval_warp for many K1h-sized curves
 constexpr int kNoFusedStaged = 1 << 30;  // internal: automatic path, but not k_fused_staged
 constexpr int kEvalNoBucket = SPLINE_NO_BUCKET;  // spline_eval: the record-gather path for long curves
+#ifndef FS_TOP_PDL
+#define FS_TOP_PDL 1
+#endif
+constexpr bool kTopPdl = FS_TOP_PDL != 0;  // K4's phases and K5 launched programmatically (launch latency hidden)
 #ifndef FS_BK_BAND
 #define FS_BK_BAND 1
 #endif
@@ -288,6 +292,8 @@ template <typename T> int launch_top(const T *recs, int ntiles, int64_t batch, i
   auto kern = k4_top<T>;
   const size_t sm = top_smem_bytes<T>();
   if (int rc = set_smem(kern, sm)) return rc;
+  if (kTopPdl) return launch_pdl(kern, dim3((unsigned)batch), dim3(kTopThreads), sm, st, recs, ntiles, up_only, root_ext,
+                                 tile_ext, root_out, foldq, ntot);
   kern<<<(unsigned)batch, kTopThreads, sm, st>>>(recs, ntiles, up_only, root_ext, tile_ext, root_out, foldq, ntot);
   return launch_rc();
 }
@@ -315,6 +321,10 @@ int launch_tile_part(const T *x, const T *y, int64_t n, int64_t rb, int64_t re, 
   const size_t sm = tile_smem_bytes<T, R>();
   if (int rc = set_smem(kern, sm)) return rc;
   if (ntiles * batch >= (int64_t(1) << 31)) return SPLINE_EINVAL;
+  if (kTopPdl && MODE == TILE_FINISH)  // K5 after K4 (which triggers at its start): programmatic launch
+    return launch_pdl(kern, dim3((unsigned)(ntiles * batch)), dim3(kTileThreads), sm, st, tl_status, x, y, n, rb, re, bc,
+                      yp1, ypn, y2, (T *)w.tile_rec, (const T *)w.tile_ext, (int *)w.badflag, (int)ntiles,
+                      tile_prefetch_blocks(kern, sm));
   kern<<<(unsigned)(ntiles * batch), kTileThreads, sm, st>>>(tl_status, x, y, n, rb, re, bc, yp1, ypn, y2, (T *)w.tile_rec,
                                                              (const T *)w.tile_ext, (int *)w.badflag, (int)ntiles,
                                                              tile_prefetch_blocks(kern, sm));
